@@ -1,0 +1,190 @@
+/* include/admm_b200.h — C ABI of the B200-native ADMM hot path (libadmm_b200.so).
+ *
+ * Drop-in boundary for the reference library admmsplit (header-only C++20 at
+ * /root/reference/proj/include/admmsplit).  Every entry point below names the
+ * reference interface it replaces (file:line, relative to that directory).  The
+ * C++ shim include/admmgpu/admmgpu.hpp re-exposes these with the reference's own
+ * signatures and exception types; INTEGRATION.md shows the bindings.
+ *
+ * Conventions
+ *   - Complex data are interleaved (re, im) IEEE binary64 (ADMM_C128) or binary32
+ *     (ADMM_C64) values; matrices are row-major, exactly the reference's CMatrix layout
+ *     (linalg.hpp:21-73) and CMAT payload (cmat_io.hpp:18-24).
+ *   - No exceptions cross the ABI.  Every call returns an admm_status; the message of
+ *     the last failure on the calling thread is admm_last_error(), and for
+ *     ADMM_E_NUMERICAL raised inside the iteration loop admm_last_good_iteration()
+ *     carries NumericalError::last_good_iteration() (errors.hpp:33-46).
+ *   - A plan owns its device memory, stream and CUDA graph.  Plans are independent;
+ *     one plan must not be used from two threads at once (GramSolver-style
+ *     reentrancy, gram.hpp:25, is provided by separate plans).
+ *   - There is no CPU fallback: without a CUDA device every compute entry point
+ *     returns ADMM_E_CUDA.
+ */
+#ifndef ADMM_B200_H
+#define ADMM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ADMM_B200_ABI_VERSION 1
+
+/* Exception classes of errors.hpp:10-81, in validation order. */
+typedef enum {
+  ADMM_OK = 0,
+  ADMM_E_DIMENSION = 1,   /* DimensionError   errors.hpp:19 */
+  ADMM_E_INDEX = 2,       /* IndexError       errors.hpp:25 */
+  ADMM_E_NUMERICAL = 3,   /* NumericalError   errors.hpp:31 */
+  ADMM_E_SINGULARITY = 4, /* SingularityError errors.hpp:48 */
+  ADMM_E_PARTITION = 5,   /* PartitionError   errors.hpp:54 */
+  ADMM_E_PARAMETER = 6,   /* ParameterError   errors.hpp:60 */
+  ADMM_E_CUDA = 7,        /* device / driver failure (no reference counterpart) */
+  ADMM_E_STATE = 8        /* API misuse (null pointer, wrong plan state) */
+} admm_status;
+
+/* The four solver entry points (reference.hpp:27, solvers.hpp:74,179,306). */
+typedef enum {
+  ADMM_REFERENCE = 0,  /* lasso_admm_reference: M = N = 1, kappa = lambda/rho */
+  ADMM_CONSENSUS = 1,  /* consensus_solve(problem, cfg, m):  M x 1 row split   */
+  ADMM_SECTIONING = 2, /* sectioning_solve(problem, cfg, n): 1 x N column split */
+  ADMM_HYBRID = 3      /* hybrid_solve(problem, cfg, m, n):  M x N grid         */
+} admm_method;
+
+typedef enum {
+  ADMM_C128 = 0, /* complex<double> storage of H and K (the reference type) */
+  ADMM_C64 = 1   /* complex<float> storage of H and K; iterates stay FP64    */
+} admm_dtype;
+
+/* SolverConfig (admm_core.hpp:17-35).  seed is carried but, as in the reference,
+ * unused by the solvers. */
+typedef struct {
+  double rho;
+  double lambda;
+  double scl;
+  uint64_t max_iters;
+  double eps_pri;
+  double eps_dual;
+  uint64_t seed;
+} admm_solver_config;
+
+/* Partition + execution options (make_partition partition.hpp:56-65 and
+ * SolveOptions report.hpp:42-46; threads has no meaning on the device). */
+typedef struct {
+  admm_method method;
+  uint64_t M;          /* row divisions (consensus m; 1 for sectioning/reference) */
+  uint64_t N;          /* column divisions (sectioning n; 1 for consensus/reference) */
+  int ragged;          /* SolveOptions::ragged */
+  admm_dtype dtype;    /* storage of the streamed matrices */
+  int device;          /* CUDA device ordinal */
+  int trace_objective; /* 1: objective every iteration (extra H pass, as the reference
+                          does at solvers.hpp:146); 0: objective of the final iterate only */
+} admm_plan_options;
+
+typedef struct admm_plan admm_plan;
+
+/* Per-iteration snapshot (IterateSnapshot, report.hpp:28-35).  Pointers are host
+ * buffers owned by the plan, valid during the callback. */
+typedef struct {
+  uint64_t iteration;          /* 1-based */
+  uint64_t n_pix;
+  const double* v;             /* n_pix complex */
+  const double* v_prev;        /* n_pix complex */
+  uint64_t n_workers;          /* M*N, worker id = i*N + j (solvers.hpp:305) */
+  const double* const* replica_u; /* n_workers pointers, segment-length complex each */
+  const uint64_t* replica_len; /* n_workers */
+  double primal, dual;         /* this iteration's residual norms */
+} admm_snapshot;
+typedef void (*admm_observer_fn)(const admm_snapshot* snap, void* user);
+
+/* Setup: validates (cfg -> problem -> partition -> Gram factor, the reference order),
+ * uploads the blocks, forms rho I + H_b H_b^H and its inverse on the device.
+ * Replaces the setup loops solvers.hpp:92-101 / 197-209 / 325-341 and
+ * GramSolver::GramSolver (gram.hpp:48-53).
+ *   h: n_meas x n_pix row-major host matrix of type h_dtype; g: n_meas complex128. */
+admm_status admm_plan_create(const admm_plan_options* opts, const admm_solver_config* cfg,
+                             uint64_t n_meas, uint64_t n_pix, const void* h, admm_dtype h_dtype,
+                             const double* g, admm_plan** out);
+
+/* Replace the measurement vector g (H, the partition and the factors are kept). */
+admm_status admm_plan_set_g(admm_plan* plan, const double* g);
+/* Replace lambda (kappa follows). */
+admm_status admm_plan_set_lambda(admm_plan* plan, double lambda);
+/* max_t |(H^H g)_t| of the (scaled) problem, computed on the device; used for the
+ * relative lambda rule of BASELINE.json (lambda = c * max|H^H g|). */
+admm_status admm_plan_max_abs_adjoint(admm_plan* plan, double* out);
+
+/* Full solve from u = s = v = 0 (solvers.hpp:108-166 and siblings).
+ *   solution: n_pix complex (SolveReport::solution, the final v);
+ *   trace:    max_iters x 3 doubles (primal, dual, objective) or NULL;
+ *   observer: NULL for the captured-graph fast path. */
+admm_status admm_plan_solve(admm_plan* plan, double* solution, double* trace,
+                            uint64_t* iterations_run, double* objective, admm_observer_fn observer,
+                            void* user);
+
+/* Benchmark entry points: reset the iterates, enqueue `iters` iterations on the
+ * plan's stream (CUDA-graph replays, no host sync), and expose that stream. */
+admm_status admm_plan_reset(admm_plan* plan);
+admm_status admm_plan_enqueue(admm_plan* plan, uint64_t iters);
+admm_status admm_plan_sync(admm_plan* plan);
+void* admm_plan_stream(admm_plan* plan);
+
+/* Per-kernel device time of one iteration, measured with CUDA events around
+ * individually launched kernels on the plan's stream (averaged over `iters`).
+ * names/ms: arrays of at least admm_plan_kernel_count() entries. */
+uint32_t admm_plan_kernel_count(const admm_plan* plan);
+admm_status admm_plan_profile(admm_plan* plan, uint64_t iters, const char** names, double* ms);
+
+typedef struct {
+  uint64_t n_blocks;
+  uint64_t h_bytes;             /* bytes of H storage (both passes stream it) */
+  uint64_t k_bytes;             /* bytes of K storage (one pass per iteration) */
+  uint64_t h_stream_bytes_per_iter; /* 2 * H bytes (algorithmic) */
+  uint64_t bytes_per_iter;      /* algorithmic HBM bytes per iteration incl. K + vectors */
+  uint64_t launches_per_iter;   /* kernels in one captured iteration */
+  uint64_t grid_gemv_n, grid_gemv_h;
+  double setup_seconds;         /* upload + Gram + inverse (host wall clock) */
+  uint64_t inner_dim_max;       /* largest factored dimension */
+} admm_plan_info;
+admm_status admm_plan_get_info(const admm_plan* plan, admm_plan_info* info);
+
+/* Current iterate getters (host copies): which = 0 v (n_pix), 1 v_prev (n_pix),
+ * 2 u of every worker concatenated in worker order (sum of segment lengths). */
+admm_status admm_plan_read(admm_plan* plan, int which, double* dst, uint64_t count);
+
+void admm_plan_destroy(admm_plan* plan);
+
+/* ---- L0/L1 operations on the device (KAT surface of linalg.hpp / prox.hpp / gram.hpp) */
+/* y = A x (linalg.hpp:97-111), A rows x cols complex128. */
+admm_status admm_matvec(const double* a, uint64_t rows, uint64_t cols, const double* x, double* y,
+                        int device);
+/* y = A^H x (linalg.hpp:114-127). */
+admm_status admm_adjoint_matvec(const double* a, uint64_t rows, uint64_t cols, const double* x,
+                                double* y, int device);
+/* out = S_kappa(a) element-wise (prox.hpp:21-25). */
+admm_status admm_soft_threshold(const double* a, uint64_t n, double kappa, double* out, int device);
+/* x = (H^H H + rho I)^-1 rhs (GramSolver::solve, gram.hpp:63-78). */
+admm_status admm_gram_solve(const double* h, uint64_t rows, uint64_t cols, double rho,
+                            const double* rhs, double* x, int device);
+
+/* ---- input tooling (host; not the hot path) */
+/* gen_problem (generate.hpp:32-89) with the reference's RNG stream (rng.hpp); H is
+ * written as complex128 or complex64 (rounded from the same FP64 values). */
+admm_status admm_gen_problem(uint64_t n_meas, uint64_t n_pix, uint64_t k, double snr_db, uint64_t seed,
+                             int kind, void* h, admm_dtype h_dtype, double* g, double* truth,
+                             double* noise_sigma);
+/* CRA-like structured H of BASELINE configs 3/5 (conventions in DESIGN.md). */
+admm_status admm_gen_cra(uint64_t n_tx, uint64_t n_freq, uint64_t grid, double spacing, double z0,
+                         double aperture, double f0, double f1, uint64_t n_facets, uint64_t seed,
+                         void* h, admm_dtype h_dtype);
+
+const char* admm_last_error(void);
+uint64_t admm_last_good_iteration(void);
+int admm_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ADMM_B200_H */

@@ -1,0 +1,83 @@
+"""ctypes binding of libadmm_b200.so (the C ABI declared in include/admm_b200.h).
+
+There is deliberately no fallback: if the shared library is missing the import of
+this module raises, and every compute call returns ADMM_E_CUDA without a device.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG_DIR, "libadmm_b200.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+        "(nvcc, sm_100a).  There is no CPU fallback.")
+
+_u64, _dbl, _ptr, _i32, _u32 = (ctypes.c_uint64, ctypes.c_double, ctypes.c_void_p, ctypes.c_int,
+                                ctypes.c_uint32)
+
+
+class SolverConfigC(ctypes.Structure):
+    _fields_ = [("rho", _dbl), ("lambda_", _dbl), ("scl", _dbl), ("max_iters", _u64),
+                ("eps_pri", _dbl), ("eps_dual", _dbl), ("seed", _u64)]
+
+
+class PlanOptionsC(ctypes.Structure):
+    _fields_ = [("method", _i32), ("M", _u64), ("N", _u64), ("ragged", _i32), ("dtype", _i32),
+                ("device", _i32), ("trace_objective", _i32)]
+
+
+class SnapshotC(ctypes.Structure):
+    _fields_ = [("iteration", _u64), ("n_pix", _u64), ("v", ctypes.POINTER(_dbl)),
+                ("v_prev", ctypes.POINTER(_dbl)), ("n_workers", _u64),
+                ("replica_u", ctypes.POINTER(ctypes.POINTER(_dbl))),
+                ("replica_len", ctypes.POINTER(_u64)), ("primal", _dbl), ("dual", _dbl)]
+
+
+class PlanInfoC(ctypes.Structure):
+    _fields_ = [("n_blocks", _u64), ("h_bytes", _u64), ("k_bytes", _u64),
+                ("h_stream_bytes_per_iter", _u64), ("bytes_per_iter", _u64),
+                ("launches_per_iter", _u64), ("grid_gemv_n", _u64), ("grid_gemv_h", _u64),
+                ("setup_seconds", _dbl), ("inner_dim_max", _u64)]
+
+
+OBSERVER = ctypes.CFUNCTYPE(None, ctypes.POINTER(SnapshotC), ctypes.c_void_p)
+
+lib = ctypes.CDLL(LIB_PATH)
+
+_SIGS = {
+    "admm_abi_version": ([], _i32),
+    "admm_last_error": ([], ctypes.c_char_p),
+    "admm_last_good_iteration": ([], _u64),
+    "admm_plan_create": ([ctypes.POINTER(PlanOptionsC), ctypes.POINTER(SolverConfigC), _u64, _u64,
+                          _ptr, _i32, _ptr, ctypes.POINTER(_ptr)], _i32),
+    "admm_plan_set_g": ([_ptr, _ptr], _i32),
+    "admm_plan_set_lambda": ([_ptr, _dbl], _i32),
+    "admm_plan_max_abs_adjoint": ([_ptr, ctypes.POINTER(_dbl)], _i32),
+    "admm_plan_solve": ([_ptr, _ptr, _ptr, ctypes.POINTER(_u64), ctypes.POINTER(_dbl), OBSERVER,
+                         _ptr], _i32),
+    "admm_plan_reset": ([_ptr], _i32),
+    "admm_plan_enqueue": ([_ptr, _u64], _i32),
+    "admm_plan_sync": ([_ptr], _i32),
+    "admm_plan_stream": ([_ptr], _ptr),
+    "admm_plan_kernel_count": ([_ptr], _u32),
+    "admm_plan_profile": ([_ptr, _u64, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(_dbl)], _i32),
+    "admm_plan_get_info": ([_ptr, ctypes.POINTER(PlanInfoC)], _i32),
+    "admm_plan_read": ([_ptr, _i32, _ptr, _u64], _i32),
+    "admm_plan_destroy": ([_ptr], None),
+    "admm_matvec": ([_ptr, _u64, _u64, _ptr, _ptr, _i32], _i32),
+    "admm_adjoint_matvec": ([_ptr, _u64, _u64, _ptr, _ptr, _i32], _i32),
+    "admm_soft_threshold": ([_ptr, _u64, _dbl, _ptr, _i32], _i32),
+    "admm_gram_solve": ([_ptr, _u64, _u64, _dbl, _ptr, _ptr, _i32], _i32),
+    "admm_gen_problem": ([_u64, _u64, _u64, _dbl, _u64, _i32, _ptr, _i32, _ptr, _ptr, _ptr], _i32),
+    "admm_gen_cra": ([_u64, _u64, _u64, _dbl, _dbl, _dbl, _dbl, _dbl, _u64, _u64, _ptr, _i32], _i32),
+}
+for _name, (_args, _res) in _SIGS.items():
+    _f = getattr(lib, _name)
+    _f.argtypes = _args
+    _f.restype = _res
+
+EXPORTED = tuple(_SIGS)

@@ -1,0 +1,125 @@
+// admm_common.cuh — shared device helpers for the B200 ADMM engine (sm_100a).
+//
+// Complex data are interleaved (re, im).  Storage of H and of the Woodbury
+// inverse K is either complex128 (double2) or complex64 (float2); all arithmetic
+// and every vector iterate is FP64 (double2) regardless of storage, so the c64
+// path only rounds the two streamed matrices.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace admm {
+
+constexpr int kWarp = 32;
+constexpr int kCtaThreads = 256;  // 8 warps per CTA for every streaming kernel
+constexpr int kCtaWarps = kCtaThreads / kWarp;
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+// acc += a * b
+__device__ __forceinline__ void cmac(double2& acc, double2 a, double2 b) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(a.y, b.x, acc.y);
+}
+// acc += conj(a) * b
+__device__ __forceinline__ void cmac_conj(double2& acc, double2 a, double2 b) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(-a.y, b.x, acc.y);
+}
+__device__ __forceinline__ double cabs2(double2 a) { return a.x * a.x + a.y * a.y; }
+__device__ __forceinline__ bool cfinite(double2 a) { return isfinite(a.x) && isfinite(a.y); }
+
+// prox.hpp:15-19: |a| > kappa ? a (1 - kappa/|a|) : 0, with |a| = hypot.
+__device__ __forceinline__ double2 soft_threshold(double2 a, double kappa) {
+  const double mag = hypot(a.x, a.y);
+  if (mag > kappa) {
+    const double f = 1.0 - kappa / mag;
+    return make_double2(a.x * f, a.y * f);
+  }
+  return make_double2(0.0, 0.0);
+}
+
+// ---- streaming loads of the matrix operand (read once per pass) -------------
+// 256-bit LDG with L1 no-allocate.  EvictFirst=true adds the L2 evict-first hint
+// (used when the operand is much larger than L2 and would only pollute it).
+struct V256 {
+  uint64_t w[4];
+};
+template <bool EvictFirst>
+__device__ __forceinline__ V256 ld_stream256(const void* p) {
+  V256 r;
+  if constexpr (EvictFirst) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v4.b64 {%0,%1,%2,%3}, [%4];"
+                 : "=l"(r.w[0]), "=l"(r.w[1]), "=l"(r.w[2]), "=l"(r.w[3])
+                 : "l"(p));
+  } else {
+    asm volatile("ld.global.nc.L1::no_allocate.v4.b64 {%0,%1,%2,%3}, [%4];"
+                 : "=l"(r.w[0]), "=l"(r.w[1]), "=l"(r.w[2]), "=l"(r.w[3])
+                 : "l"(p));
+  }
+  return r;
+}
+
+// Storage traits: how many complex elements one 32-byte vector carries and how
+// to widen them to FP64.
+template <typename S>
+struct Store;
+template <>
+struct Store<double2> {
+  static constexpr int kPerVec = 2;  // 2 x 16 B
+  __device__ __forceinline__ static double2 get(const V256& v, int e) {
+    return make_double2(__longlong_as_double((long long)v.w[2 * e]),
+                        __longlong_as_double((long long)v.w[2 * e + 1]));
+  }
+  __device__ __forceinline__ static double2 widen(double2 a) { return a; }
+  __device__ __forceinline__ static double2 narrow(double2 a) { return a; }
+};
+template <>
+struct Store<float2> {
+  static constexpr int kPerVec = 4;  // 4 x 8 B
+  __device__ __forceinline__ static double2 get(const V256& v, int e) {
+    const uint64_t w = v.w[e];
+    return make_double2((double)__uint_as_float((unsigned)(w & 0xffffffffu)),
+                        (double)__uint_as_float((unsigned)(w >> 32)));
+  }
+  __device__ __forceinline__ static double2 widen(float2 a) { return make_double2(a.x, a.y); }
+  __device__ __forceinline__ static float2 narrow(double2 a) {
+    return make_float2((float)a.x, (float)a.y);
+  }
+};
+
+// ---- stream-K work split ----------------------------------------------------
+// Units [0, U) are split over P CTAs: CTA p owns [lo(p), lo(p+1)), lo(p) = p*U/P.
+__host__ __device__ __forceinline__ uint64_t sk_lo(uint64_t p, uint64_t U, uint64_t P) {
+  return (p * U) / P;
+}
+// The CTA that owns unit x.
+__host__ __device__ __forceinline__ uint64_t sk_owner(uint64_t x, uint64_t U, uint64_t P) {
+  return ((x + 1) * P - 1) / U;
+}
+
+// ---- deterministic block reduction (fixed tree, no atomics) -----------------
+template <int kThreads>
+__device__ __forceinline__ double block_sum(double v, double* smem) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+  __syncthreads();
+  if (lane == 0) smem[warp] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (warp == 0) {
+    r = lane < kThreads / kWarp ? smem[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+  }
+  return r;  // valid in thread 0
+}
+
+}  // namespace admm

@@ -1,0 +1,1084 @@
+// admm_plan.cu — host runtime of the B200 ADMM engine and its C ABI (admm_b200.h).
+//
+// One plan = one solve configuration on one device: the partition (partition.hpp),
+// the uploaded blocks, the per-block Woodbury inverses (gram.hpp), the iterate
+// vectors, and a captured CUDA graph of one ADMM iteration.  The reference's
+// simulated node runtime (parallel_for + coordinator copies, parallel.hpp /
+// solvers.hpp:109-136) becomes a single stream: all M*N blocks are processed by
+// each kernel launch, and the coordinator reductions are fixed-order device sums.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <limits>
+#include <memory>
+#include <string>
+#include <type_traits>
+#include <thread>
+#include <vector>
+
+#include "admm_b200.h"
+#include "admm_kernels.cuh"
+#include "admm_setup.cuh"
+
+using namespace admm;
+
+namespace {
+
+thread_local std::string g_last_error;
+thread_local uint64_t g_last_good = 0;
+
+struct Fail {
+  admm_status st;
+  std::string msg;
+  uint64_t last_good = 0;
+};
+
+#define CK(call)                                                                         \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      throw Fail{ADMM_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)};       \
+  } while (0)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  void alloc(size_t b) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = b;
+    CK(cudaMalloc(&p, std::max<size_t>(b, 256)));
+    CK(cudaMemset(p, 0, std::max<size_t>(b, 256)));
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+uint64_t round_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+uint64_t cdiv(uint64_t x, uint64_t a) { return (x + a - 1) / a; }
+
+// partition.hpp:34-52 (split_bounds) with the reference's PartitionError texts.
+std::vector<uint64_t> split_bounds(uint64_t total, uint64_t parts, bool ragged, const char* axis) {
+  if (parts < 1 || parts > total)
+    throw Fail{ADMM_E_PARTITION, std::string("make_partition: ") + axis + " division count " +
+                                     std::to_string(parts) + " not in [1, " + std::to_string(total) + "]"};
+  if (!ragged && total % parts != 0)
+    throw Fail{ADMM_E_PARTITION, "make_partition: " + std::to_string(parts) + " does not divide " +
+                                     std::to_string(total) + " " + axis +
+                                     "s (pass ragged=true to allow uneven blocks)"};
+  const uint64_t base = total / parts, rem = total % parts;
+  std::vector<uint64_t> b(parts + 1, 0);
+  for (uint64_t k = 0; k < parts; ++k) b[k + 1] = b[k] + base + (k < rem ? 1 : 0);
+  return b;
+}
+
+template <typename T>
+bool host_all_finite(const T* p, uint64_t n) {  // multi-threaded problem.validate() scan
+  unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  if (n < (1u << 20)) nt = 1;
+  std::vector<char> ok(nt, 1);
+  std::vector<std::thread> th;
+  for (unsigned t = 0; t < nt; ++t)
+    th.emplace_back([&, t] {
+      const uint64_t lo = n * t / nt, hi = n * (t + 1) / nt;
+      for (uint64_t i = lo; i < hi; ++i)
+        if (!std::isfinite(p[i])) {
+          ok[t] = 0;
+          return;
+        }
+    });
+  for (auto& x : th) x.join();
+  for (char c : ok)
+    if (!c) return false;
+  return true;
+}
+
+// Streaming geometry (see admm_kernels.cuh).
+constexpr int kVN = 4;  // 32-byte vectors per lane per row in gemv_n
+constexpr int kVH = 2;  // 32-byte vectors per lane per row in gemv_h
+template <typename S>
+constexpr int chunk_n() { return kWarp * kVN * Store<S>::kPerVec; }
+template <typename S>
+constexpr int chunk_h() { return kWarp * kVH * Store<S>::kPerVec; }
+
+struct Geom {
+  uint64_t U = 0, P = 0;
+};
+
+}  // namespace
+
+struct admm_plan {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  admm_dtype dtype = ADMM_C128;
+  admm_method method = ADMM_HYBRID;
+  uint64_t n_meas = 0, n_pix = 0, M = 1, N = 1;
+  bool ragged = false, trace_obj = false;
+  admm_solver_config cfg{};
+  std::vector<uint64_t> rb, cb;
+  std::vector<BlockDesc> blocks;
+  std::vector<MatDesc> hN, hNv, kN, hH, hHg;
+  std::vector<GramDesc> gram;
+  uint64_t mvec_total = 0, vec_total = 0, seg_total = 0, h_elems = 0, k_elems = 0, a_elems = 0;
+  uint32_t max_rows = 0, max_seg = 0, max_rowblock = 0, max_m = 0;
+  DevBuf dH, dK, dg, dghat, dgij, dr, dq, du, ds, dc, dv, dvprev;
+  DevBuf dwpart, dqpart, dzpart, dopart, dgpart;
+  DevBuf dred, dored, dtrace, dstate, dparams, dblocks, dhN, dhNv, dkN, dhH, dhHg, dgram, dobj;
+  Geom gN, gK, gH, gO, gG;
+  uint32_t zgx = 0, rgx = 0, ogx = 0, nz = 0, no = 0;
+  uint64_t trace_cap = 0;
+  cudaGraphExec_t exec = nullptr;
+  uint64_t graph_iters = 0;
+  double setup_s = 0.0;
+  size_t elem = 16;
+  int num_sms = 148;
+  Params params{};
+  // host scratch for snapshots
+  std::vector<double> h_v, h_vprev, h_u, h_seg;
+
+  ~admm_plan() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+template <typename S, typename K>
+uint64_t grid_for(K kernel, uint64_t U, int sms, size_t smem = 0) {
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kCtaThreads, smem));
+  occ = std::max(occ, 1);
+  return std::max<uint64_t>(1, std::min<uint64_t>(U, (uint64_t)sms * occ));
+}
+
+template <typename S>
+void build_geometry(admm_plan* p) {
+  const uint64_t CN = chunk_n<S>(), CH = chunk_h<S>();
+  const uint64_t nb = p->blocks.size();
+  p->hN.assign(nb, {});
+  p->hNv.assign(nb, {});
+  p->kN.assign(nb, {});
+  p->hH.assign(nb, {});
+  p->hHg.assign(nb, {});
+  p->gram.assign(nb, {});
+  uint64_t uN = 0, uK = 0, uH = 0, pN = 0, pK = 0, pH = 0, hoff = 0, koff = 0, aoff = 0;
+  for (uint64_t b = 0; b < nb; ++b) {
+    const BlockDesc& bd = p->blocks[b];
+    const uint32_t ld = (uint32_t)round_up(bd.cols, 8), ldk = (uint32_t)round_up(bd.rows, 8);
+    MatDesc n{};
+    n.a_off = hoff;
+    n.x_off = bd.vec_off;
+    n.rows = bd.rows;
+    n.cols = bd.cols;
+    n.ld = ld;
+    n.n_chunks = (uint32_t)cdiv(bd.cols, CN);
+    n.n_tiles = (uint32_t)cdiv(bd.rows, kRowsPerGroup);
+    n.unit0 = uN;
+    n.part_off = pN;
+    uN += (uint64_t)n.n_chunks * n.n_tiles;
+    pN += (uint64_t)n.n_chunks * n.n_tiles * kRowsPerGroup;
+    p->hN[b] = n;
+    MatDesc nv = n;
+    nv.x_off = bd.seg_off;
+    p->hNv[b] = nv;
+    MatDesc k{};
+    k.a_off = koff;
+    k.x_off = bd.mvec_off;
+    k.rows = bd.rows;
+    k.cols = bd.rows;
+    k.ld = ldk;
+    k.n_chunks = (uint32_t)cdiv(bd.rows, CN);
+    k.n_tiles = (uint32_t)cdiv(bd.rows, kRowsPerGroup);
+    k.unit0 = uK;
+    k.part_off = pK;
+    uK += (uint64_t)k.n_chunks * k.n_tiles;
+    pK += (uint64_t)k.n_chunks * k.n_tiles * kRowsPerGroup;
+    p->kN[b] = k;
+    MatDesc h{};
+    h.a_off = hoff;
+    h.x_off = bd.mvec_off;
+    h.rows = bd.rows;
+    h.cols = bd.cols;
+    h.ld = ld;
+    h.n_chunks = (uint32_t)cdiv(bd.cols, CH);
+    h.n_tiles = (uint32_t)cdiv(bd.rows, kRowTileH);
+    h.unit0 = uH;
+    h.part_off = pH;
+    uH += (uint64_t)h.n_chunks * h.n_tiles;
+    pH += (uint64_t)h.n_chunks * h.n_tiles * CH;
+    p->hH[b] = h;
+    MatDesc hg = h;
+    hg.x_off = bd.row0;  // gemv_h over g itself: Q = g (global rows)
+    p->hHg[b] = hg;
+    GramDesc gd{};
+    gd.h_off = hoff;
+    gd.a_off = aoff;
+    gd.k_off = koff;
+    gd.m = bd.rows;
+    gd.n = bd.cols;
+    gd.ld = ld;
+    gd.ldk = ldk;
+    p->gram[b] = gd;
+    hoff += (uint64_t)bd.rows * ld;
+    koff += (uint64_t)bd.rows * ldk;
+    aoff += (uint64_t)bd.rows * bd.rows;
+  }
+  p->h_elems = hoff;
+  p->k_elems = koff;
+  p->a_elems = aoff;
+  p->gN.U = uN;
+  p->gK.U = uK;
+  p->gH.U = uH;
+  p->gO.U = uN;
+  p->gG.U = uH;
+  p->gN.P = grid_for<S>(gemv_n_kernel<S, kVN, false>, uN, p->num_sms);
+  p->gK.P = grid_for<S>(gemv_n_kernel<S, kVN, false>, uK, p->num_sms);
+  p->gH.P = grid_for<S>(gemv_h_kernel<S, kVH, false>, uH, p->num_sms);
+  p->gO.P = p->gN.P;
+  p->gG.P = p->gH.P;
+  p->dwpart.alloc(pN * sizeof(double2));
+  p->dopart.alloc(pN * sizeof(double2));
+  p->dqpart.alloc(pK * sizeof(double2));
+  p->dzpart.alloc(pH * sizeof(double2));
+  p->dgpart.alloc(pH * sizeof(double2));
+}
+
+void upload_desc(DevBuf& d, const void* src, size_t bytes) {
+  d.alloc(bytes);
+  CK(cudaMemcpy(d.p, src, bytes, cudaMemcpyHostToDevice));
+}
+
+// Upload the blocks of the host matrix into the storage arena (partition.hpp:79-125
+// materialises the same blocks as host copies).
+template <typename S>
+void upload_h(admm_plan* p, const void* h, admm_dtype h_dtype) {
+  p->dH.alloc(p->h_elems * sizeof(S));
+  const size_t hsz = h_dtype == ADMM_C128 ? 16 : 8;
+  const bool direct = (h_dtype == ADMM_C128) == std::is_same<S, double2>::value;
+  DevBuf tmp;
+  if (!direct) {
+    uint64_t maxe = 0;
+    for (auto& b : p->blocks) maxe = std::max<uint64_t>(maxe, (uint64_t)b.rows * b.cols);
+    tmp.alloc(std::min<uint64_t>(maxe, 1ull << 26) * 16);
+  }
+  for (size_t b = 0; b < p->blocks.size(); ++b) {
+    const BlockDesc& bd = p->blocks[b];
+    const MatDesc& md = p->hN[b];
+    const char* src = static_cast<const char*>(h) + ((uint64_t)bd.row0 * p->n_pix + bd.col0) * hsz;
+    if (direct) {
+      CK(cudaMemcpy2DAsync(p->dH.as<S>() + md.a_off, (size_t)md.ld * sizeof(S), src, p->n_pix * hsz,
+                           (size_t)bd.cols * sizeof(S), bd.rows, cudaMemcpyHostToDevice, p->stream));
+      continue;
+    }
+    // convert through an FP64 staging buffer, a slab of rows at a time
+    const uint64_t slab = std::max<uint64_t>(1, (tmp.bytes / 16) / std::max<uint32_t>(bd.cols, 1));
+    for (uint64_t r0 = 0; r0 < bd.rows; r0 += slab) {
+      const uint32_t nr = (uint32_t)std::min<uint64_t>(slab, bd.rows - r0);
+      if (h_dtype == ADMM_C64) {  // float host -> widen on the host side of the copy
+        std::vector<double> w((size_t)nr * bd.cols * 2);
+        const float* fs = reinterpret_cast<const float*>(src) + r0 * p->n_pix * 2;
+        for (uint32_t r = 0; r < nr; ++r)
+          for (uint32_t c = 0; c < 2 * bd.cols; ++c) w[(size_t)r * 2 * bd.cols + c] = fs[(size_t)r * 2 * p->n_pix + c];
+        CK(cudaMemcpyAsync(tmp.p, w.data(), w.size() * 8, cudaMemcpyHostToDevice, p->stream));
+        CK(cudaStreamSynchronize(p->stream));
+      } else {
+        CK(cudaMemcpy2DAsync(tmp.p, (size_t)bd.cols * 16, src + r0 * p->n_pix * hsz, p->n_pix * hsz,
+                             (size_t)bd.cols * 16, nr, cudaMemcpyHostToDevice, p->stream));
+      }
+      dim3 grid((unsigned)std::min<uint64_t>(cdiv(bd.cols, 256), 64), nr);
+      narrow_rows_kernel<S><<<grid, 256, 0, p->stream>>>(tmp.as<double2>(), bd.cols,
+                                                          p->dH.as<S>() + md.a_off + r0 * md.ld, md.ld,
+                                                          nr, bd.cols, p->cfg.scl);
+      CK(cudaGetLastError());
+      CK(cudaStreamSynchronize(p->stream));
+    }
+  }
+  if (direct && p->cfg.scl != 1.0) {  // apply_scaling, problem.hpp:59-66 (converted
+                                      // uploads scale in FP64 before rounding)
+    scale_kernel<S><<<p->num_sms * 8, 256, 0, p->stream>>>(p->dH.as<S>(), p->h_elems, p->cfg.scl);
+    CK(cudaGetLastError());
+  }
+  DevBuf flag;
+  flag.alloc(4);
+  finite_kernel<S><<<p->num_sms * 8, 256, 0, p->stream>>>(p->dH.as<S>(), p->h_elems, flag.as<unsigned>());
+  CK(cudaGetLastError());
+  unsigned hf = 0;
+  CK(cudaMemcpyAsync(&hf, flag.p, 4, cudaMemcpyDeviceToHost, p->stream));
+  CK(cudaStreamSynchronize(p->stream));
+  if (hf) throw Fail{ADMM_E_NUMERICAL, "SensingProblem: non-finite entries"};
+}
+
+// rho I + H H^H per block, Gauss-Jordan inverse, store K (gram.hpp:48-53,92-122;
+// cholesky.hpp:48-74).
+template <typename S>
+void factor_blocks(admm_plan* p) {
+  const uint64_t nb = p->blocks.size();
+  upload_desc(p->dgram, p->gram.data(), nb * sizeof(GramDesc));
+  DevBuf A, rowk, colk, flag;
+  A.alloc(p->a_elems * sizeof(double2));
+  rowk.alloc((uint64_t)nb * p->max_m * sizeof(double2));
+  colk.alloc((uint64_t)nb * p->max_m * sizeof(double2));
+  flag.alloc(4);
+  const uint32_t tiles = (uint32_t)cdiv(p->max_m, kGT);
+  gram_kernel<S><<<dim3(tiles, tiles, (unsigned)nb), 256, 0, p->stream>>>(
+      p->dH.as<S>(), p->dgram.as<GramDesc>(), A.as<double2>(), p->cfg.rho, flag.as<unsigned>());
+  CK(cudaGetLastError());
+  unsigned hf = 0;
+  CK(cudaMemcpyAsync(&hf, flag.p, 4, cudaMemcpyDeviceToHost, p->stream));
+  CK(cudaStreamSynchronize(p->stream));
+  if (hf & 1u) throw Fail{ADMM_E_NUMERICAL, "CholeskyFactor: non-finite entries in input matrix"};
+  const unsigned gx = (unsigned)std::min<uint64_t>(cdiv(p->max_m, 256), 8);
+  for (uint32_t k = 0; k < p->max_m; ++k) {
+    gj_save_kernel<<<dim3((unsigned)cdiv(p->max_m, 256), (unsigned)nb), 256, 0, p->stream>>>(
+        A.as<double2>(), p->dgram.as<GramDesc>(), rowk.as<double2>(), colk.as<double2>(), p->max_m, k,
+        flag.as<unsigned>());
+    gj_update_kernel<<<dim3(gx, p->max_m, (unsigned)nb), 256, 0, p->stream>>>(
+        A.as<double2>(), p->dgram.as<GramDesc>(), rowk.as<double2>(), colk.as<double2>(), p->max_m, k);
+  }
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(&hf, flag.p, 4, cudaMemcpyDeviceToHost, p->stream));
+  CK(cudaStreamSynchronize(p->stream));
+  if (hf & 2u)
+    throw Fail{ADMM_E_SINGULARITY,
+               "CholeskyFactor: pivot is not positive (matrix not positive definite or "
+               "contaminated by non-finite values)"};
+  p->dK.alloc(p->k_elems * sizeof(S));
+  k_store_kernel<S><<<dim3(gx, p->max_m, (unsigned)nb), 256, 0, p->stream>>>(
+      A.as<double2>(), p->dgram.as<GramDesc>(), p->dK.as<S>(), flag.as<unsigned>());
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(&hf, flag.p, 4, cudaMemcpyDeviceToHost, p->stream));
+  CK(cudaStreamSynchronize(p->stream));
+  if (hf & 1u) throw Fail{ADMM_E_NUMERICAL, "GramSolver: non-finite inverse"};
+}
+
+RowVecs row_vecs(admm_plan* p) {
+  return RowVecs{p->dg.as<double2>(), p->dghat.as<double2>(), p->dgij.as<double2>(), p->dr.as<double2>(),
+                 p->dq.as<double2>()};
+}
+ColVecs col_vecs(admm_plan* p) {
+  return ColVecs{p->du.as<double2>(), p->ds.as<double2>(), p->dc.as<double2>(), p->dv.as<double2>(),
+                 p->dvprev.as<double2>()};
+}
+
+// Launch list of one iteration (the order of solvers.hpp's phases).
+template <typename S>
+void enqueue_iteration(admm_plan* p, cudaStream_t s, bool with_objective, std::vector<cudaEvent_t>* ev) {
+  constexpr int CH = chunk_h<S>();
+  const int nb = (int)p->blocks.size();
+  const uint32_t N = (uint32_t)p->N, M = (uint32_t)p->M;
+  auto mark = [&](size_t k) {
+    if (ev) CK(cudaEventRecord((*ev)[k], s));
+  };
+  mark(0);
+  gemv_n_kernel<S, kVN, false><<<(unsigned)p->gN.P, kCtaThreads, 0, s>>>(
+      p->dH.as<S>(), p->dc.as<double2>(), p->dwpart.as<double2>(), p->dhN.as<MatDesc>(), nb, p->gN.U);
+  mark(1);
+  rows_finalize_kernel<kRhs><<<dim3(p->rgx, nb), kCtaThreads, 0, s>>>(
+      row_vecs(p), p->dwpart.as<double2>(), p->dhN.as<MatDesc>(), p->dblocks.as<BlockDesc>(), N, p->gN.U,
+      p->gN.P, p->dparams.as<Params>());
+  mark(2);
+  gemv_n_kernel<S, kVN, false><<<(unsigned)p->gK.P, kCtaThreads, 0, s>>>(
+      p->dK.as<S>(), p->dr.as<double2>(), p->dqpart.as<double2>(), p->dkN.as<MatDesc>(), nb, p->gK.U);
+  mark(3);
+  rows_finalize_kernel<kQ><<<dim3(p->rgx, nb), kCtaThreads, 0, s>>>(
+      row_vecs(p), p->dqpart.as<double2>(), p->dkN.as<MatDesc>(), p->dblocks.as<BlockDesc>(), N, p->gK.U,
+      p->gK.P, p->dparams.as<Params>());
+  mark(4);
+  gemv_h_kernel<S, kVH, false><<<(unsigned)p->gH.P, kCtaThreads, 0, s>>>(
+      p->dH.as<S>(), p->dq.as<double2>(), p->dzpart.as<double2>(), p->dhH.as<MatDesc>(), nb, p->gH.U);
+  mark(5);
+  zupdate_kernel<CH><<<dim3(p->zgx, N), kCtaThreads, 0, s>>>(
+      col_vecs(p), p->dzpart.as<double2>(), p->dhH.as<MatDesc>(), p->dblocks.as<BlockDesc>(), M, N, p->gH.U,
+      p->gH.P, p->dparams.as<Params>(), p->dred.as<double>(), p->dstate.as<IterState>());
+  mark(6);
+  if (with_objective) {
+    gemv_n_kernel<S, kVN, false><<<(unsigned)p->gO.P, kCtaThreads, 0, s>>>(
+        p->dH.as<S>(), p->dv.as<double2>(), p->dopart.as<double2>(), p->dhNv.as<MatDesc>(), nb, p->gO.U);
+    objective_rows_kernel<<<dim3(p->ogx, M), kCtaThreads, 0, s>>>(
+        p->dg.as<double2>(), p->dopart.as<double2>(), p->dhNv.as<MatDesc>(), p->dblocks.as<BlockDesc>(), N,
+        p->gO.U, p->gO.P, p->dored.as<double>());
+  }
+  finalize_kernel<<<1, kCtaThreads, 0, s>>>(p->dred.as<double>(), p->nz, p->dored.as<double>(),
+                                            with_objective ? p->no : 0, p->dparams.as<Params>(),
+                                            p->dtrace.as<double>(), p->trace_cap, p->dstate.as<IterState>());
+  mark(7);
+  CK(cudaGetLastError());
+}
+
+void enqueue_iteration_any(admm_plan* p, cudaStream_t s, bool obj, std::vector<cudaEvent_t>* ev) {
+  if (p->dtype == ADMM_C128)
+    enqueue_iteration<double2>(p, s, obj, ev);
+  else
+    enqueue_iteration<float2>(p, s, obj, ev);
+}
+
+// Objective of the current v (admm_core.hpp:60-64) into *d_obj, without touching
+// the iteration state.
+__global__ void objective_final_kernel(const double* __restrict__ red, uint32_t nz,
+                                       const double* __restrict__ ored, uint32_t no,
+                                       const Params* __restrict__ prm, double* out) {
+  __shared__ double sm[kCtaWarps];
+  double l = 0.0, o = 0.0;
+  for (uint32_t k = threadIdx.x; k < nz; k += kCtaThreads) l += red[2 * nz + k];
+  for (uint32_t k = threadIdx.x; k < no; k += kCtaThreads) o += ored[k];
+  l = block_sum<kCtaThreads>(l, sm);
+  o = block_sum<kCtaThreads>(o, sm);
+  if (threadIdx.x == 0) *out = 0.5 * o + prm->lambda * l;
+}
+
+template <typename S>
+void enqueue_objective(admm_plan* p, cudaStream_t s) {
+  const int nb = (int)p->blocks.size();
+  gemv_n_kernel<S, kVN, false><<<(unsigned)p->gO.P, kCtaThreads, 0, s>>>(
+      p->dH.as<S>(), p->dv.as<double2>(), p->dopart.as<double2>(), p->dhNv.as<MatDesc>(), nb, p->gO.U);
+  objective_rows_kernel<<<dim3(p->ogx, (unsigned)p->M), kCtaThreads, 0, s>>>(
+      p->dg.as<double2>(), p->dopart.as<double2>(), p->dhNv.as<MatDesc>(), p->dblocks.as<BlockDesc>(),
+      (uint32_t)p->N, p->gO.U, p->gO.P, p->dored.as<double>());
+  objective_final_kernel<<<1, kCtaThreads, 0, s>>>(p->dred.as<double>(), p->nz, p->dored.as<double>(), p->no,
+                                                   p->dparams.as<Params>(), p->dobj.as<double>());
+  CK(cudaGetLastError());
+}
+
+// max |(H^H g)_t| over all columns: gemv_h with q = g, then the row-block sum.
+template <int CH>
+__global__ void adjoint_absmax_kernel(const double2* __restrict__ part, const MatDesc* __restrict__ mats,
+                                      const BlockDesc* __restrict__ blocks, uint32_t M, uint32_t N, uint64_t U,
+                                      uint64_t P, double* __restrict__ out) {
+  __shared__ double sm[kCtaThreads];
+  const uint32_t j = blockIdx.y;
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  double m = 0.0;
+  if (t < blocks[j].cols) {
+    double2 z = make_double2(0.0, 0.0);
+    for (uint32_t i = 0; i < M; ++i) z = cadd(z, sum_cols_part<CH>(part, mats[i * N + j], t, U, P));
+    m = hypot(z.x, z.y);
+  }
+  sm[threadIdx.x] = m;
+  __syncthreads();
+  for (int o = kCtaThreads / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sm[threadIdx.x] = fmax(sm[threadIdx.x], sm[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[blockIdx.y * gridDim.x + blockIdx.x] = sm[0];
+}
+
+void set_params(admm_plan* p) {
+  const double m = (double)p->M;
+  p->params.rho = p->cfg.rho;
+  p->params.lambda = p->cfg.lambda;
+  p->params.m_rep = m;
+  // kappa: solvers.hpp:104 / 344 (lambda/(M rho)); solvers.hpp:212 and
+  // reference.hpp:43 (lambda/rho).
+  p->params.kappa = (p->method == ADMM_CONSENSUS || p->method == ADMM_HYBRID)
+                        ? p->cfg.lambda / (m * p->cfg.rho)
+                        : p->cfg.lambda / p->cfg.rho;
+  CK(cudaMemcpyAsync(p->dparams.p, &p->params, sizeof(Params), cudaMemcpyHostToDevice, p->stream));
+}
+
+void upload_g(admm_plan* p, const double* g) {
+  CK(cudaMemcpyAsync(p->dg.p, g, p->n_meas * 16, cudaMemcpyHostToDevice, p->stream));
+  if (p->cfg.scl != 1.0) {
+    scale_vec_kernel<<<64, 256, 0, p->stream>>>(p->dg.as<double2>(), p->n_meas, p->cfg.scl);
+    CK(cudaGetLastError());
+  }
+}
+
+void reset_state(admm_plan* p) {
+  cudaStream_t s = p->stream;
+  for (DevBuf* d : {&p->du, &p->ds, &p->dc, &p->dv, &p->dvprev, &p->dghat, &p->dgij, &p->dr, &p->dq})
+    CK(cudaMemsetAsync(d->p, 0, d->bytes, s));
+  IterState st{0, ~0ull, 0u, 0u};
+  CK(cudaMemcpyAsync(p->dstate.p, &st, sizeof(st), cudaMemcpyHostToDevice, s));
+}
+
+void ensure_trace(admm_plan* p, uint64_t iters) {
+  if (iters <= p->trace_cap) return;
+  p->trace_cap = std::max<uint64_t>(iters, 64);
+  p->dtrace.alloc(p->trace_cap * 3 * sizeof(double));
+  if (p->exec) {  // the graph captured the old trace pointer
+    cudaGraphExecDestroy(p->exec);
+    p->exec = nullptr;
+  }
+}
+
+constexpr uint64_t kGraphIters = 8;  // iterations per captured graph
+
+void ensure_graph(admm_plan* p) {
+  if (p->exec) return;
+  cudaGraph_t g = nullptr;
+  CK(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
+  try {
+    for (uint64_t k = 0; k < kGraphIters; ++k) enqueue_iteration_any(p, p->stream, p->trace_obj, nullptr);
+  } catch (...) {
+    cudaStreamEndCapture(p->stream, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  CK(cudaStreamEndCapture(p->stream, &g));
+  cudaError_t e = cudaGraphInstantiate(&p->exec, g, 0);
+  cudaGraphDestroy(g);
+  CK(e);
+  // single-iteration graph for the tail / stepping path
+  p->graph_iters = kGraphIters;
+}
+
+void enqueue_iters(admm_plan* p, uint64_t iters) {
+  ensure_graph(p);
+  uint64_t k = 0;
+  for (; k + kGraphIters <= iters; k += kGraphIters) CK(cudaGraphLaunch(p->exec, p->stream));
+  for (; k < iters; ++k) enqueue_iteration_any(p, p->stream, p->trace_obj, nullptr);
+}
+
+IterState read_state(admm_plan* p) {
+  IterState st{};
+  CK(cudaMemcpyAsync(&st, p->dstate.p, sizeof(st), cudaMemcpyDeviceToHost, p->stream));
+  CK(cudaStreamSynchronize(p->stream));
+  return st;
+}
+
+void read_segments(admm_plan* p, const DevBuf& src, double* dst) {
+  p->h_seg.resize(p->seg_total * 2);
+  CK(cudaMemcpyAsync(p->h_seg.data(), src.p, p->seg_total * 16, cudaMemcpyDeviceToHost, p->stream));
+  CK(cudaStreamSynchronize(p->stream));
+  for (uint64_t j = 0; j < p->N; ++j) {
+    const BlockDesc& b = p->blocks[j];
+    std::memcpy(dst + 2 * b.col0, p->h_seg.data() + 2 * (uint64_t)b.seg_off, (size_t)b.cols * 16);
+  }
+}
+
+admm_status run_guarded(const std::function<void()>& fn) {
+  try {
+    fn();
+    return ADMM_OK;
+  } catch (const Fail& f) {
+    g_last_error = f.msg;
+    g_last_good = f.last_good;
+    return f.st;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return ADMM_E_CUDA;
+  }
+}
+
+void validate_cfg(const admm_solver_config& c) {  // SolverConfig::validate, admm_core.hpp:26-34
+  if (!(c.rho > 0.0)) throw Fail{ADMM_E_PARAMETER, "SolverConfig: rho must be positive"};
+  if (!(c.lambda > 0.0)) throw Fail{ADMM_E_PARAMETER, "SolverConfig: lambda must be positive"};
+  if (!(c.scl > 0.0)) throw Fail{ADMM_E_PARAMETER, "SolverConfig: scl must be positive"};
+  if (c.max_iters < 1) throw Fail{ADMM_E_PARAMETER, "SolverConfig: max_iters must be >= 1"};
+  if (c.eps_pri < 0.0 || c.eps_dual < 0.0)
+    throw Fail{ADMM_E_PARAMETER, "SolverConfig: residual thresholds must be non-negative"};
+}
+
+// Build a plan.  skip_cfg_validation is used by the GramSolver op (no lambda).
+admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg, uint64_t n_meas,
+                       uint64_t n_pix, const void* h, admm_dtype h_dtype, const double* g,
+                       bool skip_cfg_validation) {
+  const auto t0 = std::chrono::steady_clock::now();
+  if (!skip_cfg_validation) validate_cfg(cfg);
+  // SensingProblem::validate (problem.hpp:35-49)
+  if (n_meas == 0 || n_pix == 0 || !h || !g)
+    throw Fail{ADMM_E_DIMENSION, "SensingProblem: empty sensing matrix"};
+  const bool hfin = h_dtype == ADMM_C128
+                        ? host_all_finite(static_cast<const double*>(h), 2 * n_meas * n_pix)
+                        : host_all_finite(static_cast<const float*>(h), 2 * n_meas * n_pix);
+  if (!hfin || !host_all_finite(g, 2 * n_meas)) throw Fail{ADMM_E_NUMERICAL, "SensingProblem: non-finite entries"};
+  if (o.method < ADMM_REFERENCE || o.method > ADMM_HYBRID) throw Fail{ADMM_E_PARAMETER, "unknown method"};
+  if (o.dtype != ADMM_C128 && o.dtype != ADMM_C64) throw Fail{ADMM_E_PARAMETER, "unknown dtype"};
+
+  auto p = std::make_unique<admm_plan>();
+  p->device = o.device;
+  p->dtype = o.dtype;
+  p->method = o.method;
+  p->n_meas = n_meas;
+  p->n_pix = n_pix;
+  p->cfg = cfg;
+  p->ragged = o.ragged != 0;
+  p->trace_obj = o.trace_objective != 0;
+  p->M = (o.method == ADMM_CONSENSUS || o.method == ADMM_HYBRID) ? o.M : 1;
+  p->N = (o.method == ADMM_SECTIONING || o.method == ADMM_HYBRID) ? o.N : 1;
+  p->elem = o.dtype == ADMM_C128 ? 16 : 8;
+  // make_partition (partition.hpp:56-65): rows then columns
+  p->rb = split_bounds(n_meas, p->M, p->ragged, "row");
+  p->cb = split_bounds(n_pix, p->N, p->ragged, "column");
+  if (p->M * p->N > 65535) throw Fail{ADMM_E_PARAMETER, "too many blocks"};
+
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    throw Fail{ADMM_E_CUDA, "no CUDA device: libadmm_b200 has no CPU fallback"};
+  CK(cudaSetDevice(o.device));
+  CK(cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, o.device));
+  CK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+
+  // block table; worker id = i*N + j (solvers.hpp:305)
+  uint64_t mv = 0, vv = 0, sv = 0;
+  std::vector<uint64_t> seg_off(p->N);
+  for (uint64_t j = 0; j < p->N; ++j) {
+    seg_off[j] = sv;
+    sv += round_up(p->cb[j + 1] - p->cb[j], 4);
+    p->max_seg = std::max<uint32_t>(p->max_seg, (uint32_t)(p->cb[j + 1] - p->cb[j]));
+  }
+  for (uint64_t i = 0; i < p->M; ++i) {
+    p->max_rowblock = std::max<uint32_t>(p->max_rowblock, (uint32_t)(p->rb[i + 1] - p->rb[i]));
+    for (uint64_t j = 0; j < p->N; ++j) {
+      BlockDesc b{};
+      b.i = (uint32_t)i;
+      b.j = (uint32_t)j;
+      b.rows = (uint32_t)(p->rb[i + 1] - p->rb[i]);
+      b.cols = (uint32_t)(p->cb[j + 1] - p->cb[j]);
+      b.row0 = (uint32_t)p->rb[i];
+      b.col0 = (uint32_t)p->cb[j];
+      b.mvec_off = (uint32_t)mv;
+      b.vec_off = (uint32_t)vv;
+      b.seg_off = (uint32_t)seg_off[j];
+      mv += round_up(b.rows, 4);
+      vv += round_up(b.cols, 4);
+      p->max_rows = std::max(p->max_rows, b.rows);
+      p->max_m = std::max(p->max_m, b.rows);
+      p->blocks.push_back(b);
+    }
+  }
+  p->mvec_total = mv;
+  p->vec_total = vv;
+  p->seg_total = sv;
+
+  if (p->dtype == ADMM_C128)
+    build_geometry<double2>(p.get());
+  else
+    build_geometry<float2>(p.get());
+  const size_t nb = p->blocks.size();
+  upload_desc(p->dblocks, p->blocks.data(), nb * sizeof(BlockDesc));
+  upload_desc(p->dhN, p->hN.data(), nb * sizeof(MatDesc));
+  upload_desc(p->dhNv, p->hNv.data(), nb * sizeof(MatDesc));
+  upload_desc(p->dkN, p->kN.data(), nb * sizeof(MatDesc));
+  upload_desc(p->dhH, p->hH.data(), nb * sizeof(MatDesc));
+  upload_desc(p->dhHg, p->hHg.data(), nb * sizeof(MatDesc));
+  for (DevBuf* d : {&p->dghat, &p->dgij, &p->dr, &p->dq}) d->alloc(p->mvec_total * 16);
+  for (DevBuf* d : {&p->du, &p->ds, &p->dc}) d->alloc(p->vec_total * 16);
+  for (DevBuf* d : {&p->dv, &p->dvprev}) d->alloc(p->seg_total * 16);
+  p->dg.alloc(p->n_meas * 16);
+  p->dparams.alloc(sizeof(Params));
+  p->dstate.alloc(sizeof(IterState));
+  p->dobj.alloc(sizeof(double));
+  p->rgx = (uint32_t)cdiv(p->max_rows, kCtaThreads);
+  p->zgx = (uint32_t)cdiv(p->max_seg, kCtaThreads);
+  p->ogx = (uint32_t)cdiv(p->max_rowblock, kCtaThreads);
+  p->nz = p->zgx * (uint32_t)p->N;
+  p->no = p->ogx * (uint32_t)p->M;
+  p->dred.alloc((size_t)3 * p->nz * sizeof(double));
+  p->dored.alloc((size_t)std::max<uint32_t>(p->no, p->zgx * (uint32_t)p->N) * sizeof(double));
+  ensure_trace(p.get(), std::max<uint64_t>(cfg.max_iters, 1));
+
+  if (p->dtype == ADMM_C128) {
+    upload_h<double2>(p.get(), h, h_dtype);
+    factor_blocks<double2>(p.get());
+  } else {
+    upload_h<float2>(p.get(), h, h_dtype);
+    factor_blocks<float2>(p.get());
+  }
+  upload_g(p.get(), g);
+  set_params(p.get());
+  reset_state(p.get());
+  CK(cudaStreamSynchronize(p->stream));
+  p->setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return p.release();
+}
+
+void check_plan(const admm_plan* p) {
+  if (!p) throw Fail{ADMM_E_STATE, "null plan"};
+  CK(cudaSetDevice(p->device));
+}
+
+}  // namespace
+
+// ----------------------------------------------------------------------- C ABI
+extern "C" {
+
+int admm_abi_version(void) { return ADMM_B200_ABI_VERSION; }
+const char* admm_last_error(void) { return g_last_error.c_str(); }
+uint64_t admm_last_good_iteration(void) { return g_last_good; }
+
+admm_status admm_plan_create(const admm_plan_options* opts, const admm_solver_config* cfg, uint64_t n_meas,
+                             uint64_t n_pix, const void* h, admm_dtype h_dtype, const double* g,
+                             admm_plan** out) {
+  return run_guarded([&] {
+    if (!opts || !cfg || !out) throw Fail{ADMM_E_STATE, "null argument"};
+    *out = nullptr;
+    *out = create_plan(*opts, *cfg, n_meas, n_pix, h, h_dtype, g, false);
+  });
+}
+
+void admm_plan_destroy(admm_plan* plan) {
+  if (plan) {
+    cudaSetDevice(plan->device);
+    delete plan;
+  }
+}
+
+admm_status admm_plan_set_g(admm_plan* p, const double* g) {
+  return run_guarded([&] {
+    check_plan(p);
+    if (!g) throw Fail{ADMM_E_STATE, "null g"};
+    if (!host_all_finite(g, 2 * p->n_meas)) throw Fail{ADMM_E_NUMERICAL, "SensingProblem: non-finite entries"};
+    upload_g(p, g);
+  });
+}
+
+admm_status admm_plan_set_lambda(admm_plan* p, double lambda) {
+  return run_guarded([&] {
+    check_plan(p);
+    if (!(lambda > 0.0)) throw Fail{ADMM_E_PARAMETER, "SolverConfig: lambda must be positive"};
+    p->cfg.lambda = lambda;
+    set_params(p);
+  });
+}
+
+admm_status admm_plan_max_abs_adjoint(admm_plan* p, double* out) {
+  return run_guarded([&] {
+    check_plan(p);
+    const int nb = (int)p->blocks.size();
+    const uint32_t gx = p->zgx;
+    DevBuf res;
+    res.alloc((size_t)gx * p->N * sizeof(double));
+    if (p->dtype == ADMM_C128) {
+      gemv_h_kernel<double2, kVH, false><<<(unsigned)p->gG.P, kCtaThreads, 0, p->stream>>>(
+          p->dH.as<double2>(), p->dg.as<double2>(), p->dgpart.as<double2>(), p->dhHg.as<MatDesc>(), nb, p->gG.U);
+      adjoint_absmax_kernel<chunk_h<double2>()><<<dim3(gx, (unsigned)p->N), kCtaThreads, 0, p->stream>>>(
+          p->dgpart.as<double2>(), p->dhHg.as<MatDesc>(), p->dblocks.as<BlockDesc>(), (uint32_t)p->M,
+          (uint32_t)p->N, p->gG.U, p->gG.P, res.as<double>());
+    } else {
+      gemv_h_kernel<float2, kVH, false><<<(unsigned)p->gG.P, kCtaThreads, 0, p->stream>>>(
+          p->dH.as<float2>(), p->dg.as<double2>(), p->dgpart.as<double2>(), p->dhHg.as<MatDesc>(), nb, p->gG.U);
+      adjoint_absmax_kernel<chunk_h<float2>()><<<dim3(gx, (unsigned)p->N), kCtaThreads, 0, p->stream>>>(
+          p->dgpart.as<double2>(), p->dhHg.as<MatDesc>(), p->dblocks.as<BlockDesc>(), (uint32_t)p->M,
+          (uint32_t)p->N, p->gG.U, p->gG.P, res.as<double>());
+    }
+    CK(cudaGetLastError());
+    std::vector<double> h((size_t)gx * p->N);
+    CK(cudaMemcpyAsync(h.data(), res.p, h.size() * 8, cudaMemcpyDeviceToHost, p->stream));
+    CK(cudaStreamSynchronize(p->stream));
+    double m = 0.0;
+    for (double x : h) m = std::max(m, x);
+    *out = m;
+  });
+}
+
+admm_status admm_plan_reset(admm_plan* p) {
+  return run_guarded([&] {
+    check_plan(p);
+    reset_state(p);
+  });
+}
+
+admm_status admm_plan_enqueue(admm_plan* p, uint64_t iters) {
+  return run_guarded([&] {
+    check_plan(p);
+    enqueue_iters(p, iters);
+  });
+}
+
+admm_status admm_plan_sync(admm_plan* p) {
+  return run_guarded([&] {
+    check_plan(p);
+    CK(cudaStreamSynchronize(p->stream));
+  });
+}
+
+void* admm_plan_stream(admm_plan* p) { return p ? (void*)p->stream : nullptr; }
+
+uint32_t admm_plan_kernel_count(const admm_plan*) { return 7; }
+
+admm_status admm_plan_profile(admm_plan* p, uint64_t iters, const char** names, double* ms) {
+  static const char* kNames[7] = {"gemv_n(H,c)", "rows_finalize(rhs)", "gemv_n(K,r)", "rows_finalize(q)",
+                                  "gemv_h(H,q)", "zupdate", "finalize"};
+  return run_guarded([&] {
+    check_plan(p);
+    std::vector<cudaEvent_t> ev(8);
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+    std::vector<double> acc(7, 0.0);
+    for (uint64_t k = 0; k < iters; ++k) {
+      enqueue_iteration_any(p, p->stream, false, &ev);
+      CK(cudaEventSynchronize(ev[7]));
+      for (int q = 0; q < 7; ++q) {
+        float t = 0.f;
+        CK(cudaEventElapsedTime(&t, ev[q], ev[q + 1]));
+        acc[q] += t;
+      }
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    for (int q = 0; q < 7; ++q) {
+      if (names) names[q] = kNames[q];
+      if (ms) ms[q] = acc[q] / (double)std::max<uint64_t>(iters, 1);
+    }
+  });
+}
+
+admm_status admm_plan_get_info(const admm_plan* p, admm_plan_info* info) {
+  return run_guarded([&] {
+    if (!p || !info) throw Fail{ADMM_E_STATE, "null argument"};
+    admm_plan_info r{};
+    r.n_blocks = p->blocks.size();
+    uint64_t hb = 0, kb = 0, vb = 0;
+    for (const auto& b : p->blocks) {
+      hb += (uint64_t)b.rows * b.cols * p->elem;
+      kb += (uint64_t)b.rows * b.rows * p->elem;
+      vb += (uint64_t)b.cols * 16 * 6 + (uint64_t)b.rows * 16 * 8;
+    }
+    r.h_bytes = hb;
+    r.k_bytes = kb;
+    r.h_stream_bytes_per_iter = 2 * hb;
+    r.bytes_per_iter = 2 * hb + kb + vb;
+    r.launches_per_iter = p->trace_obj ? 9 : 7;
+    r.grid_gemv_n = p->gN.P;
+    r.grid_gemv_h = p->gH.P;
+    r.setup_seconds = p->setup_s;
+    r.inner_dim_max = p->max_m;
+    *info = r;
+  });
+}
+
+admm_status admm_plan_read(admm_plan* p, int which, double* dst, uint64_t count) {
+  return run_guarded([&] {
+    check_plan(p);
+    if (!dst) throw Fail{ADMM_E_STATE, "null destination"};
+    if (which == 0 || which == 1) {
+      if (count < p->n_pix) throw Fail{ADMM_E_DIMENSION, "destination too small"};
+      read_segments(p, which == 0 ? p->dv : p->dvprev, dst);
+    } else if (which == 2) {
+      uint64_t tot = 0;
+      for (auto& b : p->blocks) tot += b.cols;
+      if (count < tot) throw Fail{ADMM_E_DIMENSION, "destination too small"};
+      std::vector<double> tmp(p->vec_total * 2);
+      CK(cudaMemcpyAsync(tmp.data(), p->du.p, p->vec_total * 16, cudaMemcpyDeviceToHost, p->stream));
+      CK(cudaStreamSynchronize(p->stream));
+      uint64_t o = 0;
+      for (auto& b : p->blocks) {
+        std::memcpy(dst + 2 * o, tmp.data() + 2 * (uint64_t)b.vec_off, (size_t)b.cols * 16);
+        o += b.cols;
+      }
+    } else {
+      throw Fail{ADMM_E_PARAMETER, "unknown iterate"};
+    }
+  });
+}
+
+admm_status admm_plan_solve(admm_plan* p, double* solution, double* trace, uint64_t* iterations_run,
+                            double* objective, admm_observer_fn observer, void* user) {
+  return run_guarded([&] {
+    check_plan(p);
+    const uint64_t iters = p->cfg.max_iters;
+    ensure_trace(p, iters);
+    reset_state(p);
+    const bool stepping = observer || p->cfg.eps_pri != 0.0 || p->cfg.eps_dual != 0.0;
+    uint64_t done = 0;
+    if (!stepping) {
+      enqueue_iters(p, iters);
+      const IterState st = read_state(p);
+      if (st.first_bad != ~0ull)
+        throw Fail{ADMM_E_NUMERICAL,
+                   "non-finite iterate at iteration " + std::to_string(st.first_bad + 1), st.first_bad};
+      done = st.iter;
+    } else {
+      // per-iteration path: stop_now (admm_core.hpp:52-57) and the observer
+      // (solvers.hpp:150-160) need the host after every iteration.
+      uint64_t total_u = 0;
+      for (auto& b : p->blocks) total_u += b.cols;
+      std::vector<const double*> uptr(p->blocks.size());
+      std::vector<uint64_t> ulen(p->blocks.size());
+      for (uint64_t k = 0; k < iters; ++k) {
+        enqueue_iteration_any(p, p->stream, p->trace_obj, nullptr);
+        const IterState st = read_state(p);
+        if (st.first_bad != ~0ull)
+          throw Fail{ADMM_E_NUMERICAL, "non-finite iterate at iteration " + std::to_string(st.first_bad + 1),
+                     st.first_bad};
+        double tr[3];
+        CK(cudaMemcpyAsync(tr, p->dtrace.as<double>() + 3 * k, sizeof(tr), cudaMemcpyDeviceToHost, p->stream));
+        CK(cudaStreamSynchronize(p->stream));
+        done = k + 1;
+        if (observer) {
+          p->h_v.resize(2 * p->n_pix);
+          p->h_vprev.resize(2 * p->n_pix);
+          p->h_u.resize(2 * total_u);
+          read_segments(p, p->dv, p->h_v.data());
+          read_segments(p, p->dvprev, p->h_vprev.data());
+          std::vector<double> tmp(p->vec_total * 2);
+          CK(cudaMemcpyAsync(tmp.data(), p->du.p, p->vec_total * 16, cudaMemcpyDeviceToHost, p->stream));
+          CK(cudaStreamSynchronize(p->stream));
+          uint64_t o = 0;
+          for (size_t b = 0; b < p->blocks.size(); ++b) {
+            std::memcpy(p->h_u.data() + 2 * o, tmp.data() + 2 * (uint64_t)p->blocks[b].vec_off,
+                        (size_t)p->blocks[b].cols * 16);
+            uptr[b] = p->h_u.data() + 2 * o;
+            ulen[b] = p->blocks[b].cols;
+            o += p->blocks[b].cols;
+          }
+          admm_snapshot snap{};
+          snap.iteration = k + 1;
+          snap.n_pix = p->n_pix;
+          snap.v = p->h_v.data();
+          snap.v_prev = p->h_vprev.data();
+          snap.n_workers = p->blocks.size();
+          snap.replica_u = uptr.data();
+          snap.replica_len = ulen.data();
+          snap.primal = tr[0];
+          snap.dual = tr[1];
+          observer(&snap, user);
+        }
+        // stop_now: both thresholds 0 never stops; otherwise every enabled one must hold
+        const double e1 = p->cfg.eps_pri, e2 = p->cfg.eps_dual;
+        if (e1 != 0.0 || e2 != 0.0) {
+          const bool pri = e1 == 0.0 || tr[0] <= e1;
+          const bool dua = e2 == 0.0 || tr[1] <= e2;
+          if (pri && dua) break;
+        }
+      }
+    }
+    if (iterations_run) *iterations_run = done;
+    double obj = 0.0;
+    if (p->trace_obj) {
+      CK(cudaMemcpyAsync(&obj, p->dtrace.as<double>() + 3 * (done - 1) + 2, 8, cudaMemcpyDeviceToHost, p->stream));
+      CK(cudaStreamSynchronize(p->stream));
+    } else {
+      if (p->dtype == ADMM_C128)
+        enqueue_objective<double2>(p, p->stream);
+      else
+        enqueue_objective<float2>(p, p->stream);
+      CK(cudaMemcpyAsync(&obj, p->dobj.p, 8, cudaMemcpyDeviceToHost, p->stream));
+      CK(cudaStreamSynchronize(p->stream));
+    }
+    if (objective) *objective = obj;
+    if (trace) {
+      CK(cudaMemcpyAsync(trace, p->dtrace.p, done * 3 * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+      CK(cudaStreamSynchronize(p->stream));
+      if (!p->trace_obj) trace[3 * (done - 1) + 2] = obj;
+    }
+    if (solution) read_segments(p, p->dv, solution);
+  });
+}
+
+}  // extern "C"
+
+// ---- L0/L1 operations -------------------------------------------------------
+
+namespace {
+
+__global__ void soft_threshold_kernel(const double2* __restrict__ a, uint64_t n, double kappa,
+                                      double2* __restrict__ out) {
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n; t += (uint64_t)gridDim.x * blockDim.x)
+    out[t] = soft_threshold(a[t], kappa);
+}
+
+__global__ void rows_sum_kernel(const double2* __restrict__ part, const MatDesc* __restrict__ mats,
+                                uint64_t U, uint64_t P, double2* __restrict__ y) {
+  const MatDesc md = mats[0];
+  const uint32_t row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row < md.rows) y[row] = sum_rows_part(part, md, row, U, P);
+}
+
+template <int CH>
+__global__ void cols_sum_kernel(const double2* __restrict__ part, const MatDesc* __restrict__ mats,
+                                uint64_t U, uint64_t P, double2* __restrict__ y) {
+  const MatDesc md = mats[0];
+  const uint32_t col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col < md.cols) y[col] = sum_cols_part<CH>(part, md, col, U, P);
+}
+
+admm_plan_options single_block(int device) {
+  admm_plan_options o{};
+  o.method = ADMM_REFERENCE;
+  o.M = o.N = 1;
+  o.dtype = ADMM_C128;
+  o.device = device;
+  return o;
+}
+
+}  // namespace
+
+extern "C" {
+
+admm_status admm_matvec(const double* a, uint64_t rows, uint64_t cols, const double* x, double* y, int device) {
+  return run_guarded([&] {
+    if (!a || !x || !y) throw Fail{ADMM_E_STATE, "null argument"};
+    admm_solver_config cfg{1.0, 1.0, 1.0, 1, 0.0, 0.0, 0};
+    std::vector<double> g(2 * rows, 0.0);
+    std::unique_ptr<admm_plan> p(create_plan(single_block(device), cfg, rows, cols, a, ADMM_C128, g.data(), true));
+    std::vector<double> xs(2 * round_up(cols, 4), 0.0);
+    std::memcpy(xs.data(), x, cols * 16);
+    CK(cudaMemcpyAsync(p->dc.p, xs.data(), cols * 16, cudaMemcpyHostToDevice, p->stream));
+    gemv_n_kernel<double2, kVN, false><<<(unsigned)p->gN.P, kCtaThreads, 0, p->stream>>>(
+        p->dH.as<double2>(), p->dc.as<double2>(), p->dwpart.as<double2>(), p->dhN.as<MatDesc>(), 1, p->gN.U);
+    rows_sum_kernel<<<(unsigned)cdiv(rows, 256), 256, 0, p->stream>>>(p->dwpart.as<double2>(), p->dhN.as<MatDesc>(),
+                                                                     p->gN.U, p->gN.P, p->dr.as<double2>());
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(y, p->dr.p, rows * 16, cudaMemcpyDeviceToHost, p->stream));
+    CK(cudaStreamSynchronize(p->stream));
+  });
+}
+
+admm_status admm_adjoint_matvec(const double* a, uint64_t rows, uint64_t cols, const double* x, double* y,
+                                int device) {
+  return run_guarded([&] {
+    if (!a || !x || !y) throw Fail{ADMM_E_STATE, "null argument"};
+    admm_solver_config cfg{1.0, 1.0, 1.0, 1, 0.0, 0.0, 0};
+    std::vector<double> g(2 * rows, 0.0);
+    std::unique_ptr<admm_plan> p(create_plan(single_block(device), cfg, rows, cols, a, ADMM_C128, g.data(), true));
+    CK(cudaMemcpyAsync(p->dq.p, x, rows * 16, cudaMemcpyHostToDevice, p->stream));
+    gemv_h_kernel<double2, kVH, false><<<(unsigned)p->gH.P, kCtaThreads, 0, p->stream>>>(
+        p->dH.as<double2>(), p->dq.as<double2>(), p->dzpart.as<double2>(), p->dhH.as<MatDesc>(), 1, p->gH.U);
+    cols_sum_kernel<chunk_h<double2>()><<<(unsigned)cdiv(cols, 256), 256, 0, p->stream>>>(
+        p->dzpart.as<double2>(), p->dhH.as<MatDesc>(), p->gH.U, p->gH.P, p->du.as<double2>());
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(y, p->du.p, cols * 16, cudaMemcpyDeviceToHost, p->stream));
+    CK(cudaStreamSynchronize(p->stream));
+  });
+}
+
+admm_status admm_soft_threshold(const double* a, uint64_t n, double kappa, double* out, int device) {
+  return run_guarded([&] {
+    if (!a || !out) throw Fail{ADMM_E_STATE, "null argument"};
+    if (n == 0) return;
+    CK(cudaSetDevice(device));
+    DevBuf da, db;
+    da.alloc(n * 16);
+    db.alloc(n * 16);
+    CK(cudaMemcpy(da.p, a, n * 16, cudaMemcpyHostToDevice));
+    soft_threshold_kernel<<<(unsigned)std::min<uint64_t>(cdiv(n, 256), 4096), 256>>>(da.as<double2>(), n, kappa,
+                                                                                    db.as<double2>());
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(out, db.p, n * 16, cudaMemcpyDeviceToHost));
+  });
+}
+
+admm_status admm_gram_solve(const double* h, uint64_t rows, uint64_t cols, double rho, const double* rhs,
+                            double* x, int device) {
+  return run_guarded([&] {
+    if (!h || !rhs || !x) throw Fail{ADMM_E_STATE, "null argument"};
+    if (rows == 0 || cols == 0) throw Fail{ADMM_E_PARAMETER, "GramSolver: empty block"};
+    if (!(rho > 0.0)) throw Fail{ADMM_E_PARAMETER, "GramSolver: rho must be positive"};
+    if (!host_all_finite(h, 2 * rows * cols)) throw Fail{ADMM_E_NUMERICAL, "GramSolver: non-finite entries in block"};
+    // (H^H H + rho I)^-1 rhs = c - H^H K H c with c = rhs/rho, K = (rho I + H H^H)^-1:
+    // one u-update of the engine with g = 0 (gram.hpp:71-77, inversion lemma).
+    admm_solver_config cfg{rho, 1.0, 1.0, 1, 0.0, 0.0, 0};
+    std::vector<double> g(2 * rows, 0.0);
+    std::unique_ptr<admm_plan> p(create_plan(single_block(device), cfg, rows, cols, h, ADMM_C128, g.data(), true));
+    std::vector<double> c(2 * cols);
+    for (uint64_t t = 0; t < 2 * cols; ++t) c[t] = rhs[t] / rho;
+    CK(cudaMemcpyAsync(p->dc.p, c.data(), cols * 16, cudaMemcpyHostToDevice, p->stream));
+    enqueue_iteration<double2>(p.get(), p->stream, false, nullptr);
+    CK(cudaMemcpyAsync(x, p->du.p, cols * 16, cudaMemcpyDeviceToHost, p->stream));
+    CK(cudaStreamSynchronize(p->stream));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,65 @@
+"""Exception hierarchy of the reference (errors.hpp:10-81), raised from C-ABI status codes."""
+from __future__ import annotations
+
+
+class Error(RuntimeError):
+    """errors.hpp:10 — base class of all library errors."""
+
+
+class DimensionError(Error):
+    """errors.hpp:19 — operand shapes do not conform."""
+
+
+class IndexError(Error):  # noqa: A001  (the reference's name)
+    """errors.hpp:25 — block or node index outside the partition."""
+
+
+class NumericalError(Error):
+    """errors.hpp:31 — non-finite values; carries the last good iteration."""
+
+    def __init__(self, what: str, last_good_iteration: int = 0):
+        super().__init__(what)
+        self._last_good = int(last_good_iteration)
+
+    def last_good_iteration(self) -> int:
+        return self._last_good
+
+
+class SingularityError(Error):
+    """errors.hpp:48 — factorization breakdown."""
+
+
+class PartitionError(Error):
+    """errors.hpp:54 — invalid or non-divisible partition."""
+
+
+class ParameterError(Error):
+    """errors.hpp:60 — invalid scalar parameter."""
+
+
+class MetricsError(Error):
+    """errors.hpp:78 — recovery metrics undefined."""
+
+
+class DeviceError(Error):
+    """CUDA / driver failure (no reference counterpart; ADMM_E_CUDA)."""
+
+
+class StateError(Error):
+    """API misuse (ADMM_E_STATE)."""
+
+
+STATUS = {1: DimensionError, 2: IndexError, 3: NumericalError, 4: SingularityError,
+          5: PartitionError, 6: ParameterError, 7: DeviceError, 8: StateError}
+
+
+def check(status: int) -> None:
+    """Map an admm_status to the reference exception class (no-op for ADMM_OK)."""
+    if status == 0:
+        return
+    from . import _lib
+    msg = _lib.lib.admm_last_error().decode(errors="replace")
+    cls = STATUS.get(status, Error)
+    if cls is NumericalError:
+        raise NumericalError(msg, _lib.lib.admm_last_good_iteration())
+    raise cls(msg)

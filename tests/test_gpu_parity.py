@@ -1,0 +1,260 @@
+"""GPU parity: the B200 engine (libadmm_b200.so, via the reference-shaped API) against
+fixtures made by the unmodified reference and against the bit-pinned C oracle.
+
+Tolerances (BASELINE.json north_star): complex128 relative L2 error of the solution
+<= 1e-9 after the fixed iteration count; complex64 <= 1e-4 with identical support above
+1e-3 max|u|.  Relative errors are scale-safe (both vectors divided by max|ref|) because
+the divergent configs overflow ||v||^2.
+"""
+import numpy as np
+import pytest
+
+import golden_cases as gc
+import oracle_lib as orc
+
+pytestmark = pytest.mark.gpu
+
+C128_TOL = 1e-9
+C64_TOL = 1e-4
+
+
+def admm():
+    import paper_1811_05571_b200 as a
+    return a
+
+
+def rel(a, b):
+    s = float(np.max(np.abs(b))) if b.size else 0.0
+    if s == 0.0 or not np.isfinite(s):
+        return float(np.max(np.abs(a - b))) if np.isfinite(s) else 0.0
+    return float(np.linalg.norm(a / s - b / s) / max(np.linalg.norm(b / s), 1e-300))
+
+
+def support(v):
+    return np.abs(v) > 1e-3 * np.max(np.abs(v))
+
+
+def run(method, problem, args, opts=None, **kw):
+    a = admm()
+    cfg = a.SolverConfig(rho=args["rho"], lambda_=args["lam"], scl=args["scl"],
+                         max_iters=args["iters"], eps_pri=args["eps_pri"], eps_dual=args["eps_dual"])
+    opts = opts or a.SolveOptions(ragged=args["ragged"], **kw)
+    if method == "reference":
+        return a.lasso_admm_reference(problem, cfg, opts)
+    if method == "consensus":
+        return a.consensus_solve(problem, cfg, args["M"], opts)
+    if method == "sectioning":
+        return a.sectioning_solve(problem, cfg, args["N"], opts)
+    return a.hybrid_solve(problem, cfg, args["M"], args["N"], opts)
+
+
+def problem_for(entry):
+    a = admm()
+    h, g, t = gc.problem(entry, orc.gen_problem)
+    return a.SensingProblem(h, g, t)
+
+
+# ------------------------------------------------------------------ L0 / L1 KATs
+def test_matvec_known_answers():
+    a = admm()
+    x = np.array([1, 2j, -1])
+    assert np.array_equal(a.matvec(np.eye(3), x), x)                   # test_linalg.cpp:21-28
+    assert np.array_equal(a.matvec(np.zeros((2, 3)), x), np.zeros(2))
+    y = a.matvec(np.array([[1, 1j], [0, 2]]), np.array([1, 1]))         # test_linalg.cpp:30-38
+    assert np.array_equal(y, np.array([1 + 1j, 2]))
+    assert a.adjoint_matvec(np.array([[1j]]), np.array([1]))[0] == -1j  # test_linalg.cpp:46-53
+    with pytest.raises(a.DimensionError):
+        a.matvec(np.zeros((2, 3)), np.zeros(2))
+    with pytest.raises(a.DimensionError):
+        a.adjoint_matvec(np.zeros((2, 3)), np.zeros(3))
+
+
+@pytest.mark.parametrize("shape", [(7, 5), (64, 2048), (37, 1001), (300, 4099), (1024, 4096)])
+def test_gemv_pair_vs_oracle(shape):
+    a = admm()
+    h = orc.random_gauss(shape[0] * shape[1], 3).reshape(shape)
+    x = orc.random_gauss(shape[1], 4)
+    y = orc.random_gauss(shape[0], 5)
+    assert rel(a.matvec(h, x), orc.matvec(h, x)) <= 1e-13
+    assert rel(a.adjoint_matvec(h, y), orc.adjoint_matvec(h, y)) <= 1e-13
+    # adjoint identity <Hx, y> = <x, H^H y> (test_linalg.cpp:63-72)
+    lhs = np.vdot(a.matvec(h, x), y)
+    rhs = np.vdot(x, a.adjoint_matvec(h, y))
+    assert abs(lhs - rhs) <= 1e-10 * max(1.0, abs(lhs))
+
+
+def test_soft_threshold_known_answers():
+    a = admm()
+    out = a.soft_threshold_vec(np.array([5, -1, 2, -5, 3 + 4j]), 2.0)   # test_prox.cpp:8-20
+    assert out[0] == 3 and out[1] == 0 and out[2] == 0 and out[3] == -3
+    assert abs(out[4] - (1.8 + 2.4j)) < 1e-15
+    z = orc.random_gauss(500, 9)
+    np.testing.assert_array_equal(a.soft_threshold_vec(z, 0.7), orc.soft_threshold_vec(z, 0.7))
+    np.testing.assert_array_equal(a.soft_threshold_vec(z, 0.0), z)
+
+
+def test_gram_solver_known_answers_and_oracle():
+    a = admm()
+    x = a.GramSolver(np.zeros((2, 2)), 2.0).solve(np.array([4, 6]))     # test_linalg.cpp:88-98
+    assert np.allclose(x, [2, 3], atol=1e-12)
+    x = a.GramSolver(np.eye(2), 1.0).solve(np.array([4, 4]))
+    assert np.allclose(x, [2, 2], atol=1e-12)
+    for seed in range(1, 9):  # Woodbury vs dense oracle / residual (test_linalg.cpp:112-151)
+        wide = seed % 2 == 0
+        shape = (5, 14) if wide else (14, 5)
+        h = orc.random_gauss(70, seed).reshape(shape)
+        rhs = orc.random_gauss(shape[1], 300 + seed)
+        got = a.GramSolver(h, 1.5).solve(rhs)
+        want = orc.gram_solve(h, 1.5, rhs)
+        assert rel(got, want) <= 1e-12
+        resid = h.conj().T @ (h @ got) + 1.5 * got - rhs
+        assert np.linalg.norm(resid) / np.linalg.norm(rhs) <= 1e-8
+    assert a.GramSolver.strategy_for(540, 22500) == a.GramSolver.Strategy.Woodbury
+    assert a.GramSolver.strategy_for(2160, 2160) == a.GramSolver.Strategy.Direct
+    with pytest.raises(a.ParameterError):
+        a.GramSolver(np.ones((2, 3)), 0.0)
+    bad = np.zeros((2, 2), complex)
+    bad[0, 0] = np.nan
+    with pytest.raises(a.NumericalError):
+        a.GramSolver(bad, 1.0)
+
+
+# -------------------------------------------------------- solver parity vs reference
+CASES = [c for c in gc.solve_cases()]
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_solver_parity_vs_reference_fixture(name):
+    entry, ref = gc.load(name)
+    args = gc.solver_args(entry)
+    a = admm()
+    p = problem_for(entry)
+    snaps = []
+    obs = (lambda s: snaps.append(s.v.copy())) if "snapshots" in ref else None
+    opts = a.SolveOptions(ragged=args["ragged"], observer=obs)
+    if entry["error"] != "none":
+        exc = getattr(a, entry["error"])
+        with pytest.raises(exc) as ei:
+            run(args["method"], p, args, opts)
+        if entry["error"] == "NumericalError":
+            assert ei.value.last_good_iteration() == entry["last_good"]
+        return
+    r = run(args["method"], p, args, opts)
+    assert r.iterations_run == entry["iterations_run"]
+    err = rel(r.solution, ref["solution"])
+    assert err <= C128_TOL, err
+    tr = np.stack([r.trace.primal, r.trace.dual, r.trace.objective], 1)
+    for col in range(3):
+        assert rel(tr[:, col], ref["trace"][:, col]) <= 1e-8, col
+    if snaps:  # per-iterate agreement (test_solvers.cpp:42-93 bound, 1e-12 absolute)
+        s = np.array(snaps)
+        assert np.max(np.abs(s - ref["snapshots"])) <= 1e-12 * max(1.0, np.max(np.abs(ref["snapshots"])))
+    np.testing.assert_array_equal(r.ledger.as_array(), ref["ledger"]) if ref["ledger"].size else None
+
+
+def test_degeneracy_lattice_on_device():
+    """consensus(M=1) = sectioning(N=1) = hybrid(1,1) = reference; hybrid(M,1) =
+    consensus(M); hybrid(1,N) = sectioning(N) (test_solvers.cpp:42-93), on the GPU."""
+    a = admm()
+    entry, _ = gc.load("lattice_reference")
+    p = problem_for(entry)
+    args = gc.solver_args(entry)
+    cfg = a.SolverConfig(rho=1.0, lambda_=args["lam"], max_iters=10)
+
+    def series(fn):
+        out = []
+        fn(a.SolveOptions(observer=lambda s: out.append(s.v.copy())))
+        return np.array(out)
+
+    ref = series(lambda o: a.lasso_admm_reference(p, cfg, o))
+    for fn in [lambda o: a.consensus_solve(p, cfg, 1, o), lambda o: a.sectioning_solve(p, cfg, 1, o),
+               lambda o: a.hybrid_solve(p, cfg, 1, 1, o)]:
+        assert np.max(np.abs(series(fn) - ref)) <= 1e-12
+    assert np.max(np.abs(series(lambda o: a.consensus_solve(p, cfg, 2, o)) -
+                         series(lambda o: a.hybrid_solve(p, cfg, 2, 1, o)))) <= 1e-12
+    assert np.max(np.abs(series(lambda o: a.sectioning_solve(p, cfg, 2, o)) -
+                         series(lambda o: a.hybrid_solve(p, cfg, 1, 2, o)))) <= 1e-12
+
+
+def test_residuals_recomputed_from_snapshots():
+    """test_solvers.cpp:134-180 on the device."""
+    a = admm()
+    entry, _ = gc.load("resid_hybrid34")
+    p = problem_for(entry)
+    args = gc.solver_args(entry)
+    cfg = a.SolverConfig(rho=1.0, lambda_=args["lam"], max_iters=8)
+    for method, m, n in [("consensus", 3, 1), ("sectioning", 1, 4), ("hybrid", 3, 4)]:
+        snaps = []
+        opts = a.SolveOptions(observer=lambda s: snaps.append(s))
+        r = run(method, p, dict(args, M=m, N=n, iters=8), opts)
+        for k, s in enumerate(snaps):
+            segs = len(s.segment_v)
+            rp2 = sum(np.sum(np.abs(u - s.segment_v[i % segs]) ** 2) for i, u in enumerate(s.replica_u))
+            d2 = sum(np.sum(np.abs(s.segment_v[j] - s.segment_v_prev[j]) ** 2) for j in range(segs))
+            reps = len(s.replica_u) // segs
+            assert abs(np.sqrt(rp2) - r.trace.primal[k]) <= 1e-12 * max(1.0, r.trace.primal[k])
+            assert abs(np.sqrt(reps * d2) - r.trace.dual[k]) <= 1e-12 * max(1.0, r.trace.dual[k])
+
+
+def test_repeat_runs_are_bit_identical():
+    a = admm()
+    entry, _ = gc.load("ledger_hybrid34")
+    p = problem_for(entry)
+    cfg = a.SolverConfig(rho=1.0, lambda_=gc.solver_args(entry)["lam"], max_iters=6)
+    r1 = a.hybrid_solve(p, cfg, 3, 4)
+    r2 = a.hybrid_solve(p, cfg, 3, 4)
+    np.testing.assert_array_equal(r1.solution, r2.solution)
+    np.testing.assert_array_equal(r1.trace.primal, r2.trace.primal)
+
+
+def test_config1_full_size_parity():
+    """BASELINE config 1 exactly: consensus M=4, 256x2048 c128, 200 iterations."""
+    entry, ref = gc.load("cfg1_consensus4")
+    a = admm()
+    p = a.gen_problem(256, 2048, 16, 30.0, 1)
+    args = gc.solver_args(entry)
+    r = run("consensus", p, args)
+    assert rel(r.solution, ref["solution"]) <= C128_TOL
+    assert abs(r.objective - entry["objective"]) <= 1e-9 * abs(entry["objective"])
+    assert r.metrics.support_precision == 1.0 and r.metrics.support_recall == 1.0
+
+
+def test_config1_c64_storage():
+    """complex64 storage of H and K: <= 1e-4 and identical support (north star)."""
+    entry, ref = gc.load("cfg1_consensus4")
+    a = admm()
+    p = a.gen_problem(256, 2048, 16, 30.0, 1, dtype="c64")
+    args = gc.solver_args(entry)
+    r = run("consensus", p, args, dtype="c64")
+    assert rel(r.solution, ref["solution"]) <= C64_TOL
+    assert np.array_equal(support(r.solution), support(ref["solution"]))
+
+
+def test_config2_first_iterations_parity():
+    """BASELINE config 2 (1024x32768, sectioning N=8), first 20 iterations vs reference."""
+    if "cfg2_sectioning8_it20" not in gc.index():
+        pytest.skip("fixture not generated")
+    entry, ref = gc.load("cfg2_sectioning8_it20")
+    a = admm()
+    p = a.gen_problem(1024, 32768, 64, 30.0, 2)
+    r = run("sectioning", p, gc.solver_args(entry), trace_objective=False)
+    assert rel(r.solution, ref["solution"]) <= C128_TOL
+    assert rel(r.trace.primal, ref["trace"][:, 0]) <= 1e-8
+
+
+def test_numerical_blowup_and_errors():
+    a = admm()
+    p = a.gen_problem(6, 9, 2, float("inf"), 1008, a.ProblemKind.RandomPhase)
+    huge = a.SensingProblem(p.h * 1e300, p.g * 1e300)
+    with pytest.raises(a.NumericalError):
+        a.consensus_solve(huge, a.SolverConfig(lambda_=1e-3, max_iters=5), 2)
+    with pytest.raises(a.PartitionError):
+        a.consensus_solve(p, a.SolverConfig(lambda_=1e-3), 4)
+    with pytest.raises(a.ParameterError):
+        a.consensus_solve(p, a.SolverConfig(rho=0.0), 2)
+    bad = a.SensingProblem(p.h, p.g.copy())
+    bad.g[0] = np.nan
+    with pytest.raises(a.NumericalError):  # NumericalError wins over PartitionError (order)
+        a.consensus_solve(bad, a.SolverConfig(lambda_=1e-3), 4)
+    with pytest.raises(a.DimensionError):
+        a.consensus_solve(a.SensingProblem(p.h, p.g[:5]), a.SolverConfig(), 1)
