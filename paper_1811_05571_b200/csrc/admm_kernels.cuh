@@ -67,7 +67,8 @@ struct IterState {
   uint32_t pad_;
 };
 
-constexpr int kRowsPerGroup = kCtaWarps;  // gemv_n: one row per warp
+constexpr int kRowsPerWarpN = 4;          // gemv_n: rows per warp per unit
+constexpr int kRowsPerGroup = kCtaWarps * kRowsPerWarpN;  // gemv_n: rows per unit
 constexpr int kRowsPerWarpH = 4;          // gemv_h: rows per warp per tile
 constexpr int kRowTileH = kCtaWarps * kRowsPerWarpH;
 
@@ -91,13 +92,15 @@ __device__ __forceinline__ void load_x(const double2* __restrict__ x, double2 (&
 }
 
 // y_b = A_b x_b for a set of matrices; linalg.hpp:97-111 (matvec).
-// Unit = (matrix, group of 8 rows, chunk of CN columns); each warp owns one row.
+// Unit = (matrix, group of 32 rows, chunk of CN columns).  Lanes own columns, each
+// warp owns 4 rows of the group, so one load of x (L1) serves 4 streamed rows of A.
 template <typename S, int VN, bool EF>
-__global__ void __launch_bounds__(kCtaThreads, 3)
+__global__ void __launch_bounds__(kCtaThreads, 2)
 gemv_n_kernel(const S* __restrict__ A, const double2* __restrict__ X, double2* __restrict__ part,
               const MatDesc* __restrict__ mats, int nmats, uint64_t U) {
   constexpr int PV = Store<S>::kPerVec;
   constexpr int CN = kWarp * VN * PV;
+  constexpr int RW = kRowsPerWarpN;
   const uint64_t P = gridDim.x, p = blockIdx.x;
   uint64_t x = sk_lo(p, U, P);
   const uint64_t xe = sk_lo(p + 1, U, P);
@@ -108,45 +111,56 @@ gemv_n_kernel(const S* __restrict__ A, const double2* __restrict__ X, double2* _
   MatDesc md = mats[b];
   uint64_t local = x - md.unit0;
   uint32_t rg = (uint32_t)(local / md.n_chunks), cc = (uint32_t)(local % md.n_chunks);
-  double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
+  double2 acc[RW];
+#pragma unroll
+  for (int r = 0; r < RW; ++r) acc[r] = make_double2(0.0, 0.0);
   for (;;) {
-    const uint32_t row = rg * kRowsPerGroup + warp;
-    if (row < md.rows) {
-      const S* arow = A + md.a_off + (uint64_t)row * md.ld;
-      const double2* xv = X + md.x_off;
-      const uint32_t c0 = cc * CN + lane * PV;
-      V256 hv[VN];
+    const uint32_t row0 = rg * kRowsPerGroup + warp * RW;
+    const uint32_t c0 = cc * CN + lane * PV;
+    V256 hv[RW][VN];
+#pragma unroll
+    for (int r = 0; r < RW; ++r) {
+      const S* arow = A + md.a_off + (uint64_t)(row0 + r) * md.ld;
 #pragma unroll
       for (int v = 0; v < VN; ++v) {
         const uint32_t col = c0 + v * kWarp * PV;
-        if (col < md.cols) hv[v] = ld_stream256<EF>(arow + col);
-      }
-#pragma unroll
-      for (int v = 0; v < VN; ++v) {
-        const uint32_t col = c0 + v * kWarp * PV;
-        if (col < md.cols) {
-          double2 xs[PV];
-          load_x<PV>(xv + col, xs);
-#pragma unroll
-          for (int e = 0; e < PV; ++e) cmac((e & 1) ? acc1 : acc0, Store<S>::get(hv[v], e), xs[e]);
+        if (row0 + r < md.rows && col < md.cols) {
+          hv[r][v] = ld_stream256<EF>(arow + col);
+        } else {
+          hv[r][v].w[0] = hv[r][v].w[1] = hv[r][v].w[2] = hv[r][v].w[3] = 0;
         }
+      }
+    }
+    const double2* xv = X + md.x_off;
+#pragma unroll
+    for (int v = 0; v < VN; ++v) {
+      const uint32_t col = c0 + v * kWarp * PV;
+      if (col < md.cols) {
+        double2 xs[PV];
+        load_x<PV>(xv + col, xs);
+#pragma unroll
+        for (int r = 0; r < RW; ++r)
+#pragma unroll
+          for (int e = 0; e < PV; ++e) cmac(acc[r], Store<S>::get(hv[r][v], e), xs[e]);
       }
     }
     ++x;
     ++cc;
     if (cc == md.n_chunks || x == xe) {  // flush this row group's partial
-      double2 acc = cadd(acc0, acc1);
+      const uint64_t first = md.unit0 + (uint64_t)rg * md.n_chunks;
+      const uint64_t seg = p - sk_owner(first, U, P);
+      double2* dst = part + md.part_off + ((uint64_t)rg * md.n_chunks + seg) * kRowsPerGroup + warp * RW;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
-        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+      for (int r = 0; r < RW; ++r) {
+        double2 a = acc[r];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          a.x += __shfl_xor_sync(0xffffffffu, a.x, o);
+          a.y += __shfl_xor_sync(0xffffffffu, a.y, o);
+        }
+        if (lane == 0 && row0 + r < md.rows) dst[r] = a;
+        acc[r] = make_double2(0.0, 0.0);
       }
-      if (lane == 0 && row < md.rows) {
-        const uint64_t first = md.unit0 + (uint64_t)rg * md.n_chunks;
-        const uint64_t seg = p - sk_owner(first, U, P);
-        part[md.part_off + ((uint64_t)rg * md.n_chunks + seg) * kRowsPerGroup + warp] = acc;
-      }
-      acc0 = acc1 = make_double2(0.0, 0.0);
       if (x == xe) break;
       if (cc == md.n_chunks) {
         cc = 0;
