@@ -230,7 +230,10 @@ def bench_ours(args, cfg):
     # ---- per-kernel device time (roofline of the dominant kernel)
     kern = plan.profile(iters=10)
     hb, kb = info["h_bytes"], info["k_bytes"]
-    algo = {"gemv_n(H,c)": hb, "gemv_h(H,q)": hb, "gemv_n(K,r)": kb}
+    # algorithmic HBM bytes per launch: each H pass / the sweep streams H once from HBM
+    # (the sweep's second, L2-resident read of each strip is not HBM traffic), K once.
+    algo = {"gemv_n(H,c)": hb, "gemv_h(H,q)": hb, "gemv_n(K,r)": kb, "sweep(H)": hb}
+    algo = {k: v for k, v in algo.items() if k in kern}
     dom = max(algo, key=lambda x: kern[x])
     peak, peak_kind = peaks()
     achieved = algo[dom] / (kern[dom] / 1000.0) / 1e9
@@ -286,6 +289,8 @@ def bench_ours(args, cfg):
                    "parallelism": "replicas" if ws > 1 else "single GPU, all blocks",
                    "lambda": lam},
         "h_stream_gbs": h_stream_gbs, "h_stream_frac_of_peak": h_stream_gbs / peak,
+        "hbm_compulsory_gbs": info["hbm_bytes_per_iter"] / (ms_per_step / 1000.0) / 1e9,
+        "schedule": {1: "two-pass", 2: "single-HBM-pass sweep"}[int(info["schedule"])],
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "algorithmic_bytes_per_launch": algo[dom],

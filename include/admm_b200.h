@@ -81,6 +81,8 @@ typedef struct {
   int device;          /* CUDA device ordinal */
   int trace_objective; /* 1: objective every iteration (extra H pass, as the reference
                           does at solvers.hpp:146); 0: objective of the final iterate only */
+  int schedule;        /* 0 auto, 1 two-pass (H streamed twice per iteration), 2 single-HBM-pass
+                          column-strip sweep; env ADMM_B200_SCHEDULE overrides */
 } admm_plan_options;
 
 typedef struct admm_plan admm_plan;
@@ -147,6 +149,9 @@ typedef struct {
   uint64_t grid_gemv_n, grid_gemv_h;
   double setup_seconds;         /* upload + Gram + inverse (host wall clock) */
   uint64_t inner_dim_max;       /* largest factored dimension */
+  uint64_t schedule;            /* 1 two-pass, 2 sweep */
+  uint64_t grid_sweep;
+  uint64_t hbm_bytes_per_iter;  /* compulsory HBM bytes of the chosen schedule */
 } admm_plan_info;
 admm_status admm_plan_get_info(const admm_plan* plan, admm_plan_info* info);
 

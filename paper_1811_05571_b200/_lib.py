@@ -27,7 +27,7 @@ class SolverConfigC(ctypes.Structure):
 
 class PlanOptionsC(ctypes.Structure):
     _fields_ = [("method", _i32), ("M", _u64), ("N", _u64), ("ragged", _i32), ("dtype", _i32),
-                ("device", _i32), ("trace_objective", _i32)]
+                ("device", _i32), ("trace_objective", _i32), ("schedule", _i32)]
 
 
 class SnapshotC(ctypes.Structure):
@@ -41,7 +41,8 @@ class PlanInfoC(ctypes.Structure):
     _fields_ = [("n_blocks", _u64), ("h_bytes", _u64), ("k_bytes", _u64),
                 ("h_stream_bytes_per_iter", _u64), ("bytes_per_iter", _u64),
                 ("launches_per_iter", _u64), ("grid_gemv_n", _u64), ("grid_gemv_h", _u64),
-                ("setup_seconds", _dbl), ("inner_dim_max", _u64)]
+                ("setup_seconds", _dbl), ("inner_dim_max", _u64), ("schedule", _u64),
+                ("grid_sweep", _u64), ("hbm_bytes_per_iter", _u64)]
 
 
 OBSERVER = ctypes.CFUNCTYPE(None, ctypes.POINTER(SnapshotC), ctypes.c_void_p)

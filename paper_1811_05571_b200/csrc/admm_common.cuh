@@ -46,16 +46,22 @@ __device__ __forceinline__ double2 soft_threshold(double2 a, double kappa) {
 }
 
 // ---- streaming loads of the matrix operand (read once per pass) -------------
-// 256-bit LDG with L1 no-allocate.  EvictFirst=true adds the L2 evict-first hint
-// (used when the operand is much larger than L2 and would only pollute it).
+// 256-bit LDG with L1 no-allocate and an L2 eviction priority:
+//   kEvictNormal (default), kEvictFirst (stream through: the line is dead after this
+//   read), kEvictLast (the line will be re-read soon — the fused sweep's second pass).
 struct V256 {
   uint64_t w[4];
 };
-template <bool EvictFirst>
+enum L2Hint { kEvictNormal = 0, kEvictFirst = 1, kEvictLast = 2 };
+template <int Hint>
 __device__ __forceinline__ V256 ld_stream256(const void* p) {
   V256 r;
-  if constexpr (EvictFirst) {
+  if constexpr (Hint == kEvictFirst) {
     asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v4.b64 {%0,%1,%2,%3}, [%4];"
+                 : "=l"(r.w[0]), "=l"(r.w[1]), "=l"(r.w[2]), "=l"(r.w[3])
+                 : "l"(p));
+  } else if constexpr (Hint == kEvictLast) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_last.v4.b64 {%0,%1,%2,%3}, [%4];"
                  : "=l"(r.w[0]), "=l"(r.w[1]), "=l"(r.w[2]), "=l"(r.w[3])
                  : "l"(p));
   } else {

@@ -94,7 +94,7 @@ __device__ __forceinline__ void load_x(const double2* __restrict__ x, double2 (&
 // y_b = A_b x_b for a set of matrices; linalg.hpp:97-111 (matvec).
 // Unit = (matrix, group of 32 rows, chunk of CN columns).  Lanes own columns, each
 // warp owns 4 rows of the group, so one load of x (L1) serves 4 streamed rows of A.
-template <typename S, int VN, bool EF>
+template <typename S, int VN, int EF>
 __global__ void __launch_bounds__(kCtaThreads, 2)
 gemv_n_kernel(const S* __restrict__ A, const double2* __restrict__ X, double2* __restrict__ part,
               const MatDesc* __restrict__ mats, int nmats, uint64_t U) {
@@ -176,7 +176,7 @@ gemv_n_kernel(const S* __restrict__ A, const double2* __restrict__ X, double2* _
 // z_b = A_b^H q_b for a set of matrices; linalg.hpp:114-127 (adjoint_matvec).
 // Unit = (matrix, chunk of CH columns, tile of 32 rows); lanes own columns,
 // warps split the rows; partials are combined across warps through SMEM.
-template <typename S, int VH, bool EF>
+template <typename S, int VH, int EF>
 __global__ void __launch_bounds__(kCtaThreads, 3)
 gemv_h_kernel(const S* __restrict__ A, const double2* __restrict__ Q, double2* __restrict__ part,
               const MatDesc* __restrict__ mats, int nmats, uint64_t U) {

@@ -10,6 +10,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <limits>
@@ -22,6 +23,7 @@
 #include "admm_b200.h"
 #include "admm_kernels.cuh"
 #include "admm_setup.cuh"
+#include "admm_sweep.cuh"
 
 using namespace admm;
 
@@ -136,6 +138,13 @@ struct admm_plan {
   DevBuf dwpart, dqpart, dzpart, dopart, dgpart;
   DevBuf dred, dored, dtrace, dstate, dparams, dblocks, dhN, dhNv, dkN, dhH, dhHg, dgram, dobj;
   Geom gN, gK, gH, gO, gG;
+  // sweep schedule (admm_sweep.cuh)
+  int schedule = 1;             // 1 two-pass, 2 single-HBM-pass sweep
+  int sweep_lpr = 8;
+  std::vector<SweepDesc> segs;
+  DevBuf dsegs, dwpart_s;
+  Geom gS;
+  size_t sweep_smem = 0;
   uint32_t zgx = 0, rgx = 0, ogx = 0, nz = 0, no = 0;
   uint64_t trace_cap = 0;
   cudaGraphExec_t exec = nullptr;
@@ -243,9 +252,9 @@ void build_geometry(admm_plan* p) {
   p->gH.U = uH;
   p->gO.U = uN;
   p->gG.U = uH;
-  p->gN.P = grid_for<S>(gemv_n_kernel<S, kVN, false>, uN, p->num_sms);
-  p->gK.P = grid_for<S>(gemv_n_kernel<S, kVN, false>, uK, p->num_sms);
-  p->gH.P = grid_for<S>(gemv_h_kernel<S, kVH, false>, uH, p->num_sms);
+  p->gN.P = grid_for<S>(gemv_n_kernel<S, kVN, kEvictNormal>, uN, p->num_sms);
+  p->gK.P = grid_for<S>(gemv_n_kernel<S, kVN, kEvictNormal>, uK, p->num_sms);
+  p->gH.P = grid_for<S>(gemv_h_kernel<S, kVH, kEvictNormal>, uH, p->num_sms);
   p->gO.P = p->gN.P;
   p->gG.P = p->gH.P;
   p->dwpart.alloc(pN * sizeof(double2));
@@ -253,6 +262,63 @@ void build_geometry(admm_plan* p) {
   p->dqpart.alloc(pK * sizeof(double2));
   p->dzpart.alloc(pH * sizeof(double2));
   p->dgpart.alloc(pH * sizeof(double2));
+}
+
+void upload_desc(DevBuf& d, const void* src, size_t bytes);
+
+template <typename S, int LPR>
+size_t sweep_smem_bytes(const admm_plan* p) {
+  constexpr int W = LPR * Store<S>::kPerVec;
+  return ((size_t)p->n_meas + (size_t)kCtaWarps * W + 2 * (size_t)p->M * W) * sizeof(double2);
+}
+
+// Try to configure the single-HBM-pass sweep with LPR lanes per row.  Returns false
+// when the segment rows do not fit the SMEM accumulator or the resident strips would
+// not fit in L2 (then the two-pass schedule is used).
+template <typename S, int LPR>
+bool try_sweep(admm_plan* p, size_t l2_budget) {
+  constexpr int W = LPR * Store<S>::kPerVec;
+  const size_t smem = sweep_smem_bytes<S, LPR>(p);
+  if (smem > 200 * 1024) return false;
+  CK(cudaFuncSetAttribute(sweep_kernel<S, LPR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_kernel<S, LPR>, kCtaThreads, smem));
+  if (occ < 1) return false;
+  std::vector<SweepDesc> segs(p->N);
+  uint64_t u = 0, po = 0;
+  for (uint64_t j = 0; j < p->N; ++j) {
+    const uint32_t cols = (uint32_t)(p->cb[j + 1] - p->cb[j]);
+    segs[j] = SweepDesc{u, po, (uint32_t)cdiv(cols, W), cols};
+    u += segs[j].n_strips;
+    po += (uint64_t)segs[j].n_strips * p->n_meas;
+  }
+  uint64_t P = std::min<uint64_t>(u, (uint64_t)p->num_sms * occ);
+  const uint64_t strip = (uint64_t)p->n_meas * W * sizeof(S);
+  if (P * strip > l2_budget) {
+    const uint64_t cap = l2_budget / strip;
+    if (cap < (uint64_t)p->num_sms) return false;
+    P = std::min<uint64_t>(P, cap);
+  }
+  p->segs = segs;
+  p->gS.U = u;
+  p->gS.P = P;
+  p->sweep_lpr = LPR;
+  p->sweep_smem = smem;
+  p->dwpart_s.alloc(po * sizeof(double2));
+  upload_desc(p->dsegs, segs.data(), segs.size() * sizeof(SweepDesc));
+  return true;
+}
+
+template <typename S>
+void choose_schedule(admm_plan* p, int requested) {
+  p->schedule = 1;
+  if (requested == 1) return;
+  const size_t budget = 64ull << 20;  // resident strips must stay well inside the 126 MB L2
+  if (try_sweep<S, 8>(p, budget) || try_sweep<S, 4>(p, budget)) {
+    p->schedule = 2;
+    return;
+  }
+  if (requested == 2) throw Fail{ADMM_E_PARAMETER, "sweep schedule not possible for this shape"};
 }
 
 void upload_desc(DevBuf& d, const void* src, size_t bytes) {
@@ -363,6 +429,23 @@ void factor_blocks(admm_plan* p) {
   if (hf & 1u) throw Fail{ADMM_E_NUMERICAL, "GramSolver: non-finite inverse"};
 }
 
+// Sweep schedule with a per-iteration objective: trace[k-1].objective after the
+// finalize of iteration k-1 (l1 partials of the sweep + |Hv - g|^2 partials).
+__global__ void objective_trace_kernel(const double* __restrict__ red, uint32_t P, const double* __restrict__ ored,
+                                       uint32_t no, const Params* __restrict__ prm, double* __restrict__ trace,
+                                       uint64_t trace_cap, const IterState* st) {
+  __shared__ double sm[kCtaWarps];
+  double l = 0.0, o = 0.0;
+  for (uint32_t k = threadIdx.x; k < P; k += kCtaThreads) l += red[2 * P + k];
+  for (uint32_t k = threadIdx.x; k < no; k += kCtaThreads) o += ored[k];
+  l = block_sum<kCtaThreads>(l, sm);
+  o = block_sum<kCtaThreads>(o, sm);
+  if (threadIdx.x == 0) {
+    const uint64_t k = st->iter - 1;
+    if (k < trace_cap) trace[3 * k + 2] = 0.5 * o + prm->lambda * l;
+  }
+}
+
 RowVecs row_vecs(admm_plan* p) {
   return RowVecs{p->dg.as<double2>(), p->dghat.as<double2>(), p->dgij.as<double2>(), p->dr.as<double2>(),
                  p->dq.as<double2>()};
@@ -374,7 +457,7 @@ ColVecs col_vecs(admm_plan* p) {
 
 // Launch list of one iteration (the order of solvers.hpp's phases).
 template <typename S>
-void enqueue_iteration(admm_plan* p, cudaStream_t s, bool with_objective, std::vector<cudaEvent_t>* ev) {
+void enqueue_iteration_twopass(admm_plan* p, cudaStream_t s, bool with_objective, std::vector<cudaEvent_t>* ev) {
   constexpr int CH = chunk_h<S>();
   const int nb = (int)p->blocks.size();
   const uint32_t N = (uint32_t)p->N, M = (uint32_t)p->M;
@@ -382,21 +465,21 @@ void enqueue_iteration(admm_plan* p, cudaStream_t s, bool with_objective, std::v
     if (ev) CK(cudaEventRecord((*ev)[k], s));
   };
   mark(0);
-  gemv_n_kernel<S, kVN, false><<<(unsigned)p->gN.P, kCtaThreads, 0, s>>>(
+  gemv_n_kernel<S, kVN, kEvictNormal><<<(unsigned)p->gN.P, kCtaThreads, 0, s>>>(
       p->dH.as<S>(), p->dc.as<double2>(), p->dwpart.as<double2>(), p->dhN.as<MatDesc>(), nb, p->gN.U);
   mark(1);
   rows_finalize_kernel<kRhs><<<dim3(p->rgx, nb), kCtaThreads, 0, s>>>(
       row_vecs(p), p->dwpart.as<double2>(), p->dhN.as<MatDesc>(), p->dblocks.as<BlockDesc>(), N, p->gN.U,
       p->gN.P, p->dparams.as<Params>());
   mark(2);
-  gemv_n_kernel<S, kVN, false><<<(unsigned)p->gK.P, kCtaThreads, 0, s>>>(
+  gemv_n_kernel<S, kVN, kEvictNormal><<<(unsigned)p->gK.P, kCtaThreads, 0, s>>>(
       p->dK.as<S>(), p->dr.as<double2>(), p->dqpart.as<double2>(), p->dkN.as<MatDesc>(), nb, p->gK.U);
   mark(3);
   rows_finalize_kernel<kQ><<<dim3(p->rgx, nb), kCtaThreads, 0, s>>>(
       row_vecs(p), p->dqpart.as<double2>(), p->dkN.as<MatDesc>(), p->dblocks.as<BlockDesc>(), N, p->gK.U,
       p->gK.P, p->dparams.as<Params>());
   mark(4);
-  gemv_h_kernel<S, kVH, false><<<(unsigned)p->gH.P, kCtaThreads, 0, s>>>(
+  gemv_h_kernel<S, kVH, kEvictNormal><<<(unsigned)p->gH.P, kCtaThreads, 0, s>>>(
       p->dH.as<S>(), p->dq.as<double2>(), p->dzpart.as<double2>(), p->dhH.as<MatDesc>(), nb, p->gH.U);
   mark(5);
   zupdate_kernel<CH><<<dim3(p->zgx, N), kCtaThreads, 0, s>>>(
@@ -404,7 +487,7 @@ void enqueue_iteration(admm_plan* p, cudaStream_t s, bool with_objective, std::v
       p->gH.P, p->dparams.as<Params>(), p->dred.as<double>(), p->dstate.as<IterState>());
   mark(6);
   if (with_objective) {
-    gemv_n_kernel<S, kVN, false><<<(unsigned)p->gO.P, kCtaThreads, 0, s>>>(
+    gemv_n_kernel<S, kVN, kEvictNormal><<<(unsigned)p->gO.P, kCtaThreads, 0, s>>>(
         p->dH.as<S>(), p->dv.as<double2>(), p->dopart.as<double2>(), p->dhNv.as<MatDesc>(), nb, p->gO.U);
     objective_rows_kernel<<<dim3(p->ogx, M), kCtaThreads, 0, s>>>(
         p->dg.as<double2>(), p->dopart.as<double2>(), p->dhNv.as<MatDesc>(), p->dblocks.as<BlockDesc>(), N,
@@ -417,11 +500,81 @@ void enqueue_iteration(admm_plan* p, cudaStream_t s, bool with_objective, std::v
   CK(cudaGetLastError());
 }
 
-void enqueue_iteration_any(admm_plan* p, cudaStream_t s, bool obj, std::vector<cudaEvent_t>* ev) {
-  if (p->dtype == ADMM_C128)
-    enqueue_iteration<double2>(p, s, obj, ev);
+// Sweep schedule.  Prologue (after reset): r = g_ij (w = H c^0 = 0), q = K r, ghat.
+template <typename S>
+void enqueue_sweep_prologue(admm_plan* p, cudaStream_t s) {
+  const int nb = (int)p->blocks.size();
+  rows_finalize_sweep_kernel<<<dim3(p->rgx, nb), kCtaThreads, 0, s>>>(
+      row_vecs(p), p->dwpart_s.as<double2>(), p->dsegs.as<SweepDesc>(), p->dblocks.as<BlockDesc>(),
+      (uint32_t)p->N, (uint32_t)p->n_meas, p->gS.U, p->gS.P, 1, 0, p->dred.as<double>(), p->dparams.as<Params>(),
+      p->dtrace.as<double>(), p->trace_cap, p->dstate.as<IterState>());
+  gemv_n_kernel<S, kVN, kEvictNormal><<<(unsigned)p->gK.P, kCtaThreads, 0, s>>>(
+      p->dK.as<S>(), p->dr.as<double2>(), p->dqpart.as<double2>(), p->dkN.as<MatDesc>(), nb, p->gK.U);
+  rows_finalize_kernel<kQ><<<dim3(p->rgx, nb), kCtaThreads, 0, s>>>(
+      row_vecs(p), p->dqpart.as<double2>(), p->dkN.as<MatDesc>(), p->dblocks.as<BlockDesc>(), (uint32_t)p->N,
+      p->gK.U, p->gK.P, p->dparams.as<Params>());
+  CK(cudaGetLastError());
+}
+
+// One iteration: sweep (z, u/v/s/c, next w) -> [objective] -> r (+ close iteration) ->
+// q = K r -> ghat.
+template <typename S>
+void enqueue_iteration_sweep(admm_plan* p, cudaStream_t s, bool with_objective, std::vector<cudaEvent_t>* ev) {
+  const int nb = (int)p->blocks.size();
+  auto mark = [&](size_t k) {
+    if (ev) CK(cudaEventRecord((*ev)[k], s));
+  };
+  mark(0);
+  if (p->sweep_lpr == 8)
+    sweep_kernel<S, 8><<<(unsigned)p->gS.P, kCtaThreads, p->sweep_smem, s>>>(
+        p->dH.as<S>(), p->dhN.as<MatDesc>(), p->dblocks.as<BlockDesc>(), p->dsegs.as<SweepDesc>(), (uint32_t)p->M,
+        (uint32_t)p->N, (uint32_t)p->n_meas, p->gS.U, p->dq.as<double2>(), col_vecs(p), p->dwpart_s.as<double2>(),
+        p->dparams.as<Params>(), p->dred.as<double>(), p->dstate.as<IterState>());
   else
-    enqueue_iteration<float2>(p, s, obj, ev);
+    sweep_kernel<S, 4><<<(unsigned)p->gS.P, kCtaThreads, p->sweep_smem, s>>>(
+        p->dH.as<S>(), p->dhN.as<MatDesc>(), p->dblocks.as<BlockDesc>(), p->dsegs.as<SweepDesc>(), (uint32_t)p->M,
+        (uint32_t)p->N, (uint32_t)p->n_meas, p->gS.U, p->dq.as<double2>(), col_vecs(p), p->dwpart_s.as<double2>(),
+        p->dparams.as<Params>(), p->dred.as<double>(), p->dstate.as<IterState>());
+  mark(1);
+  if (with_objective) {
+    gemv_n_kernel<S, kVN, kEvictNormal><<<(unsigned)p->gO.P, kCtaThreads, 0, s>>>(
+        p->dH.as<S>(), p->dv.as<double2>(), p->dopart.as<double2>(), p->dhNv.as<MatDesc>(), nb, p->gO.U);
+    objective_rows_kernel<<<dim3(p->ogx, (uint32_t)p->M), kCtaThreads, 0, s>>>(
+        p->dg.as<double2>(), p->dopart.as<double2>(), p->dhNv.as<MatDesc>(), p->dblocks.as<BlockDesc>(),
+        (uint32_t)p->N, p->gO.U, p->gO.P, p->dored.as<double>());
+  }
+  rows_finalize_sweep_kernel<<<dim3(p->rgx, nb), kCtaThreads, 0, s>>>(
+      row_vecs(p), p->dwpart_s.as<double2>(), p->dsegs.as<SweepDesc>(), p->dblocks.as<BlockDesc>(),
+      (uint32_t)p->N, (uint32_t)p->n_meas, p->gS.U, p->gS.P, 0, 1, p->dred.as<double>(), p->dparams.as<Params>(),
+      p->dtrace.as<double>(), p->trace_cap, p->dstate.as<IterState>());
+  mark(2);
+  if (with_objective) {  // the sweep's finalize wrote NaN: fill the objective of this iteration
+    objective_trace_kernel<<<1, kCtaThreads, 0, s>>>(p->dred.as<double>(), (uint32_t)p->gS.P, p->dored.as<double>(),
+                                                     p->no, p->dparams.as<Params>(), p->dtrace.as<double>(),
+                                                     p->trace_cap, p->dstate.as<IterState>());
+  }
+  gemv_n_kernel<S, kVN, kEvictNormal><<<(unsigned)p->gK.P, kCtaThreads, 0, s>>>(
+      p->dK.as<S>(), p->dr.as<double2>(), p->dqpart.as<double2>(), p->dkN.as<MatDesc>(), nb, p->gK.U);
+  mark(3);
+  rows_finalize_kernel<kQ><<<dim3(p->rgx, nb), kCtaThreads, 0, s>>>(
+      row_vecs(p), p->dqpart.as<double2>(), p->dkN.as<MatDesc>(), p->dblocks.as<BlockDesc>(), (uint32_t)p->N,
+      p->gK.U, p->gK.P, p->dparams.as<Params>());
+  mark(4);
+  CK(cudaGetLastError());
+}
+
+void enqueue_iteration_any(admm_plan* p, cudaStream_t s, bool obj, std::vector<cudaEvent_t>* ev) {
+  if (p->schedule == 2) {
+    if (p->dtype == ADMM_C128)
+      enqueue_iteration_sweep<double2>(p, s, obj, ev);
+    else
+      enqueue_iteration_sweep<float2>(p, s, obj, ev);
+  } else {
+    if (p->dtype == ADMM_C128)
+      enqueue_iteration_twopass<double2>(p, s, obj, ev);
+    else
+      enqueue_iteration_twopass<float2>(p, s, obj, ev);
+  }
 }
 
 // Objective of the current v (admm_core.hpp:60-64) into *d_obj, without touching
@@ -441,12 +594,13 @@ __global__ void objective_final_kernel(const double* __restrict__ red, uint32_t 
 template <typename S>
 void enqueue_objective(admm_plan* p, cudaStream_t s) {
   const int nb = (int)p->blocks.size();
-  gemv_n_kernel<S, kVN, false><<<(unsigned)p->gO.P, kCtaThreads, 0, s>>>(
+  gemv_n_kernel<S, kVN, kEvictNormal><<<(unsigned)p->gO.P, kCtaThreads, 0, s>>>(
       p->dH.as<S>(), p->dv.as<double2>(), p->dopart.as<double2>(), p->dhNv.as<MatDesc>(), nb, p->gO.U);
   objective_rows_kernel<<<dim3(p->ogx, (unsigned)p->M), kCtaThreads, 0, s>>>(
       p->dg.as<double2>(), p->dopart.as<double2>(), p->dhNv.as<MatDesc>(), p->dblocks.as<BlockDesc>(),
       (uint32_t)p->N, p->gO.U, p->gO.P, p->dored.as<double>());
-  objective_final_kernel<<<1, kCtaThreads, 0, s>>>(p->dred.as<double>(), p->nz, p->dored.as<double>(), p->no,
+  const uint32_t nred = p->schedule == 2 ? (uint32_t)p->gS.P : p->nz;  // l1 partials of the last update
+  objective_final_kernel<<<1, kCtaThreads, 0, s>>>(p->dred.as<double>(), nred, p->dored.as<double>(), p->no,
                                                    p->dparams.as<Params>(), p->dobj.as<double>());
   CK(cudaGetLastError());
 }
@@ -501,6 +655,12 @@ void reset_state(admm_plan* p) {
     CK(cudaMemsetAsync(d->p, 0, d->bytes, s));
   IterState st{0, ~0ull, 0u, 0u};
   CK(cudaMemcpyAsync(p->dstate.p, &st, sizeof(st), cudaMemcpyHostToDevice, s));
+  if (p->schedule == 2) {
+    if (p->dtype == ADMM_C128)
+      enqueue_sweep_prologue<double2>(p, s);
+    else
+      enqueue_sweep_prologue<float2>(p, s);
+  }
 }
 
 void ensure_trace(admm_plan* p, uint64_t iters) {
@@ -653,10 +813,19 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
   p->vec_total = vv;
   p->seg_total = sv;
 
-  if (p->dtype == ADMM_C128)
+  int requested = o.schedule;
+  if (const char* env = std::getenv("ADMM_B200_SCHEDULE")) {
+    if (!std::strcmp(env, "twopass")) requested = 1;
+    if (!std::strcmp(env, "sweep")) requested = 2;
+  }
+  if (skip_cfg_validation) requested = 1;  // single-block L0/L1 helper plans
+  if (p->dtype == ADMM_C128) {
     build_geometry<double2>(p.get());
-  else
+    choose_schedule<double2>(p.get(), requested);
+  } else {
     build_geometry<float2>(p.get());
+    choose_schedule<float2>(p.get(), requested);
+  }
   const size_t nb = p->blocks.size();
   upload_desc(p->dblocks, p->blocks.data(), nb * sizeof(BlockDesc));
   upload_desc(p->dhN, p->hN.data(), nb * sizeof(MatDesc));
@@ -676,7 +845,7 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
   p->ogx = (uint32_t)cdiv(p->max_rowblock, kCtaThreads);
   p->nz = p->zgx * (uint32_t)p->N;
   p->no = p->ogx * (uint32_t)p->M;
-  p->dred.alloc((size_t)3 * p->nz * sizeof(double));
+  p->dred.alloc((size_t)3 * std::max<uint64_t>(p->nz, p->gS.P) * sizeof(double));
   p->dored.alloc((size_t)std::max<uint32_t>(p->no, p->zgx * (uint32_t)p->N) * sizeof(double));
   ensure_trace(p.get(), std::max<uint64_t>(cfg.max_iters, 1));
 
@@ -752,13 +921,13 @@ admm_status admm_plan_max_abs_adjoint(admm_plan* p, double* out) {
     DevBuf res;
     res.alloc((size_t)gx * p->N * sizeof(double));
     if (p->dtype == ADMM_C128) {
-      gemv_h_kernel<double2, kVH, false><<<(unsigned)p->gG.P, kCtaThreads, 0, p->stream>>>(
+      gemv_h_kernel<double2, kVH, kEvictNormal><<<(unsigned)p->gG.P, kCtaThreads, 0, p->stream>>>(
           p->dH.as<double2>(), p->dg.as<double2>(), p->dgpart.as<double2>(), p->dhHg.as<MatDesc>(), nb, p->gG.U);
       adjoint_absmax_kernel<chunk_h<double2>()><<<dim3(gx, (unsigned)p->N), kCtaThreads, 0, p->stream>>>(
           p->dgpart.as<double2>(), p->dhHg.as<MatDesc>(), p->dblocks.as<BlockDesc>(), (uint32_t)p->M,
           (uint32_t)p->N, p->gG.U, p->gG.P, res.as<double>());
     } else {
-      gemv_h_kernel<float2, kVH, false><<<(unsigned)p->gG.P, kCtaThreads, 0, p->stream>>>(
+      gemv_h_kernel<float2, kVH, kEvictNormal><<<(unsigned)p->gG.P, kCtaThreads, 0, p->stream>>>(
           p->dH.as<float2>(), p->dg.as<double2>(), p->dgpart.as<double2>(), p->dhHg.as<MatDesc>(), nb, p->gG.U);
       adjoint_absmax_kernel<chunk_h<float2>()><<<dim3(gx, (unsigned)p->N), kCtaThreads, 0, p->stream>>>(
           p->dgpart.as<double2>(), p->dhHg.as<MatDesc>(), p->dblocks.as<BlockDesc>(), (uint32_t)p->M,
@@ -797,28 +966,31 @@ admm_status admm_plan_sync(admm_plan* p) {
 
 void* admm_plan_stream(admm_plan* p) { return p ? (void*)p->stream : nullptr; }
 
-uint32_t admm_plan_kernel_count(const admm_plan*) { return 7; }
+uint32_t admm_plan_kernel_count(const admm_plan* p) { return p && p->schedule == 2 ? 4 : 7; }
 
 admm_status admm_plan_profile(admm_plan* p, uint64_t iters, const char** names, double* ms) {
-  static const char* kNames[7] = {"gemv_n(H,c)", "rows_finalize(rhs)", "gemv_n(K,r)", "rows_finalize(q)",
-                                  "gemv_h(H,q)", "zupdate", "finalize"};
+  static const char* kNames2[7] = {"gemv_n(H,c)", "rows_finalize(rhs)", "gemv_n(K,r)", "rows_finalize(q)",
+                                   "gemv_h(H,q)", "zupdate", "finalize"};
+  static const char* kNamesS[4] = {"sweep(H)", "rows_finalize(rhs)+finalize", "gemv_n(K,r)", "rows_finalize(q)"};
   return run_guarded([&] {
     check_plan(p);
-    std::vector<cudaEvent_t> ev(8);
+    const int nk = (int)admm_plan_kernel_count(p);
+    const char* const* kn = p->schedule == 2 ? kNamesS : kNames2;
+    std::vector<cudaEvent_t> ev(nk + 1);
     for (auto& e : ev) CK(cudaEventCreate(&e));
-    std::vector<double> acc(7, 0.0);
+    std::vector<double> acc(nk, 0.0);
     for (uint64_t k = 0; k < iters; ++k) {
       enqueue_iteration_any(p, p->stream, false, &ev);
-      CK(cudaEventSynchronize(ev[7]));
-      for (int q = 0; q < 7; ++q) {
+      CK(cudaEventSynchronize(ev[nk]));
+      for (int q = 0; q < nk; ++q) {
         float t = 0.f;
         CK(cudaEventElapsedTime(&t, ev[q], ev[q + 1]));
         acc[q] += t;
       }
     }
     for (auto& e : ev) cudaEventDestroy(e);
-    for (int q = 0; q < 7; ++q) {
-      if (names) names[q] = kNames[q];
+    for (int q = 0; q < nk; ++q) {
+      if (names) names[q] = kn[q];
       if (ms) ms[q] = acc[q] / (double)std::max<uint64_t>(iters, 1);
     }
   });
@@ -838,8 +1010,11 @@ admm_status admm_plan_get_info(const admm_plan* p, admm_plan_info* info) {
     r.h_bytes = hb;
     r.k_bytes = kb;
     r.h_stream_bytes_per_iter = 2 * hb;
-    r.bytes_per_iter = 2 * hb + kb + vb;
-    r.launches_per_iter = p->trace_obj ? 9 : 7;
+    r.bytes_per_iter = 2 * hb + kb + vb;  // two-pass algorithmic bytes
+    r.launches_per_iter = p->schedule == 2 ? (p->trace_obj ? 7 : 4) : (p->trace_obj ? 9 : 7);
+    r.schedule = (uint64_t)p->schedule;
+    r.grid_sweep = p->gS.P;
+    r.hbm_bytes_per_iter = (p->schedule == 2 ? hb : 2 * hb) + kb + vb;
     r.grid_gemv_n = p->gN.P;
     r.grid_gemv_h = p->gH.P;
     r.setup_seconds = p->setup_s;
@@ -1016,7 +1191,7 @@ admm_status admm_matvec(const double* a, uint64_t rows, uint64_t cols, const dou
     std::vector<double> xs(2 * round_up(cols, 4), 0.0);
     std::memcpy(xs.data(), x, cols * 16);
     CK(cudaMemcpyAsync(p->dc.p, xs.data(), cols * 16, cudaMemcpyHostToDevice, p->stream));
-    gemv_n_kernel<double2, kVN, false><<<(unsigned)p->gN.P, kCtaThreads, 0, p->stream>>>(
+    gemv_n_kernel<double2, kVN, kEvictNormal><<<(unsigned)p->gN.P, kCtaThreads, 0, p->stream>>>(
         p->dH.as<double2>(), p->dc.as<double2>(), p->dwpart.as<double2>(), p->dhN.as<MatDesc>(), 1, p->gN.U);
     rows_sum_kernel<<<(unsigned)cdiv(rows, 256), 256, 0, p->stream>>>(p->dwpart.as<double2>(), p->dhN.as<MatDesc>(),
                                                                      p->gN.U, p->gN.P, p->dr.as<double2>());
@@ -1034,7 +1209,7 @@ admm_status admm_adjoint_matvec(const double* a, uint64_t rows, uint64_t cols, c
     std::vector<double> g(2 * rows, 0.0);
     std::unique_ptr<admm_plan> p(create_plan(single_block(device), cfg, rows, cols, a, ADMM_C128, g.data(), true));
     CK(cudaMemcpyAsync(p->dq.p, x, rows * 16, cudaMemcpyHostToDevice, p->stream));
-    gemv_h_kernel<double2, kVH, false><<<(unsigned)p->gH.P, kCtaThreads, 0, p->stream>>>(
+    gemv_h_kernel<double2, kVH, kEvictNormal><<<(unsigned)p->gH.P, kCtaThreads, 0, p->stream>>>(
         p->dH.as<double2>(), p->dq.as<double2>(), p->dzpart.as<double2>(), p->dhH.as<MatDesc>(), 1, p->gH.U);
     cols_sum_kernel<chunk_h<double2>()><<<(unsigned)cdiv(cols, 256), 256, 0, p->stream>>>(
         p->dzpart.as<double2>(), p->dhH.as<MatDesc>(), p->gH.U, p->gH.P, p->du.as<double2>());
@@ -1075,7 +1250,7 @@ admm_status admm_gram_solve(const double* h, uint64_t rows, uint64_t cols, doubl
     std::vector<double> c(2 * cols);
     for (uint64_t t = 0; t < 2 * cols; ++t) c[t] = rhs[t] / rho;
     CK(cudaMemcpyAsync(p->dc.p, c.data(), cols * 16, cudaMemcpyHostToDevice, p->stream));
-    enqueue_iteration<double2>(p.get(), p->stream, false, nullptr);
+    enqueue_iteration_twopass<double2>(p.get(), p->stream, false, nullptr);
     CK(cudaMemcpyAsync(x, p->du.p, cols * 16, cudaMemcpyDeviceToHost, p->stream));
     CK(cudaStreamSynchronize(p->stream));
   });

@@ -114,6 +114,7 @@ class SolveOptions:
     dtype: str = "c128"
     device: int = 0
     trace_objective: bool = True
+    schedule: str = "auto"  # "auto" | "twopass" | "sweep"
 
 
 @dataclasses.dataclass
@@ -240,7 +241,8 @@ class AdmmPlan:
         self.cfg = dataclasses.replace(cfg)
         self.opts = opts
         o = _lib.PlanOptionsC(_METHOD[method], self.M, self.N, int(opts.ragged),
-                              _DTYPE[opts.dtype], int(opts.device), int(opts.trace_objective))
+                              _DTYPE[opts.dtype], int(opts.device), int(opts.trace_objective),
+                              {"auto": 0, "twopass": 1, "sweep": 2}[opts.schedule])
         c = self.cfg._c()
         handle = ctypes.c_void_p()
         check(_lib.lib.admm_plan_create(ctypes.byref(o), ctypes.byref(c), self.n_meas, self.n_pix,

@@ -296,3 +296,30 @@ def test_numerical_blowup_and_errors():
         a.consensus_solve(bad, a.SolverConfig(lambda_=1e-3), 4)
     with pytest.raises(a.DimensionError):
         a.consensus_solve(a.SensingProblem(p.h, p.g[:5]), a.SolverConfig(), 1)
+
+
+@pytest.mark.parametrize("shape,method,M,N,ragged,dtype", [
+    ((64, 4096), "sectioning", 1, 8, False, "c128"),
+    ((256, 2048), "consensus", 4, 1, False, "c128"),
+    ((96, 1000), "hybrid", 3, 4, True, "c128"),
+    ((130, 777), "hybrid", 2, 3, True, "c64"),
+    ((192, 4096), "hybrid", 2, 4, False, "c64"),
+    ((40, 120), "reference", 1, 1, False, "c128"),
+])
+def test_sweep_schedule_equals_twopass(shape, method, M, N, ragged, dtype):
+    """The single-HBM-pass sweep computes the same iterates as the two-pass schedule
+    (only the summation order of the products differs)."""
+    a = admm()
+    p = a.gen_problem(shape[0], shape[1], 8, 30.0, 17, dtype=dtype)
+    lam = 0.05 * float(np.max(np.abs(orc.adjoint_matvec(p.h.astype(np.complex128), p.g))))
+    cfg = a.SolverConfig(rho=1.0, lambda_=lam, max_iters=25)
+    outs = {}
+    for sched in ("twopass", "sweep"):
+        opts = a.SolveOptions(ragged=ragged, dtype=dtype, schedule=sched)
+        with a.AdmmPlan(p, cfg, method, M, N, opts) as plan:
+            assert plan.info()["schedule"] == (1 if sched == "twopass" else 2)
+            outs[sched] = plan.solve()
+    t, s = outs["twopass"], outs["sweep"]
+    assert rel(s.solution, t.solution) <= 1e-12
+    assert rel(s.trace.dual, t.trace.dual) <= 1e-10
+    assert abs(s.objective - t.objective) <= 1e-12 * abs(t.objective)
