@@ -9,7 +9,7 @@ import ctypes
 import os
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libadmm_b200.so")
+LIB_PATH = os.environ.get("ADMM_B200_LIB", os.path.join(PKG_DIR, "libadmm_b200.so"))
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

@@ -64,6 +64,9 @@ sweep_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const Bloc
     for (uint32_t r = threadIdx.x; r < n_meas; r += kCtaThreads) wacc[r] = make_double2(0.0, 0.0);
     __syncthreads();
     for (;;) {
+#ifdef ADMM_DEBUG_SWEEP
+      if (threadIdx.x == 0) printf("cta %llu x %llu xe %llu j %u\n", (unsigned long long)p, (unsigned long long)x, (unsigned long long)xe, j);
+#endif
       const uint32_t col_lo = (uint32_t)(x - sd.unit0) * W;
       const uint32_t col = col_lo + lc * PV;
       const bool cok = col < sd.cols;
@@ -114,6 +117,9 @@ sweep_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const Bloc
         }
         __syncthreads();
       }
+#ifdef ADMM_DEBUG_SWEEP
+      if (threadIdx.x == 0) printf("cta %llu C done\n", (unsigned long long)p);
+#endif
       // ---- (D) u, replica mean, v = S_kappa, residual partials, dual update, next c
       if (threadIdx.x < W) {
         const uint32_t t = threadIdx.x, cc = col_lo + t;
@@ -150,6 +156,9 @@ sweep_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const Bloc
         }
       }
       __syncthreads();
+#ifdef ADMM_DEBUG_SWEEP
+      if (threadIdx.x == 0) printf("cta %llu D done\n", (unsigned long long)p);
+#endif
       // ---- (A) next iteration's w_i += H_ij[:, strip] c_i[strip]  (L2 re-read)
       for (uint32_t i = 0; i < M; ++i) {
         const MatDesc md = hm[i * N + j];
@@ -188,6 +197,9 @@ sweep_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const Bloc
           }
         }
       }
+#ifdef ADMM_DEBUG_SWEEP
+      if (threadIdx.x == 0) printf("cta %llu A done\n", (unsigned long long)p);
+#endif
       ++x;
       const bool seg_end = (x == sd.unit0 + sd.n_strips);
       if (seg_end || x == xe) {  // flush this segment's w partial
