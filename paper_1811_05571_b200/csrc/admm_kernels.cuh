@@ -264,7 +264,8 @@ __device__ __forceinline__ double2 sum_rows_part(const double2* __restrict__ par
   const uint32_t nseg = seg_count(first, md.n_chunks, U, P);
   const double2* src = part + md.part_off + (uint64_t)rg * md.n_chunks * kRowsPerGroup + w;
   double2 s = src[0];
-  for (uint32_t k = 1; k < nseg; ++k) s = cadd(s, src[(uint64_t)k * kRowsPerGroup]);
+#pragma unroll 8
+  for (uint32_t k = 1; k < nseg; ++k) s = cadd(s, src[(uint64_t)k * kRowsPerGroup]);  // loads hoisted, adds in order
   return s;
 }
 
@@ -277,6 +278,7 @@ __device__ __forceinline__ double2 sum_cols_part(const double2* __restrict__ par
   const uint32_t nseg = seg_count(first, md.n_tiles, U, P);
   const double2* src = part + md.part_off + (uint64_t)cc * md.n_tiles * CH + cl;
   double2 s = src[0];
+#pragma unroll 8
   for (uint32_t k = 1; k < nseg; ++k) s = cadd(s, src[(uint64_t)k * CH]);
   return s;
 }

@@ -269,7 +269,7 @@ void upload_desc(DevBuf& d, const void* src, size_t bytes);
 template <typename S, int LPR>
 size_t sweep_smem_bytes(const admm_plan* p) {
   constexpr int W = LPR * Store<S>::kPerVec;
-  return ((size_t)p->n_meas + (size_t)kCtaWarps * W + 2 * (size_t)p->M * W) * sizeof(double2);
+  return ((size_t)p->n_meas + (size_t)kGroupWarps * W + 4 * (size_t)p->M * W) * sizeof(double2);
 }
 
 // Try to configure the single-HBM-pass sweep with LPR lanes per row.  Returns false
@@ -282,8 +282,9 @@ bool try_sweep(admm_plan* p, size_t l2_budget) {
   if (smem > 200 * 1024) return false;
   CK(cudaFuncSetAttribute(sweep_kernel<S, LPR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_kernel<S, LPR>, kCtaThreads, smem));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_kernel<S, LPR>, kSweepThreads, smem));
   if (occ < 1) return false;
+  occ = 1;  // one warp-specialised CTA per SM (exactly num_sms CTAs: no wave imbalance)
   std::vector<SweepDesc> segs(p->N);
   uint64_t u = 0, po = 0;
   for (uint64_t j = 0; j < p->N; ++j) {
@@ -293,7 +294,7 @@ bool try_sweep(admm_plan* p, size_t l2_budget) {
     po += (uint64_t)segs[j].n_strips * p->n_meas;
   }
   uint64_t P = std::min<uint64_t>(u, (uint64_t)p->num_sms * occ);
-  const uint64_t strip = (uint64_t)p->n_meas * W * sizeof(S);
+  const uint64_t strip = 2 * (uint64_t)p->n_meas * W * sizeof(S);  // two strips open per CTA
   if (P * strip > l2_budget) {
     const uint64_t cap = l2_budget / strip;
     if (cap < (uint64_t)p->num_sms) return false;
@@ -313,7 +314,7 @@ template <typename S>
 void choose_schedule(admm_plan* p, int requested) {
   p->schedule = 1;
   if (requested == 1) return;
-  const size_t budget = 64ull << 20;  // resident strips must stay well inside the 126 MB L2
+  const size_t budget = 80ull << 20;  // open strips must stay well inside the 126 MB L2
   if (try_sweep<S, 8>(p, budget) || try_sweep<S, 4>(p, budget)) {
     p->schedule = 2;
     return;
@@ -526,12 +527,12 @@ void enqueue_iteration_sweep(admm_plan* p, cudaStream_t s, bool with_objective, 
   };
   mark(0);
   if (p->sweep_lpr == 8)
-    sweep_kernel<S, 8><<<(unsigned)p->gS.P, kCtaThreads, p->sweep_smem, s>>>(
+    sweep_kernel<S, 8><<<(unsigned)p->gS.P, kSweepThreads, p->sweep_smem, s>>>(
         p->dH.as<S>(), p->dhN.as<MatDesc>(), p->dblocks.as<BlockDesc>(), p->dsegs.as<SweepDesc>(), (uint32_t)p->M,
         (uint32_t)p->N, (uint32_t)p->n_meas, p->gS.U, p->dq.as<double2>(), col_vecs(p), p->dwpart_s.as<double2>(),
         p->dparams.as<Params>(), p->dred.as<double>(), p->dstate.as<IterState>());
   else
-    sweep_kernel<S, 4><<<(unsigned)p->gS.P, kCtaThreads, p->sweep_smem, s>>>(
+    sweep_kernel<S, 4><<<(unsigned)p->gS.P, kSweepThreads, p->sweep_smem, s>>>(
         p->dH.as<S>(), p->dhN.as<MatDesc>(), p->dblocks.as<BlockDesc>(), p->dsegs.as<SweepDesc>(), (uint32_t)p->M,
         (uint32_t)p->N, (uint32_t)p->n_meas, p->gS.U, p->dq.as<double2>(), col_vecs(p), p->dwpart_s.as<double2>(),
         p->dparams.as<Params>(), p->dred.as<double>(), p->dstate.as<IterState>());

@@ -32,8 +32,21 @@ struct SweepDesc {    // one per segment j
 
 constexpr int kSweepU = 8;  // row-instructions in flight per lane
 
+// Named barriers (id 0 is __syncthreads).
+__device__ __forceinline__ void nb_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void nb_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+constexpr int kSweepThreads = 512;           // 16 warps: 8 producer (C) + 8 consumer (D, A)
+constexpr int kGroupThreads = 256;
+constexpr int kGroupWarps = kGroupThreads / kWarp;
+enum SweepBar { kBarC = 1, kBarA = 2, kBarFull0 = 3, kBarEmpty0 = 5 };
+
+// Warp-specialised sweep: warps 0-7 stream strip s+1 from HBM and reduce z while
+// warps 8-15 finish strip s (u/v/s/c update and the L2 re-read for w).  z is handed
+// over through a double-buffered SMEM slot guarded by named FULL/EMPTY barriers, so
+// the HBM stream never waits for the elementwise phase or the second pass.
 template <typename S, int LPR>
-__global__ void __launch_bounds__(kCtaThreads, 2)
+__global__ void __launch_bounds__(kSweepThreads, 1)
 sweep_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const BlockDesc* __restrict__ blocks,
              const SweepDesc* __restrict__ segs, uint32_t M, uint32_t N, uint32_t n_meas, uint64_t Utot,
              const double2* __restrict__ q, ColVecs cv, double2* __restrict__ wpart,
@@ -41,187 +54,198 @@ sweep_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const Bloc
   constexpr int PV = Store<S>::kPerVec;
   constexpr int W = LPR * PV;            // columns per strip
   constexpr int RPI = kWarp / LPR;       // rows per warp instruction
-  constexpr int ROWSTEP = kCtaWarps * RPI;
+  constexpr int ROWSTEP = kGroupWarps * RPI;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* wacc = reinterpret_cast<double2*>(smem_raw);            // n_meas
-  double2* zred = wacc + n_meas;                                     // kCtaWarps x W
-  double2* zs = zred + kCtaWarps * W;                                // M x W (z, then u)
-  double2* cs = zs + (size_t)M * W;                                  // M x W (next c)
-  __shared__ double sm_red[kCtaWarps];
+  double2* wacc = reinterpret_cast<double2*>(smem_raw);            // n_meas          (consumer)
+  double2* zred = wacc + n_meas;                                     // 8 x W           (producer)
+  double2* zbuf = zred + kGroupWarps * W;                            // 2 x M x W       (hand-over)
+  double2* us = zbuf + 2 * (size_t)M * W;                            // M x W           (consumer)
+  double2* cs = us + (size_t)M * W;                                  // M x W           (consumer)
+  __shared__ double sm_red[kSweepThreads / kWarp];
 
   const uint64_t P = gridDim.x, p = blockIdx.x;
-  uint64_t x = sk_lo(p, Utot, P);
+  const uint64_t x0 = sk_lo(p, Utot, P);
   const uint64_t xe = sk_lo(p + 1, Utot, P);
-  const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+  const int gwarp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+  const bool producer = gwarp < kGroupWarps;
+  const int warp = producer ? gwarp : gwarp - kGroupWarps;
+  const int gt = threadIdx.x % kGroupThreads;  // thread index within the group
   const int lr = lane / LPR, lc = lane % LPR;
   double rp2 = 0.0, rd2 = 0.0, l1 = 0.0;
   bool bad = false;
 
-  if (x < xe) {
+  if (x0 < xe) {
     uint32_t j = 0;
-    while (j + 1 < N && segs[j + 1].unit0 <= x) ++j;
+    while (j + 1 < N && segs[j + 1].unit0 <= x0) ++j;
     SweepDesc sd = segs[j];
-    for (uint32_t r = threadIdx.x; r < n_meas; r += kCtaThreads) wacc[r] = make_double2(0.0, 0.0);
-    __syncthreads();
-    for (;;) {
-#ifdef ADMM_DEBUG_SWEEP
-      if (threadIdx.x == 0) printf("cta %llu x %llu xe %llu j %u\n", (unsigned long long)p, (unsigned long long)x, (unsigned long long)xe, j);
-#endif
-      const uint32_t col_lo = (uint32_t)(x - sd.unit0) * W;
-      const uint32_t col = col_lo + lc * PV;
-      const bool cok = col < sd.cols;
-      // ---- (C) z_i = H_ij^H q_i over the strip, replica by replica
-      for (uint32_t i = 0; i < M; ++i) {
-        const MatDesc md = hm[i * N + j];
-        const BlockDesc bd = blocks[i * N + j];
-        const S* hb = H + md.a_off + col;
-        const double2* qb = q + bd.mvec_off;
-        double2 acc[PV];
+    if (producer) {
+      // ------------------------------------------------ (C) z = H^H q per strip
+      uint32_t k = 0;
+      for (uint64_t x = x0; x < xe; ++x, ++k) {
+        if (x == sd.unit0 + sd.n_strips) sd = segs[++j];
+        const int slot = k & 1;
+        if (k >= 2) nb_sync(kBarEmpty0 + slot, kSweepThreads);  // consumer released the slot
+        const uint32_t col = (uint32_t)(x - sd.unit0) * W + lc * PV;
+        const bool cok = col < sd.cols;
+        for (uint32_t i = 0; i < M; ++i) {
+          const MatDesc md = hm[i * N + j];
+          const S* hb = H + md.a_off + col;
+          const double2* qb = q + blocks[i * N + j].mvec_off;
+          double2 acc[PV];
 #pragma unroll
-        for (int e = 0; e < PV; ++e) acc[e] = make_double2(0.0, 0.0);
-        for (uint32_t rb = warp * RPI; rb < md.rows; rb += ROWSTEP * kSweepU) {  // warp-uniform trip count
-          const uint32_t r0 = rb + lr;
-          V256 hv[kSweepU];
+          for (int e = 0; e < PV; ++e) acc[e] = make_double2(0.0, 0.0);
+          for (uint32_t rb = warp * RPI; rb < md.rows; rb += ROWSTEP * kSweepU) {  // warp-uniform
+            const uint32_t r0 = rb + lr;
+            V256 hv[kSweepU];
 #pragma unroll
-          for (int u = 0; u < kSweepU; ++u) {
-            const uint32_t row = r0 + u * ROWSTEP;
-            if (row < md.rows && cok) {
-              hv[u] = ld_stream256<kEvictLast>(hb + (uint64_t)row * md.ld);
-            } else {
-              hv[u].w[0] = hv[u].w[1] = hv[u].w[2] = hv[u].w[3] = 0;
+            for (int u = 0; u < kSweepU; ++u) {
+              const uint32_t row = r0 + u * ROWSTEP;
+              if (row < md.rows && cok) {
+                hv[u] = ld_stream256<kEvictLast>(hb + (uint64_t)row * md.ld);
+              } else {
+                hv[u].w[0] = hv[u].w[1] = hv[u].w[2] = hv[u].w[3] = 0;
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < kSweepU; ++u) {
+              const uint32_t row = r0 + u * ROWSTEP;
+              const double2 qv = row < md.rows ? __ldg(qb + row) : make_double2(0.0, 0.0);
+#pragma unroll
+              for (int e = 0; e < PV; ++e) cmac_conj(acc[e], Store<S>::get(hv[u], e), qv);
             }
           }
 #pragma unroll
-          for (int u = 0; u < kSweepU; ++u) {
-            const uint32_t row = r0 + u * ROWSTEP;
-            const double2 qv = row < md.rows ? __ldg(qb + row) : make_double2(0.0, 0.0);  // L1 hit
+          for (int e = 0; e < PV; ++e) {
 #pragma unroll
-            for (int e = 0; e < PV; ++e) cmac_conj(acc[e], Store<S>::get(hv[u], e), qv);
+            for (int o = LPR; o < kWarp; o <<= 1) {
+              acc[e].x += __shfl_xor_sync(0xffffffffu, acc[e].x, o);
+              acc[e].y += __shfl_xor_sync(0xffffffffu, acc[e].y, o);
+            }
+            if (lr == 0) zred[warp * W + lc * PV + e] = acc[e];
           }
-        }
+          nb_sync(kBarC, kGroupThreads);
+          if (gt < W) {
+            double2 z = zred[gt];
 #pragma unroll
-        for (int e = 0; e < PV; ++e) {
-#pragma unroll
-          for (int o = LPR; o < kWarp; o <<= 1) {
-            acc[e].x += __shfl_xor_sync(0xffffffffu, acc[e].x, o);
-            acc[e].y += __shfl_xor_sync(0xffffffffu, acc[e].y, o);
+            for (int w = 1; w < kGroupWarps; ++w) z = cadd(z, zred[w * W + gt]);
+            zbuf[((size_t)slot * M + i) * W + gt] = z;
           }
-          if (lr == 0) zred[warp * W + lc * PV + e] = acc[e];
+          nb_sync(kBarC, kGroupThreads);
         }
-        __syncthreads();
-        if (threadIdx.x < W) {
-          double2 z = zred[threadIdx.x];
-#pragma unroll
-          for (int w = 1; w < kCtaWarps; ++w) z = cadd(z, zred[w * W + threadIdx.x]);
-          zs[i * W + threadIdx.x] = z;
-        }
-        __syncthreads();
+        nb_arrive(kBarFull0 + slot, kSweepThreads);  // z of this strip is ready
       }
-#ifdef ADMM_DEBUG_SWEEP
-      if (threadIdx.x == 0) printf("cta %llu C done\n", (unsigned long long)p);
-#endif
-      // ---- (D) u, replica mean, v = S_kappa, residual partials, dual update, next c
-      if (threadIdx.x < W) {
-        const uint32_t t = threadIdx.x, cc = col_lo + t;
-        if (cc < sd.cols) {
-          double2 mean = make_double2(0.0, 0.0);
-          for (uint32_t i = 0; i < M; ++i) {
-            const uint32_t o = blocks[i * N + j].vec_off + cc;
-            const double2 u = cadd(cv.c[o], zs[i * W + t]);
-            bad |= !cfinite(u);
-            cv.u[o] = u;
-            zs[i * W + t] = u;
-            mean = cadd(mean, cadd(u, cv.s[o]));
-          }
-          mean = make_double2(mean.x / prm->m_rep, mean.y / prm->m_rep);
-          const double2 vn = soft_threshold(mean, prm->kappa);
-          const uint32_t so = blocks[j].seg_off + cc;
-          const double2 vo = cv.v[so];
-          cv.vprev[so] = vo;
-          cv.v[so] = vn;
-          rd2 += cabs2(csub(vn, vo));
-          l1 += hypot(vn.x, vn.y);
-          for (uint32_t i = 0; i < M; ++i) {
-            const uint32_t o = blocks[i * N + j].vec_off + cc;
-            const double2 u = zs[i * W + t];
-            rp2 += cabs2(csub(u, vn));
-            const double2 s = csub(cadd(cv.s[o], u), vn);
-            cv.s[o] = s;
-            const double2 c = csub(vn, s);
-            cv.c[o] = c;
-            cs[i * W + t] = c;
-          }
-        } else {
-          for (uint32_t i = 0; i < M; ++i) cs[i * W + t] = make_double2(0.0, 0.0);
-        }
-      }
-      __syncthreads();
-#ifdef ADMM_DEBUG_SWEEP
-      if (threadIdx.x == 0) printf("cta %llu D done\n", (unsigned long long)p);
-#endif
-      // ---- (A) next iteration's w_i += H_ij[:, strip] c_i[strip]  (L2 re-read)
-      for (uint32_t i = 0; i < M; ++i) {
-        const MatDesc md = hm[i * N + j];
-        const BlockDesc bd = blocks[i * N + j];
-        const S* hb = H + md.a_off + col;
-        double2 cx[PV];
-#pragma unroll
-        for (int e = 0; e < PV; ++e) cx[e] = cs[i * W + lc * PV + e];
-        for (uint32_t rb = warp * RPI; rb < md.rows; rb += ROWSTEP * kSweepU) {  // warp-uniform trip count
-          const uint32_t r0 = rb + lr;
-          V256 hv[kSweepU];
-#pragma unroll
-          for (int u = 0; u < kSweepU; ++u) {
-            const uint32_t row = r0 + u * ROWSTEP;
-            if (row < md.rows && cok) {
-              hv[u] = ld_stream256<kEvictFirst>(hb + (uint64_t)row * md.ld);
-            } else {
-              hv[u].w[0] = hv[u].w[1] = hv[u].w[2] = hv[u].w[3] = 0;
+      // drain: wait for the consumer's last releases so every barrier phase completes
+      const uint32_t nk = k;
+      for (uint32_t kk = (nk >= 2 ? nk - 2 : 0); kk < nk; ++kk) nb_sync(kBarEmpty0 + (kk & 1), kSweepThreads);
+    } else {
+      for (uint32_t r = gt; r < n_meas; r += kGroupThreads) wacc[r] = make_double2(0.0, 0.0);
+      uint32_t k = 0;
+      for (uint64_t x = x0; x < xe; ++x, ++k) {
+        const int slot = k & 1;
+        const uint32_t col_lo = (uint32_t)(x - sd.unit0) * W;
+        nb_sync(kBarFull0 + slot, kSweepThreads);  // wait for z of strip x
+        // ------------------------------------- (D) u, mean, v, residuals, s, next c
+        if (gt < W) {
+          const uint32_t t = gt, cc = col_lo + t;
+          if (cc < sd.cols) {
+            double2 mean = make_double2(0.0, 0.0);
+            for (uint32_t i = 0; i < M; ++i) {
+              const uint32_t o = blocks[i * N + j].vec_off + cc;
+              const double2 u = cadd(cv.c[o], zbuf[((size_t)slot * M + i) * W + t]);
+              bad |= !cfinite(u);
+              cv.u[o] = u;
+              us[i * W + t] = u;
+              mean = cadd(mean, cadd(u, cv.s[o]));
             }
-          }
-#pragma unroll
-          for (int u = 0; u < kSweepU; ++u) {
-            double2 a = make_double2(0.0, 0.0);
-#pragma unroll
-            for (int e = 0; e < PV; ++e) cmac(a, Store<S>::get(hv[u], e), cx[e]);
-#pragma unroll
-            for (int o = 1; o < LPR; o <<= 1) {
-              a.x += __shfl_xor_sync(0xffffffffu, a.x, o);
-              a.y += __shfl_xor_sync(0xffffffffu, a.y, o);
+            mean = make_double2(mean.x / prm->m_rep, mean.y / prm->m_rep);
+            const double2 vn = soft_threshold(mean, prm->kappa);
+            const uint32_t so = blocks[j].seg_off + cc;
+            const double2 vo = cv.v[so];
+            cv.vprev[so] = vo;
+            cv.v[so] = vn;
+            rd2 += cabs2(csub(vn, vo));
+            l1 += hypot(vn.x, vn.y);
+            for (uint32_t i = 0; i < M; ++i) {
+              const uint32_t o = blocks[i * N + j].vec_off + cc;
+              const double2 u = us[i * W + t];
+              rp2 += cabs2(csub(u, vn));
+              const double2 s = csub(cadd(cv.s[o], u), vn);
+              cv.s[o] = s;
+              const double2 c = csub(vn, s);
+              cv.c[o] = c;
+              cs[i * W + t] = c;
             }
-            const uint32_t row = r0 + u * ROWSTEP;
-            if (lc == 0 && row < md.rows) {
-              double2& dst = wacc[bd.row0 + row];  // each row is owned by one lane group
-              dst = cadd(dst, a);
-            }
+          } else {
+            for (uint32_t i = 0; i < M; ++i) cs[i * W + t] = make_double2(0.0, 0.0);
           }
         }
-      }
-#ifdef ADMM_DEBUG_SWEEP
-      if (threadIdx.x == 0) printf("cta %llu A done\n", (unsigned long long)p);
-#endif
-      ++x;
-      const bool seg_end = (x == sd.unit0 + sd.n_strips);
-      if (seg_end || x == xe) {  // flush this segment's w partial
-        __syncthreads();
-        const uint64_t slot = p - sk_owner(sd.unit0, Utot, P);
-        double2* dst = wpart + sd.part_off + slot * n_meas;
-        for (uint32_t r = threadIdx.x; r < n_meas; r += kCtaThreads) {
-          dst[r] = wacc[r];
-          wacc[r] = make_double2(0.0, 0.0);
+        nb_sync(kBarA, kGroupThreads);               // cs visible to the consumer group
+        nb_arrive(kBarEmpty0 + slot, kSweepThreads);  // zbuf[slot] may be refilled
+        // ------------------------------------- (A) w_i += H_ij[:, strip] c_i  (L2 re-read)
+        const uint32_t col = col_lo + lc * PV;
+        const bool cok = col < sd.cols;
+        for (uint32_t i = 0; i < M; ++i) {
+          const MatDesc md = hm[i * N + j];
+          const uint32_t row0 = blocks[i * N + j].row0;
+          const S* hb = H + md.a_off + col;
+          double2 cx[PV];
+#pragma unroll
+          for (int e = 0; e < PV; ++e) cx[e] = cs[i * W + lc * PV + e];
+          for (uint32_t rb = warp * RPI; rb < md.rows; rb += ROWSTEP * kSweepU) {  // warp-uniform
+            const uint32_t r0 = rb + lr;
+            V256 hv[kSweepU];
+#pragma unroll
+            for (int u = 0; u < kSweepU; ++u) {
+              const uint32_t row = r0 + u * ROWSTEP;
+              if (row < md.rows && cok) {
+                hv[u] = ld_stream256<kEvictFirst>(hb + (uint64_t)row * md.ld);
+              } else {
+                hv[u].w[0] = hv[u].w[1] = hv[u].w[2] = hv[u].w[3] = 0;
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < kSweepU; ++u) {
+              double2 a = make_double2(0.0, 0.0);
+#pragma unroll
+              for (int e = 0; e < PV; ++e) cmac(a, Store<S>::get(hv[u], e), cx[e]);
+#pragma unroll
+              for (int o = 1; o < LPR; o <<= 1) {
+                a.x += __shfl_xor_sync(0xffffffffu, a.x, o);
+                a.y += __shfl_xor_sync(0xffffffffu, a.y, o);
+              }
+              const uint32_t row = r0 + u * ROWSTEP;
+              if (lc == 0 && row < md.rows) {  // each row is owned by one lane group
+                double2& dst = wacc[row0 + row];
+                dst = cadd(dst, a);
+              }
+            }
+          }
         }
-        __syncthreads();
-        if (x == xe) break;
-        sd = segs[++j];
+        const bool seg_end = (x + 1 == sd.unit0 + sd.n_strips);
+        if (seg_end || x + 1 == xe) {  // flush this segment's w partial
+          nb_sync(kBarA, kGroupThreads);
+          const uint64_t slotp = p - sk_owner(sd.unit0, Utot, P);
+          double2* dst = wpart + sd.part_off + slotp * n_meas;
+          for (uint32_t r = gt; r < n_meas; r += kGroupThreads) {
+            dst[r] = wacc[r];
+            wacc[r] = make_double2(0.0, 0.0);
+          }
+          nb_sync(kBarA, kGroupThreads);
+          if (seg_end && x + 1 < xe) sd = segs[++j];
+        }
+        // the next strip's (D) reads cs/us only after its FULL barrier, and this
+        // group's (A) reads of cs finished before that (program order within the group
+        // is enforced by the kBarA barrier at the next (D)).
+        nb_sync(kBarA, kGroupThreads);
       }
     }
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) st->nonfinite = 1u;
-  double r = block_sum<kCtaThreads>(rp2, sm_red);
+  double r = block_sum<kSweepThreads>(rp2, sm_red);
   if (threadIdx.x == 0) red[p] = r;
-  r = block_sum<kCtaThreads>(rd2, sm_red);
+  r = block_sum<kSweepThreads>(rd2, sm_red);
   if (threadIdx.x == 0) red[P + p] = r;
-  r = block_sum<kCtaThreads>(l1, sm_red);
+  r = block_sum<kSweepThreads>(l1, sm_red);
   if (threadIdx.x == 0) red[2 * P + p] = r;
 }
 
@@ -245,6 +269,7 @@ rows_finalize_sweep_kernel(RowVecs rv, const double2* __restrict__ wpart, const 
       const uint32_t ns = seg_count(sd.unit0, sd.n_strips, Utot, Psweep);
       const double2* src = wpart + sd.part_off + bd.row0 + row;
       w = src[0];
+#pragma unroll 8
       for (uint32_t k = 1; k < ns; ++k) w = cadd(w, src[(uint64_t)k * n_meas]);
     }
     double2 gij = rv.g[bd.row0 + row];
