@@ -36,15 +36,17 @@ constexpr int kSweepU = 8;  // row-instructions in flight per lane
 __device__ __forceinline__ void nb_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void nb_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-constexpr int kSweepThreads = 512;           // 16 warps: 8 producer (C) + 8 consumer (D, A)
-constexpr int kGroupThreads = 256;
-constexpr int kGroupWarps = kGroupThreads / kWarp;
-enum SweepBar { kBarC = 1, kBarA = 2, kBarFull0 = 3, kBarEmpty0 = 5 };
+constexpr int kSweepThreads = 512;           // 16 warps
+constexpr int kProdWarps = 12;               // (C) HBM stream
+constexpr int kConsWarps = 4;                // (D) column update + (A) L2 re-read
+constexpr int kConsThreads = kConsWarps * kWarp;
+enum SweepBar { kBarA = 2, kBarFull0 = 3, kBarEmpty0 = 5 };
 
-// Warp-specialised sweep: warps 0-7 stream strip s+1 from HBM and reduce z while
-// warps 8-15 finish strip s (u/v/s/c update and the L2 re-read for w).  z is handed
-// over through a double-buffered SMEM slot guarded by named FULL/EMPTY barriers, so
-// the HBM stream never waits for the elementwise phase or the second pass.
+// Warp-specialised sweep: 12 producer warps stream strip s+1 from HBM and reduce z
+// while 4 consumer warps finish strip s (u/v/s/c update and the L2 re-read for w).
+// Each producer warp hands its partial z over through a double-buffered SMEM slot
+// guarded by named FULL/EMPTY barriers (the consumer adds the 12 partials in warp
+// order), so the HBM stream never waits on a barrier of its own group.
 template <typename S, int LPR>
 __global__ void __launch_bounds__(kSweepThreads, 1)
 sweep_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const BlockDesc* __restrict__ blocks,
@@ -54,22 +56,22 @@ sweep_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const Bloc
   constexpr int PV = Store<S>::kPerVec;
   constexpr int W = LPR * PV;            // columns per strip
   constexpr int RPI = kWarp / LPR;       // rows per warp instruction
-  constexpr int ROWSTEP = kGroupWarps * RPI;
+  constexpr int PSTEP = kProdWarps * RPI;
+  constexpr int CSTEP = kConsWarps * RPI;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* wacc = reinterpret_cast<double2*>(smem_raw);            // n_meas          (consumer)
-  double2* zred = wacc + n_meas;                                     // 8 x W           (producer)
-  double2* zbuf = zred + kGroupWarps * W;                            // 2 x M x W       (hand-over)
-  double2* us = zbuf + 2 * (size_t)M * W;                            // M x W           (consumer)
-  double2* cs = us + (size_t)M * W;                                  // M x W           (consumer)
+  double2* wacc = reinterpret_cast<double2*>(smem_raw);            // n_meas               (consumer)
+  double2* zbuf = wacc + n_meas;                                     // 2 x 12 x M x W       (hand-over)
+  double2* us = zbuf + 2 * (size_t)kProdWarps * M * W;               // M x W                (consumer)
+  double2* cs = us + (size_t)M * W;                                  // M x W                (consumer)
   __shared__ double sm_red[kSweepThreads / kWarp];
 
   const uint64_t P = gridDim.x, p = blockIdx.x;
   const uint64_t x0 = sk_lo(p, Utot, P);
   const uint64_t xe = sk_lo(p + 1, Utot, P);
   const int gwarp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
-  const bool producer = gwarp < kGroupWarps;
-  const int warp = producer ? gwarp : gwarp - kGroupWarps;
-  const int gt = threadIdx.x % kGroupThreads;  // thread index within the group
+  const bool producer = gwarp < kProdWarps;
+  const int warp = producer ? gwarp : gwarp - kProdWarps;
+  const int gt = threadIdx.x - (producer ? 0 : kProdWarps * kWarp);  // index within the group
   const int lr = lane / LPR, lc = lane % LPR;
   double rp2 = 0.0, rd2 = 0.0, l1 = 0.0;
   bool bad = false;
@@ -94,12 +96,12 @@ sweep_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const Bloc
           double2 acc[PV];
 #pragma unroll
           for (int e = 0; e < PV; ++e) acc[e] = make_double2(0.0, 0.0);
-          for (uint32_t rb = warp * RPI; rb < md.rows; rb += ROWSTEP * kSweepU) {  // warp-uniform
+          for (uint32_t rb = warp * RPI; rb < md.rows; rb += PSTEP * kSweepU) {  // warp-uniform
             const uint32_t r0 = rb + lr;
             V256 hv[kSweepU];
 #pragma unroll
             for (int u = 0; u < kSweepU; ++u) {
-              const uint32_t row = r0 + u * ROWSTEP;
+              const uint32_t row = r0 + u * PSTEP;
               if (row < md.rows && cok) {
                 hv[u] = ld_stream256<kEvictLast>(hb + (uint64_t)row * md.ld);
               } else {
@@ -108,7 +110,7 @@ sweep_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const Bloc
             }
 #pragma unroll
             for (int u = 0; u < kSweepU; ++u) {
-              const uint32_t row = r0 + u * ROWSTEP;
+              const uint32_t row = r0 + u * PSTEP;
               const double2 qv = row < md.rows ? __ldg(qb + row) : make_double2(0.0, 0.0);
 #pragma unroll
               for (int e = 0; e < PV; ++e) cmac_conj(acc[e], Store<S>::get(hv[u], e), qv);
@@ -121,16 +123,8 @@ sweep_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const Bloc
               acc[e].x += __shfl_xor_sync(0xffffffffu, acc[e].x, o);
               acc[e].y += __shfl_xor_sync(0xffffffffu, acc[e].y, o);
             }
-            if (lr == 0) zred[warp * W + lc * PV + e] = acc[e];
+            if (lr == 0) zbuf[(((size_t)slot * kProdWarps + warp) * M + i) * W + lc * PV + e] = acc[e];
           }
-          nb_sync(kBarC, kGroupThreads);
-          if (gt < W) {
-            double2 z = zred[gt];
-#pragma unroll
-            for (int w = 1; w < kGroupWarps; ++w) z = cadd(z, zred[w * W + gt]);
-            zbuf[((size_t)slot * M + i) * W + gt] = z;
-          }
-          nb_sync(kBarC, kGroupThreads);
         }
         nb_arrive(kBarFull0 + slot, kSweepThreads);  // z of this strip is ready
       }
@@ -138,7 +132,7 @@ sweep_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const Bloc
       const uint32_t nk = k;
       for (uint32_t kk = (nk >= 2 ? nk - 2 : 0); kk < nk; ++kk) nb_sync(kBarEmpty0 + (kk & 1), kSweepThreads);
     } else {
-      for (uint32_t r = gt; r < n_meas; r += kGroupThreads) wacc[r] = make_double2(0.0, 0.0);
+      for (uint32_t r = gt; r < n_meas; r += kConsThreads) wacc[r] = make_double2(0.0, 0.0);
       uint32_t k = 0;
       for (uint64_t x = x0; x < xe; ++x, ++k) {
         const int slot = k & 1;
@@ -151,7 +145,10 @@ sweep_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const Bloc
             double2 mean = make_double2(0.0, 0.0);
             for (uint32_t i = 0; i < M; ++i) {
               const uint32_t o = blocks[i * N + j].vec_off + cc;
-              const double2 u = cadd(cv.c[o], zbuf[((size_t)slot * M + i) * W + t]);
+              double2 z = zbuf[((size_t)slot * kProdWarps * M + i) * W + t];
+#pragma unroll
+              for (int w = 1; w < kProdWarps; ++w) z = cadd(z, zbuf[(((size_t)slot * kProdWarps + w) * M + i) * W + t]);
+              const double2 u = cadd(cv.c[o], z);
               bad |= !cfinite(u);
               cv.u[o] = u;
               us[i * W + t] = u;
@@ -179,7 +176,7 @@ sweep_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const Bloc
             for (uint32_t i = 0; i < M; ++i) cs[i * W + t] = make_double2(0.0, 0.0);
           }
         }
-        nb_sync(kBarA, kGroupThreads);               // cs visible to the consumer group
+        nb_sync(kBarA, kConsThreads);               // cs visible to the consumer group
         nb_arrive(kBarEmpty0 + slot, kSweepThreads);  // zbuf[slot] may be refilled
         // ------------------------------------- (A) w_i += H_ij[:, strip] c_i  (L2 re-read)
         const uint32_t col = col_lo + lc * PV;
@@ -191,12 +188,12 @@ sweep_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const Bloc
           double2 cx[PV];
 #pragma unroll
           for (int e = 0; e < PV; ++e) cx[e] = cs[i * W + lc * PV + e];
-          for (uint32_t rb = warp * RPI; rb < md.rows; rb += ROWSTEP * kSweepU) {  // warp-uniform
+          for (uint32_t rb = warp * RPI; rb < md.rows; rb += CSTEP * kSweepU) {  // warp-uniform
             const uint32_t r0 = rb + lr;
             V256 hv[kSweepU];
 #pragma unroll
             for (int u = 0; u < kSweepU; ++u) {
-              const uint32_t row = r0 + u * ROWSTEP;
+              const uint32_t row = r0 + u * CSTEP;
               if (row < md.rows && cok) {
                 hv[u] = ld_stream256<kEvictFirst>(hb + (uint64_t)row * md.ld);
               } else {
@@ -213,7 +210,7 @@ sweep_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const Bloc
                 a.x += __shfl_xor_sync(0xffffffffu, a.x, o);
                 a.y += __shfl_xor_sync(0xffffffffu, a.y, o);
               }
-              const uint32_t row = r0 + u * ROWSTEP;
+              const uint32_t row = r0 + u * CSTEP;
               if (lc == 0 && row < md.rows) {  // each row is owned by one lane group
                 double2& dst = wacc[row0 + row];
                 dst = cadd(dst, a);
@@ -223,20 +220,20 @@ sweep_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const Bloc
         }
         const bool seg_end = (x + 1 == sd.unit0 + sd.n_strips);
         if (seg_end || x + 1 == xe) {  // flush this segment's w partial
-          nb_sync(kBarA, kGroupThreads);
+          nb_sync(kBarA, kConsThreads);
           const uint64_t slotp = p - sk_owner(sd.unit0, Utot, P);
           double2* dst = wpart + sd.part_off + slotp * n_meas;
-          for (uint32_t r = gt; r < n_meas; r += kGroupThreads) {
+          for (uint32_t r = gt; r < n_meas; r += kConsThreads) {
             dst[r] = wacc[r];
             wacc[r] = make_double2(0.0, 0.0);
           }
-          nb_sync(kBarA, kGroupThreads);
+          nb_sync(kBarA, kConsThreads);
           if (seg_end && x + 1 < xe) sd = segs[++j];
         }
         // the next strip's (D) reads cs/us only after its FULL barrier, and this
         // group's (A) reads of cs finished before that (program order within the group
         // is enforced by the kBarA barrier at the next (D)).
-        nb_sync(kBarA, kGroupThreads);
+        nb_sync(kBarA, kConsThreads);
       }
     }
   }
