@@ -269,7 +269,7 @@ void upload_desc(DevBuf& d, const void* src, size_t bytes);
 template <typename S, int LPR>
 size_t sweep_smem_bytes(const admm_plan* p) {
   constexpr int W = LPR * Store<S>::kPerVec;
-  return ((size_t)p->n_meas + (2 * (size_t)kProdWarps + 2) * p->M * W) * sizeof(double2);
+  return ((size_t)p->n_meas + (2 * (size_t)kProdWarps + 4) * p->M * W) * sizeof(double2);
 }
 
 // Try to configure the single-HBM-pass sweep with LPR lanes per row.  Returns false

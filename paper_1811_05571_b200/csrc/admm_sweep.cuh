@@ -30,22 +30,23 @@ struct SweepDesc {    // one per segment j
   uint32_t cols;      // segment width
 };
 
-constexpr int kSweepU = 8;  // row-instructions in flight per lane
+constexpr int kSweepU = 8;   // producer: row-instructions in flight per lane
+constexpr int kSweepUA = 8;  // consumer (L2 re-read): row-instructions in flight per lane
 
 // Named barriers (id 0 is __syncthreads).
 __device__ __forceinline__ void nb_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void nb_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 constexpr int kSweepThreads = 512;           // 16 warps
-constexpr int kProdWarps = 12;               // (C) HBM stream
-constexpr int kConsWarps = 4;                // (D) column update + (A) L2 re-read
+constexpr int kProdWarps = 8;                // (C) HBM stream
+constexpr int kConsWarps = 8;                // (D) column update + (A) L2 re-read
 constexpr int kConsThreads = kConsWarps * kWarp;
 enum SweepBar { kBarA = 2, kBarFull0 = 3, kBarEmpty0 = 5 };
 
-// Warp-specialised sweep: 12 producer warps stream strip s+1 from HBM and reduce z
-// while 4 consumer warps finish strip s (u/v/s/c update and the L2 re-read for w).
+// Warp-specialised sweep: 8 producer warps stream strip s+1 from HBM and reduce z
+// while 8 consumer warps finish strip s (u/v/s/c update and the L2 re-read for w).
 // Each producer warp hands its partial z over through a double-buffered SMEM slot
-// guarded by named FULL/EMPTY barriers (the consumer adds the 12 partials in warp
+// guarded by named FULL/EMPTY barriers (the consumer adds the 8 partials in warp
 // order), so the HBM stream never waits on a barrier of its own group.
 template <typename S, int LPR>
 __global__ void __launch_bounds__(kSweepThreads, 1)
@@ -63,6 +64,7 @@ sweep_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const Bloc
   double2* zbuf = wacc + n_meas;                                     // 2 x 12 x M x W       (hand-over)
   double2* us = zbuf + 2 * (size_t)kProdWarps * M * W;               // M x W                (consumer)
   double2* cs = us + (size_t)M * W;                                  // M x W                (consumer)
+  double2* pre = cs + (size_t)M * W;                                 // 2 x M x W            (consumer)
   __shared__ double sm_red[kSweepThreads / kWarp];
 
   const uint64_t P = gridDim.x, p = blockIdx.x;
@@ -137,27 +139,39 @@ sweep_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const Bloc
       for (uint64_t x = x0; x < xe; ++x, ++k) {
         const int slot = k & 1;
         const uint32_t col_lo = (uint32_t)(x - sd.unit0) * W;
+        // prefetch this strip's iterates (independent of z) before waiting for z
+        const uint32_t t = gt, cc = col_lo + t;
+        const bool dcol = gt < W && cc < sd.cols;
+        double2 vo = make_double2(0.0, 0.0);
+        if (dcol) {  // pre[i] = c_i, pre[M + i] = s_i (SMEM: no dynamic register indexing)
+          for (uint32_t i = 0; i < M; ++i) {
+            const uint32_t o = blocks[i * N + j].vec_off + cc;
+            pre[i * W + t] = cv.c[o];
+            pre[(M + i) * W + t] = cv.s[o];
+          }
+          vo = cv.v[blocks[j].seg_off + cc];
+        }
         nb_sync(kBarFull0 + slot, kSweepThreads);  // wait for z of strip x
         // ------------------------------------- (D) u, mean, v, residuals, s, next c
         if (gt < W) {
-          const uint32_t t = gt, cc = col_lo + t;
-          if (cc < sd.cols) {
+          if (dcol) {
             double2 mean = make_double2(0.0, 0.0);
             for (uint32_t i = 0; i < M; ++i) {
               const uint32_t o = blocks[i * N + j].vec_off + cc;
               double2 z = zbuf[((size_t)slot * kProdWarps * M + i) * W + t];
 #pragma unroll
               for (int w = 1; w < kProdWarps; ++w) z = cadd(z, zbuf[(((size_t)slot * kProdWarps + w) * M + i) * W + t]);
-              const double2 u = cadd(cv.c[o], z);
+              const double2 ci = pre[i * W + t];
+              const double2 si = pre[(M + i) * W + t];
+              const double2 u = cadd(ci, z);
               bad |= !cfinite(u);
               cv.u[o] = u;
               us[i * W + t] = u;
-              mean = cadd(mean, cadd(u, cv.s[o]));
+              mean = cadd(mean, cadd(u, si));
             }
             mean = make_double2(mean.x / prm->m_rep, mean.y / prm->m_rep);
             const double2 vn = soft_threshold(mean, prm->kappa);
             const uint32_t so = blocks[j].seg_off + cc;
-            const double2 vo = cv.v[so];
             cv.vprev[so] = vo;
             cv.v[so] = vn;
             rd2 += cabs2(csub(vn, vo));
@@ -166,7 +180,7 @@ sweep_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const Bloc
               const uint32_t o = blocks[i * N + j].vec_off + cc;
               const double2 u = us[i * W + t];
               rp2 += cabs2(csub(u, vn));
-              const double2 s = csub(cadd(cv.s[o], u), vn);
+              const double2 s = csub(cadd(pre[(M + i) * W + t], u), vn);
               cv.s[o] = s;
               const double2 c = csub(vn, s);
               cv.c[o] = c;
@@ -188,11 +202,11 @@ sweep_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const Bloc
           double2 cx[PV];
 #pragma unroll
           for (int e = 0; e < PV; ++e) cx[e] = cs[i * W + lc * PV + e];
-          for (uint32_t rb = warp * RPI; rb < md.rows; rb += CSTEP * kSweepU) {  // warp-uniform
+          for (uint32_t rb = warp * RPI; rb < md.rows; rb += CSTEP * kSweepUA) {  // warp-uniform
             const uint32_t r0 = rb + lr;
-            V256 hv[kSweepU];
+            V256 hv[kSweepUA];
 #pragma unroll
-            for (int u = 0; u < kSweepU; ++u) {
+            for (int u = 0; u < kSweepUA; ++u) {
               const uint32_t row = r0 + u * CSTEP;
               if (row < md.rows && cok) {
                 hv[u] = ld_stream256<kEvictFirst>(hb + (uint64_t)row * md.ld);
@@ -201,7 +215,7 @@ sweep_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const Bloc
               }
             }
 #pragma unroll
-            for (int u = 0; u < kSweepU; ++u) {
+            for (int u = 0; u < kSweepUA; ++u) {
               double2 a = make_double2(0.0, 0.0);
 #pragma unroll
               for (int e = 0; e < PV; ++e) cmac(a, Store<S>::get(hv[u], e), cx[e]);
