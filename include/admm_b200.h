@@ -110,6 +110,33 @@ admm_status admm_plan_create(const admm_plan_options* opts, const admm_solver_co
                              uint64_t n_meas, uint64_t n_pix, const void* h, admm_dtype h_dtype,
                              const double* g, admm_plan** out);
 
+/* ---- multi-GPU: one plan per GPU over a Pr x Pc process grid -------
+ * The plan owns row blocks [pr*M/Pr, (pr+1)*M/Pr) x column blocks [pc*N/Pc, ...).  The
+ * caller runs the exchanges (all-gathers) between phases on the plan's stream, over
+ * buffers it attaches; the engine never waits on a peer inside a kernel.
+ *   iteration (sweep schedule, Pr == 1):  phase 1, X_ghat, X_scal, phase 4
+ *   iteration (two-pass schedule):        phase 1, X_ghat, phase 2, X_outbox, phase 3, X_scal, phase 4
+ * X_ghat: all-gather over the row communicator (ranks with the same pr, ordered by pc);
+ * X_outbox: all-gather over the column communicator (same pc, ordered by pr);
+ * X_scal: all-gather over all Pr*Pc ranks (rank = pr*Pc + pc).  Each rank's slot is
+ * [my_offset, my_offset + my_bytes) of a buffer of total_bytes; in-place all-gather. */
+typedef struct {
+  uint64_t Pr, Pc; /* process grid (Pr | M, Pc | N) */
+  uint64_t pr, pc; /* this plan's coordinates */
+} admm_shard;
+enum { ADMM_X_GHAT = 0, ADMM_X_OUTBOX = 1, ADMM_X_SCAL = 2 };
+admm_status admm_plan_create_sharded(const admm_plan_options* opts, const admm_solver_config* cfg,
+                                     uint64_t n_meas, uint64_t n_pix, const void* h, admm_dtype h_dtype,
+                                     const double* g, const admm_shard* shard, admm_plan** out);
+admm_status admm_plan_exchange_info(const admm_plan* plan, int which, uint64_t* total_bytes,
+                                    uint64_t* my_offset, uint64_t* my_bytes);
+/* Use caller-owned device memory (total_bytes) for exchange buffer `which`. */
+admm_status admm_plan_attach(admm_plan* plan, int which, void* device_ptr);
+/* Enqueue phase 1..4 of one iteration on the plan's stream (no host sync). */
+admm_status admm_plan_run_phase(admm_plan* plan, int phase);
+/* 1 = sweep, 2 = two-pass: the phase sequence the caller must drive. */
+admm_status admm_plan_schedule(const admm_plan* plan, int* schedule);
+
 /* Replace the measurement vector g (H, the partition and the factors are kept). */
 admm_status admm_plan_set_g(admm_plan* plan, const double* g);
 /* Replace lambda (kappa follows). */
@@ -156,7 +183,9 @@ typedef struct {
 admm_status admm_plan_get_info(const admm_plan* plan, admm_plan_info* info);
 
 /* Current iterate getters (host copies): which = 0 v (n_pix), 1 v_prev (n_pix),
- * 2 u of every worker concatenated in worker order (sum of segment lengths). */
+ * 2 u of every worker concatenated in worker order (sum of segment lengths),
+ * 3 the trace (3 doubles per completed iteration), 4 {iterations completed,
+ * first iteration with a non-finite u or -1}. */
 admm_status admm_plan_read(admm_plan* plan, int which, double* dst, uint64_t count);
 
 void admm_plan_destroy(admm_plan* plan);

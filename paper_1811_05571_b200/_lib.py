@@ -45,6 +45,10 @@ class PlanInfoC(ctypes.Structure):
                 ("grid_sweep", _u64), ("hbm_bytes_per_iter", _u64)]
 
 
+class ShardC(ctypes.Structure):
+    _fields_ = [("Pr", _u64), ("Pc", _u64), ("pr", _u64), ("pc", _u64)]
+
+
 OBSERVER = ctypes.CFUNCTYPE(None, ctypes.POINTER(SnapshotC), ctypes.c_void_p)
 
 lib = ctypes.CDLL(LIB_PATH)
@@ -55,6 +59,13 @@ _SIGS = {
     "admm_last_good_iteration": ([], _u64),
     "admm_plan_create": ([ctypes.POINTER(PlanOptionsC), ctypes.POINTER(SolverConfigC), _u64, _u64,
                           _ptr, _i32, _ptr, ctypes.POINTER(_ptr)], _i32),
+    "admm_plan_create_sharded": ([ctypes.POINTER(PlanOptionsC), ctypes.POINTER(SolverConfigC), _u64, _u64,
+                                  _ptr, _i32, _ptr, ctypes.POINTER(ShardC), ctypes.POINTER(_ptr)], _i32),
+    "admm_plan_exchange_info": ([_ptr, _i32, ctypes.POINTER(_u64), ctypes.POINTER(_u64),
+                                 ctypes.POINTER(_u64)], _i32),
+    "admm_plan_attach": ([_ptr, _i32, _ptr], _i32),
+    "admm_plan_run_phase": ([_ptr, _i32], _i32),
+    "admm_plan_schedule": ([_ptr, ctypes.POINTER(_i32)], _i32),
     "admm_plan_set_g": ([_ptr, _ptr], _i32),
     "admm_plan_set_lambda": ([_ptr, _dbl], _i32),
     "admm_plan_max_abs_adjoint": ([_ptr, ctypes.POINTER(_dbl)], _i32),

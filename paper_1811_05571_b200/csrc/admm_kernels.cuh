@@ -36,7 +36,7 @@ struct MatDesc {
   uint32_t rows, cols, ld;
   uint32_t n_chunks;  // gemv_n: column chunks per row group | gemv_h: column chunks
   uint32_t n_tiles;   // gemv_n: row groups                   | gemv_h: row tiles
-  uint32_t pad_;
+  uint32_t lid;       // local block index (row of the plan's block table)
 };
 
 // Per-block indexing used by the elementwise kernels.
@@ -47,6 +47,8 @@ struct BlockDesc {
   uint32_t mvec_off;    // offset of the block's m-vectors (ghat, g_ij, r, q)
   uint32_t vec_off;     // offset of the block's n-vectors (u, s, c)
   uint32_t seg_off;     // offset of segment j in the segment arena (v, v_prev)
+  uint32_t jl;          // local segment index of column block j (sharded plans)
+  uint32_t box_off;     // offset of the block's u+s in the outbox exchange buffer
   uint32_t pad_;
 };
 
@@ -298,8 +300,8 @@ enum RowStage { kRhs = 0, kQ = 1 };
 template <int Stage>
 __global__ void __launch_bounds__(kCtaThreads)
 rows_finalize_kernel(RowVecs rv, const double2* __restrict__ part, const MatDesc* __restrict__ mats,
-                     const BlockDesc* __restrict__ blocks, uint32_t N, uint64_t U, uint64_t P,
-                     const Params* __restrict__ prm) {
+                     const BlockDesc* __restrict__ blocks, const BlockDesc* __restrict__ gblocks, uint32_t N,
+                     uint64_t U, uint64_t P, const Params* __restrict__ prm) {
   const uint32_t b = blockIdx.y;
   const BlockDesc bd = blocks[b];
   const uint32_t row = blockIdx.x * blockDim.x + threadIdx.x;
@@ -311,7 +313,7 @@ rows_finalize_kernel(RowVecs rv, const double2* __restrict__ part, const MatDesc
     double2 gij = rv.g[bd.row0 + row];
     for (uint32_t qj = 0; qj < N; ++qj) {
       if (qj == bd.j) continue;
-      gij = csub(gij, rv.ghat[blocks[bd.i * N + qj].mvec_off + row]);
+      gij = csub(gij, rv.ghat[gblocks[bd.i * N + qj].mvec_off + row]);  // global table: peers too
     }
     rv.gij[o] = gij;
     rv.r[o] = csub(gij, s);
@@ -435,6 +437,118 @@ finalize_kernel(const double* __restrict__ red, uint32_t nz, const double* __res
     st->nonfinite = 0u;
     st->iter = k + 1;
   }
+}
+
+// ---- sharded two-pass iteration (replicas of a segment on different GPUs) -------
+// (after gemv_h) u_b = c_b + z_b for the local blocks; u_b + s_b goes to this rank's
+// slot of the outbox exchange buffer (all-gathered over the column communicator).
+template <int CH>
+__global__ void __launch_bounds__(kCtaThreads)
+uupdate_kernel(ColVecs cv, double2* __restrict__ outbox, const double2* __restrict__ part,
+               const MatDesc* __restrict__ mats, const BlockDesc* __restrict__ blocks, uint64_t U, uint64_t P,
+               IterState* st) {
+  const uint32_t b = blockIdx.y;
+  const BlockDesc bd = blocks[b];
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  bool bad = false;
+  if (t < bd.cols) {
+    const double2 z = sum_cols_part<CH>(part, mats[b], t, U, P);
+    const uint32_t o = bd.vec_off + t;
+    const double2 u = cadd(cv.c[o], z);
+    bad = !cfinite(u);
+    cv.u[o] = u;
+    outbox[bd.box_off + t] = cadd(u, cv.s[o]);
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) st->nonfinite = 1u;
+}
+
+// (after the outbox all-gather) per local segment jl: the replica mean over ALL M row
+// blocks in ascending i (solvers.hpp:404-415), v = S_kappa(mean), and the dual / next-c
+// update of the local blocks.  r_d and |v|_1 are counted by the pr == 0 rank only (the
+// other ranks of the column communicator hold the same segment).
+__global__ void __launch_bounds__(kCtaThreads)
+zfinal_kernel(ColVecs cv, const double2* __restrict__ outbox, const BlockDesc* __restrict__ blocks,
+              uint32_t M, uint32_t Mr, uint32_t Nc, uint32_t npad, int count_v, const Params* __restrict__ prm,
+              double* __restrict__ red) {
+  __shared__ double sm[kCtaWarps];
+  const uint32_t jl = blockIdx.y;
+  const BlockDesc b0 = blocks[jl];
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  double rp2 = 0.0, rd2 = 0.0, l1 = 0.0;
+  if (t < b0.cols) {
+    double2 mean = make_double2(0.0, 0.0);
+    for (uint32_t i = 0; i < M; ++i) mean = cadd(mean, outbox[((uint64_t)i * Nc + jl) * npad + t]);
+    mean = make_double2(mean.x / prm->m_rep, mean.y / prm->m_rep);
+    const double2 vn = soft_threshold(mean, prm->kappa);
+    const uint32_t so = b0.seg_off + t;
+    const double2 vo = cv.v[so];
+    cv.vprev[so] = vo;
+    cv.v[so] = vn;
+    if (count_v) {
+      rd2 = cabs2(csub(vn, vo));
+      l1 = hypot(vn.x, vn.y);
+    }
+    for (uint32_t il = 0; il < Mr; ++il) {
+      const uint32_t o = blocks[il * Nc + jl].vec_off + t;
+      const double2 u = cv.u[o];
+      rp2 += cabs2(csub(u, vn));
+      const double2 s = csub(cadd(cv.s[o], u), vn);
+      cv.s[o] = s;
+      cv.c[o] = csub(vn, s);
+    }
+  }
+  const uint32_t cta = blockIdx.y * gridDim.x + blockIdx.x, nct = gridDim.x * gridDim.y;
+  double r = block_sum<kCtaThreads>(rp2, sm);
+  if (threadIdx.x == 0) red[cta] = r;
+  r = block_sum<kCtaThreads>(rd2, sm);
+  if (threadIdx.x == 0) red[nct + cta] = r;
+  r = block_sum<kCtaThreads>(l1, sm);
+  if (threadIdx.x == 0) red[2 * nct + cta] = r;
+}
+
+// This rank's iteration scalars (rp2, rd2, l1, non-finite) into its slot of the
+// scalar exchange buffer (all-gathered over all ranks).
+__global__ void local_scalars_kernel(const double* __restrict__ red, uint32_t n, double* __restrict__ slot,
+                                     IterState* st) {
+  __shared__ double sm[kCtaWarps];
+  double a = 0.0, d = 0.0, l = 0.0;
+  for (uint32_t k = threadIdx.x; k < n; k += kCtaThreads) {
+    a += red[k];
+    d += red[n + k];
+    l += red[2 * n + k];
+  }
+  a = block_sum<kCtaThreads>(a, sm);
+  d = block_sum<kCtaThreads>(d, sm);
+  l = block_sum<kCtaThreads>(l, sm);
+  if (threadIdx.x == 0) {
+    slot[0] = a;
+    slot[1] = d;
+    slot[2] = l;
+    slot[3] = st->nonfinite ? 1.0 : 0.0;
+    st->nonfinite = 0u;
+  }
+}
+
+// Close an iteration from the all-gathered scalars (rank order): trace[k] and the
+// non-finite bookkeeping, identically on every rank.
+__global__ void close_kernel(const double* __restrict__ all, uint32_t nranks, const Params* __restrict__ prm,
+                             double* __restrict__ trace, uint64_t trace_cap, IterState* st) {
+  if (threadIdx.x != 0) return;
+  double a = 0.0, d = 0.0;
+  bool bad = false;
+  for (uint32_t r = 0; r < nranks; ++r) {
+    a += all[4 * r];
+    d += all[4 * r + 1];
+    bad |= all[4 * r + 3] != 0.0;
+  }
+  const uint64_t k = st->iter;
+  if (k < trace_cap) {
+    trace[3 * k] = sqrt(a);
+    trace[3 * k + 1] = sqrt(prm->rho * prm->rho * prm->m_rep * d);
+    trace[3 * k + 2] = __longlong_as_double(0x7ff8000000000000ll);
+  }
+  if (bad && st->first_bad == ~0ull) st->first_bad = k;
+  st->iter = k + 1;
 }
 
 }  // namespace admm

@@ -126,6 +126,14 @@ struct admm_plan {
   admm_dtype dtype = ADMM_C128;
   admm_method method = ADMM_HYBRID;
   uint64_t n_meas = 0, n_pix = 0, M = 1, N = 1;
+  // sharding over a Pr x Pc process grid; 1 x 1 for a single GPU
+  uint64_t Pr = 1, Pc = 1, pr = 0, pc = 0, Mr = 1, Nc = 1, i0 = 0, j0 = 0;
+  uint64_t mpad = 0, npad = 0, outbox_total = 0;
+  std::vector<BlockDesc> gblocks;  // global M x N table (ghost entries for exchange layouts)
+  DevBuf dgblocks, doutbox, dscal;
+  double2* ghat_ptr = nullptr;     // ghat exchange buffer (internal or attached)
+  double2* outbox_ptr = nullptr;
+  double* scal_ptr = nullptr;
   bool ragged = false, trace_obj = false;
   admm_solver_config cfg{};
   std::vector<uint64_t> rb, cb;
@@ -269,7 +277,7 @@ void upload_desc(DevBuf& d, const void* src, size_t bytes);
 template <typename S, int LPR>
 size_t sweep_smem_bytes(const admm_plan* p) {
   constexpr int W = LPR * Store<S>::kPerVec;
-  return ((size_t)p->n_meas + (2 * (size_t)kProdWarps + 4) * p->M * W) * sizeof(double2);
+  return ((size_t)p->n_meas + (2 * (size_t)kProdWarps + 4) * p->Mr * W) * sizeof(double2);
 }
 
 // Try to configure the single-HBM-pass sweep with LPR lanes per row.  Returns false
@@ -285,10 +293,11 @@ bool try_sweep(admm_plan* p, size_t l2_budget) {
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_kernel<S, LPR>, kSweepThreads, smem));
   if (occ < 1) return false;
   occ = 1;  // one warp-specialised CTA per SM (exactly num_sms CTAs: no wave imbalance)
-  std::vector<SweepDesc> segs(p->N);
+  if (p->Pr != 1) return false;  // the replica mean needs every row block of a strip
+  std::vector<SweepDesc> segs(p->Nc);
   uint64_t u = 0, po = 0;
-  for (uint64_t j = 0; j < p->N; ++j) {
-    const uint32_t cols = (uint32_t)(p->cb[j + 1] - p->cb[j]);
+  for (uint64_t j = 0; j < p->Nc; ++j) {
+    const uint32_t cols = p->blocks[j].cols;
     segs[j] = SweepDesc{u, po, (uint32_t)cdiv(cols, W), cols};
     u += segs[j].n_strips;
     po += (uint64_t)segs[j].n_strips * p->n_meas;
@@ -448,7 +457,7 @@ __global__ void objective_trace_kernel(const double* __restrict__ red, uint32_t 
 }
 
 RowVecs row_vecs(admm_plan* p) {
-  return RowVecs{p->dg.as<double2>(), p->dghat.as<double2>(), p->dgij.as<double2>(), p->dr.as<double2>(),
+  return RowVecs{p->dg.as<double2>(), p->ghat_ptr, p->dgij.as<double2>(), p->dr.as<double2>(),
                  p->dq.as<double2>()};
 }
 ColVecs col_vecs(admm_plan* p) {
@@ -461,7 +470,7 @@ template <typename S>
 void enqueue_iteration_twopass(admm_plan* p, cudaStream_t s, bool with_objective, std::vector<cudaEvent_t>* ev) {
   constexpr int CH = chunk_h<S>();
   const int nb = (int)p->blocks.size();
-  const uint32_t N = (uint32_t)p->N, M = (uint32_t)p->M;
+  const uint32_t N = (uint32_t)p->Nc, M = (uint32_t)p->Mr;  // local table
   auto mark = [&](size_t k) {
     if (ev) CK(cudaEventRecord((*ev)[k], s));
   };
@@ -470,14 +479,16 @@ void enqueue_iteration_twopass(admm_plan* p, cudaStream_t s, bool with_objective
       p->dH.as<S>(), p->dc.as<double2>(), p->dwpart.as<double2>(), p->dhN.as<MatDesc>(), nb, p->gN.U);
   mark(1);
   rows_finalize_kernel<kRhs><<<dim3(p->rgx, nb), kCtaThreads, 0, s>>>(
-      row_vecs(p), p->dwpart.as<double2>(), p->dhN.as<MatDesc>(), p->dblocks.as<BlockDesc>(), N, p->gN.U,
+      row_vecs(p), p->dwpart.as<double2>(), p->dhN.as<MatDesc>(), p->dblocks.as<BlockDesc>(),
+      p->dgblocks.as<BlockDesc>(), (uint32_t)p->N, p->gN.U,
       p->gN.P, p->dparams.as<Params>());
   mark(2);
   gemv_n_kernel<S, kVN, kEvictNormal><<<(unsigned)p->gK.P, kCtaThreads, 0, s>>>(
       p->dK.as<S>(), p->dr.as<double2>(), p->dqpart.as<double2>(), p->dkN.as<MatDesc>(), nb, p->gK.U);
   mark(3);
   rows_finalize_kernel<kQ><<<dim3(p->rgx, nb), kCtaThreads, 0, s>>>(
-      row_vecs(p), p->dqpart.as<double2>(), p->dkN.as<MatDesc>(), p->dblocks.as<BlockDesc>(), N, p->gK.U,
+      row_vecs(p), p->dqpart.as<double2>(), p->dkN.as<MatDesc>(), p->dblocks.as<BlockDesc>(),
+      p->dgblocks.as<BlockDesc>(), (uint32_t)p->N, p->gK.U,
       p->gK.P, p->dparams.as<Params>());
   mark(4);
   gemv_h_kernel<S, kVH, kEvictNormal><<<(unsigned)p->gH.P, kCtaThreads, 0, s>>>(
@@ -507,12 +518,13 @@ void enqueue_sweep_prologue(admm_plan* p, cudaStream_t s) {
   const int nb = (int)p->blocks.size();
   rows_finalize_sweep_kernel<<<dim3(p->rgx, nb), kCtaThreads, 0, s>>>(
       row_vecs(p), p->dwpart_s.as<double2>(), p->dsegs.as<SweepDesc>(), p->dblocks.as<BlockDesc>(),
-      (uint32_t)p->N, (uint32_t)p->n_meas, p->gS.U, p->gS.P, 1, 0, p->dred.as<double>(), p->dparams.as<Params>(),
+      p->dgblocks.as<BlockDesc>(), (uint32_t)p->N, (uint32_t)p->n_meas, p->gS.U, p->gS.P, 1, 0, p->dred.as<double>(), p->dparams.as<Params>(),
       p->dtrace.as<double>(), p->trace_cap, p->dstate.as<IterState>());
   gemv_n_kernel<S, kVN, kEvictNormal><<<(unsigned)p->gK.P, kCtaThreads, 0, s>>>(
       p->dK.as<S>(), p->dr.as<double2>(), p->dqpart.as<double2>(), p->dkN.as<MatDesc>(), nb, p->gK.U);
   rows_finalize_kernel<kQ><<<dim3(p->rgx, nb), kCtaThreads, 0, s>>>(
-      row_vecs(p), p->dqpart.as<double2>(), p->dkN.as<MatDesc>(), p->dblocks.as<BlockDesc>(), (uint32_t)p->N,
+      row_vecs(p), p->dqpart.as<double2>(), p->dkN.as<MatDesc>(), p->dblocks.as<BlockDesc>(),
+      p->dgblocks.as<BlockDesc>(), (uint32_t)p->N,
       p->gK.U, p->gK.P, p->dparams.as<Params>());
   CK(cudaGetLastError());
 }
@@ -528,25 +540,25 @@ void enqueue_iteration_sweep(admm_plan* p, cudaStream_t s, bool with_objective, 
   mark(0);
   if (p->sweep_lpr == 8)
     sweep_kernel<S, 8><<<(unsigned)p->gS.P, kSweepThreads, p->sweep_smem, s>>>(
-        p->dH.as<S>(), p->dhN.as<MatDesc>(), p->dblocks.as<BlockDesc>(), p->dsegs.as<SweepDesc>(), (uint32_t)p->M,
-        (uint32_t)p->N, (uint32_t)p->n_meas, p->gS.U, p->dq.as<double2>(), col_vecs(p), p->dwpart_s.as<double2>(),
+        p->dH.as<S>(), p->dhN.as<MatDesc>(), p->dblocks.as<BlockDesc>(), p->dsegs.as<SweepDesc>(), (uint32_t)p->Mr,
+        (uint32_t)p->Nc, (uint32_t)p->n_meas, p->gS.U, p->dq.as<double2>(), col_vecs(p), p->dwpart_s.as<double2>(),
         p->dparams.as<Params>(), p->dred.as<double>(), p->dstate.as<IterState>());
   else
     sweep_kernel<S, 4><<<(unsigned)p->gS.P, kSweepThreads, p->sweep_smem, s>>>(
-        p->dH.as<S>(), p->dhN.as<MatDesc>(), p->dblocks.as<BlockDesc>(), p->dsegs.as<SweepDesc>(), (uint32_t)p->M,
-        (uint32_t)p->N, (uint32_t)p->n_meas, p->gS.U, p->dq.as<double2>(), col_vecs(p), p->dwpart_s.as<double2>(),
+        p->dH.as<S>(), p->dhN.as<MatDesc>(), p->dblocks.as<BlockDesc>(), p->dsegs.as<SweepDesc>(), (uint32_t)p->Mr,
+        (uint32_t)p->Nc, (uint32_t)p->n_meas, p->gS.U, p->dq.as<double2>(), col_vecs(p), p->dwpart_s.as<double2>(),
         p->dparams.as<Params>(), p->dred.as<double>(), p->dstate.as<IterState>());
   mark(1);
   if (with_objective) {
     gemv_n_kernel<S, kVN, kEvictNormal><<<(unsigned)p->gO.P, kCtaThreads, 0, s>>>(
         p->dH.as<S>(), p->dv.as<double2>(), p->dopart.as<double2>(), p->dhNv.as<MatDesc>(), nb, p->gO.U);
-    objective_rows_kernel<<<dim3(p->ogx, (uint32_t)p->M), kCtaThreads, 0, s>>>(
+    objective_rows_kernel<<<dim3(p->ogx, (uint32_t)p->Mr), kCtaThreads, 0, s>>>(
         p->dg.as<double2>(), p->dopart.as<double2>(), p->dhNv.as<MatDesc>(), p->dblocks.as<BlockDesc>(),
-        (uint32_t)p->N, p->gO.U, p->gO.P, p->dored.as<double>());
+        (uint32_t)p->Nc, p->gO.U, p->gO.P, p->dored.as<double>());
   }
   rows_finalize_sweep_kernel<<<dim3(p->rgx, nb), kCtaThreads, 0, s>>>(
       row_vecs(p), p->dwpart_s.as<double2>(), p->dsegs.as<SweepDesc>(), p->dblocks.as<BlockDesc>(),
-      (uint32_t)p->N, (uint32_t)p->n_meas, p->gS.U, p->gS.P, 0, 1, p->dred.as<double>(), p->dparams.as<Params>(),
+      p->dgblocks.as<BlockDesc>(), (uint32_t)p->N, (uint32_t)p->n_meas, p->gS.U, p->gS.P, 0, 1, p->dred.as<double>(), p->dparams.as<Params>(),
       p->dtrace.as<double>(), p->trace_cap, p->dstate.as<IterState>());
   mark(2);
   if (with_objective) {  // the sweep's finalize wrote NaN: fill the objective of this iteration
@@ -558,7 +570,8 @@ void enqueue_iteration_sweep(admm_plan* p, cudaStream_t s, bool with_objective, 
       p->dK.as<S>(), p->dr.as<double2>(), p->dqpart.as<double2>(), p->dkN.as<MatDesc>(), nb, p->gK.U);
   mark(3);
   rows_finalize_kernel<kQ><<<dim3(p->rgx, nb), kCtaThreads, 0, s>>>(
-      row_vecs(p), p->dqpart.as<double2>(), p->dkN.as<MatDesc>(), p->dblocks.as<BlockDesc>(), (uint32_t)p->N,
+      row_vecs(p), p->dqpart.as<double2>(), p->dkN.as<MatDesc>(), p->dblocks.as<BlockDesc>(),
+      p->dgblocks.as<BlockDesc>(), (uint32_t)p->N,
       p->gK.U, p->gK.P, p->dparams.as<Params>());
   mark(4);
   CK(cudaGetLastError());
@@ -597,9 +610,9 @@ void enqueue_objective(admm_plan* p, cudaStream_t s) {
   const int nb = (int)p->blocks.size();
   gemv_n_kernel<S, kVN, kEvictNormal><<<(unsigned)p->gO.P, kCtaThreads, 0, s>>>(
       p->dH.as<S>(), p->dv.as<double2>(), p->dopart.as<double2>(), p->dhNv.as<MatDesc>(), nb, p->gO.U);
-  objective_rows_kernel<<<dim3(p->ogx, (unsigned)p->M), kCtaThreads, 0, s>>>(
+  objective_rows_kernel<<<dim3(p->ogx, (unsigned)p->Mr), kCtaThreads, 0, s>>>(
       p->dg.as<double2>(), p->dopart.as<double2>(), p->dhNv.as<MatDesc>(), p->dblocks.as<BlockDesc>(),
-      (uint32_t)p->N, p->gO.U, p->gO.P, p->dored.as<double>());
+      (uint32_t)p->Nc, p->gO.U, p->gO.P, p->dored.as<double>());
   const uint32_t nred = p->schedule == 2 ? (uint32_t)p->gS.P : p->nz;  // l1 partials of the last update
   objective_final_kernel<<<1, kCtaThreads, 0, s>>>(p->dred.as<double>(), nred, p->dored.as<double>(), p->no,
                                                    p->dparams.as<Params>(), p->dobj.as<double>());
@@ -652,8 +665,10 @@ void upload_g(admm_plan* p, const double* g) {
 
 void reset_state(admm_plan* p) {
   cudaStream_t s = p->stream;
-  for (DevBuf* d : {&p->du, &p->ds, &p->dc, &p->dv, &p->dvprev, &p->dghat, &p->dgij, &p->dr, &p->dq})
+  for (DevBuf* d : {&p->du, &p->ds, &p->dc, &p->dv, &p->dvprev, &p->dgij, &p->dr, &p->dq})
     CK(cudaMemsetAsync(d->p, 0, d->bytes, s));
+  CK(cudaMemsetAsync(p->ghat_ptr, 0, p->mvec_total * 16, s));
+  CK(cudaMemsetAsync(p->outbox_ptr, 0, p->outbox_total * 16, s));
   IterState st{0, ~0ull, 0u, 0u};
   CK(cudaMemcpyAsync(p->dstate.p, &st, sizeof(st), cudaMemcpyHostToDevice, s));
   if (p->schedule == 2) {
@@ -713,7 +728,7 @@ void read_segments(admm_plan* p, const DevBuf& src, double* dst) {
   p->h_seg.resize(p->seg_total * 2);
   CK(cudaMemcpyAsync(p->h_seg.data(), src.p, p->seg_total * 16, cudaMemcpyDeviceToHost, p->stream));
   CK(cudaStreamSynchronize(p->stream));
-  for (uint64_t j = 0; j < p->N; ++j) {
+  for (uint64_t j = 0; j < p->Nc; ++j) {  // local segments (all of them on a single GPU)
     const BlockDesc& b = p->blocks[j];
     std::memcpy(dst + 2 * b.col0, p->h_seg.data() + 2 * (uint64_t)b.seg_off, (size_t)b.cols * 16);
   }
@@ -745,7 +760,7 @@ void validate_cfg(const admm_solver_config& c) {  // SolverConfig::validate, adm
 // Build a plan.  skip_cfg_validation is used by the GramSolver op (no lambda).
 admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg, uint64_t n_meas,
                        uint64_t n_pix, const void* h, admm_dtype h_dtype, const double* g,
-                       bool skip_cfg_validation) {
+                       bool skip_cfg_validation, const admm_shard* shard = nullptr) {
   const auto t0 = std::chrono::steady_clock::now();
   if (!skip_cfg_validation) validate_cfg(cfg);
   // SensingProblem::validate (problem.hpp:35-49)
@@ -782,37 +797,69 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
   CK(cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, o.device));
   CK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
 
-  // block table; worker id = i*N + j (solvers.hpp:305)
-  uint64_t mv = 0, vv = 0, sv = 0;
-  std::vector<uint64_t> seg_off(p->N);
-  for (uint64_t j = 0; j < p->N; ++j) {
-    seg_off[j] = sv;
-    sv += round_up(p->cb[j + 1] - p->cb[j], 4);
-    p->max_seg = std::max<uint32_t>(p->max_seg, (uint32_t)(p->cb[j + 1] - p->cb[j]));
+  // sharding: this plan owns row blocks [i0, i0+Mr) x column blocks [j0, j0+Nc)
+  if (shard) {
+    p->Pr = shard->Pr;
+    p->Pc = shard->Pc;
+    p->pr = shard->pr;
+    p->pc = shard->pc;
+    if (p->Pr < 1 || p->Pc < 1 || p->pr >= p->Pr || p->pc >= p->Pc)
+      throw Fail{ADMM_E_INDEX, "shard coordinates out of range"};
+    if (p->M % p->Pr || p->N % p->Pc)
+      throw Fail{ADMM_E_PARTITION, "process grid " + std::to_string(p->Pr) + "x" + std::to_string(p->Pc) +
+                                       " does not divide the " + std::to_string(p->M) + "x" +
+                                       std::to_string(p->N) + " block grid"};
+    if (p->Pr * p->Pc > 1 && p->ragged) throw Fail{ADMM_E_PARTITION, "sharded plans need uniform blocks"};
   }
-  for (uint64_t i = 0; i < p->M; ++i) {
-    p->max_rowblock = std::max<uint32_t>(p->max_rowblock, (uint32_t)(p->rb[i + 1] - p->rb[i]));
-    for (uint64_t j = 0; j < p->N; ++j) {
-      BlockDesc b{};
+  p->Mr = p->M / p->Pr;
+  p->Nc = p->N / p->Pc;
+  p->i0 = p->pr * p->Mr;
+  p->j0 = p->pc * p->Nc;
+  uint64_t mmax = 0, nmax = 0;
+  for (uint64_t i = 0; i < p->M; ++i) mmax = std::max<uint64_t>(mmax, p->rb[i + 1] - p->rb[i]);
+  for (uint64_t j = 0; j < p->N; ++j) nmax = std::max<uint64_t>(nmax, p->cb[j + 1] - p->cb[j]);
+  p->mpad = round_up(mmax, 4);
+  p->npad = round_up(nmax, 4);
+  // Global table (worker id = i*N + j, solvers.hpp:305).  Offsets follow the exchange
+  // layouts so that all-gathers land every peer vector where the kernels look for it:
+  //   ghat:   [pc'][il][jl][mpad]  for blocks in this plan's row blocks (row comm order)
+  //   outbox: [i][jl][npad]        for blocks in this plan's column blocks (column comm order)
+  p->gblocks.assign(p->M * p->N, BlockDesc{});
+  for (uint64_t i = 0; i < p->M; ++i)
+    for (uint64_t q = 0; q < p->N; ++q) {
+      BlockDesc& b = p->gblocks[i * p->N + q];
       b.i = (uint32_t)i;
-      b.j = (uint32_t)j;
+      b.j = (uint32_t)q;
       b.rows = (uint32_t)(p->rb[i + 1] - p->rb[i]);
-      b.cols = (uint32_t)(p->cb[j + 1] - p->cb[j]);
+      b.cols = (uint32_t)(p->cb[q + 1] - p->cb[q]);
       b.row0 = (uint32_t)p->rb[i];
-      b.col0 = (uint32_t)p->cb[j];
-      b.mvec_off = (uint32_t)mv;
-      b.vec_off = (uint32_t)vv;
-      b.seg_off = (uint32_t)seg_off[j];
-      mv += round_up(b.rows, 4);
-      vv += round_up(b.cols, 4);
+      b.col0 = (uint32_t)p->cb[q];
+      const bool own_row = i >= p->i0 && i < p->i0 + p->Mr;
+      const bool own_col = q >= p->j0 && q < p->j0 + p->Nc;
+      const uint64_t il = i - p->i0, jl = q - p->j0;
+      if (own_row) b.mvec_off = (uint32_t)((((q / p->Nc) * p->Mr + il) * p->Nc + q % p->Nc) * p->mpad);
+      if (own_col) {
+        b.jl = (uint32_t)jl;
+        b.seg_off = (uint32_t)(jl * p->npad);
+        b.box_off = (uint32_t)((i * p->Nc + jl) * p->npad);
+      }
+      if (own_row && own_col) b.vec_off = (uint32_t)((il * p->Nc + jl) * p->npad);
+    }
+  for (uint64_t il = 0; il < p->Mr; ++il)
+    for (uint64_t jl = 0; jl < p->Nc; ++jl) {
+      const BlockDesc& b = p->gblocks[(p->i0 + il) * p->N + p->j0 + jl];
+      p->blocks.push_back(b);
       p->max_rows = std::max(p->max_rows, b.rows);
       p->max_m = std::max(p->max_m, b.rows);
-      p->blocks.push_back(b);
+      p->max_seg = std::max(p->max_seg, b.cols);
+      p->max_rowblock = std::max(p->max_rowblock, b.rows);
     }
-  }
-  p->mvec_total = mv;
-  p->vec_total = vv;
-  p->seg_total = sv;
+  p->mvec_total = p->Pc * p->Mr * p->Nc * p->mpad;
+  p->vec_total = p->Mr * p->Nc * p->npad;
+  p->seg_total = p->Nc * p->npad;
+  p->outbox_total = p->M * p->Nc * p->npad;
+  // a sharded plan's solve needs its peers: no per-iteration objective on the device
+  if (p->Pr * p->Pc > 1) p->trace_obj = false;
 
   int requested = o.schedule;
   if (const char* env = std::getenv("ADMM_B200_SCHEDULE")) {
@@ -829,12 +876,18 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
   }
   const size_t nb = p->blocks.size();
   upload_desc(p->dblocks, p->blocks.data(), nb * sizeof(BlockDesc));
+  upload_desc(p->dgblocks, p->gblocks.data(), p->gblocks.size() * sizeof(BlockDesc));
+  p->doutbox.alloc(p->outbox_total * 16);
+  p->dscal.alloc(p->Pr * p->Pc * 4 * sizeof(double));
   upload_desc(p->dhN, p->hN.data(), nb * sizeof(MatDesc));
   upload_desc(p->dhNv, p->hNv.data(), nb * sizeof(MatDesc));
   upload_desc(p->dkN, p->kN.data(), nb * sizeof(MatDesc));
   upload_desc(p->dhH, p->hH.data(), nb * sizeof(MatDesc));
   upload_desc(p->dhHg, p->hHg.data(), nb * sizeof(MatDesc));
   for (DevBuf* d : {&p->dghat, &p->dgij, &p->dr, &p->dq}) d->alloc(p->mvec_total * 16);
+  p->ghat_ptr = p->dghat.as<double2>();
+  p->outbox_ptr = p->doutbox.as<double2>();
+  p->scal_ptr = p->dscal.as<double>();
   for (DevBuf* d : {&p->du, &p->ds, &p->dc}) d->alloc(p->vec_total * 16);
   for (DevBuf* d : {&p->dv, &p->dvprev}) d->alloc(p->seg_total * 16);
   p->dg.alloc(p->n_meas * 16);
@@ -844,10 +897,10 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
   p->rgx = (uint32_t)cdiv(p->max_rows, kCtaThreads);
   p->zgx = (uint32_t)cdiv(p->max_seg, kCtaThreads);
   p->ogx = (uint32_t)cdiv(p->max_rowblock, kCtaThreads);
-  p->nz = p->zgx * (uint32_t)p->N;
-  p->no = p->ogx * (uint32_t)p->M;
+  p->nz = p->zgx * (uint32_t)p->Nc;
+  p->no = p->ogx * (uint32_t)p->Mr;
   p->dred.alloc((size_t)3 * std::max<uint64_t>(p->nz, p->gS.P) * sizeof(double));
-  p->dored.alloc((size_t)std::max<uint32_t>(p->no, p->zgx * (uint32_t)p->N) * sizeof(double));
+  p->dored.alloc((size_t)std::max<uint32_t>(p->no, p->zgx * (uint32_t)p->Nc) * sizeof(double));
   ensure_trace(p.get(), std::max<uint64_t>(cfg.max_iters, 1));
 
   if (p->dtype == ADMM_C128) {
@@ -920,6 +973,7 @@ admm_status admm_plan_max_abs_adjoint(admm_plan* p, double* out) {
     const int nb = (int)p->blocks.size();
     const uint32_t gx = p->zgx;
     DevBuf res;
+    if (p->Pr * p->Pc != 1) throw Fail{ADMM_E_STATE, "max_abs_adjoint: single-GPU plans only"};
     res.alloc((size_t)gx * p->N * sizeof(double));
     if (p->dtype == ADMM_C128) {
       gemv_h_kernel<double2, kVH, kEvictNormal><<<(unsigned)p->gG.P, kCtaThreads, 0, p->stream>>>(
@@ -1043,6 +1097,17 @@ admm_status admm_plan_read(admm_plan* p, int which, double* dst, uint64_t count)
         std::memcpy(dst + 2 * o, tmp.data() + 2 * (uint64_t)b.vec_off, (size_t)b.cols * 16);
         o += b.cols;
       }
+    } else if (which == 3) {  // trace of the iterations completed since reset (3 per row)
+      const IterState st = read_state(p);
+      const uint64_t n = std::min<uint64_t>(st.iter, p->trace_cap);
+      if (count < 3 * n) throw Fail{ADMM_E_DIMENSION, "destination too small"};
+      CK(cudaMemcpyAsync(dst, p->dtrace.p, n * 3 * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+      CK(cudaStreamSynchronize(p->stream));
+    } else if (which == 4) {  // {iterations completed, first non-finite iteration or -1}
+      if (count < 2) throw Fail{ADMM_E_DIMENSION, "destination too small"};
+      const IterState st = read_state(p);
+      dst[0] = (double)st.iter;
+      dst[1] = st.first_bad == ~0ull ? -1.0 : (double)st.first_bad;
     } else {
       throw Fail{ADMM_E_PARAMETER, "unknown iterate"};
     }
@@ -1140,6 +1205,146 @@ admm_status admm_plan_solve(admm_plan* p, double* solution, double* trace, uint6
       if (!p->trace_obj) trace[3 * (done - 1) + 2] = obj;
     }
     if (solution) read_segments(p, p->dv, solution);
+  });
+}
+
+}  // extern "C"
+
+// ---- multi-GPU phases (admm_b200.h) --------------------------------------------
+namespace {
+
+template <typename S>
+void enqueue_phase(admm_plan* p, int phase) {
+  cudaStream_t s = p->stream;
+  const int nb = (int)p->blocks.size();
+  if (phase == 1) {
+    if (p->schedule == 2) {
+      if (p->sweep_lpr == 8)
+        sweep_kernel<S, 8><<<(unsigned)p->gS.P, kSweepThreads, p->sweep_smem, s>>>(
+            p->dH.as<S>(), p->dhN.as<MatDesc>(), p->dblocks.as<BlockDesc>(), p->dsegs.as<SweepDesc>(),
+            (uint32_t)p->Mr, (uint32_t)p->Nc, (uint32_t)p->n_meas, p->gS.U, p->dq.as<double2>(), col_vecs(p),
+            p->dwpart_s.as<double2>(), p->dparams.as<Params>(), p->dred.as<double>(), p->dstate.as<IterState>());
+      else
+        sweep_kernel<S, 4><<<(unsigned)p->gS.P, kSweepThreads, p->sweep_smem, s>>>(
+            p->dH.as<S>(), p->dhN.as<MatDesc>(), p->dblocks.as<BlockDesc>(), p->dsegs.as<SweepDesc>(),
+            (uint32_t)p->Mr, (uint32_t)p->Nc, (uint32_t)p->n_meas, p->gS.U, p->dq.as<double2>(), col_vecs(p),
+            p->dwpart_s.as<double2>(), p->dparams.as<Params>(), p->dred.as<double>(), p->dstate.as<IterState>());
+      rows_finalize_sweep_kernel<<<dim3(p->rgx, nb), kCtaThreads, 0, s>>>(
+          row_vecs(p), p->dwpart_s.as<double2>(), p->dsegs.as<SweepDesc>(), p->dblocks.as<BlockDesc>(),
+          p->dgblocks.as<BlockDesc>(), (uint32_t)p->N, (uint32_t)p->n_meas, p->gS.U, p->gS.P, 0, 0,
+          p->dred.as<double>(), p->dparams.as<Params>(), p->dtrace.as<double>(), p->trace_cap,
+          p->dstate.as<IterState>());
+      local_scalars_kernel<<<1, kCtaThreads, 0, s>>>(p->dred.as<double>(), (uint32_t)p->gS.P,
+                                                     p->scal_ptr + 4 * (p->pr * p->Pc + p->pc),
+                                                     p->dstate.as<IterState>());
+    } else {
+      gemv_n_kernel<S, kVN, kEvictNormal><<<(unsigned)p->gN.P, kCtaThreads, 0, s>>>(
+          p->dH.as<S>(), p->dc.as<double2>(), p->dwpart.as<double2>(), p->dhN.as<MatDesc>(), nb, p->gN.U);
+      rows_finalize_kernel<kRhs><<<dim3(p->rgx, nb), kCtaThreads, 0, s>>>(
+          row_vecs(p), p->dwpart.as<double2>(), p->dhN.as<MatDesc>(), p->dblocks.as<BlockDesc>(),
+          p->dgblocks.as<BlockDesc>(), (uint32_t)p->N, p->gN.U, p->gN.P, p->dparams.as<Params>());
+    }
+    gemv_n_kernel<S, kVN, kEvictNormal><<<(unsigned)p->gK.P, kCtaThreads, 0, s>>>(
+        p->dK.as<S>(), p->dr.as<double2>(), p->dqpart.as<double2>(), p->dkN.as<MatDesc>(), nb, p->gK.U);
+    rows_finalize_kernel<kQ><<<dim3(p->rgx, nb), kCtaThreads, 0, s>>>(
+        row_vecs(p), p->dqpart.as<double2>(), p->dkN.as<MatDesc>(), p->dblocks.as<BlockDesc>(),
+        p->dgblocks.as<BlockDesc>(), (uint32_t)p->N, p->gK.U, p->gK.P, p->dparams.as<Params>());
+  } else if (phase == 2) {
+    if (p->schedule == 2) throw Fail{ADMM_E_STATE, "phase 2 belongs to the two-pass schedule"};
+    gemv_h_kernel<S, kVH, kEvictNormal><<<(unsigned)p->gH.P, kCtaThreads, 0, s>>>(
+        p->dH.as<S>(), p->dq.as<double2>(), p->dzpart.as<double2>(), p->dhH.as<MatDesc>(), nb, p->gH.U);
+    uupdate_kernel<chunk_h<S>()><<<dim3(p->zgx, nb), kCtaThreads, 0, s>>>(
+        col_vecs(p), p->outbox_ptr, p->dzpart.as<double2>(), p->dhH.as<MatDesc>(), p->dblocks.as<BlockDesc>(),
+        p->gH.U, p->gH.P, p->dstate.as<IterState>());
+  } else if (phase == 3) {
+    if (p->schedule == 2) throw Fail{ADMM_E_STATE, "phase 3 belongs to the two-pass schedule"};
+    zfinal_kernel<<<dim3(p->zgx, (unsigned)p->Nc), kCtaThreads, 0, s>>>(
+        col_vecs(p), p->outbox_ptr, p->dblocks.as<BlockDesc>(), (uint32_t)p->M, (uint32_t)p->Mr,
+        (uint32_t)p->Nc, (uint32_t)p->npad, p->pr == 0 ? 1 : 0, p->dparams.as<Params>(), p->dred.as<double>());
+    local_scalars_kernel<<<1, kCtaThreads, 0, s>>>(p->dred.as<double>(), p->nz,
+                                                   p->scal_ptr + 4 * (p->pr * p->Pc + p->pc),
+                                                   p->dstate.as<IterState>());
+  } else if (phase == 4) {
+    close_kernel<<<1, 32, 0, s>>>(p->scal_ptr, (uint32_t)(p->Pr * p->Pc), p->dparams.as<Params>(),
+                                  p->dtrace.as<double>(), p->trace_cap, p->dstate.as<IterState>());
+  } else {
+    throw Fail{ADMM_E_PARAMETER, "unknown phase"};
+  }
+  CK(cudaGetLastError());
+}
+
+}  // namespace
+
+extern "C" {
+
+admm_status admm_plan_create_sharded(const admm_plan_options* opts, const admm_solver_config* cfg, uint64_t n_meas,
+                                     uint64_t n_pix, const void* h, admm_dtype h_dtype, const double* g,
+                                     const admm_shard* shard, admm_plan** out) {
+  return run_guarded([&] {
+    if (!opts || !cfg || !out || !shard) throw Fail{ADMM_E_STATE, "null argument"};
+    *out = nullptr;
+    *out = create_plan(*opts, *cfg, n_meas, n_pix, h, h_dtype, g, false, shard);
+  });
+}
+
+admm_status admm_plan_exchange_info(const admm_plan* p, int which, uint64_t* total, uint64_t* off, uint64_t* bytes) {
+  return run_guarded([&] {
+    if (!p) throw Fail{ADMM_E_STATE, "null plan"};
+    uint64_t t = 0, o = 0, b = 0;
+    if (which == ADMM_X_GHAT) {  // [pc][Mr][Nc][mpad]
+      b = p->Mr * p->Nc * p->mpad * 16;
+      t = p->Pc * b;
+      o = p->pc * b;
+    } else if (which == ADMM_X_OUTBOX) {  // [i = pr*Mr + il][Nc][npad]
+      b = p->Mr * p->Nc * p->npad * 16;
+      t = p->Pr * b;
+      o = p->pr * b;
+    } else if (which == ADMM_X_SCAL) {  // [rank][4]
+      b = 4 * sizeof(double);
+      t = p->Pr * p->Pc * b;
+      o = (p->pr * p->Pc + p->pc) * b;
+    } else {
+      throw Fail{ADMM_E_PARAMETER, "unknown exchange buffer"};
+    }
+    if (total) *total = t;
+    if (off) *off = o;
+    if (bytes) *bytes = b;
+  });
+}
+
+admm_status admm_plan_attach(admm_plan* p, int which, void* ptr) {
+  return run_guarded([&] {
+    check_plan(p);
+    if (!ptr) throw Fail{ADMM_E_STATE, "null device pointer"};
+    if (which == ADMM_X_GHAT)
+      p->ghat_ptr = static_cast<double2*>(ptr);
+    else if (which == ADMM_X_OUTBOX)
+      p->outbox_ptr = static_cast<double2*>(ptr);
+    else if (which == ADMM_X_SCAL)
+      p->scal_ptr = static_cast<double*>(ptr);
+    else
+      throw Fail{ADMM_E_PARAMETER, "unknown exchange buffer"};
+    if (p->exec) {  // captured graphs hold the old pointers
+      cudaGraphExecDestroy(p->exec);
+      p->exec = nullptr;
+    }
+  });
+}
+
+admm_status admm_plan_run_phase(admm_plan* p, int phase) {
+  return run_guarded([&] {
+    check_plan(p);
+    if (p->dtype == ADMM_C128)
+      enqueue_phase<double2>(p, phase);
+    else
+      enqueue_phase<float2>(p, phase);
+  });
+}
+
+admm_status admm_plan_schedule(const admm_plan* p, int* schedule) {
+  return run_guarded([&] {
+    if (!p || !schedule) throw Fail{ADMM_E_STATE, "null argument"};
+    *schedule = p->schedule == 2 ? 1 : 2;
   });
 }
 

@@ -265,7 +265,8 @@ sweep_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const Bloc
 // also closes the previous sweep's iteration (trace, non-finite bookkeeping).
 __global__ void __launch_bounds__(kCtaThreads)
 rows_finalize_sweep_kernel(RowVecs rv, const double2* __restrict__ wpart, const SweepDesc* __restrict__ segs,
-                           const BlockDesc* __restrict__ blocks, uint32_t N, uint32_t n_meas, uint64_t Utot,
+                           const BlockDesc* __restrict__ blocks, const BlockDesc* __restrict__ gblocks, uint32_t N,
+                           uint32_t n_meas, uint64_t Utot,
                            uint64_t Psweep, int first, int do_finalize, const double* __restrict__ red,
                            const Params* __restrict__ prm, double* __restrict__ trace, uint64_t trace_cap,
                            IterState* st) {
@@ -276,7 +277,7 @@ rows_finalize_sweep_kernel(RowVecs rv, const double2* __restrict__ wpart, const 
   if (row < bd.rows) {
     double2 w = make_double2(0.0, 0.0);
     if (!first) {
-      const SweepDesc sd = segs[bd.j];
+      const SweepDesc sd = segs[bd.jl];
       const uint32_t ns = seg_count(sd.unit0, sd.n_strips, Utot, Psweep);
       const double2* src = wpart + sd.part_off + bd.row0 + row;
       w = src[0];
@@ -286,7 +287,7 @@ rows_finalize_sweep_kernel(RowVecs rv, const double2* __restrict__ wpart, const 
     double2 gij = rv.g[bd.row0 + row];
     for (uint32_t qj = 0; qj < N; ++qj) {
       if (qj == bd.j) continue;
-      gij = csub(gij, rv.ghat[blocks[bd.i * N + qj].mvec_off + row]);
+      gij = csub(gij, rv.ghat[gblocks[bd.i * N + qj].mvec_off + row]);  // global table: peers too
     }
     const uint32_t o = bd.mvec_off + row;
     rv.gij[o] = gij;
