@@ -277,8 +277,7 @@ void upload_desc(DevBuf& d, const void* src, size_t bytes);
 template <typename S, int LPR>
 size_t sweep_smem_bytes(const admm_plan* p) {
   constexpr int W = LPR * Store<S>::kPerVec;
-  return ((size_t)p->n_meas + (2 * (size_t)kProdWarps + 4) * p->Mr * W) * sizeof(double2) +
-         (size_t)kProdWarps * kSweepDepth * kWarp * 32;  // producer cp.async queue
+  return ((size_t)p->n_meas + (2 * (size_t)kProdWarps + 4) * p->Mr * W) * sizeof(double2);
 }
 
 // Try to configure the single-HBM-pass sweep with LPR lanes per row.  Returns false
@@ -288,7 +287,7 @@ template <typename S, int LPR>
 bool try_sweep(admm_plan* p, size_t l2_budget) {
   constexpr int W = LPR * Store<S>::kPerVec;
   const size_t smem = sweep_smem_bytes<S, LPR>(p);
-  if (smem > 225 * 1024) return false;
+  if (smem > 200 * 1024) return false;
   CK(cudaFuncSetAttribute(sweep_kernel<S, LPR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_kernel<S, LPR>, kSweepThreads, smem));

@@ -37,31 +37,6 @@ constexpr int kSweepUA = 8;  // consumer (L2 re-read): row-instructions in fligh
 __device__ __forceinline__ void nb_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void nb_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-// cp.async (LDGSTS) 16-byte copy global -> shared with an L2 eviction policy; src_bytes = 0
-// zero-fills (rows past the block edge).  Each lane later reads back only what it wrote.
-__device__ __forceinline__ uint64_t l2_policy_evict_last() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes, uint64_t pol) {
-  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;" ::"r"(dst), "l"(src),
-               "r"(src_bytes), "l"(pol)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-__device__ __forceinline__ V256 lds256(uint32_t addr) {
-  V256 r;
-  asm volatile("ld.shared.v2.b64 {%0,%1}, [%2];" : "=l"(r.w[0]), "=l"(r.w[1]) : "r"(addr));
-  asm volatile("ld.shared.v2.b64 {%0,%1}, [%2];" : "=l"(r.w[2]), "=l"(r.w[3]) : "r"(addr + 16));
-  return r;
-}
-
-constexpr int kSweepDepth = 16;              // producer prefetch queue (row-instructions per warp)
 constexpr int kSweepThreads = 512;           // 16 warps
 constexpr int kProdWarps = 8;                // (C) HBM stream
 constexpr int kConsWarps = 8;                // (D) column update + (A) L2 re-read
@@ -90,8 +65,6 @@ sweep_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const Bloc
   double2* us = zbuf + 2 * (size_t)kProdWarps * M * W;               // M x W                (consumer)
   double2* cs = us + (size_t)M * W;                                  // M x W                (consumer)
   double2* pre = cs + (size_t)M * W;                                 // 2 x M x W            (consumer)
-  unsigned char* ring_base = reinterpret_cast<unsigned char*>(pre + 2 * (size_t)M * W);  // producer queue
-  // ring_base: 8 warps x kSweepDepth x 32 lanes x 32 B = 128 KiB, 16-byte aligned
   __shared__ double sm_red[kSweepThreads / kWarp];
 
   const uint64_t P = gridDim.x, p = blockIdx.x;
@@ -111,68 +84,40 @@ sweep_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const Bloc
     SweepDesc sd = segs[j];
     if (producer) {
       // ------------------------------------------------ (C) z = H^H q per strip
-      // The warp's row-instructions over (strip x, replica i, row step t) form one
-      // stream; a 16-deep cp.async queue in SMEM runs ahead of the FMAs across block
-      // and strip boundaries, so HBM always has ~128 KiB per SM in flight.
-      const uint64_t pol = l2_policy_evict_last();
-      const uint32_t ring = (uint32_t)__cvta_generic_to_shared(ring_base) + (uint32_t)((warp * kSweepDepth * kWarp + lane) * 32);
-      // prefetch cursor (runs kSweepDepth row-instructions ahead of the consumer cursor)
-      uint64_t xp = x0;
-      uint32_t ip = 0, tp = 0, jp = j;
-      SweepDesc sdp = sd;
-      auto steps_of = [&](uint32_t rows) { return (rows + PSTEP - 1) / PSTEP; };
-      auto issue = [&](int slot) {
-        uint32_t bytes = 0;
-        const S* src = H;
-        if (xp < xe) {
-          const MatDesc md = hm[ip * N + jp];
-          const uint32_t colp = (uint32_t)(xp - sdp.unit0) * W + lc * PV;
-          const uint32_t row = warp * RPI + tp * PSTEP + lr;
-          if (row < md.rows && colp < sdp.cols) {
-            src = H + md.a_off + (uint64_t)row * md.ld + colp;
-            bytes = 16;
-          }
-          // advance the prefetch cursor
-          if (++tp == steps_of(md.rows)) {
-            tp = 0;
-            if (++ip == M) {
-              ip = 0;
-              if (++xp < xe && xp == sdp.unit0 + sdp.n_strips) sdp = segs[++jp];
-            }
-          }
-        }
-        const uint32_t dst = ring + (uint32_t)(slot * kWarp * 32);
-        cp_async16(dst, src, bytes, pol);
-        cp_async16(dst + 16, reinterpret_cast<const char*>(src) + 16, bytes, pol);
-        cp_async_commit();
-      };
-#pragma unroll 1
-      for (int d = 0; d < kSweepDepth; ++d) issue(d);
-      int slot = 0;
       uint32_t k = 0;
       for (uint64_t x = x0; x < xe; ++x, ++k) {
         if (x == sd.unit0 + sd.n_strips) sd = segs[++j];
-        const int zslot = k & 1;
+        const int slot = k & 1;
+        if (k >= 2) nb_sync(kBarEmpty0 + slot, kSweepThreads);  // consumer released the slot
         const uint32_t col = (uint32_t)(x - sd.unit0) * W + lc * PV;
-        (void)col;
+        const bool cok = col < sd.cols;
         for (uint32_t i = 0; i < M; ++i) {
           const MatDesc md = hm[i * N + j];
+          const S* hb = H + md.a_off + col;
           const double2* qb = q + blocks[i * N + j].mvec_off;
           double2 acc[PV];
 #pragma unroll
           for (int e = 0; e < PV; ++e) acc[e] = make_double2(0.0, 0.0);
-          const uint32_t T = steps_of(md.rows);
-          for (uint32_t t = 0; t < T; ++t) {
-            cp_async_wait<kSweepDepth - 1>();
-            const V256 hv = lds256(ring + (uint32_t)(slot * kWarp * 32));
-            issue(slot);  // refill the slot just consumed
-            slot = slot + 1 == kSweepDepth ? 0 : slot + 1;
-            const uint32_t row = warp * RPI + t * PSTEP + lr;
-            const double2 qv = row < md.rows ? __ldg(qb + row) : make_double2(0.0, 0.0);
+          for (uint32_t rb = warp * RPI; rb < md.rows; rb += PSTEP * kSweepU) {  // warp-uniform
+            const uint32_t r0 = rb + lr;
+            V256 hv[kSweepU];
 #pragma unroll
-            for (int e = 0; e < PV; ++e) cmac_conj(acc[e], Store<S>::get(hv, e), qv);
+            for (int u = 0; u < kSweepU; ++u) {
+              const uint32_t row = r0 + u * PSTEP;
+              if (row < md.rows && cok) {
+                hv[u] = ld_stream256<kEvictLast>(hb + (uint64_t)row * md.ld);
+              } else {
+                hv[u].w[0] = hv[u].w[1] = hv[u].w[2] = hv[u].w[3] = 0;
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < kSweepU; ++u) {
+              const uint32_t row = r0 + u * PSTEP;
+              const double2 qv = row < md.rows ? __ldg(qb + row) : make_double2(0.0, 0.0);
+#pragma unroll
+              for (int e = 0; e < PV; ++e) cmac_conj(acc[e], Store<S>::get(hv[u], e), qv);
+            }
           }
-          if (i == 0 && k >= 2) nb_sync(kBarEmpty0 + zslot, kSweepThreads);  // consumer released zbuf[zslot]
 #pragma unroll
           for (int e = 0; e < PV; ++e) {
 #pragma unroll
@@ -180,12 +125,11 @@ sweep_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const Bloc
               acc[e].x += __shfl_xor_sync(0xffffffffu, acc[e].x, o);
               acc[e].y += __shfl_xor_sync(0xffffffffu, acc[e].y, o);
             }
-            if (lr == 0) zbuf[(((size_t)zslot * kProdWarps + warp) * M + i) * W + lc * PV + e] = acc[e];
+            if (lr == 0) zbuf[(((size_t)slot * kProdWarps + warp) * M + i) * W + lc * PV + e] = acc[e];
           }
         }
-        nb_arrive(kBarFull0 + zslot, kSweepThreads);  // z of this strip is ready
+        nb_arrive(kBarFull0 + slot, kSweepThreads);  // z of this strip is ready
       }
-      cp_async_wait<0>();
       // drain: wait for the consumer's last releases so every barrier phase completes
       const uint32_t nk = k;
       for (uint32_t kk = (nk >= 2 ? nk - 2 : 0); kk < nk; ++kk) nb_sync(kBarEmpty0 + (kk & 1), kSweepThreads);
