@@ -35,13 +35,17 @@ CONFIGS = {
     # name: (method, rows, cols, k, snr, seed, kind, M, N, lambda_rel, iters, dtype)
     "1": ("consensus", 256, 2048, 16, 30.0, 1, "cg", 4, 1, 0.05, 200, "c128"),
     "2": ("sectioning", 1024, 32768, 64, 30.0, 2, "cg", 1, 8, 0.05, 300, "c128"),
-    "4s": ("consensus", 2048, 65536, 128, 30.0, 4, "cg", 8, 1, 0.05, 1000, "c64"),
+    "3": ("hybrid", 3072, 32768, 300, 30.0, 3, "cra", 2, 4, 0.03, 500, "c64"),
+    "4": ("consensus", 16384, 262144, 1000, 30.0, 4, "cg", 8, 1, 0.05, 1000, "c64"),
 }
 
 
 def describe(cfg):
     method, m, n, k, snr, seed, kind, M, N, lr, iters, dtype = cfg
     grid = f"M={M}" if method == "consensus" else f"N={N}" if method == "sectioning" else f"{M}x{N}"
+    if kind == "cra":
+        return (f"{method} ADMM {dtype} CRA-like H {m}x{n} (24 tx x 128 freq, 32^3 voxels), {k}-voxel "
+                f"planar patch, {snr:g} dB seed {seed}, {grid}, rho=1, lambda={lr}*max|H^H g|, {iters} iterations")
     return (f"{method} ADMM {dtype} H {m}x{n} CN(0,1/{m}) {k}-sparse {snr:g} dB seed {seed}, "
             f"{grid}, rho=1, lambda={lr}*max|H^H g|, {iters} iterations")
 
@@ -104,6 +108,8 @@ class ClockSampler:
 def make_problem(cfg):
     import paper_1811_05571_b200 as admm
     method, m, n, k, snr, seed, kind, M, N, lr, iters, dtype = cfg
+    if kind == "cra":  # BASELINE config 3: CRA-like structured H
+        return admm.cra_problem(seed=seed, n_vox=k, snr_db=snr, dtype=dtype)
     p = admm.gen_problem(m, n, k, snr, seed,
                          admm.ProblemKind.ComplexGaussian if kind == "cg" else admm.ProblemKind.RandomPhase,
                          dtype=dtype)

@@ -324,7 +324,7 @@ void choose_schedule(admm_plan* p, int requested) {
   p->schedule = 1;
   if (requested == 1) return;
   const size_t budget = 80ull << 20;  // open strips must stay well inside the 126 MB L2
-  if (try_sweep<S, 8>(p, budget) || try_sweep<S, 4>(p, budget)) {
+  if (try_sweep<S, 8>(p, budget) || try_sweep<S, 4>(p, budget) || try_sweep<S, 2>(p, budget)) {
     p->schedule = 2;
     return;
   }
@@ -529,6 +529,24 @@ void enqueue_sweep_prologue(admm_plan* p, cudaStream_t s) {
   CK(cudaGetLastError());
 }
 
+template <typename S, int LPR>
+void launch_sweep_lpr(admm_plan* p, cudaStream_t s) {
+  sweep_kernel<S, LPR><<<(unsigned)p->gS.P, kSweepThreads, p->sweep_smem, s>>>(
+      p->dH.as<S>(), p->dhN.as<MatDesc>(), p->dblocks.as<BlockDesc>(), p->dsegs.as<SweepDesc>(), (uint32_t)p->Mr,
+      (uint32_t)p->Nc, (uint32_t)p->n_meas, p->gS.U, p->dq.as<double2>(), col_vecs(p), p->dwpart_s.as<double2>(),
+      p->dparams.as<Params>(), p->dred.as<double>(), p->dstate.as<IterState>());
+}
+
+template <typename S>
+void launch_sweep(admm_plan* p, cudaStream_t s) {
+  if (p->sweep_lpr == 8)
+    launch_sweep_lpr<S, 8>(p, s);
+  else if (p->sweep_lpr == 4)
+    launch_sweep_lpr<S, 4>(p, s);
+  else
+    launch_sweep_lpr<S, 2>(p, s);
+}
+
 // One iteration: sweep (z, u/v/s/c, next w) -> [objective] -> r (+ close iteration) ->
 // q = K r -> ghat.
 template <typename S>
@@ -538,16 +556,7 @@ void enqueue_iteration_sweep(admm_plan* p, cudaStream_t s, bool with_objective, 
     if (ev) CK(cudaEventRecord((*ev)[k], s));
   };
   mark(0);
-  if (p->sweep_lpr == 8)
-    sweep_kernel<S, 8><<<(unsigned)p->gS.P, kSweepThreads, p->sweep_smem, s>>>(
-        p->dH.as<S>(), p->dhN.as<MatDesc>(), p->dblocks.as<BlockDesc>(), p->dsegs.as<SweepDesc>(), (uint32_t)p->Mr,
-        (uint32_t)p->Nc, (uint32_t)p->n_meas, p->gS.U, p->dq.as<double2>(), col_vecs(p), p->dwpart_s.as<double2>(),
-        p->dparams.as<Params>(), p->dred.as<double>(), p->dstate.as<IterState>());
-  else
-    sweep_kernel<S, 4><<<(unsigned)p->gS.P, kSweepThreads, p->sweep_smem, s>>>(
-        p->dH.as<S>(), p->dhN.as<MatDesc>(), p->dblocks.as<BlockDesc>(), p->dsegs.as<SweepDesc>(), (uint32_t)p->Mr,
-        (uint32_t)p->Nc, (uint32_t)p->n_meas, p->gS.U, p->dq.as<double2>(), col_vecs(p), p->dwpart_s.as<double2>(),
-        p->dparams.as<Params>(), p->dred.as<double>(), p->dstate.as<IterState>());
+  launch_sweep<S>(p, s);
   mark(1);
   if (with_objective) {
     gemv_n_kernel<S, kVN, kEvictNormal><<<(unsigned)p->gO.P, kCtaThreads, 0, s>>>(
@@ -1219,16 +1228,7 @@ void enqueue_phase(admm_plan* p, int phase) {
   const int nb = (int)p->blocks.size();
   if (phase == 1) {
     if (p->schedule == 2) {
-      if (p->sweep_lpr == 8)
-        sweep_kernel<S, 8><<<(unsigned)p->gS.P, kSweepThreads, p->sweep_smem, s>>>(
-            p->dH.as<S>(), p->dhN.as<MatDesc>(), p->dblocks.as<BlockDesc>(), p->dsegs.as<SweepDesc>(),
-            (uint32_t)p->Mr, (uint32_t)p->Nc, (uint32_t)p->n_meas, p->gS.U, p->dq.as<double2>(), col_vecs(p),
-            p->dwpart_s.as<double2>(), p->dparams.as<Params>(), p->dred.as<double>(), p->dstate.as<IterState>());
-      else
-        sweep_kernel<S, 4><<<(unsigned)p->gS.P, kSweepThreads, p->sweep_smem, s>>>(
-            p->dH.as<S>(), p->dhN.as<MatDesc>(), p->dblocks.as<BlockDesc>(), p->dsegs.as<SweepDesc>(),
-            (uint32_t)p->Mr, (uint32_t)p->Nc, (uint32_t)p->n_meas, p->gS.U, p->dq.as<double2>(), col_vecs(p),
-            p->dwpart_s.as<double2>(), p->dparams.as<Params>(), p->dred.as<double>(), p->dstate.as<IterState>());
+      launch_sweep<S>(p, s);
       rows_finalize_sweep_kernel<<<dim3(p->rgx, nb), kCtaThreads, 0, s>>>(
           row_vecs(p), p->dwpart_s.as<double2>(), p->dsegs.as<SweepDesc>(), p->dblocks.as<BlockDesc>(),
           p->dgblocks.as<BlockDesc>(), (uint32_t)p->N, (uint32_t)p->n_meas, p->gS.U, p->gS.P, 0, 0,
