@@ -324,7 +324,8 @@ void choose_schedule(admm_plan* p, int requested) {
   p->schedule = 1;
   if (requested == 1) return;
   const size_t budget = 80ull << 20;  // open strips must stay well inside the 126 MB L2
-  if (try_sweep<S, 8>(p, budget) || try_sweep<S, 4>(p, budget) || try_sweep<S, 2>(p, budget)) {
+  // 64-byte strips (LPR = 2) only on request: measured slower than two-pass on config 3
+  if (try_sweep<S, 8>(p, budget) || try_sweep<S, 4>(p, budget) || (requested == 2 && try_sweep<S, 2>(p, budget))) {
     p->schedule = 2;
     return;
   }
