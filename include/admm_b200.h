@@ -83,6 +83,9 @@ typedef struct {
                           does at solvers.hpp:146); 0: objective of the final iterate only */
   int schedule;        /* 0 auto, 1 two-pass (H streamed twice per iteration), 2 single-HBM-pass
                           column-strip sweep; env ADMM_B200_SCHEDULE overrides */
+  uint64_t batch;      /* 0/1: one scene; 2..64: independent scenes sharing H (BASELINE config 5):
+                          g is n_meas x batch (scene fastest), solutions n_pix x batch, trace
+                          iterations x batch x 3, lambda per scene via admm_plan_set_lambdas */
 } admm_plan_options;
 
 typedef struct admm_plan admm_plan;
@@ -139,6 +142,10 @@ admm_status admm_plan_schedule(const admm_plan* plan, int* schedule);
 
 /* Replace the measurement vector g (H, the partition and the factors are kept). */
 admm_status admm_plan_set_g(admm_plan* plan, const double* g);
+/* Per-scene lambdas of a batched plan (batch values). */
+admm_status admm_plan_set_lambdas(admm_plan* plan, const double* lambdas);
+/* Per-scene max_t |(H^H g_b)_t| of a batched plan (batch values). */
+admm_status admm_plan_max_abs_adjoint_batched(admm_plan* plan, double* out);
 /* Replace lambda (kappa follows). */
 admm_status admm_plan_set_lambda(admm_plan* plan, double lambda);
 /* max_t |(H^H g)_t| of the (scaled) problem, computed on the device; used for the

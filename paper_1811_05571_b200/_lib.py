@@ -27,7 +27,7 @@ class SolverConfigC(ctypes.Structure):
 
 class PlanOptionsC(ctypes.Structure):
     _fields_ = [("method", _i32), ("M", _u64), ("N", _u64), ("ragged", _i32), ("dtype", _i32),
-                ("device", _i32), ("trace_objective", _i32), ("schedule", _i32)]
+                ("device", _i32), ("trace_objective", _i32), ("schedule", _i32), ("batch", _u64)]
 
 
 class SnapshotC(ctypes.Structure):
@@ -68,6 +68,8 @@ _SIGS = {
     "admm_plan_schedule": ([_ptr, ctypes.POINTER(_i32)], _i32),
     "admm_plan_set_g": ([_ptr, _ptr], _i32),
     "admm_plan_set_lambda": ([_ptr, _dbl], _i32),
+    "admm_plan_set_lambdas": ([_ptr, _ptr], _i32),
+    "admm_plan_max_abs_adjoint_batched": ([_ptr, _ptr], _i32),
     "admm_plan_max_abs_adjoint": ([_ptr, ctypes.POINTER(_dbl)], _i32),
     "admm_plan_solve": ([_ptr, _ptr, _ptr, ctypes.POINTER(_u64), ctypes.POINTER(_dbl), OBSERVER,
                          _ptr], _i32),

@@ -24,6 +24,7 @@
 #include "admm_kernels.cuh"
 #include "admm_setup.cuh"
 #include "admm_sweep.cuh"
+#include "admm_batched.cuh"
 
 using namespace admm;
 
@@ -146,6 +147,12 @@ struct admm_plan {
   DevBuf dwpart, dqpart, dzpart, dopart, dgpart;
   DevBuf dred, dored, dtrace, dstate, dparams, dblocks, dhN, dhNv, dkN, dhH, dhHg, dgram, dobj;
   Geom gN, gK, gH, gO, gG;
+  // batched scenes (admm_batched.cuh): B right-hand sides sharing H and the factors
+  uint64_t batch = 1;
+  std::vector<BTile> tN, tK, tH, tG;
+  DevBuf dtN, dtK, dtH, dtG, dz, dkappa, dbred;
+  uint32_t splitN = 1, splitK = 1, pz = 1;
+  std::vector<double> lambdas;
   // sweep schedule (admm_sweep.cuh)
   int schedule = 1;             // 1 two-pass, 2 single-HBM-pass sweep
   int sweep_lpr = 8;
@@ -587,7 +594,105 @@ void enqueue_iteration_sweep(admm_plan* p, cudaStream_t s, bool with_objective, 
   CK(cudaGetLastError());
 }
 
+// ---- batched scenes (config 5) ----------------------------------------------------
+void build_batched(admm_plan* p) {
+  const uint64_t B = p->batch;
+  const uint64_t nb = p->blocks.size();
+  uint64_t rtiles = 0;
+  for (auto& b : p->blocks) rtiles += cdiv(b.rows, kBT);
+  const uint64_t target = 4ull * p->num_sms;  // split-K until the N-GEMMs have ~4 waves
+  p->splitN = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(16, cdiv(target, rtiles)));
+  p->splitK = p->splitN;
+  const uint64_t stride = p->mvec_total * B;
+  p->tN.clear();
+  p->tK.clear();
+  p->tH.clear();
+  p->tG.clear();
+  for (uint64_t b = 0; b < nb; ++b) {
+    const BlockDesc& bd = p->blocks[b];
+    const MatDesc& hn = p->hN[b];
+    const MatDesc& kn = p->kN[b];
+    const uint32_t kcN = (uint32_t)round_up(cdiv(bd.cols, p->splitN), kBK);
+    const uint32_t kcK = (uint32_t)round_up(cdiv(bd.rows, p->splitK), kBK);
+    for (uint32_t t0 = 0; t0 < bd.rows; t0 += kBT)
+      for (uint32_t sp = 0; sp < p->splitN; ++sp) {
+        BTile t{hn.a_off, (uint64_t)bd.vec_off * B, sp * stride + (uint64_t)bd.mvec_off * B, hn.ld, bd.rows,
+                bd.cols, t0, std::min(bd.cols, sp * kcN), std::min(bd.cols, (sp + 1) * kcN)};
+        p->tN.push_back(t);
+      }
+    for (uint32_t t0 = 0; t0 < bd.rows; t0 += kBT)
+      for (uint32_t sp = 0; sp < p->splitK; ++sp) {
+        BTile t{kn.a_off, (uint64_t)bd.mvec_off * B, sp * stride + (uint64_t)bd.mvec_off * B, kn.ld, bd.rows,
+                bd.rows, t0, std::min(bd.rows, sp * kcK), std::min(bd.rows, (sp + 1) * kcK)};
+        p->tK.push_back(t);
+      }
+    for (uint32_t t0 = 0; t0 < bd.cols; t0 += kBT) {
+      p->tH.push_back(BTile{hn.a_off, (uint64_t)bd.mvec_off * B, (uint64_t)bd.vec_off * B, hn.ld, bd.rows,
+                            bd.cols, t0, 0, bd.rows});
+      p->tG.push_back(BTile{hn.a_off, (uint64_t)bd.row0 * B, (uint64_t)bd.vec_off * B, hn.ld, bd.rows, bd.cols, t0,
+                            0, bd.rows});
+    }
+  }
+  upload_desc(p->dtN, p->tN.data(), p->tN.size() * sizeof(BTile));
+  upload_desc(p->dtK, p->tK.data(), p->tK.size() * sizeof(BTile));
+  upload_desc(p->dtH, p->tH.data(), p->tH.size() * sizeof(BTile));
+  upload_desc(p->dtG, p->tG.data(), p->tG.size() * sizeof(BTile));
+  p->dwpart.alloc((size_t)p->splitN * stride * 16);
+  p->dqpart.alloc((size_t)p->splitK * stride * 16);
+  p->dz.alloc(p->vec_total * B * 16);
+  p->dkappa.alloc(B * sizeof(double));
+  p->pz = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(4ull * p->num_sms, cdiv(p->max_seg, 4)));
+  p->dbred.alloc((size_t)3 * p->pz * kBB * sizeof(double));
+}
+
+BRowVecs brow_vecs(admm_plan* p) {
+  return BRowVecs{p->dg.as<double2>(), p->ghat_ptr, p->dgij.as<double2>(), p->dr.as<double2>(), p->dq.as<double2>()};
+}
+
+template <typename S>
+void enqueue_iteration_batched(admm_plan* p, cudaStream_t s, std::vector<cudaEvent_t>* ev) {
+  const uint32_t B = (uint32_t)p->batch, nb = (uint32_t)p->blocks.size();
+  const uint64_t stride = p->mvec_total * B;
+  const unsigned rgx = (unsigned)cdiv((uint64_t)p->max_rows * B, kCtaThreads);
+  auto mark = [&](size_t k) {
+    if (ev) CK(cudaEventRecord((*ev)[k], s));
+  };
+  mark(0);
+  bgemm_kernel<S, false><<<(unsigned)p->tN.size(), 256, 0, s>>>(p->dH.as<S>(), p->dtN.as<BTile>(),
+                                                                  p->dc.as<double2>(), p->dwpart.as<double2>(), B);
+  mark(1);
+  brows_kernel<kRhs><<<dim3(rgx, nb), kCtaThreads, 0, s>>>(brow_vecs(p), p->dwpart.as<double2>(), stride, p->splitN,
+                                                          p->dblocks.as<BlockDesc>(), (uint32_t)p->Nc, B,
+                                                          p->dparams.as<Params>());
+  mark(2);
+  bgemm_kernel<S, false><<<(unsigned)p->tK.size(), 256, 0, s>>>(p->dK.as<S>(), p->dtK.as<BTile>(),
+                                                                  p->dr.as<double2>(), p->dqpart.as<double2>(), B);
+  mark(3);
+  brows_kernel<kQ><<<dim3(rgx, nb), kCtaThreads, 0, s>>>(brow_vecs(p), p->dqpart.as<double2>(), stride, p->splitK,
+                                                        p->dblocks.as<BlockDesc>(), (uint32_t)p->Nc, B,
+                                                        p->dparams.as<Params>());
+  mark(4);
+  bgemm_kernel<S, true><<<(unsigned)p->tH.size(), 256, 0, s>>>(p->dH.as<S>(), p->dtH.as<BTile>(), p->dq.as<double2>(),
+                                                                 p->dz.as<double2>(), B);
+  mark(5);
+  bzupdate_kernel<<<p->pz, kCtaThreads, 0, s>>>(col_vecs(p), p->dz.as<double2>(), p->dblocks.as<BlockDesc>(),
+                                                (uint32_t)p->Mr, (uint32_t)p->Nc, B, p->dkappa.as<double>(),
+                                                p->dbred.as<double>(), p->dstate.as<IterState>());
+  mark(6);
+  bfinalize_kernel<<<1, kBB, 0, s>>>(p->dbred.as<double>(), p->pz, B, p->dparams.as<Params>(), p->dtrace.as<double>(),
+                                     p->trace_cap, p->dstate.as<IterState>());
+  mark(7);
+  CK(cudaGetLastError());
+}
+
 void enqueue_iteration_any(admm_plan* p, cudaStream_t s, bool obj, std::vector<cudaEvent_t>* ev) {
+  if (p->batch > 1) {
+    if (p->dtype == ADMM_C128)
+      enqueue_iteration_batched<double2>(p, s, ev);
+    else
+      enqueue_iteration_batched<float2>(p, s, ev);
+    return;
+  }
   if (p->schedule == 2) {
     if (p->dtype == ADMM_C128)
       enqueue_iteration_sweep<double2>(p, s, obj, ev);
@@ -663,12 +768,19 @@ void set_params(admm_plan* p) {
                         ? p->cfg.lambda / (m * p->cfg.rho)
                         : p->cfg.lambda / p->cfg.rho;
   CK(cudaMemcpyAsync(p->dparams.p, &p->params, sizeof(Params), cudaMemcpyHostToDevice, p->stream));
+  if (p->batch > 1) {  // per-scene kappa_b (same rule, lambda_b per scene)
+    if (p->lambdas.size() != p->batch) p->lambdas.assign(p->batch, p->cfg.lambda);
+    std::vector<double> k(p->batch);
+    for (uint64_t b = 0; b < p->batch; ++b) k[b] = p->params.kappa * (p->lambdas[b] / p->cfg.lambda);
+    CK(cudaMemcpyAsync(p->dkappa.p, k.data(), k.size() * 8, cudaMemcpyHostToDevice, p->stream));
+    CK(cudaStreamSynchronize(p->stream));
+  }
 }
 
 void upload_g(admm_plan* p, const double* g) {
-  CK(cudaMemcpyAsync(p->dg.p, g, p->n_meas * 16, cudaMemcpyHostToDevice, p->stream));
+  CK(cudaMemcpyAsync(p->dg.p, g, p->n_meas * p->batch * 16, cudaMemcpyHostToDevice, p->stream));
   if (p->cfg.scl != 1.0) {
-    scale_vec_kernel<<<64, 256, 0, p->stream>>>(p->dg.as<double2>(), p->n_meas, p->cfg.scl);
+    scale_vec_kernel<<<64, 256, 0, p->stream>>>(p->dg.as<double2>(), p->n_meas * p->batch, p->cfg.scl);
     CK(cudaGetLastError());
   }
 }
@@ -677,7 +789,7 @@ void reset_state(admm_plan* p) {
   cudaStream_t s = p->stream;
   for (DevBuf* d : {&p->du, &p->ds, &p->dc, &p->dv, &p->dvprev, &p->dgij, &p->dr, &p->dq})
     CK(cudaMemsetAsync(d->p, 0, d->bytes, s));
-  CK(cudaMemsetAsync(p->ghat_ptr, 0, p->mvec_total * 16, s));
+  CK(cudaMemsetAsync(p->ghat_ptr, 0, p->mvec_total * 16 * p->batch, s));
   CK(cudaMemsetAsync(p->outbox_ptr, 0, p->outbox_total * 16, s));
   IterState st{0, ~0ull, 0u, 0u};
   CK(cudaMemcpyAsync(p->dstate.p, &st, sizeof(st), cudaMemcpyHostToDevice, s));
@@ -692,7 +804,7 @@ void reset_state(admm_plan* p) {
 void ensure_trace(admm_plan* p, uint64_t iters) {
   if (iters <= p->trace_cap) return;
   p->trace_cap = std::max<uint64_t>(iters, 64);
-  p->dtrace.alloc(p->trace_cap * 3 * sizeof(double));
+  p->dtrace.alloc(p->trace_cap * 3 * p->batch * sizeof(double));
   if (p->exec) {  // the graph captured the old trace pointer
     cudaGraphExecDestroy(p->exec);
     p->exec = nullptr;
@@ -735,12 +847,13 @@ IterState read_state(admm_plan* p) {
 }
 
 void read_segments(admm_plan* p, const DevBuf& src, double* dst) {
-  p->h_seg.resize(p->seg_total * 2);
-  CK(cudaMemcpyAsync(p->h_seg.data(), src.p, p->seg_total * 16, cudaMemcpyDeviceToHost, p->stream));
+  const uint64_t B = p->batch;  // rows of B scenes
+  p->h_seg.resize(p->seg_total * 2 * B);
+  CK(cudaMemcpyAsync(p->h_seg.data(), src.p, p->seg_total * 16 * B, cudaMemcpyDeviceToHost, p->stream));
   CK(cudaStreamSynchronize(p->stream));
   for (uint64_t j = 0; j < p->Nc; ++j) {  // local segments (all of them on a single GPU)
     const BlockDesc& b = p->blocks[j];
-    std::memcpy(dst + 2 * b.col0, p->h_seg.data() + 2 * (uint64_t)b.seg_off, (size_t)b.cols * 16);
+    std::memcpy(dst + 2 * (uint64_t)b.col0 * B, p->h_seg.data() + 2 * (uint64_t)b.seg_off * B, (size_t)b.cols * 16 * B);
   }
 }
 
@@ -779,7 +892,8 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
   const bool hfin = h_dtype == ADMM_C128
                         ? host_all_finite(static_cast<const double*>(h), 2 * n_meas * n_pix)
                         : host_all_finite(static_cast<const float*>(h), 2 * n_meas * n_pix);
-  if (!hfin || !host_all_finite(g, 2 * n_meas)) throw Fail{ADMM_E_NUMERICAL, "SensingProblem: non-finite entries"};
+  if (!hfin || !host_all_finite(g, 2 * n_meas * std::max<uint64_t>(1, o.batch)))
+    throw Fail{ADMM_E_NUMERICAL, "SensingProblem: non-finite entries"};
   if (o.method < ADMM_REFERENCE || o.method > ADMM_HYBRID) throw Fail{ADMM_E_PARAMETER, "unknown method"};
   if (o.dtype != ADMM_C128 && o.dtype != ADMM_C64) throw Fail{ADMM_E_PARAMETER, "unknown dtype"};
 
@@ -795,6 +909,12 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
   p->M = (o.method == ADMM_CONSENSUS || o.method == ADMM_HYBRID) ? o.M : 1;
   p->N = (o.method == ADMM_SECTIONING || o.method == ADMM_HYBRID) ? o.N : 1;
   p->elem = o.dtype == ADMM_C128 ? 16 : 8;
+  p->batch = std::max<uint64_t>(1, o.batch);
+  if (p->batch > kBB) throw Fail{ADMM_E_PARAMETER, "batch larger than 64 scenes"};
+  if (p->batch > 1 && shard && shard->Pr * shard->Pc > 1)
+    throw Fail{ADMM_E_PARAMETER, "batched scenes run on a single GPU"};
+  if (p->batch > 1 && (cfg.eps_pri != 0.0 || cfg.eps_dual != 0.0))
+    throw Fail{ADMM_E_PARAMETER, "batched scenes run a fixed iteration count (eps = 0)"};
   // make_partition (partition.hpp:56-65): rows then columns
   p->rb = split_bounds(n_meas, p->M, p->ragged, "row");
   p->cb = split_bounds(n_pix, p->N, p->ragged, "column");
@@ -876,7 +996,7 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
     if (!std::strcmp(env, "twopass")) requested = 1;
     if (!std::strcmp(env, "sweep")) requested = 2;
   }
-  if (skip_cfg_validation) requested = 1;  // single-block L0/L1 helper plans
+  if (skip_cfg_validation || o.batch > 1) requested = 1;  // helper plans / batched scenes
   if (p->dtype == ADMM_C128) {
     build_geometry<double2>(p.get());
     choose_schedule<double2>(p.get(), requested);
@@ -894,13 +1014,13 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
   upload_desc(p->dkN, p->kN.data(), nb * sizeof(MatDesc));
   upload_desc(p->dhH, p->hH.data(), nb * sizeof(MatDesc));
   upload_desc(p->dhHg, p->hHg.data(), nb * sizeof(MatDesc));
-  for (DevBuf* d : {&p->dghat, &p->dgij, &p->dr, &p->dq}) d->alloc(p->mvec_total * 16);
+  for (DevBuf* d : {&p->dghat, &p->dgij, &p->dr, &p->dq}) d->alloc(p->mvec_total * 16 * p->batch);
   p->ghat_ptr = p->dghat.as<double2>();
   p->outbox_ptr = p->doutbox.as<double2>();
   p->scal_ptr = p->dscal.as<double>();
-  for (DevBuf* d : {&p->du, &p->ds, &p->dc}) d->alloc(p->vec_total * 16);
-  for (DevBuf* d : {&p->dv, &p->dvprev}) d->alloc(p->seg_total * 16);
-  p->dg.alloc(p->n_meas * 16);
+  for (DevBuf* d : {&p->du, &p->ds, &p->dc}) d->alloc(p->vec_total * 16 * p->batch);
+  for (DevBuf* d : {&p->dv, &p->dvprev}) d->alloc(p->seg_total * 16 * p->batch);
+  p->dg.alloc(p->n_meas * 16 * p->batch);
   p->dparams.alloc(sizeof(Params));
   p->dstate.alloc(sizeof(IterState));
   p->dobj.alloc(sizeof(double));
@@ -919,6 +1039,10 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
   } else {
     upload_h<float2>(p.get(), h, h_dtype);
     factor_blocks<float2>(p.get());
+  }
+  if (p->batch > 1) {
+    build_batched(p.get());
+    p->schedule = 3;
   }
   upload_g(p.get(), g);
   set_params(p.get());
@@ -963,7 +1087,8 @@ admm_status admm_plan_set_g(admm_plan* p, const double* g) {
   return run_guarded([&] {
     check_plan(p);
     if (!g) throw Fail{ADMM_E_STATE, "null g"};
-    if (!host_all_finite(g, 2 * p->n_meas)) throw Fail{ADMM_E_NUMERICAL, "SensingProblem: non-finite entries"};
+    if (!host_all_finite(g, 2 * p->n_meas * p->batch))
+      throw Fail{ADMM_E_NUMERICAL, "SensingProblem: non-finite entries"};
     upload_g(p, g);
   });
 }
@@ -1033,14 +1158,56 @@ void* admm_plan_stream(admm_plan* p) { return p ? (void*)p->stream : nullptr; }
 
 uint32_t admm_plan_kernel_count(const admm_plan* p) { return p && p->schedule == 2 ? 4 : 7; }
 
+admm_status admm_plan_set_lambdas(admm_plan* p, const double* lambdas) {
+  return run_guarded([&] {
+    check_plan(p);
+    if (p->batch < 2) throw Fail{ADMM_E_STATE, "set_lambdas: not a batched plan"};
+    if (!lambdas) throw Fail{ADMM_E_STATE, "null lambdas"};
+    for (uint64_t b = 0; b < p->batch; ++b)
+      if (!(lambdas[b] > 0.0)) throw Fail{ADMM_E_PARAMETER, "SolverConfig: lambda must be positive"};
+    p->lambdas.assign(lambdas, lambdas + p->batch);
+    set_params(p);
+  });
+}
+
+admm_status admm_plan_max_abs_adjoint_batched(admm_plan* p, double* out) {
+  return run_guarded([&] {
+    check_plan(p);
+    if (p->batch < 2) throw Fail{ADMM_E_STATE, "not a batched plan"};
+    const uint32_t B = (uint32_t)p->batch;
+    if (p->dtype == ADMM_C128)
+      bgemm_kernel<double2, true><<<(unsigned)p->tG.size(), 256, 0, p->stream>>>(
+          p->dH.as<double2>(), p->dtG.as<BTile>(), p->dg.as<double2>(), p->dz.as<double2>(), B);
+    else
+      bgemm_kernel<float2, true><<<(unsigned)p->tG.size(), 256, 0, p->stream>>>(
+          p->dH.as<float2>(), p->dtG.as<BTile>(), p->dg.as<double2>(), p->dz.as<double2>(), B);
+    const unsigned gx = p->pz;
+    DevBuf res;
+    res.alloc((size_t)gx * kBB * sizeof(double));
+    babsmax_kernel<<<gx, kCtaThreads, 0, p->stream>>>(p->dz.as<double2>(), p->dblocks.as<BlockDesc>(),
+                                                      (uint32_t)p->Mr, (uint32_t)p->Nc, B, res.as<double>());
+    CK(cudaGetLastError());
+    std::vector<double> h((size_t)gx * kBB);
+    CK(cudaMemcpyAsync(h.data(), res.p, h.size() * 8, cudaMemcpyDeviceToHost, p->stream));
+    CK(cudaStreamSynchronize(p->stream));
+    for (uint32_t b = 0; b < B; ++b) {
+      double m = 0.0;
+      for (unsigned c = 0; c < gx; ++c) m = std::max(m, h[(size_t)c * kBB + b]);
+      out[b] = m;
+    }
+  });
+}
+
 admm_status admm_plan_profile(admm_plan* p, uint64_t iters, const char** names, double* ms) {
   static const char* kNames2[7] = {"gemv_n(H,c)", "rows_finalize(rhs)", "gemv_n(K,r)", "rows_finalize(q)",
                                    "gemv_h(H,q)", "zupdate", "finalize"};
   static const char* kNamesS[4] = {"sweep(H)", "rows_finalize(rhs)+finalize", "gemv_n(K,r)", "rows_finalize(q)"};
+  static const char* kNamesB[7] = {"bgemm(H,C)", "brows(rhs)", "bgemm(K,R)", "brows(q)", "bgemm_adj(H,Q)",
+                                   "bzupdate", "bfinalize"};
   return run_guarded([&] {
     check_plan(p);
     const int nk = (int)admm_plan_kernel_count(p);
-    const char* const* kn = p->schedule == 2 ? kNamesS : kNames2;
+    const char* const* kn = p->schedule == 2 ? kNamesS : p->schedule == 3 ? kNamesB : kNames2;
     std::vector<cudaEvent_t> ev(nk + 1);
     for (auto& e : ev) CK(cudaEventCreate(&e));
     std::vector<double> acc(nk, 0.0);
@@ -1076,7 +1243,7 @@ admm_status admm_plan_get_info(const admm_plan* p, admm_plan_info* info) {
     r.k_bytes = kb;
     r.h_stream_bytes_per_iter = 2 * hb;
     r.bytes_per_iter = 2 * hb + kb + vb;  // two-pass algorithmic bytes
-    r.launches_per_iter = p->schedule == 2 ? (p->trace_obj ? 7 : 4) : (p->trace_obj ? 9 : 7);
+    r.launches_per_iter = p->schedule == 3 ? 7 : p->schedule == 2 ? (p->trace_obj ? 7 : 4) : (p->trace_obj ? 9 : 7);
     r.schedule = (uint64_t)p->schedule;
     r.grid_sweep = p->gS.P;
     r.hbm_bytes_per_iter = (p->schedule == 2 ? hb : 2 * hb) + kb + vb;
@@ -1093,7 +1260,7 @@ admm_status admm_plan_read(admm_plan* p, int which, double* dst, uint64_t count)
     check_plan(p);
     if (!dst) throw Fail{ADMM_E_STATE, "null destination"};
     if (which == 0 || which == 1) {
-      if (count < p->n_pix) throw Fail{ADMM_E_DIMENSION, "destination too small"};
+      if (count < p->n_pix * p->batch) throw Fail{ADMM_E_DIMENSION, "destination too small"};
       read_segments(p, which == 0 ? p->dv : p->dvprev, dst);
     } else if (which == 2) {
       uint64_t tot = 0;
@@ -1132,6 +1299,7 @@ admm_status admm_plan_solve(admm_plan* p, double* solution, double* trace, uint6
     ensure_trace(p, iters);
     reset_state(p);
     const bool stepping = observer || p->cfg.eps_pri != 0.0 || p->cfg.eps_dual != 0.0;
+    if (p->batch > 1 && observer) throw Fail{ADMM_E_PARAMETER, "batched scenes: no observer"};
     uint64_t done = 0;
     if (!stepping) {
       enqueue_iters(p, iters);
@@ -1197,6 +1365,17 @@ admm_status admm_plan_solve(admm_plan* p, double* solution, double* trace, uint6
     }
     if (iterations_run) *iterations_run = done;
     double obj = 0.0;
+    if (p->batch > 1) {  // per-scene objective is not computed for batched plans
+      obj = std::numeric_limits<double>::quiet_NaN();
+      if (objective) *objective = obj;
+      if (trace) {
+        CK(cudaMemcpyAsync(trace, p->dtrace.p, done * 3 * p->batch * sizeof(double), cudaMemcpyDeviceToHost,
+                           p->stream));
+        CK(cudaStreamSynchronize(p->stream));
+      }
+      if (solution) read_segments(p, p->dv, solution);
+      return;
+    }
     if (p->trace_obj) {
       CK(cudaMemcpyAsync(&obj, p->dtrace.as<double>() + 3 * (done - 1) + 2, 8, cudaMemcpyDeviceToHost, p->stream));
       CK(cudaStreamSynchronize(p->stream));

@@ -81,8 +81,8 @@ class SensingProblem:
     def validate(self) -> None:
         if self.h.ndim != 2 or self.h.size == 0:
             raise DimensionError("SensingProblem: empty sensing matrix")
-        if self.g.shape != (self.h.shape[0],):
-            raise DimensionError(f"SensingProblem: g length {self.g.size} != H rows {self.h.shape[0]}")
+        if self.g.shape[0] != self.h.shape[0] or self.g.ndim not in (1, 2):
+            raise DimensionError(f"SensingProblem: g length {self.g.shape[0]} != H rows {self.h.shape[0]}")
         if self.truth is not None and self.truth.shape != (self.h.shape[1],):
             raise DimensionError(f"SensingProblem: truth length {self.truth.size} != H cols "
                                  f"{self.h.shape[1]}")
@@ -234,6 +234,7 @@ class AdmmPlan:
             h_dtype = 0
             h = _as_c128(h)
         g = _as_c128(problem.g)
+        self.batch = int(g.shape[1]) if g.ndim == 2 else 1  # scenes (BASELINE config 5)
         self.method = method
         self.n_meas, self.n_pix = h.shape
         self.M = M if method in ("consensus", "hybrid") else 1
@@ -242,7 +243,7 @@ class AdmmPlan:
         self.opts = opts
         o = _lib.PlanOptionsC(_METHOD[method], self.M, self.N, int(opts.ragged),
                               _DTYPE[opts.dtype], int(opts.device), int(opts.trace_objective),
-                              {"auto": 0, "twopass": 1, "sweep": 2}[opts.schedule])
+                              {"auto": 0, "twopass": 1, "sweep": 2}[opts.schedule], self.batch)
         c = self.cfg._c()
         handle = ctypes.c_void_p()
         check(_lib.lib.admm_plan_create(ctypes.byref(o), ctypes.byref(c), self.n_meas, self.n_pix,
@@ -269,13 +270,25 @@ class AdmmPlan:
     # -- configuration -------------------------------------------------------------
     def set_g(self, g: np.ndarray) -> None:
         g = _as_c128(g)
-        if g.shape != (self.n_meas,):
+        if g.shape != ((self.n_meas,) if self.batch == 1 else (self.n_meas, self.batch)):
             raise DimensionError("set_g: length mismatch")
         check(_lib.lib.admm_plan_set_g(self._h, _ptr(g)))
 
     def set_lambda(self, lam: float) -> None:
         check(_lib.lib.admm_plan_set_lambda(self._h, float(lam)))
         self.cfg.lambda_ = float(lam)
+
+    def set_lambdas(self, lams) -> None:
+        """Per-scene lambda_b of a batched plan."""
+        lams = np.ascontiguousarray(lams, dtype=np.float64)
+        if lams.shape != (self.batch,):
+            raise DimensionError("set_lambdas: one lambda per scene")
+        check(_lib.lib.admm_plan_set_lambdas(self._h, _ptr(lams)))
+
+    def max_abs_adjoint_batched(self) -> np.ndarray:
+        out = np.zeros(self.batch)
+        check(_lib.lib.admm_plan_max_abs_adjoint_batched(self._h, _ptr(out)))
+        return out
 
     def max_abs_adjoint(self) -> float:
         out = ctypes.c_double()
@@ -290,8 +303,9 @@ class AdmmPlan:
     # -- running -------------------------------------------------------------------
     def solve(self, observer: Optional[IterateObserver] = None) -> SolveReport:
         iters = int(self.cfg.max_iters)
-        sol = np.zeros(self.n_pix, np.complex128)
-        trace = np.zeros((iters, 3), np.float64)
+        B = self.batch
+        sol = np.zeros(self.n_pix * B, np.complex128)
+        trace = np.zeros((iters, 3 * B), np.float64)
         it = ctypes.c_uint64()
         obj = ctypes.c_double()
         cb = _lib.OBSERVER()
@@ -316,8 +330,13 @@ class AdmmPlan:
         check(_lib.lib.admm_plan_solve(self._h, _ptr(sol), _ptr(trace), ctypes.byref(it),
                                        ctypes.byref(obj), cb, None))
         k = int(it.value)
-        tr = trace[:k]
         ledger = CommLedger.for_solve(self.method, self.spec.row_bounds, self.spec.col_bounds, k)
+        if B > 1:  # solution (n_pix, B), trace columns (iterations, B)
+            tr = trace[:k].reshape(k, B, 3)
+            return SolveReport(sol.reshape(self.n_pix, B), ResidualTrace(tr[:, :, 0].copy(), tr[:, :, 1].copy(),
+                                                                         tr[:, :, 2].copy()), ledger, k,
+                               float(obj.value))
+        tr = trace[:k, :3]
         return SolveReport(sol, ResidualTrace(tr[:, 0].copy(), tr[:, 1].copy(), tr[:, 2].copy()),
                            ledger, k, float(obj.value))
 
