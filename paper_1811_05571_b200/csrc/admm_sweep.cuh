@@ -98,24 +98,36 @@ sweep_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const Bloc
           double2 acc[PV];
 #pragma unroll
           for (int e = 0; e < PV; ++e) acc[e] = make_double2(0.0, 0.0);
-          for (uint32_t rb = warp * RPI; rb < md.rows; rb += PSTEP * kSweepU) {  // warp-uniform
-            const uint32_t r0 = rb + lr;
-            V256 hv[kSweepU];
+          // rolling register pipeline: slot u is consumed and immediately refilled with
+          // the row-instruction kSweepU steps ahead, so ~kSweepU loads stay in flight
+          const uint32_t r0 = warp * RPI + lr;
+          const uint32_t T = (md.rows + PSTEP - 1) / PSTEP;  // warp-uniform step count
+          V256 hv[kSweepU];
 #pragma unroll
-            for (int u = 0; u < kSweepU; ++u) {
-              const uint32_t row = r0 + u * PSTEP;
-              if (row < md.rows && cok) {
-                hv[u] = ld_stream256<kEvictLast>(hb + (uint64_t)row * md.ld);
-              } else {
-                hv[u].w[0] = hv[u].w[1] = hv[u].w[2] = hv[u].w[3] = 0;
-              }
+          for (int u = 0; u < kSweepU; ++u) {
+            const uint32_t row = r0 + u * PSTEP;
+            if ((uint32_t)u < T && row < md.rows && cok) {
+              hv[u] = ld_stream256<kEvictLast>(hb + (uint64_t)row * md.ld);
+            } else {
+              hv[u].w[0] = hv[u].w[1] = hv[u].w[2] = hv[u].w[3] = 0;
             }
+          }
+          for (uint32_t tb = 0; tb < T; tb += kSweepU) {
 #pragma unroll
             for (int u = 0; u < kSweepU; ++u) {
-              const uint32_t row = r0 + u * PSTEP;
-              const double2 qv = row < md.rows ? __ldg(qb + row) : make_double2(0.0, 0.0);
+              const uint32_t t = tb + u;
+              if (t < T) {
+                const uint32_t row = r0 + t * PSTEP;
+                const double2 qv = row < md.rows ? __ldg(qb + row) : make_double2(0.0, 0.0);
 #pragma unroll
-              for (int e = 0; e < PV; ++e) cmac_conj(acc[e], Store<S>::get(hv[u], e), qv);
+                for (int e = 0; e < PV; ++e) cmac_conj(acc[e], Store<S>::get(hv[u], e), qv);
+                const uint32_t rown = row + kSweepU * PSTEP;
+                if (t + kSweepU < T && rown < md.rows && cok) {
+                  hv[u] = ld_stream256<kEvictLast>(hb + (uint64_t)rown * md.ld);
+                } else {
+                  hv[u].w[0] = hv[u].w[1] = hv[u].w[2] = hv[u].w[3] = 0;
+                }
+              }
             }
           }
 #pragma unroll
