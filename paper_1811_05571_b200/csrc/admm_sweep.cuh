@@ -98,39 +98,25 @@ sweep_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const Bloc
           double2 acc[PV];
 #pragma unroll
           for (int e = 0; e < PV; ++e) acc[e] = make_double2(0.0, 0.0);
-          // two groups of kG loads double-buffered: group A is consumed while group B is in
-          // flight, then refilled (whole-group waits suit the counting scoreboards)
-          constexpr int kG = kSweepU / 2;
-          const uint32_t r0 = warp * RPI + lr;
-          const uint32_t T = (md.rows + PSTEP - 1) / PSTEP;  // warp-uniform step count
-          V256 ha[kG], hb2[kG];
-          auto load_group = [&](V256 (&h)[kG], uint32_t t0) {
+          for (uint32_t rb = warp * RPI; rb < md.rows; rb += PSTEP * kSweepU) {  // warp-uniform
+            const uint32_t r0 = rb + lr;
+            V256 hv[kSweepU];
 #pragma unroll
-            for (int u = 0; u < kG; ++u) {
-              const uint32_t row = r0 + (t0 + u) * PSTEP;
-              if (t0 + u < T && row < md.rows && cok) {
-                h[u] = ld_stream256<kEvictLast>(hb + (uint64_t)row * md.ld);
+            for (int u = 0; u < kSweepU; ++u) {
+              const uint32_t row = r0 + u * PSTEP;
+              if (row < md.rows && cok) {
+                hv[u] = ld_stream256<kEvictLast>(hb + (uint64_t)row * md.ld);
               } else {
-                h[u].w[0] = h[u].w[1] = h[u].w[2] = h[u].w[3] = 0;
+                hv[u].w[0] = hv[u].w[1] = hv[u].w[2] = hv[u].w[3] = 0;
               }
             }
-          };
-          auto use_group = [&](V256 (&h)[kG], uint32_t t0) {
 #pragma unroll
-            for (int u = 0; u < kG; ++u) {
-              const uint32_t row = r0 + (t0 + u) * PSTEP;
-              const double2 qv = (t0 + u < T && row < md.rows) ? __ldg(qb + row) : make_double2(0.0, 0.0);
+            for (int u = 0; u < kSweepU; ++u) {
+              const uint32_t row = r0 + u * PSTEP;
+              const double2 qv = row < md.rows ? __ldg(qb + row) : make_double2(0.0, 0.0);
 #pragma unroll
-              for (int e = 0; e < PV; ++e) cmac_conj(acc[e], Store<S>::get(h[u], e), qv);
+              for (int e = 0; e < PV; ++e) cmac_conj(acc[e], Store<S>::get(hv[u], e), qv);
             }
-          };
-          load_group(ha, 0);
-          load_group(hb2, kG);
-          for (uint32_t t = 0; t < T; t += 2 * kG) {
-            use_group(ha, t);
-            if (t + 2 * kG < T) load_group(ha, t + 2 * kG);
-            use_group(hb2, t + kG);
-            if (t + 3 * kG < T) load_group(hb2, t + 3 * kG);
           }
 #pragma unroll
           for (int e = 0; e < PV; ++e) {
