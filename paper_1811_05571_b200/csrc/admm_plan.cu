@@ -156,6 +156,7 @@ struct admm_plan {
   // sweep schedule (admm_sweep.cuh)
   int schedule = 1;             // 1 two-pass, 2 single-HBM-pass sweep
   int sweep_lpr = 8;
+  bool sweep_bulk = false;  // bulk-copy producer variant (sweep_bulk_kernel)
   std::vector<SweepDesc> segs;
   DevBuf dsegs, dwpart_s;
   Geom gS;
@@ -291,11 +292,32 @@ size_t sweep_smem_bytes(const admm_plan* p) {
 // when the segment rows do not fit the SMEM accumulator or the resident strips would
 // not fit in L2 (then the two-pass schedule is used).
 template <typename S, int LPR>
+size_t sweep_bulk_smem_bytes(const admm_plan* p) {
+  constexpr int W = LPR * Store<S>::kPerVec;
+  constexpr int R = (kWarp / LPR) * kBulkCompute * kBulkRI;
+  return (size_t)kBulkStages * R * W * sizeof(S) + 2 * kBulkStages * sizeof(uint64_t) +
+         ((size_t)p->n_meas + (2 * (size_t)kBulkCompute + 4) * p->Mr * W) * sizeof(double2);
+}
+
+template <typename S, int LPR>
 bool try_sweep(admm_plan* p, size_t l2_budget) {
   constexpr int W = LPR * Store<S>::kPerVec;
-  const size_t smem = sweep_smem_bytes<S, LPR>(p);
-  if (smem > 200 * 1024) return false;
-  CK(cudaFuncSetAttribute(sweep_kernel<S, LPR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  size_t smem = sweep_smem_bytes<S, LPR>(p);
+  if constexpr (LPR >= 4) {
+    const char* env = std::getenv("ADMM_B200_SWEEP");
+    p->sweep_bulk = !(env && !std::strcmp(env, "ldg"));
+    if (p->sweep_bulk) {
+      smem = sweep_bulk_smem_bytes<S, LPR>(p);
+      if (smem > 225 * 1024) p->sweep_bulk = false, smem = sweep_smem_bytes<S, LPR>(p);
+    }
+    if (p->sweep_bulk)
+      CK(cudaFuncSetAttribute(sweep_bulk_kernel<S, LPR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  } else {
+    p->sweep_bulk = false;
+  }
+  if (smem > 225 * 1024) return false;
+  CK(cudaFuncSetAttribute(sweep_kernel<S, LPR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)std::min<size_t>(smem, 225 * 1024)));
   int occ = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_kernel<S, LPR>, kSweepThreads, smem));
   if (occ < 1) return false;
@@ -539,6 +561,15 @@ void enqueue_sweep_prologue(admm_plan* p, cudaStream_t s) {
 
 template <typename S, int LPR>
 void launch_sweep_lpr(admm_plan* p, cudaStream_t s) {
+  if constexpr (LPR >= 4) {
+    if (p->sweep_bulk) {
+      sweep_bulk_kernel<S, LPR><<<(unsigned)p->gS.P, kSweepThreads, p->sweep_smem, s>>>(
+          p->dH.as<S>(), p->dhN.as<MatDesc>(), p->dblocks.as<BlockDesc>(), p->dsegs.as<SweepDesc>(), (uint32_t)p->Mr,
+          (uint32_t)p->Nc, (uint32_t)p->n_meas, p->gS.U, p->dq.as<double2>(), col_vecs(p), p->dwpart_s.as<double2>(),
+          p->dparams.as<Params>(), p->dred.as<double>(), p->dstate.as<IterState>());
+      return;
+    }
+  }
   sweep_kernel<S, LPR><<<(unsigned)p->gS.P, kSweepThreads, p->sweep_smem, s>>>(
       p->dH.as<S>(), p->dhN.as<MatDesc>(), p->dblocks.as<BlockDesc>(), p->dsegs.as<SweepDesc>(), (uint32_t)p->Mr,
       (uint32_t)p->Nc, (uint32_t)p->n_meas, p->gS.U, p->dq.as<double2>(), col_vecs(p), p->dwpart_s.as<double2>(),
