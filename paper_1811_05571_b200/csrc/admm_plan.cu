@@ -20,6 +20,9 @@
 #include <thread>
 #include <vector>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "admm_b200.h"
 #include "admm_kernels.cuh"
 #include "admm_setup.cuh"
@@ -156,7 +159,8 @@ struct admm_plan {
   // sweep schedule (admm_sweep.cuh)
   int schedule = 1;             // 1 two-pass, 2 single-HBM-pass sweep
   int sweep_lpr = 8;
-  bool sweep_bulk = false;  // bulk-copy producer variant (sweep_bulk_kernel)
+  bool sweep_bulk = false;  // TMA producer variant (sweep_bulk_kernel)
+  DevBuf dtmaps;            // one CUtensorMap per local block
   std::vector<SweepDesc> segs;
   DevBuf dsegs, dwpart_s;
   Geom gS;
@@ -278,6 +282,7 @@ void build_geometry(admm_plan* p) {
   p->dqpart.alloc(pK * sizeof(double2));
   p->dzpart.alloc(pH * sizeof(double2));
   p->dgpart.alloc(pH * sizeof(double2));
+  p->dH.alloc(p->h_elems * sizeof(S));
 }
 
 void upload_desc(DevBuf& d, const void* src, size_t bytes);
@@ -291,6 +296,38 @@ size_t sweep_smem_bytes(const admm_plan* p) {
 // Try to configure the single-HBM-pass sweep with LPR lanes per row.  Returns false
 // when the segment rows do not fit the SMEM accumulator or the resident strips would
 // not fit in L2 (then the two-pass schedule is used).
+// CUtensorMap per local block for the TMA sweep producer: H_b as a rows x (2*ld) real
+// matrix, box = {row_bytes / sizeof(real), rows_per_stage}.
+template <typename S>
+bool build_tensor_maps(admm_plan* p, int row_bytes, int rows_per_stage) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return false;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  constexpr size_t real = sizeof(S) / 2;
+  std::vector<CUtensorMap> maps(p->blocks.size());
+  for (size_t b = 0; b < p->blocks.size(); ++b) {
+    const MatDesc& md = p->hN[b];
+    const cuuint64_t dims[2] = {(cuuint64_t)md.ld * 2, (cuuint64_t)md.rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)md.ld * sizeof(S)};
+    const cuuint32_t box[2] = {(cuuint32_t)(row_bytes / real), (cuuint32_t)rows_per_stage};
+    const cuuint32_t estr[2] = {1, 1};
+    void* base = p->dH.as<S>() + md.a_off;
+    const CUresult r = encode(&maps[b], real == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                              base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return false;
+  }
+  upload_desc(p->dtmaps, maps.data(), maps.size() * sizeof(CUtensorMap));
+  return true;
+}
+
 template <typename S, int LPR>
 size_t sweep_bulk_smem_bytes(const admm_plan* p) {
   constexpr int W = LPR * Store<S>::kPerVec;
@@ -309,6 +346,11 @@ bool try_sweep(admm_plan* p, size_t l2_budget) {
     if (p->sweep_bulk) {
       smem = sweep_bulk_smem_bytes<S, LPR>(p);
       if (smem > 225 * 1024) p->sweep_bulk = false, smem = sweep_smem_bytes<S, LPR>(p);
+    }
+    if (p->sweep_bulk && !build_tensor_maps<S>(p, LPR * Store<S>::kPerVec * (int)sizeof(S),
+                                                  (kWarp / LPR) * kBulkCompute * kBulkRI)) {
+      p->sweep_bulk = false;
+      smem = sweep_smem_bytes<S, LPR>(p);
     }
     if (p->sweep_bulk)
       CK(cudaFuncSetAttribute(sweep_bulk_kernel<S, LPR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -370,7 +412,7 @@ void upload_desc(DevBuf& d, const void* src, size_t bytes) {
 // materialises the same blocks as host copies).
 template <typename S>
 void upload_h(admm_plan* p, const void* h, admm_dtype h_dtype) {
-  p->dH.alloc(p->h_elems * sizeof(S));
+  // p->dH was allocated by build_geometry (tensor maps need its address before upload)
   const size_t hsz = h_dtype == ADMM_C128 ? 16 : 8;
   const bool direct = (h_dtype == ADMM_C128) == std::is_same<S, double2>::value;
   DevBuf tmp;
@@ -566,7 +608,7 @@ void launch_sweep_lpr(admm_plan* p, cudaStream_t s) {
       sweep_bulk_kernel<S, LPR><<<(unsigned)p->gS.P, kSweepThreads, p->sweep_smem, s>>>(
           p->dH.as<S>(), p->dhN.as<MatDesc>(), p->dblocks.as<BlockDesc>(), p->dsegs.as<SweepDesc>(), (uint32_t)p->Mr,
           (uint32_t)p->Nc, (uint32_t)p->n_meas, p->gS.U, p->dq.as<double2>(), col_vecs(p), p->dwpart_s.as<double2>(),
-          p->dparams.as<Params>(), p->dred.as<double>(), p->dstate.as<IterState>());
+          p->dparams.as<Params>(), p->dred.as<double>(), p->dstate.as<IterState>(), p->dtmaps.as<unsigned char>());
       return;
     }
   }

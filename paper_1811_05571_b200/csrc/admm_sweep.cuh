@@ -297,12 +297,24 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
       : "memory");
 }
 
+// 2-D TMA: one box (inner: the strip's row segment, outer: R rows) per stage.
+__device__ __forceinline__ void tma_2d(uint32_t dst, const void* tmap, int c0, int c1, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(
+          dst),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
+// tmaps: one 128-byte CUtensorMap per local block (H_b viewed as rows x 2*ld reals),
+// box = {ROWB / sizeof(real), R}; rows past the block and columns past ld are zero-filled.
 template <typename S, int LPR>
 __global__ void __launch_bounds__(kSweepThreads, 1)
 sweep_bulk_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const BlockDesc* __restrict__ blocks,
                   const SweepDesc* __restrict__ segs, uint32_t M, uint32_t N, uint32_t n_meas, uint64_t Utot,
                   const double2* __restrict__ q, ColVecs cv, double2* __restrict__ wpart,
-                  const Params* __restrict__ prm, double* __restrict__ red, IterState* st) {
+                  const Params* __restrict__ prm, double* __restrict__ red, IterState* st,
+                  const unsigned char* __restrict__ tmaps) {
   constexpr int PV = Store<S>::kPerVec;
   constexpr int W = LPR * PV;
   constexpr int RPI = kWarp / LPR;
@@ -346,22 +358,21 @@ sweep_bulk_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const
       uint64_t pol;
       asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
       uint32_t seq = 0;
+      constexpr int kRealsPerComplex = 2;
       for (uint64_t x = x0; x < xe; ++x) {
         if (x == sd.unit0 + sd.n_strips) sd = segs[++j];
-        const uint32_t col_lo = (uint32_t)(x - sd.unit0) * W;
-        const uint32_t colbytes = (uint32_t)(((min((uint32_t)W, sd.cols - col_lo) * sizeof(S)) + 15) & ~15u);
+        const int c0 = (int)((x - sd.unit0) * W * kRealsPerComplex);
         for (uint32_t i = 0; i < M; ++i) {
           const MatDesc md = hm[i * N + j];
-          const S* hb = H + md.a_off + col_lo;
+          const unsigned char* tm = tmaps + (size_t)(i * N + j) * 128;
           for (uint32_t r0 = 0; r0 < md.rows; r0 += R, ++seq) {
             const uint32_t slot = seq % kBulkStages, ph = (seq / kBulkStages) & 1;
-            mbar_wait(&emptyb[slot], ph ^ 1);
-            const uint32_t nr = min((uint32_t)R, md.rows - r0);
-            if (lane == 0) mbar_expect_tx(&fullb[slot], nr * colbytes);
+            if (lane == 0) {
+              mbar_wait(&emptyb[slot], ph ^ 1);
+              mbar_expect_tx(&fullb[slot], STAGEB);
+              tma_2d(smem_u32(ring) + slot * STAGEB, tm, c0, (int)r0, &fullb[slot], pol);
+            }
             __syncwarp();
-            const uint32_t dst = smem_u32(ring) + slot * STAGEB;
-            for (uint32_t r = lane; r < nr; r += kWarp)
-              bulk_g2s(dst + r * ROWB, hb + (uint64_t)(r0 + r) * md.ld, colbytes, &fullb[slot], pol);
           }
         }
       }
