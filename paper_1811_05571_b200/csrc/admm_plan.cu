@@ -341,8 +341,10 @@ bool try_sweep(admm_plan* p, size_t l2_budget) {
   constexpr int W = LPR * Store<S>::kPerVec;
   size_t smem = sweep_smem_bytes<S, LPR>(p);
   if constexpr (LPR >= 4) {
+    // TMA producer only on request: measured 206 us vs 126 us for the LDG producer on
+    // config 2 (it runs ahead of the L2 re-read and loses the reuse; profiles/r01_summary.md)
     const char* env = std::getenv("ADMM_B200_SWEEP");
-    p->sweep_bulk = !(env && !std::strcmp(env, "ldg"));
+    p->sweep_bulk = env && !std::strcmp(env, "tma");
     if (p->sweep_bulk) {
       smem = sweep_bulk_smem_bytes<S, LPR>(p);
       if (smem > 225 * 1024) p->sweep_bulk = false, smem = sweep_smem_bytes<S, LPR>(p);
