@@ -6,7 +6,8 @@
 // complex GEMMs, W = H C and Z = H^H Q (C: n x B, Q: m x B), compute-bound on SIMT
 // (tensor cores are reserved for setup by the north star).  Register-tiled FP64 SIMT:
 // a 256-thread CTA owns a 64 x 64 output tile (64 rows or columns x up to 64 scenes),
-// each thread a 4 x 4 complex sub-tile; A and X stream through SMEM in k-chunks of 16.
+// each thread a 4 x 4 complex sub-tile (rows ty + 16q, scenes tx + 16w: both SMEM
+// operand reads are conflict-free); A and X stream through SMEM in k-chunks of 32.
 // Vectors are [row][scene] (scene fastest), FP64 like the single-scene engine.
 #pragma once
 
@@ -16,7 +17,7 @@ namespace admm {
 
 constexpr int kBT = 64;   // output tile: rows (N) or columns (adjoint)
 constexpr int kBB = 64;   // scenes per tile
-constexpr int kBK = 16;   // k-chunk
+constexpr int kBK = 32;   // k-chunk
 
 struct BTile {
   uint64_t a_off;   // matrix in the storage arena
@@ -74,8 +75,8 @@ bgemm_kernel(const S* __restrict__ A, const BTile* __restrict__ tiles, const dou
       double2 av[4], xv[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        av[q] = At[kk][ty * 4 + q];
-        xv[q] = Xs[kk][tx * 4 + q];
+        av[q] = At[kk][ty + 16 * q];
+        xv[q] = Xs[kk][tx + 16 * q];
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q)
@@ -86,11 +87,11 @@ bgemm_kernel(const S* __restrict__ A, const BTile* __restrict__ tiles, const dou
   }
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const uint32_t oi = t.t0 + ty * 4 + q;
+    const uint32_t oi = t.t0 + ty + 16 * q;
     if (oi >= nout) continue;
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
-      const uint32_t b = tx * 4 + w;
+      const uint32_t b = tx + 16 * w;
       if (b < B) out[t.o_off + (uint64_t)oi * B + b] = acc[q][w];
     }
   }
