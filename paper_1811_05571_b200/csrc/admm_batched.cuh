@@ -17,7 +17,7 @@ namespace admm {
 
 constexpr int kBT = 64;   // output tile: rows (N) or columns (adjoint)
 constexpr int kBB = 64;   // scenes per tile
-constexpr int kBK = 32;   // k-chunk
+constexpr int kBK = 16;   // k-chunk
 
 struct BTile {
   uint64_t a_off;   // matrix in the storage arena
@@ -28,55 +28,87 @@ struct BTile {
   uint32_t k0, k1;  // k range of this unit (split-K)
 };
 
+// cp.async helpers (size 8 or 16, zero-fill when src_bytes = 0)
+__device__ __forceinline__ void cpa(void* smem, const void* src, bool ok) {
+  const uint32_t dst = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cpa8(void* smem, const void* src, bool ok) {
+  const uint32_t dst = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "r"(ok ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // out[t0 + i][b] = sum_{k in [k0,k1)} op(A)[t0 + i][k] X[k][b]
 //   ADJ = false: op(A)[i][k] = A[i][k]          (W = H C, Q = K R)
 //   ADJ = true:  op(A)[i][k] = conj(A[k][i])    (Z = H^H Q)
+// A (storage precision) and X are staged by cp.async into double-buffered SMEM in the
+// layout their global rows arrive in (no transposing stores); A is widened at read time.
 template <typename S, bool ADJ>
 __global__ void __launch_bounds__(256, 2)
 bgemm_kernel(const S* __restrict__ A, const BTile* __restrict__ tiles, const double2* __restrict__ X,
              double2* __restrict__ out, uint32_t B) {
-  __shared__ double2 At[kBK][kBT + 1];
-  __shared__ double2 Xs[kBK][kBB + 1];
+  constexpr int AR = ADJ ? kBK : kBT;      // As[2][AR][AC + 1]
+  constexpr int AC = ADJ ? kBT : kBK;
+  extern __shared__ __align__(16) unsigned char bsm[];
+  S* As = reinterpret_cast<S*>(bsm);                                           // 2 x AR x (AC+1)
+  constexpr size_t kAsBytes = (2 * AR * (AC + 1) * sizeof(S) + 15) & ~(size_t)15;
+  double2* Xs = reinterpret_cast<double2*>(bsm + kAsBytes);  // 2 x kBK x (kBB+1)
   const BTile t = tiles[blockIdx.x];
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
   const S* a = A + t.a_off;
   const uint32_t nout = ADJ ? t.cols : t.rows;
+  auto stage = [&](int buf, uint32_t k0) {
+    S* as = As + (size_t)buf * AR * (AC + 1);
+    double2* xs = Xs + (size_t)buf * kBK * (kBB + 1);
+    for (int e = threadIdx.x; e < kBT * kBK; e += 256) {
+      const int r = e / AC, c = e % AC;  // consecutive threads -> consecutive global and SMEM
+      const uint32_t oi = t.t0 + (ADJ ? c : r), k = k0 + (ADJ ? r : c);
+      const bool ok = oi < nout && k < t.k1;
+      const S* src = ok ? (ADJ ? a + (uint64_t)k * t.ld + oi : a + (uint64_t)oi * t.ld + k) : a;
+      if constexpr (sizeof(S) == 16)
+        cpa(as + r * (AC + 1) + c, src, ok);
+      else
+        cpa8(as + r * (AC + 1) + c, src, ok);
+    }
+    for (int e = threadIdx.x; e < kBK * kBB; e += 256) {
+      const int kk = e / kBB, b = e % kBB;
+      const uint32_t k = k0 + kk;
+      const bool ok = k < t.k1 && (uint32_t)b < B;
+      cpa(xs + kk * (kBB + 1) + b, ok ? X + t.x_off + (uint64_t)k * B + b : X, ok);
+    }
+    cpa_commit();
+  };
   double2 acc[4][4];
 #pragma unroll
   for (int q = 0; q < 4; ++q)
 #pragma unroll
     for (int w = 0; w < 4; ++w) acc[q][w] = make_double2(0.0, 0.0);
+  int buf = 0;
+  stage(0, t.k0);
   for (uint32_t k0 = t.k0; k0 < t.k1; k0 += kBK) {
-    for (int e = threadIdx.x; e < kBT * kBK; e += 256) {
-      int i, kk;
-      if (ADJ) {  // coalesced along the output columns
-        kk = e / kBT;
-        i = e % kBT;
-      } else {    // coalesced along k
-        i = e / kBK;
-        kk = e % kBK;
-      }
-      const uint32_t oi = t.t0 + i, k = k0 + kk;
-      double2 v = make_double2(0.0, 0.0);
-      if (oi < nout && k < t.k1) {
-        v = Store<S>::widen(ADJ ? a[(uint64_t)k * t.ld + oi] : a[(uint64_t)oi * t.ld + k]);
-        if (ADJ) v.y = -v.y;
-      }
-      At[kk][i] = v;
-    }
-    for (int e = threadIdx.x; e < kBK * kBB; e += 256) {
-      const int kk = e / kBB, b = e % kBB;
-      const uint32_t k = k0 + kk;
-      Xs[kk][b] = (k < t.k1 && (uint32_t)b < B) ? X[t.x_off + (uint64_t)k * B + b] : make_double2(0.0, 0.0);
+    if (k0 + kBK < t.k1) {
+      stage(buf ^ 1, k0 + kBK);
+      cpa_wait<1>();
+    } else {
+      cpa_wait<0>();
     }
     __syncthreads();
+    const S* as = As + (size_t)buf * AR * (AC + 1);
+    const double2* xs = Xs + (size_t)buf * kBK * (kBB + 1);
 #pragma unroll 4
     for (int kk = 0; kk < kBK; ++kk) {
       double2 av[4], xv[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        av[q] = At[kk][ty + 16 * q];
-        xv[q] = Xs[kk][tx + 16 * q];
+        const int i = ty + 16 * q;
+        av[q] = Store<S>::widen(ADJ ? as[kk * (AC + 1) + i] : as[i * (AC + 1) + kk]);
+        if (ADJ) av[q].y = -av[q].y;
+        xv[q] = xs[kk * (kBB + 1) + tx + 16 * q];
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q)
@@ -84,6 +116,7 @@ bgemm_kernel(const S* __restrict__ A, const BTile* __restrict__ tiles, const dou
         for (int w = 0; w < 4; ++w) cmac(acc[q][w], av[q], xv[w]);
     }
     __syncthreads();
+    buf ^= 1;
   }
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
@@ -95,6 +128,13 @@ bgemm_kernel(const S* __restrict__ A, const BTile* __restrict__ tiles, const dou
       if (b < B) out[t.o_off + (uint64_t)oi * B + b] = acc[q][w];
     }
   }
+}
+
+template <typename S, bool ADJ>
+constexpr size_t bgemm_smem() {
+  constexpr int AR = ADJ ? kBK : kBT;
+  constexpr int AC = ADJ ? kBT : kBK;
+  return ((2 * AR * (AC + 1) * sizeof(S) + 15) & ~(size_t)15) + 2 * kBK * (kBB + 1) * sizeof(double2);
 }
 
 struct BRowVecs {

@@ -670,8 +670,20 @@ void enqueue_iteration_sweep(admm_plan* p, cudaStream_t s, bool with_objective, 
 }
 
 // ---- batched scenes (config 5) ----------------------------------------------------
+template <typename S>
+void bgemm_attrs() {
+  CK(cudaFuncSetAttribute(bgemm_kernel<S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)bgemm_smem<S, false>()));
+  CK(cudaFuncSetAttribute(bgemm_kernel<S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)bgemm_smem<S, true>()));
+}
+
 void build_batched(admm_plan* p) {
   const uint64_t B = p->batch;
+  if (p->dtype == ADMM_C128)
+    bgemm_attrs<double2>();
+  else
+    bgemm_attrs<float2>();
   const uint64_t nb = p->blocks.size();
   uint64_t rtiles = 0;
   for (auto& b : p->blocks) rtiles += cdiv(b.rows, kBT);
@@ -733,21 +745,21 @@ void enqueue_iteration_batched(admm_plan* p, cudaStream_t s, std::vector<cudaEve
     if (ev) CK(cudaEventRecord((*ev)[k], s));
   };
   mark(0);
-  bgemm_kernel<S, false><<<(unsigned)p->tN.size(), 256, 0, s>>>(p->dH.as<S>(), p->dtN.as<BTile>(),
+  bgemm_kernel<S, false><<<(unsigned)p->tN.size(), 256, bgemm_smem<S, false>(), s>>>(p->dH.as<S>(), p->dtN.as<BTile>(),
                                                                   p->dc.as<double2>(), p->dwpart.as<double2>(), B);
   mark(1);
   brows_kernel<kRhs><<<dim3(rgx, nb), kCtaThreads, 0, s>>>(brow_vecs(p), p->dwpart.as<double2>(), stride, p->splitN,
                                                           p->dblocks.as<BlockDesc>(), (uint32_t)p->Nc, B,
                                                           p->dparams.as<Params>());
   mark(2);
-  bgemm_kernel<S, false><<<(unsigned)p->tK.size(), 256, 0, s>>>(p->dK.as<S>(), p->dtK.as<BTile>(),
+  bgemm_kernel<S, false><<<(unsigned)p->tK.size(), 256, bgemm_smem<S, false>(), s>>>(p->dK.as<S>(), p->dtK.as<BTile>(),
                                                                   p->dr.as<double2>(), p->dqpart.as<double2>(), B);
   mark(3);
   brows_kernel<kQ><<<dim3(rgx, nb), kCtaThreads, 0, s>>>(brow_vecs(p), p->dqpart.as<double2>(), stride, p->splitK,
                                                         p->dblocks.as<BlockDesc>(), (uint32_t)p->Nc, B,
                                                         p->dparams.as<Params>());
   mark(4);
-  bgemm_kernel<S, true><<<(unsigned)p->tH.size(), 256, 0, s>>>(p->dH.as<S>(), p->dtH.as<BTile>(), p->dq.as<double2>(),
+  bgemm_kernel<S, true><<<(unsigned)p->tH.size(), 256, bgemm_smem<S, true>(), s>>>(p->dH.as<S>(), p->dtH.as<BTile>(), p->dq.as<double2>(),
                                                                  p->dz.as<double2>(), B);
   mark(5);
   bzupdate_kernel<<<p->pz, kCtaThreads, 0, s>>>(col_vecs(p), p->dz.as<double2>(), p->dblocks.as<BlockDesc>(),
@@ -1251,10 +1263,10 @@ admm_status admm_plan_max_abs_adjoint_batched(admm_plan* p, double* out) {
     if (p->batch < 2) throw Fail{ADMM_E_STATE, "not a batched plan"};
     const uint32_t B = (uint32_t)p->batch;
     if (p->dtype == ADMM_C128)
-      bgemm_kernel<double2, true><<<(unsigned)p->tG.size(), 256, 0, p->stream>>>(
+      bgemm_kernel<double2, true><<<(unsigned)p->tG.size(), 256, bgemm_smem<double2, true>(), p->stream>>>(
           p->dH.as<double2>(), p->dtG.as<BTile>(), p->dg.as<double2>(), p->dz.as<double2>(), B);
     else
-      bgemm_kernel<float2, true><<<(unsigned)p->tG.size(), 256, 0, p->stream>>>(
+      bgemm_kernel<float2, true><<<(unsigned)p->tG.size(), 256, bgemm_smem<float2, true>(), p->stream>>>(
           p->dH.as<float2>(), p->dtG.as<BTile>(), p->dg.as<double2>(), p->dz.as<double2>(), B);
     const unsigned gx = p->pz;
     DevBuf res;
