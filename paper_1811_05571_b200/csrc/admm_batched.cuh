@@ -58,6 +58,7 @@ bgemm_kernel(const S* __restrict__ A, const BTile* __restrict__ tiles, const dou
   S* As = reinterpret_cast<S*>(bsm);                                           // 2 x AR x (AC+1)
   constexpr size_t kAsBytes = (2 * AR * (AC + 1) * sizeof(S) + 15) & ~(size_t)15;
   double2* Xs = reinterpret_cast<double2*>(bsm + kAsBytes);  // 2 x kBK x (kBB+1)
+  double2* Ad = Xs + 2 * kBK * (kBB + 1);                     // AR x (AC+1) FP64 (complex64 only)
   const BTile t = tiles[blockIdx.x];
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
   const S* a = A + t.a_off;
@@ -100,13 +101,23 @@ bgemm_kernel(const S* __restrict__ A, const BTile* __restrict__ tiles, const dou
     __syncthreads();
     const S* as = As + (size_t)buf * AR * (AC + 1);
     const double2* xs = Xs + (size_t)buf * kBK * (kBB + 1);
+    const double2* ad = nullptr;  // complex64: the chunk widened once (not once per reader)
+    if constexpr (sizeof(S) == 8) {
+      for (int e = threadIdx.x; e < AR * (AC + 1); e += 256) Ad[e] = Store<S>::widen(as[e]);
+      __syncthreads();
+      ad = Ad;
+    }
 #pragma unroll 4
     for (int kk = 0; kk < kBK; ++kk) {
       double2 av[4], xv[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int i = ty + 16 * q;
-        av[q] = Store<S>::widen(ADJ ? as[kk * (AC + 1) + i] : as[i * (AC + 1) + kk]);
+        const int o = ADJ ? kk * (AC + 1) + i : i * (AC + 1) + kk;
+        if constexpr (sizeof(S) == 8)
+          av[q] = ad[o];
+        else
+          av[q] = Store<S>::widen(as[o]);
         if (ADJ) av[q].y = -av[q].y;
         xv[q] = xs[kk * (kBB + 1) + tx + 16 * q];
       }
@@ -134,7 +145,8 @@ template <typename S, bool ADJ>
 constexpr size_t bgemm_smem() {
   constexpr int AR = ADJ ? kBK : kBT;
   constexpr int AC = ADJ ? kBT : kBK;
-  return ((2 * AR * (AC + 1) * sizeof(S) + 15) & ~(size_t)15) + 2 * kBK * (kBB + 1) * sizeof(double2);
+  return ((2 * AR * (AC + 1) * sizeof(S) + 15) & ~(size_t)15) + 2 * kBK * (kBB + 1) * sizeof(double2) +
+         (sizeof(S) == 8 ? AR * (AC + 1) * sizeof(double2) : 0);
 }
 
 struct BRowVecs {
