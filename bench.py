@@ -220,20 +220,25 @@ def bench_distributed(args, cfg):
     sh = D.ShardPlan(problem, scfg, method, M, N, (Pr, Pc), (pr, pc),
                      admm.SolveOptions(dtype=dtype, device=local, trace_objective=False))
     comm = D.TorchComm(Pr, Pc)
-    D.run_iterations([sh], comm, max(args.warmup, 3))
+    D.run_iterations([sh], comm, max(args.warmup, 3))  # eager warm-up: NCCL communicators up
     sh.sync()
+    graphed = D.GraphedIterations(sh, comm, iters_per_graph=8)  # phases + all-gathers in one graph
+    steps = -(-args.steps // 8) * 8
+    graphed.run(8)
+    torch.cuda.synchronize(local)
     dist.barrier()
     torch.cuda.synchronize(local)
-    stream = sh.stream()
+    stream = graphed.stream
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(local) as clk, torch.cuda.stream(stream):
         e0.record(stream)
-        D.run_iterations([sh], comm, args.steps)
+        graphed.run(steps)
         e1.record(stream)
         e1.synchronize()
     torch.cuda.synchronize(local)
     ms = e0.elapsed_time(e1)
+    args.steps = steps
     t = torch.tensor([ms], device=f"cuda:{local}")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
@@ -243,7 +248,9 @@ def bench_distributed(args, cfg):
     # rank; a full solve of `iters` iterations + the solution gathered to every rank
     t0 = time.perf_counter()
     sh.reset()
-    D.run_iterations([sh], comm, iters)
+    D.prime([sh], comm)
+    graphed.run(iters)
+    torch.cuda.synchronize(local)
     sh.sync()
     segs = [None] * ws
     dist.all_gather_object(segs, sh.segment_v())

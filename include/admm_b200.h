@@ -166,6 +166,9 @@ admm_status admm_plan_reset(admm_plan* plan);
 admm_status admm_plan_enqueue(admm_plan* plan, uint64_t iters);
 admm_status admm_plan_sync(admm_plan* plan);
 void* admm_plan_stream(admm_plan* plan);
+/* Launch on the caller's stream from now on (NULL: back to the plan's own stream); used
+ * to capture the phases together with the caller's collectives in one CUDA graph. */
+admm_status admm_plan_set_stream(admm_plan* plan, void* stream);
 
 /* Per-kernel device time of one iteration, measured with CUDA events around
  * individually launched kernels on the plan's stream (averaged over `iters`).

@@ -77,6 +77,7 @@ _SIGS = {
     "admm_plan_enqueue": ([_ptr, _u64], _i32),
     "admm_plan_sync": ([_ptr], _i32),
     "admm_plan_stream": ([_ptr], _ptr),
+    "admm_plan_set_stream": ([_ptr, _ptr], _i32),
     "admm_plan_kernel_count": ([_ptr], _u32),
     "admm_plan_profile": ([_ptr, _u64, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(_dbl)], _i32),
     "admm_plan_get_info": ([_ptr, ctypes.POINTER(PlanInfoC)], _i32),

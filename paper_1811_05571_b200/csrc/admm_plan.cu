@@ -127,6 +127,7 @@ struct Geom {
 struct admm_plan {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t own_stream = nullptr;  // the plan's stream; `stream` may be a caller's (graph capture)
   admm_dtype dtype = ADMM_C128;
   admm_method method = ADMM_HYBRID;
   uint64_t n_meas = 0, n_pix = 0, M = 1, N = 1;
@@ -178,7 +179,7 @@ struct admm_plan {
 
   ~admm_plan() {
     if (exec) cudaGraphExecDestroy(exec);
-    if (stream) cudaStreamDestroy(stream);
+    if (own_stream) cudaStreamDestroy(own_stream);
   }
 };
 
@@ -1012,7 +1013,8 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
     throw Fail{ADMM_E_CUDA, "no CUDA device: libadmm_b200 has no CPU fallback"};
   CK(cudaSetDevice(o.device));
   CK(cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, o.device));
-  CK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&p->own_stream, cudaStreamNonBlocking));
+  p->stream = p->own_stream;
 
   // sharding: this plan owns row blocks [i0, i0+Mr) x column blocks [j0, j0+Nc)
   if (shard) {
@@ -1242,6 +1244,13 @@ admm_status admm_plan_sync(admm_plan* p) {
 }
 
 void* admm_plan_stream(admm_plan* p) { return p ? (void*)p->stream : nullptr; }
+
+admm_status admm_plan_set_stream(admm_plan* p, void* stream) {
+  return run_guarded([&] {
+    check_plan(p);
+    p->stream = stream ? static_cast<cudaStream_t>(stream) : p->own_stream;
+  });
+}
 
 uint32_t admm_plan_kernel_count(const admm_plan* p) { return p && p->schedule == 2 ? 4 : 7; }
 

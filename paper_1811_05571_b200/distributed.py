@@ -106,6 +106,11 @@ class ShardPlan:
     def reset(self) -> None:
         self._check(self._lib.lib.admm_plan_reset(self._h))
 
+    def set_stream(self, stream) -> None:
+        """Launch on `stream` (a torch.cuda.Stream; None: the plan's own stream)."""
+        ptr = ctypes.c_void_p(stream.cuda_stream) if stream is not None else None
+        self._check(self._lib.lib.admm_plan_set_stream(self._h, ptr))
+
     def phase(self, k: int) -> None:
         self._check(self._lib.lib.admm_plan_run_phase(self._h, k))
 
@@ -175,11 +180,12 @@ class TorchComm:
             if c == pc:
                 self.col = g
 
-    def exchange(self, which: int, shards: Sequence) -> None:
+    def exchange(self, which: int, shards: Sequence, in_graph: bool = False) -> None:
         (sh,) = shards
         full, mine = sh.buffer(which)
         group = {X_GHAT: self.row, X_OUTBOX: self.col, X_SCAL: None}[which]
-        ctx = _stream_ctx(sh)
+        import contextlib
+        ctx = contextlib.nullcontext() if in_graph else _stream_ctx(sh)  # capture: current stream
         with ctx:
             if full.is_cuda:  # in place: `mine` is this rank's slot of `full` (rank order = group order)
                 self.dist.all_gather_into_tensor(full, mine, group=group)
@@ -206,7 +212,8 @@ class LoopbackComm:
     def __init__(self, Pr: int, Pc: int):
         self.Pr, self.Pc = Pr, Pc
 
-    def exchange(self, which: int, shards: Sequence) -> None:
+    def exchange(self, which: int, shards: Sequence, in_graph: bool = False) -> None:
+        assert not in_graph, "LoopbackComm synchronises on the host: not capturable"
         for sh in shards:
             if hasattr(sh, "sync"):
                 sh.sync()
@@ -234,19 +241,54 @@ class LoopbackComm:
 def run_iterations(shards: List, comm, iters: int) -> None:
     """Drive `iters` ADMM iterations of every local shard (phase order in admm_b200.h).
     After reset the ghat slots hold ghat^0 (sweep prologue) or 0: exchange first."""
-    sched = shards[0].schedule
     comm.exchange(X_GHAT, shards)
+    _iterate(shards, comm, iters)
+
+
+def prime(shards, comm) -> None:
+    """After reset: the ghat of iteration 0 (sweep prologue) must reach the peers."""
+    comm.exchange(X_GHAT, shards)
+
+
+class GraphedIterations:
+    """`iters_per_graph` distributed iterations (shard phases + NCCL all-gathers) captured
+    once in a CUDA graph on a side stream and replayed: no Python or launch overhead per
+    iteration.  Requires TorchComm over NCCL (collectives are capturable once the
+    communicators are initialised — run one eager iteration first)."""
+
+    def __init__(self, shard, comm, iters_per_graph: int = 8):
+        import torch
+        self.shard, self.n = shard, iters_per_graph
+        self.stream = torch.cuda.Stream(device=shard.device)
+        self.graph = torch.cuda.CUDAGraph()
+        shard.sync()
+        torch.cuda.synchronize(shard.device)
+        shard.set_stream(self.stream)
+        try:
+            with torch.cuda.graph(self.graph, stream=self.stream):
+                _iterate([shard], comm, iters_per_graph, in_graph=True)
+        finally:
+            shard.set_stream(None)
+
+    def run(self, iters: int) -> None:
+        """Replay ceil(iters / iters_per_graph) graphs (whole graphs only)."""
+        for _ in range(-(-iters // self.n)):
+            self.graph.replay()
+
+
+def _iterate(shards, comm, iters, in_graph=False):
+    sched = shards[0].schedule
     for _ in range(iters):
         for sh in shards:
             sh.phase(1)
-        comm.exchange(X_GHAT, shards)
+        comm.exchange(X_GHAT, shards, in_graph)
         if sched == "twopass":
             for sh in shards:
                 sh.phase(2)
-            comm.exchange(X_OUTBOX, shards)
+            comm.exchange(X_OUTBOX, shards, in_graph)
             for sh in shards:
                 sh.phase(3)
-        comm.exchange(X_SCAL, shards)
+        comm.exchange(X_SCAL, shards, in_graph)
         for sh in shards:
             sh.phase(4)
 

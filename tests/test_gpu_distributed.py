@@ -42,3 +42,23 @@ def test_sharded_plans_match_oracle(method, M, N, shape, P, iters):
         np.testing.assert_array_equal(tr[:, :2], trs[0][:, :2])
     rd = trs[0][:, 1]
     assert np.max(np.abs(rd - ref["trace"][:, 1]) / np.abs(ref["trace"][:, 1])) <= 1e-8
+
+
+def test_graph_captured_nccl_iterations_match_eager():
+    """torchrun with one process (NCCL, no cross-process waiting): the CUDA-graph capture of
+    the distributed iteration (shard phases + NCCL all-gathers on one stream) reproduces the
+    eager iterations bit-for-bit."""
+    import json
+    import os
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+                        "--master-addr", "127.0.0.1", "--master-port", "29533",
+                        os.path.join(repo, "tools", "dist_check.py")], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    for method, res in out.items():
+        assert res["eager_vs_graph_maxabs"] == 0.0, (method, res)
+        assert res["iters"] == 16
+    assert out["hybrid"]["vs_single_plan_rel"] <= 1e-12
