@@ -228,10 +228,10 @@ def bench_distributed(args, cfg):
     torch.cuda.synchronize(local)
     dist.barrier()
     torch.cuda.synchronize(local)
-    stream = graphed.stream
+    stream = sh.stream()  # replays go onto the shard plan's own stream
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk, torch.cuda.stream(stream):
+    with ClockSampler(local) as clk:
         e0.record(stream)
         graphed.run(steps)
         e1.record(stream)

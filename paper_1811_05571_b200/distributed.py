@@ -271,9 +271,12 @@ class GraphedIterations:
             shard.set_stream(None)
 
     def run(self, iters: int) -> None:
-        """Replay ceil(iters / iters_per_graph) graphs (whole graphs only)."""
-        for _ in range(-(-iters // self.n)):
-            self.graph.replay()
+        """Replay ceil(iters / iters_per_graph) graphs (whole graphs only) on the shard
+        plan's own stream, ordered after its reset/prime and covered by its sync()."""
+        import torch
+        with torch.cuda.stream(self.shard.stream()):
+            for _ in range(-(-iters // self.n)):
+                self.graph.replay()
 
 
 def _iterate(shards, comm, iters, in_graph=False):
