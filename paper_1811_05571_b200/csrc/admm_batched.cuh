@@ -28,21 +28,6 @@ struct BTile {
   uint32_t k0, k1;  // k range of this unit (split-K)
 };
 
-// cp.async helpers (size 8 or 16, zero-fill when src_bytes = 0)
-__device__ __forceinline__ void cpa(void* smem, const void* src, bool ok) {
-  const uint32_t dst = (uint32_t)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0) : "memory");
-}
-__device__ __forceinline__ void cpa8(void* smem, const void* src, bool ok) {
-  const uint32_t dst = (uint32_t)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "r"(ok ? 8 : 0) : "memory");
-}
-__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cpa_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
 // out[t0 + i][b] = sum_{k in [k0,k1)} op(A)[t0 + i][k] X[k][b]
 //   ADJ = false: op(A)[i][k] = A[i][k]          (W = H C, Q = K R)
 //   ADJ = true:  op(A)[i][k] = conj(A[k][i])    (Z = H^H Q)

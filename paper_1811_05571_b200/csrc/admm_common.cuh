@@ -36,6 +36,21 @@ __device__ __forceinline__ double cabs2(double2 a) { return a.x * a.x + a.y * a.
 __device__ __forceinline__ bool cfinite(double2 a) { return isfinite(a.x) && isfinite(a.y); }
 
 // prox.hpp:15-19: |a| > kappa ? a (1 - kappa/|a|) : 0, with |a| = hypot.
+// Same result as soft_threshold, with a short path for |a| clearly below kappa (most
+// entries of a sparse iterate): |a|^2 < kappa^2 (1 - 2^-40) guarantees hypot(a) < kappa
+// (both are within a few ulp), so hypot and the division are skipped.  kappa2_lo =
+// kappa * kappa * (1 - 2^-40), precomputed.  NaN / overflow fall through to the full test.
+__device__ __forceinline__ double2 soft_threshold_fast(double2 a, double kappa, double kappa2_lo) {
+  const double r2 = a.x * a.x + a.y * a.y;
+  if (r2 < kappa2_lo) return make_double2(0.0, 0.0);
+  const double mag = hypot(a.x, a.y);
+  if (mag > kappa) {
+    const double f = 1.0 - kappa / mag;
+    return make_double2(a.x * f, a.y * f);
+  }
+  return make_double2(0.0, 0.0);
+}
+
 __device__ __forceinline__ double2 soft_threshold(double2 a, double kappa) {
   const double mag = hypot(a.x, a.y);
   if (mag > kappa) {
@@ -126,6 +141,21 @@ __device__ __forceinline__ double block_sum(double v, double* smem) {
     for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
   }
   return r;  // valid in thread 0
+}
+
+// cp.async helpers (size 8 or 16, zero-fill when src_bytes = 0)
+__device__ __forceinline__ void cpa(void* smem, const void* src, bool ok) {
+  const uint32_t dst = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cpa8(void* smem, const void* src, bool ok) {
+  const uint32_t dst = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "r"(ok ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
 }  // namespace admm

@@ -75,7 +75,7 @@ constexpr int kRowsPerWarpH = 4;          // gemv_h: rows per warp per tile
 constexpr int kRowTileH = kCtaWarps * kRowsPerWarpH;
 
 // Number of partial segments written for a run of units [first, first+count).
-__device__ __forceinline__ uint32_t seg_count(uint64_t first, uint64_t count, uint64_t U,
+__host__ __device__ __forceinline__ uint32_t seg_count(uint64_t first, uint64_t count, uint64_t U,
                                               uint64_t P) {
   return (uint32_t)(sk_owner(first + count - 1, U, P) - sk_owner(first, U, P) + 1);
 }
@@ -531,15 +531,16 @@ __global__ void local_scalars_kernel(const double* __restrict__ red, uint32_t n,
 
 // Close an iteration from the all-gathered scalars (rank order): trace[k] and the
 // non-finite bookkeeping, identically on every rank.
-__global__ void close_kernel(const double* __restrict__ all, uint32_t nranks, const Params* __restrict__ prm,
-                             double* __restrict__ trace, uint64_t trace_cap, IterState* st) {
+__global__ void close_kernel(const double* __restrict__ all, uint32_t nranks, uint64_t stride,
+                             const Params* __restrict__ prm, double* __restrict__ trace, uint64_t trace_cap,
+                             IterState* st) {
   if (threadIdx.x != 0) return;
   double a = 0.0, d = 0.0;
   bool bad = false;
-  for (uint32_t r = 0; r < nranks; ++r) {
-    a += all[4 * r];
-    d += all[4 * r + 1];
-    bad |= all[4 * r + 3] != 0.0;
+  for (uint32_t r = 0; r < nranks; ++r) {  // rank order; `stride` doubles between rank slots
+    a += all[stride * r];
+    d += all[stride * r + 1];
+    bad |= all[stride * r + 3] != 0.0;
   }
   const uint64_t k = st->iter;
   if (k < trace_cap) {

@@ -27,6 +27,7 @@
 #include "admm_kernels.cuh"
 #include "admm_setup.cuh"
 #include "admm_sweep.cuh"
+#include "admm_tile.cuh"
 #include "admm_batched.cuh"
 
 using namespace admm;
@@ -139,6 +140,9 @@ struct admm_plan {
   double2* ghat_ptr = nullptr;     // ghat exchange buffer (internal or attached)
   double2* outbox_ptr = nullptr;
   double* scal_ptr = nullptr;
+  bool fused_scal = false;   // Pr == 1, Pc > 1: scalars ride in the ghat all-gather slot
+  uint64_t gslot = 0;        // ghat slot per rank (complex elements)
+  bool keep_l2 = false;      // local H + K fit in L2: keep H resident across iterations
   bool ragged = false, trace_obj = false;
   admm_solver_config cfg{};
   std::vector<uint64_t> rb, cb;
@@ -161,12 +165,17 @@ struct admm_plan {
   int schedule = 1;             // 1 two-pass, 2 single-HBM-pass sweep
   int sweep_lpr = 8;
   bool sweep_bulk = false;  // TMA producer variant (sweep_bulk_kernel)
+  int tile_rb = 0;          // > 0: strip-major SMEM-resident sweep (sweep_tile_kernel), row bytes
+  uint32_t tile_ns = 0;     // its SMEM ring slots (32-row tasks)
+  int tile_cps = 1;         // its CTAs per SM
+  DevBuf dHt;               // strip-major copy of H for sweep_tile_kernel
+  DevBuf dtrace_tile;       // ADMM_B200_TILE_TRACE: per-strip phase timestamps
   DevBuf dtmaps;            // one CUtensorMap per local block
   std::vector<SweepDesc> segs;
   DevBuf dsegs, dwpart_s;
   Geom gS;
   size_t sweep_smem = 0;
-  uint32_t zgx = 0, rgx = 0, ogx = 0, nz = 0, no = 0;
+  uint32_t zgx = 0, rgx = 0, rgx_s = 0, ogx = 0, nz = 0, no = 0;
   uint64_t trace_cap = 0;
   cudaGraphExec_t exec = nullptr;
   uint64_t graph_iters = 0;
@@ -361,10 +370,10 @@ bool try_sweep(admm_plan* p, size_t l2_budget) {
     p->sweep_bulk = false;
   }
   if (smem > 225 * 1024) return false;
-  CK(cudaFuncSetAttribute(sweep_kernel<S, LPR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)std::min<size_t>(smem, 225 * 1024)));
+  for (auto fn : {sweep_kernel<S, LPR, false>, sweep_kernel<S, LPR, true>})
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::min<size_t>(smem, 225 * 1024)));
   int occ = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_kernel<S, LPR>, kSweepThreads, smem));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_kernel<S, LPR, false>, kSweepThreads, smem));
   if (occ < 1) return false;
   occ = 1;  // one warp-specialised CTA per SM (exactly num_sms CTAs: no wave imbalance)
   if (p->Pr != 1) return false;  // the replica mean needs every row block of a strip
@@ -388,8 +397,76 @@ bool try_sweep(admm_plan* p, size_t l2_budget) {
   p->gS.P = P;
   p->sweep_lpr = LPR;
   p->sweep_smem = smem;
+  p->keep_l2 = (p->h_elems + p->k_elems) * sizeof(S) <= (96ull << 20);
+  if (const char* env = std::getenv("ADMM_B200_KEEP_L2")) p->keep_l2 = env[0] == '1';
   p->dwpart_s.alloc(po * sizeof(double2));
   upload_desc(p->dsegs, segs.data(), segs.size() * sizeof(SweepDesc));
+  return true;
+}
+
+// Strip-major SMEM-resident sweep with RB bytes per strip row: possible when a whole
+// strip (n_meas x RB) plus two chunks of slack fits the SMEM ring next to q, w and the
+// per-strip scratch.  No L2 budget: each strip crosses L2 once.
+template <typename S, int RB>
+bool try_tile(admm_plan* p) {
+  using G = TileGeom<S, RB>;
+  constexpr int W = G::W;
+  if (p->Pr != 1) return false;  // the replica mean needs every row block of a strip
+  // opt-in while it trails the LDG sweep (profiles/r01_summary.md)
+  const char* env = std::getenv("ADMM_B200_SWEEP");
+  if (!env || std::strcmp(env, "tile") != 0) return false;
+  if (const char* rb = std::getenv("ADMM_B200_TILE_RB"))      // diagnostics: force the row width
+    if (std::atoi(rb) != RB) return false;
+  int cps = 1;  // CTAs per SM
+  if (const char* e = std::getenv("ADMM_B200_TILE_CTAS")) cps = std::max(1, std::atoi(e));
+  // dynamic SMEM per CTA: 228 KB per SM less 1 KB per CTA and the static part
+  const size_t cap = (228 * 1024) / cps - 2 * 1024;
+  const size_t fixed = tile_smem_bytes(0, G::TB, (uint32_t)p->n_meas, (uint32_t)p->Mr, (uint32_t)p->Nc, W);
+  if (fixed >= cap) return false;
+  const uint32_t ns = (uint32_t)std::min<size_t>((cap - fixed) / (G::TB + 2 * sizeof(uint64_t)), 256);
+  const uint32_t ntask = (uint32_t)cdiv(p->n_meas, kTileRows);
+  if (ns < 2 * ntask + 2) return false;  // (C) runs a strip ahead of (A)
+  const size_t smem = tile_smem_bytes(ns, G::TB, (uint32_t)p->n_meas, (uint32_t)p->Mr, (uint32_t)p->Nc, W);
+  auto k0 = cps == 2 ? sweep_tile_kernel<S, RB, false, 2> : sweep_tile_kernel<S, RB, false, 1>;
+  auto k1 = cps == 2 ? sweep_tile_kernel<S, RB, true, 2> : sweep_tile_kernel<S, RB, true, 1>;
+  for (auto fn : {k0, k1}) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k0, kTileThreads, smem));
+  if (occ < cps) return false;
+  std::vector<SweepDesc> segs(p->Nc);
+  uint64_t u = 0;
+  for (uint64_t j = 0; j < p->Nc; ++j) {
+    const uint32_t cols = p->blocks[j].cols;
+    segs[j] = SweepDesc{u, 0, (uint32_t)cdiv(cols, W), cols};
+    u += segs[j].n_strips;
+  }
+  const uint64_t P = std::min<uint64_t>(u, (uint64_t)p->num_sms * cps);
+  uint64_t po = 0;
+  for (auto& sd : segs) {  // one partial slot per CTA overlapping the segment
+    sd.part_off = po;
+    po += (uint64_t)seg_count(sd.unit0, sd.n_strips, u, P) * p->n_meas;
+  }
+  p->segs = segs;
+  p->gS.U = u;
+  p->gS.P = P;
+  p->tile_rb = RB;
+  p->tile_ns = ns;
+  p->tile_cps = cps;
+  p->sweep_smem = smem;
+  p->sweep_bulk = false;
+  p->keep_l2 = (u * p->n_meas * W + p->k_elems) * sizeof(S) <= (96ull << 20);
+  if (const char* e2 = std::getenv("ADMM_B200_KEEP_L2")) p->keep_l2 = e2[0] == '1';
+  p->dwpart_s.alloc(po * sizeof(double2));
+  upload_desc(p->dsegs, segs.data(), segs.size() * sizeof(SweepDesc));
+  p->dHt.alloc(u * p->n_meas * W * sizeof(S));
+  if (std::getenv("ADMM_B200_TILE_TRACE")) {
+    p->dtrace_tile.alloc(P * 64 * 8 * sizeof(unsigned long long));
+    CK(cudaMemset(p->dtrace_tile.p, 0, P * 64 * 8 * sizeof(unsigned long long)));
+    if (std::getenv("ADMM_B200_TILE_NOLOAD")) {  // trace[7] = 1: consumer-only timing
+      const unsigned long long one = 1;
+      CK(cudaMemcpy(p->dtrace_tile.as<unsigned long long>() + 7, &one, sizeof(one), cudaMemcpyHostToDevice));
+    }
+  }
   return true;
 }
 
@@ -397,6 +474,10 @@ template <typename S>
 void choose_schedule(admm_plan* p, int requested) {
   p->schedule = 1;
   if (requested == 1) return;
+  if (try_tile<S, 128>(p) || try_tile<S, 64>(p)) {
+    p->schedule = 2;
+    return;
+  }
   const size_t budget = 80ull << 20;  // open strips must stay well inside the 126 MB L2
   // 64-byte strips (LPR = 2) only on request: measured slower than two-pass on config 3
   if (try_sweep<S, 8>(p, budget) || try_sweep<S, 4>(p, budget) || (requested == 2 && try_sweep<S, 2>(p, budget))) {
@@ -469,6 +550,19 @@ void upload_h(admm_plan* p, const void* h, admm_dtype h_dtype) {
   CK(cudaMemcpyAsync(&hf, flag.p, 4, cudaMemcpyDeviceToHost, p->stream));
   CK(cudaStreamSynchronize(p->stream));
   if (hf) throw Fail{ADMM_E_NUMERICAL, "SensingProblem: non-finite entries"};
+}
+
+// Strip-major copy of the (scaled) H for sweep_tile_kernel.
+template <typename S>
+void build_tile(admm_plan* p) {
+  const uint32_t W = (uint32_t)(p->tile_rb / sizeof(S));
+  const uint64_t total = p->gS.U * p->n_meas * W;
+  tile_h_kernel<S><<<p->num_sms * 8, 256, 0, p->stream>>>(p->dH.as<S>(), p->dhN.as<MatDesc>(),
+                                                          p->dblocks.as<BlockDesc>(), p->dsegs.as<SweepDesc>(),
+                                                          (uint32_t)p->Mr, (uint32_t)p->Nc, (uint32_t)p->n_meas, W,
+                                                          total, p->dHt.as<S>());
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(p->stream));
 }
 
 // rho I + H H^H per block, Gauss-Jordan inverse, store K (gram.hpp:48-53,92-122;
@@ -591,10 +685,10 @@ void enqueue_iteration_twopass(admm_plan* p, cudaStream_t s, bool with_objective
 template <typename S>
 void enqueue_sweep_prologue(admm_plan* p, cudaStream_t s) {
   const int nb = (int)p->blocks.size();
-  rows_finalize_sweep_kernel<<<dim3(p->rgx, nb), kCtaThreads, 0, s>>>(
+  rows_finalize_sweep_kernel<<<dim3(p->rgx_s, nb), kCtaThreads, 0, s>>>(
       row_vecs(p), p->dwpart_s.as<double2>(), p->dsegs.as<SweepDesc>(), p->dblocks.as<BlockDesc>(),
-      p->dgblocks.as<BlockDesc>(), (uint32_t)p->N, (uint32_t)p->n_meas, p->gS.U, p->gS.P, 1, 0, p->dred.as<double>(), p->dparams.as<Params>(),
-      p->dtrace.as<double>(), p->trace_cap, p->dstate.as<IterState>());
+      p->dgblocks.as<BlockDesc>(), (uint32_t)p->N, (uint32_t)p->n_meas, p->gS.U, p->gS.P, 1, 0, p->dred.as<double>(),
+      p->dparams.as<Params>(), p->dtrace.as<double>(), p->trace_cap, p->dstate.as<IterState>(), nullptr);
   gemv_n_kernel<S, kVN, kEvictNormal><<<(unsigned)p->gK.P, kCtaThreads, 0, s>>>(
       p->dK.as<S>(), p->dr.as<double2>(), p->dqpart.as<double2>(), p->dkN.as<MatDesc>(), nb, p->gK.U);
   rows_finalize_kernel<kQ><<<dim3(p->rgx, nb), kCtaThreads, 0, s>>>(
@@ -615,15 +709,31 @@ void launch_sweep_lpr(admm_plan* p, cudaStream_t s) {
       return;
     }
   }
-  sweep_kernel<S, LPR><<<(unsigned)p->gS.P, kSweepThreads, p->sweep_smem, s>>>(
+  auto fn = p->keep_l2 ? sweep_kernel<S, LPR, true> : sweep_kernel<S, LPR, false>;
+  fn<<<(unsigned)p->gS.P, kSweepThreads, p->sweep_smem, s>>>(
       p->dH.as<S>(), p->dhN.as<MatDesc>(), p->dblocks.as<BlockDesc>(), p->dsegs.as<SweepDesc>(), (uint32_t)p->Mr,
       (uint32_t)p->Nc, (uint32_t)p->n_meas, p->gS.U, p->dq.as<double2>(), col_vecs(p), p->dwpart_s.as<double2>(),
       p->dparams.as<Params>(), p->dred.as<double>(), p->dstate.as<IterState>());
 }
 
+template <typename S, int RB>
+void launch_tile_rb(admm_plan* p, cudaStream_t s) {
+  auto fn = p->tile_cps == 2 ? (p->keep_l2 ? sweep_tile_kernel<S, RB, true, 2> : sweep_tile_kernel<S, RB, false, 2>)
+                             : (p->keep_l2 ? sweep_tile_kernel<S, RB, true, 1> : sweep_tile_kernel<S, RB, false, 1>);
+  fn<<<(unsigned)p->gS.P, kTileThreads, p->sweep_smem, s>>>(
+      p->dHt.as<S>(), p->dblocks.as<BlockDesc>(), p->dsegs.as<SweepDesc>(), (uint32_t)p->Mr, (uint32_t)p->Nc,
+      (uint32_t)p->n_meas, p->gS.U, p->tile_ns, p->dq.as<double2>(), col_vecs(p), p->dwpart_s.as<double2>(),
+      p->dparams.as<Params>(), p->dred.as<double>(), p->dstate.as<IterState>(),
+      p->dtrace_tile.p ? p->dtrace_tile.as<unsigned long long>() : nullptr);
+}
+
 template <typename S>
 void launch_sweep(admm_plan* p, cudaStream_t s) {
-  if (p->sweep_lpr == 8)
+  if (p->tile_rb == 128)
+    launch_tile_rb<S, 128>(p, s);
+  else if (p->tile_rb == 64)
+    launch_tile_rb<S, 64>(p, s);
+  else if (p->sweep_lpr == 8)
     launch_sweep_lpr<S, 8>(p, s);
   else if (p->sweep_lpr == 4)
     launch_sweep_lpr<S, 4>(p, s);
@@ -649,10 +759,10 @@ void enqueue_iteration_sweep(admm_plan* p, cudaStream_t s, bool with_objective, 
         p->dg.as<double2>(), p->dopart.as<double2>(), p->dhNv.as<MatDesc>(), p->dblocks.as<BlockDesc>(),
         (uint32_t)p->Nc, p->gO.U, p->gO.P, p->dored.as<double>());
   }
-  rows_finalize_sweep_kernel<<<dim3(p->rgx, nb), kCtaThreads, 0, s>>>(
+  rows_finalize_sweep_kernel<<<dim3(p->rgx_s, nb), kCtaThreads, 0, s>>>(
       row_vecs(p), p->dwpart_s.as<double2>(), p->dsegs.as<SweepDesc>(), p->dblocks.as<BlockDesc>(),
-      p->dgblocks.as<BlockDesc>(), (uint32_t)p->N, (uint32_t)p->n_meas, p->gS.U, p->gS.P, 0, 1, p->dred.as<double>(), p->dparams.as<Params>(),
-      p->dtrace.as<double>(), p->trace_cap, p->dstate.as<IterState>());
+      p->dgblocks.as<BlockDesc>(), (uint32_t)p->N, (uint32_t)p->n_meas, p->gS.U, p->gS.P, 0, 1, p->dred.as<double>(),
+      p->dparams.as<Params>(), p->dtrace.as<double>(), p->trace_cap, p->dstate.as<IterState>(), nullptr);
   mark(2);
   if (with_objective) {  // the sweep's finalize wrote NaN: fill the objective of this iteration
     objective_trace_kernel<<<1, kCtaThreads, 0, s>>>(p->dred.as<double>(), (uint32_t)p->gS.P, p->dored.as<double>(),
@@ -1043,6 +1153,9 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
   // layouts so that all-gathers land every peer vector where the kernels look for it:
   //   ghat:   [pc'][il][jl][mpad]  for blocks in this plan's row blocks (row comm order)
   //   outbox: [i][jl][npad]        for blocks in this plan's column blocks (column comm order)
+  // column-sharded grids reserve 4 doubles after each rank's ghat slot; the sweep schedule
+  // (scalars ready before the ghat exchange) uses them instead of a separate all-gather
+  p->gslot = p->Mr * p->Nc * p->mpad + (p->Pr == 1 && p->Pc > 1 ? 2 : 0);
   p->gblocks.assign(p->M * p->N, BlockDesc{});
   for (uint64_t i = 0; i < p->M; ++i)
     for (uint64_t q = 0; q < p->N; ++q) {
@@ -1056,7 +1169,7 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
       const bool own_row = i >= p->i0 && i < p->i0 + p->Mr;
       const bool own_col = q >= p->j0 && q < p->j0 + p->Nc;
       const uint64_t il = i - p->i0, jl = q - p->j0;
-      if (own_row) b.mvec_off = (uint32_t)((((q / p->Nc) * p->Mr + il) * p->Nc + q % p->Nc) * p->mpad);
+      if (own_row) b.mvec_off = (uint32_t)((q / p->Nc) * p->gslot + (il * p->Nc + q % p->Nc) * p->mpad);
       if (own_col) {
         b.jl = (uint32_t)jl;
         b.seg_off = (uint32_t)(jl * p->npad);
@@ -1073,7 +1186,7 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
       p->max_seg = std::max(p->max_seg, b.cols);
       p->max_rowblock = std::max(p->max_rowblock, b.rows);
     }
-  p->mvec_total = p->Pc * p->Mr * p->Nc * p->mpad;
+  p->mvec_total = p->Pc * p->gslot;
   p->vec_total = p->Mr * p->Nc * p->npad;
   p->seg_total = p->Nc * p->npad;
   p->outbox_total = p->M * p->Nc * p->npad;
@@ -1106,7 +1219,9 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
   for (DevBuf* d : {&p->dghat, &p->dgij, &p->dr, &p->dq}) d->alloc(p->mvec_total * 16 * p->batch);
   p->ghat_ptr = p->dghat.as<double2>();
   p->outbox_ptr = p->doutbox.as<double2>();
-  p->scal_ptr = p->dscal.as<double>();
+  p->fused_scal = p->Pr == 1 && p->Pc > 1 && p->schedule == 2;
+  p->scal_ptr = p->fused_scal ? reinterpret_cast<double*>(p->ghat_ptr + p->Mr * p->Nc * p->mpad)
+                              : p->dscal.as<double>();
   for (DevBuf* d : {&p->du, &p->ds, &p->dc}) d->alloc(p->vec_total * 16 * p->batch);
   for (DevBuf* d : {&p->dv, &p->dvprev}) d->alloc(p->seg_total * 16 * p->batch);
   p->dg.alloc(p->n_meas * 16 * p->batch);
@@ -1114,6 +1229,7 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
   p->dstate.alloc(sizeof(IterState));
   p->dobj.alloc(sizeof(double));
   p->rgx = (uint32_t)cdiv(p->max_rows, kCtaThreads);
+  p->rgx_s = (uint32_t)cdiv(p->max_rows, kRfRows);
   p->zgx = (uint32_t)cdiv(p->max_seg, kCtaThreads);
   p->ogx = (uint32_t)cdiv(p->max_rowblock, kCtaThreads);
   p->nz = p->zgx * (uint32_t)p->Nc;
@@ -1124,9 +1240,11 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
 
   if (p->dtype == ADMM_C128) {
     upload_h<double2>(p.get(), h, h_dtype);
+    if (p->tile_rb) build_tile<double2>(p.get());
     factor_blocks<double2>(p.get());
   } else {
     upload_h<float2>(p.get(), h, h_dtype);
+    if (p->tile_rb) build_tile<float2>(p.get());
     factor_blocks<float2>(p.get());
   }
   if (p->batch > 1) {
@@ -1168,6 +1286,28 @@ admm_status admm_plan_create(const admm_plan_options* opts, const admm_solver_co
 void admm_plan_destroy(admm_plan* plan) {
   if (plan) {
     cudaSetDevice(plan->device);
+    if (plan->dtrace_tile.p) {  // diagnostics: mean phase durations of the last sweep launch
+      const size_t n = plan->gS.P * 64 * 8;
+      std::vector<unsigned long long> t(n);
+      cudaMemcpy(t.data(), plan->dtrace_tile.p, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+      double acc[5] = {0, 0, 0, 0, 0};
+      uint64_t cnt = 0;
+      for (uint64_t c = 0; c < plan->gS.P; ++c)
+        for (int x = 1; x + 1 < 64; ++x) {
+          const unsigned long long* d = &t[(c * 64 + x - 1) * 8];
+          const unsigned long long* e = &t[(c * 64 + x) * 8];
+          if (!e[0] || !e[4] || !d[4]) continue;
+          acc[0] += (double)(e[1] - e[0]);  // (C)
+          acc[1] += (double)(e[0] - d[1]);  // (C) side: waiting for zred / loop
+          acc[2] += (double)(e[2] - d[4]);  // (A) side: waiting for (C)
+          acc[3] += (double)(e[3] - e[2]);  // (D)
+          acc[4] += (double)(e[4] - e[3]);  // stores + (A)
+          ++cnt;
+        }
+      if (cnt)
+        std::fprintf(stderr, "tile trace (SM cycles/strip over %llu strips): C %.0f  C-wait %.0f | A-wait %.0f  D %.0f  A %.0f\n",
+                     (unsigned long long)cnt, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt);
+    }
     delete plan;
   }
 }
@@ -1498,6 +1638,9 @@ admm_status admm_plan_solve(admm_plan* p, double* solution, double* trace, uint6
 // ---- multi-GPU phases (admm_b200.h) --------------------------------------------
 namespace {
 
+// doubles between consecutive ranks' scalar slots
+uint64_t scal_stride(const admm_plan* p) { return p->fused_scal ? 2 * p->gslot : 4; }
+
 template <typename S>
 void enqueue_phase(admm_plan* p, int phase) {
   cudaStream_t s = p->stream;
@@ -1505,14 +1648,11 @@ void enqueue_phase(admm_plan* p, int phase) {
   if (phase == 1) {
     if (p->schedule == 2) {
       launch_sweep<S>(p, s);
-      rows_finalize_sweep_kernel<<<dim3(p->rgx, nb), kCtaThreads, 0, s>>>(
+      rows_finalize_sweep_kernel<<<dim3(p->rgx_s, nb), kCtaThreads, 0, s>>>(
           row_vecs(p), p->dwpart_s.as<double2>(), p->dsegs.as<SweepDesc>(), p->dblocks.as<BlockDesc>(),
-          p->dgblocks.as<BlockDesc>(), (uint32_t)p->N, (uint32_t)p->n_meas, p->gS.U, p->gS.P, 0, 0,
+          p->dgblocks.as<BlockDesc>(), (uint32_t)p->N, (uint32_t)p->n_meas, p->gS.U, p->gS.P, 0, 2,
           p->dred.as<double>(), p->dparams.as<Params>(), p->dtrace.as<double>(), p->trace_cap,
-          p->dstate.as<IterState>());
-      local_scalars_kernel<<<1, kCtaThreads, 0, s>>>(p->dred.as<double>(), (uint32_t)p->gS.P,
-                                                     p->scal_ptr + 4 * (p->pr * p->Pc + p->pc),
-                                                     p->dstate.as<IterState>());
+          p->dstate.as<IterState>(), p->scal_ptr + scal_stride(p) * (p->pr * p->Pc + p->pc));
     } else {
       gemv_n_kernel<S, kVN, kEvictNormal><<<(unsigned)p->gN.P, kCtaThreads, 0, s>>>(
           p->dH.as<S>(), p->dc.as<double2>(), p->dwpart.as<double2>(), p->dhN.as<MatDesc>(), nb, p->gN.U);
@@ -1538,10 +1678,10 @@ void enqueue_phase(admm_plan* p, int phase) {
         col_vecs(p), p->outbox_ptr, p->dblocks.as<BlockDesc>(), (uint32_t)p->M, (uint32_t)p->Mr,
         (uint32_t)p->Nc, (uint32_t)p->npad, p->pr == 0 ? 1 : 0, p->dparams.as<Params>(), p->dred.as<double>());
     local_scalars_kernel<<<1, kCtaThreads, 0, s>>>(p->dred.as<double>(), p->nz,
-                                                   p->scal_ptr + 4 * (p->pr * p->Pc + p->pc),
+                                                   p->scal_ptr + scal_stride(p) * (p->pr * p->Pc + p->pc),
                                                    p->dstate.as<IterState>());
   } else if (phase == 4) {
-    close_kernel<<<1, 32, 0, s>>>(p->scal_ptr, (uint32_t)(p->Pr * p->Pc), p->dparams.as<Params>(),
+    close_kernel<<<1, 32, 0, s>>>(p->scal_ptr, (uint32_t)(p->Pr * p->Pc), scal_stride(p), p->dparams.as<Params>(),
                                   p->dtrace.as<double>(), p->trace_cap, p->dstate.as<IterState>());
   } else {
     throw Fail{ADMM_E_PARAMETER, "unknown phase"};
@@ -1567,16 +1707,16 @@ admm_status admm_plan_exchange_info(const admm_plan* p, int which, uint64_t* tot
   return run_guarded([&] {
     if (!p) throw Fail{ADMM_E_STATE, "null plan"};
     uint64_t t = 0, o = 0, b = 0;
-    if (which == ADMM_X_GHAT) {  // [pc][Mr][Nc][mpad]
-      b = p->Mr * p->Nc * p->mpad * 16;
+    if (which == ADMM_X_GHAT) {  // [pc][Mr][Nc][mpad] (+ 4 scalar doubles when fused)
+      b = p->gslot * 16;
       t = p->Pc * b;
       o = p->pc * b;
     } else if (which == ADMM_X_OUTBOX) {  // [i = pr*Mr + il][Nc][npad]
       b = p->Mr * p->Nc * p->npad * 16;
       t = p->Pr * b;
       o = p->pr * b;
-    } else if (which == ADMM_X_SCAL) {  // [rank][4]
-      b = 4 * sizeof(double);
+    } else if (which == ADMM_X_SCAL) {  // [rank][4]; 0 bytes: fused into the ghat exchange
+      b = p->fused_scal ? 0 : 4 * sizeof(double);
       t = p->Pr * p->Pc * b;
       o = (p->pr * p->Pc + p->pc) * b;
     } else {
@@ -1592,14 +1732,16 @@ admm_status admm_plan_attach(admm_plan* p, int which, void* ptr) {
   return run_guarded([&] {
     check_plan(p);
     if (!ptr) throw Fail{ADMM_E_STATE, "null device pointer"};
-    if (which == ADMM_X_GHAT)
+    if (which == ADMM_X_GHAT) {
       p->ghat_ptr = static_cast<double2*>(ptr);
-    else if (which == ADMM_X_OUTBOX)
+      if (p->fused_scal) p->scal_ptr = reinterpret_cast<double*>(p->ghat_ptr + p->Mr * p->Nc * p->mpad);
+    } else if (which == ADMM_X_OUTBOX) {
       p->outbox_ptr = static_cast<double2*>(ptr);
-    else if (which == ADMM_X_SCAL)
-      p->scal_ptr = static_cast<double*>(ptr);
-    else
+    } else if (which == ADMM_X_SCAL) {
+      if (!p->fused_scal) p->scal_ptr = static_cast<double*>(ptr);
+    } else {
       throw Fail{ADMM_E_PARAMETER, "unknown exchange buffer"};
+    }
     if (p->exec) {  // captured graphs hold the old pointers
       cudaGraphExecDestroy(p->exec);
       p->exec = nullptr;

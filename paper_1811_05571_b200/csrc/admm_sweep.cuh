@@ -48,7 +48,9 @@ enum SweepBar { kBarA = 2, kBarFull0 = 3, kBarEmpty0 = 5 };
 // Each producer warp hands its partial z over through a double-buffered SMEM slot
 // guarded by named FULL/EMPTY barriers (the consumer adds the 8 partials in warp
 // order), so the HBM stream never waits on a barrier of its own group.
-template <typename S, int LPR>
+// KeepL2: the whole local H (+ K) fits in L2 (multi-GPU shards): the re-read keeps the
+// lines (evict_last) so the next iteration's stream is an L2 hit too.
+template <typename S, int LPR, bool KeepL2>
 __global__ void __launch_bounds__(kSweepThreads, 1)
 sweep_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const BlockDesc* __restrict__ blocks,
              const SweepDesc* __restrict__ segs, uint32_t M, uint32_t N, uint32_t n_meas, uint64_t Utot,
@@ -209,7 +211,7 @@ sweep_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const Bloc
             for (int u = 0; u < kSweepUA; ++u) {
               const uint32_t row = r0 + u * CSTEP;
               if (row < md.rows && cok) {
-                hv[u] = ld_stream256<kEvictFirst>(hb + (uint64_t)row * md.ld);
+                hv[u] = ld_stream256<KeepL2 ? kEvictLast : kEvictFirst>(hb + (uint64_t)row * md.ld);
               } else {
                 hv[u].w[0] = hv[u].w[1] = hv[u].w[2] = hv[u].w[3] = 0;
               }
@@ -551,47 +553,70 @@ sweep_bulk_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const
 }
 
 // r_b = g_ij - w_b with w_b summed from the sweep partials of segment j in fixed
-// CTA order (first = 1: w = 0, the prologue of a solve since c^0 = 0).  CTA (0,0)
-// also closes the previous sweep's iteration (trace, non-finite bookkeeping).
+// order (first = 1: w = 0, the prologue of a solve since c^0 = 0).  A CTA owns
+// kRfRows rows; its kRfGroups warps-per-row-tile each sum every kRfGroups-th
+// partial (a segment may have one partial per sweep CTA, ~148 when one block is
+// resident), then group 0 adds the group sums in order: bit-reproducible.
+// CTA (0,0) also closes the sweep's iteration: fin = 1 writes trace[k] (one
+// device), fin = 2 writes this rank's 4 scalars into `slot` (sharded plans).
+constexpr int kRfRows = 32;
+constexpr int kRfGroups = kCtaThreads / kRfRows;
+
 __global__ void __launch_bounds__(kCtaThreads)
 rows_finalize_sweep_kernel(RowVecs rv, const double2* __restrict__ wpart, const SweepDesc* __restrict__ segs,
                            const BlockDesc* __restrict__ blocks, const BlockDesc* __restrict__ gblocks, uint32_t N,
-                           uint32_t n_meas, uint64_t Utot,
-                           uint64_t Psweep, int first, int do_finalize, const double* __restrict__ red,
-                           const Params* __restrict__ prm, double* __restrict__ trace, uint64_t trace_cap,
-                           IterState* st) {
+                           uint32_t n_meas, uint64_t Utot, uint64_t Psweep, int first, int fin,
+                           const double* __restrict__ red, const Params* __restrict__ prm,
+                           double* __restrict__ trace, uint64_t trace_cap, IterState* st,
+                           double* __restrict__ slot) {
   __shared__ double sm[kCtaWarps];
+  __shared__ double2 gsum[kRfGroups][kRfRows];
   const uint32_t b = blockIdx.y;
   const BlockDesc bd = blocks[b];
-  const uint32_t row = blockIdx.x * blockDim.x + threadIdx.x;
-  if (row < bd.rows) {
+  const uint32_t tr = threadIdx.x % kRfRows, grp = threadIdx.x / kRfRows;
+  const uint32_t row = blockIdx.x * kRfRows + tr;
+  if (blockIdx.x * kRfRows < bd.rows) {  // CTA-uniform
     double2 w = make_double2(0.0, 0.0);
-    if (!first) {
+    if (!first && row < bd.rows) {
       const SweepDesc sd = segs[bd.jl];
       const uint32_t ns = seg_count(sd.unit0, sd.n_strips, Utot, Psweep);
       const double2* src = wpart + sd.part_off + bd.row0 + row;
-      w = src[0];
-#pragma unroll 8
-      for (uint32_t k = 1; k < ns; ++k) w = cadd(w, src[(uint64_t)k * n_meas]);
+#pragma unroll 4
+      for (uint32_t k = grp; k < ns; k += kRfGroups) w = cadd(w, src[(uint64_t)k * n_meas]);
     }
-    double2 gij = rv.g[bd.row0 + row];
-    for (uint32_t qj = 0; qj < N; ++qj) {
-      if (qj == bd.j) continue;
-      gij = csub(gij, rv.ghat[gblocks[bd.i * N + qj].mvec_off + row]);  // global table: peers too
+    gsum[grp][tr] = w;
+    __syncthreads();
+    if (grp == 0 && row < bd.rows) {
+      for (int g2 = 1; g2 < kRfGroups; ++g2) w = cadd(w, gsum[g2][tr]);
+      double2 gij = rv.g[bd.row0 + row];
+      for (uint32_t qj = 0; qj < N; ++qj) {
+        if (qj == bd.j) continue;
+        gij = csub(gij, rv.ghat[gblocks[bd.i * N + qj].mvec_off + row]);  // global table: peers too
+      }
+      const uint32_t o = bd.mvec_off + row;
+      rv.gij[o] = gij;
+      rv.r[o] = csub(gij, w);
     }
-    const uint32_t o = bd.mvec_off + row;
-    rv.gij[o] = gij;
-    rv.r[o] = csub(gij, w);
   }
-  if (do_finalize && blockIdx.x == 0 && blockIdx.y == 0) {
-    double a = 0.0, d = 0.0;
+  if (fin && blockIdx.x == 0 && blockIdx.y == 0) {
+    double a = 0.0, d = 0.0, l = 0.0;
     for (uint32_t k = threadIdx.x; k < Psweep; k += kCtaThreads) {
       a += red[k];
       d += red[Psweep + k];
+      if (fin == 2) l += red[2 * Psweep + k];
     }
     a = block_sum<kCtaThreads>(a, sm);
     d = block_sum<kCtaThreads>(d, sm);
+    if (fin == 2) l = block_sum<kCtaThreads>(l, sm);
     if (threadIdx.x == 0) {
+      if (fin == 2) {  // same values and order as local_scalars_kernel
+        slot[0] = a;
+        slot[1] = d;
+        slot[2] = l;
+        slot[3] = st->nonfinite ? 1.0 : 0.0;
+        st->nonfinite = 0u;
+        return;
+      }
       const uint64_t k = st->iter;
       if (k < trace_cap) {
         trace[3 * k] = sqrt(a);

@@ -84,11 +84,15 @@ class ShardPlan:
         check(_lib.lib.admm_plan_schedule(handle, ctypes.byref(sched)))
         self.schedule = "sweep" if sched.value == 1 else "twopass"
         self.buffers, self.slots = {}, {}
+        self.fused_scal = False
         dev = torch.device("cuda", self.device)
         for which in (X_GHAT, X_OUTBOX, X_SCAL):
             tot, off, nb = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
             check(_lib.lib.admm_plan_exchange_info(handle, which, ctypes.byref(tot), ctypes.byref(off),
                                                    ctypes.byref(nb)))
+            if tot.value == 0:  # scalars fused into the ghat exchange (Pr == 1)
+                self.fused_scal = True
+                continue
             buf = torch.zeros(tot.value // 8, dtype=torch.float64, device=dev)
             check(_lib.lib.admm_plan_attach(handle, which, ctypes.c_void_p(buf.data_ptr())))
             self.buffers[which] = buf
@@ -291,7 +295,8 @@ def _iterate(shards, comm, iters, in_graph=False):
             comm.exchange(X_OUTBOX, shards, in_graph)
             for sh in shards:
                 sh.phase(3)
-        comm.exchange(X_SCAL, shards, in_graph)
+        if not getattr(shards[0], "fused_scal", False):  # else the scalars rode with ghat
+            comm.exchange(X_SCAL, shards, in_graph)
         for sh in shards:
             sh.phase(4)
 

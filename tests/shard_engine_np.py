@@ -45,15 +45,27 @@ class NumpyShard:
                 hb = h[i * self.mb:(i + 1) * self.mb, j * self.nb:(j + 1) * self.nb]
                 self.H[il, jl] = hb
                 self.K[il, jl] = np.linalg.inv(rho * np.eye(self.mb) + hb @ hb.conj().T)
-        # exchange buffers (float64 views of complex arrays), slots in rank order
-        self.ghat = np.zeros((self.Pc, self.Mr, self.Nc, self.mb), np.complex128)
+        # exchange buffers (float64 views of complex arrays), slots in rank order.  Column
+        # sharding (Pr == 1) on the sweep schedule carries each rank's 4 scalars in 2 extra
+        # complex elements after its ghat slot: one all-gather per iteration (admm_plan.cu).
+        self.fused_scal = self.Pr == 1 and self.Pc > 1
+        nmv = self.Mr * self.Nc * self.mb
+        gslot = nmv + (2 if self.fused_scal else 0)
+        gbuf = np.zeros((self.Pc, gslot), np.complex128)
+        self.ghat = gbuf[:, :nmv].reshape(self.Pc, self.Mr, self.Nc, self.mb)
+        assert np.shares_memory(self.ghat, gbuf)
         self.outbox = np.zeros((M, self.Nc, self.nb), np.complex128)
-        self.scal = np.zeros((self.Pr * self.Pc, 4))
-        self.buffers = {X_GHAT: torch.from_numpy(self.ghat.view(np.float64).reshape(-1)),
-                        X_OUTBOX: torch.from_numpy(self.outbox.view(np.float64).reshape(-1)),
-                        X_SCAL: torch.from_numpy(self.scal.reshape(-1))}
-        sz = {X_GHAT: self.Mr * self.Nc * self.mb * 2, X_OUTBOX: self.Mr * self.Nc * self.nb * 2, X_SCAL: 4}
-        off = {X_GHAT: self.pc * sz[X_GHAT], X_OUTBOX: self.pr * sz[X_OUTBOX], X_SCAL: self.rank * 4}
+        if self.fused_scal:
+            self.scal = gbuf[:, nmv:].view(np.float64)  # [rank == pc][4]
+        else:
+            self.scal = np.zeros((self.Pr * self.Pc, 4))
+        self.buffers = {X_GHAT: torch.from_numpy(gbuf.view(np.float64).reshape(-1)),
+                        X_OUTBOX: torch.from_numpy(self.outbox.view(np.float64).reshape(-1))}
+        sz = {X_GHAT: gslot * 2, X_OUTBOX: self.Mr * self.Nc * self.nb * 2}
+        off = {X_GHAT: self.pc * sz[X_GHAT], X_OUTBOX: self.pr * sz[X_OUTBOX]}
+        if not self.fused_scal:
+            self.buffers[X_SCAL] = torch.from_numpy(self.scal.reshape(-1))
+            sz[X_SCAL], off[X_SCAL] = 4, self.rank * 4
         self.slots = {w: (off[w], sz[w]) for w in sz}
         self.reset()
 
@@ -80,7 +92,7 @@ class NumpyShard:
         self.c = {b: z(self.nb) for b in self.H}
         self.q = {b: z(self.mb) for b in self.H}
         self.v = {jl: z(self.nb) for jl in range(self.Nc)}
-        self.ghat[:] = 0
+        self.ghat[...] = 0
         self.outbox[:] = 0
         self.trace_rows = []
         if self.schedule == "sweep":  # prologue: w = H c^0 = 0
