@@ -1,0 +1,227 @@
+// admm_hemv.cuh — q_b = K_b r_b with K_b = (rho I + H_b H_b^H)^-1 Hermitian, streamed
+// from a packed lower triangle: half the bytes of the dense K per iteration.
+//
+// Packed layout per block: 64 x 64 tiles (I, J), I >= J, in row-major tile order
+// (unit u = I (I + 1) / 2 + J), each tile row-major; rows/columns past m are zero.  The
+// diagonal tiles are stored full.  A tile (I, J), I > J, contributes
+//     N part:  y_I += K_IJ r_J            (rows of the tile)
+//     H part:  y_J += K_IJ^H r_I          (columns of the tile)
+// and a diagonal tile only its N part.  Tiles are split stream-K over a persistent grid.
+// Each warp owns 8 rows of a tile, each lane 2 columns (one 32-byte / 16-byte load per
+// row): N partials stay in registers along a tile row and are reduced once per tile-row
+// segment; H partials are reduced over the 8 warps through SMEM once per tile.  Both go
+// to a partial buffer that hemv_finalize_kernel sums in a fixed order (no atomics).
+// Numerics: K_IJ (lower) stands for both triangles — the inverse is Hermitian up to
+// rounding (~1e-16 relative).
+#pragma once
+
+#include "admm_kernels.cuh"
+
+namespace admm {
+
+constexpr int kHT = 64;                 // tile edge
+constexpr int kHRows = kHT / kCtaWarps;  // rows per warp (8)
+
+struct HemvDesc {       // one per local block
+  uint64_t k_off;       // element offset of the block's packed tiles
+  uint64_t unit0;       // first global unit (tile) of the block
+  uint64_t part_off;    // double2 offset of the block's partials: N [n_units][64], H [n_units][64]
+  uint32_t m;           // rows (= columns)
+  uint32_t nT;          // tile rows
+  uint32_t x_off;       // offset of r / q / ghat / gij (the block's mvec_off)
+  uint32_t n_units;     // nT (nT + 1) / 2
+};
+
+// Two complex elements of a tile row, widened to FP64 (c128: one 32-byte load; c64:
+// one 16-byte load), L1 no-allocate, L2 policy `pol` (createpolicy).
+template <typename S>
+__device__ __forceinline__ void ld_pair(const S* p, double2 (&o)[2], uint64_t pol) {
+  if constexpr (sizeof(S) == 16) {
+    double a, b, c, d;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
+                 : "l"(p), "l"(pol));
+    o[0] = make_double2(a, b);
+    o[1] = make_double2(c, d);
+  } else {
+    float4 f;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(f.x), "=f"(f.y), "=f"(f.z), "=f"(f.w)
+                 : "l"(p), "l"(pol));
+    o[0] = make_double2(f.x, f.y);
+    o[1] = make_double2(f.z, f.w);
+  }
+}
+
+__device__ __forceinline__ double2 ld_masked(const double2* x, uint32_t i, uint32_t m) {
+  return i < m ? x[i] : make_double2(0.0, 0.0);
+}
+
+// keep: K fits in L2 next to the sweep's open strips -> evict_last (re-read next
+// iteration), else evict_first.
+template <typename S, int OCC>
+__global__ void __launch_bounds__(kCtaThreads, OCC)
+hemv_kernel(const S* __restrict__ Kp, const double2* __restrict__ X, double2* __restrict__ part,
+            const HemvDesc* __restrict__ hd, int nb, uint64_t U, int keep) {
+  constexpr bool kPrefetch = OCC == 1;  // two tiles in registers only at one CTA per SM
+  __shared__ double2 hbuf[2][kCtaWarps][kHT];
+  uint64_t pol;
+  if (keep)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  const uint64_t P = gridDim.x, p = blockIdx.x;
+  uint64_t x = sk_lo(p, U, P);
+  const uint64_t xe = sk_lo(p + 1, U, P);
+  if (x >= xe) return;
+  const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+  int b = 0;
+  while (b + 1 < nb && hd[b + 1].unit0 <= x) ++b;
+  HemvDesc d = hd[b];
+  uint32_t u = (uint32_t)(x - d.unit0);
+  uint32_t I = 0;
+  while ((I + 1) * (I + 2) / 2 <= u) ++I;
+  uint32_t J = u - I * (I + 1) / 2;
+  double2 accN[kHRows];
+  double2 xI[kHRows];  // r_I on this warp's rows
+  auto load_xI = [&]() {
+#pragma unroll
+    for (int k = 0; k < kHRows; ++k) xI[k] = ld_masked(X + d.x_off, I * kHT + warp * kHRows + k, d.m);
+  };
+#pragma unroll
+  for (int k = 0; k < kHRows; ++k) accN[k] = make_double2(0.0, 0.0);
+  load_xI();
+  uint32_t par = 0;
+  // Tiles of all blocks are contiguous in unit order (k_off = unit0 * 64 * 64), so unit
+  // x + 1 is the next 64 x 64 tile: its rows are loaded before tile x is reduced.
+  const S* tp = Kp + x * (uint64_t)(kHT * kHT) + (uint64_t)(warp * kHRows) * kHT + lane * 2;
+  double2 h[kHRows][2], hn[kHRows][2];
+  if (kPrefetch) {
+#pragma unroll
+    for (int k = 0; k < kHRows; ++k) ld_pair<S>(tp + (uint64_t)k * kHT, h[k], pol);
+  }
+  for (;;) {
+    if (kPrefetch) {
+      if (x + 1 < xe) {
+#pragma unroll
+        for (int k = 0; k < kHRows; ++k) ld_pair<S>(tp + kHT * kHT + (uint64_t)k * kHT, hn[k], pol);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < kHRows; ++k) ld_pair<S>(tp + (uint64_t)k * kHT, h[k], pol);
+    }
+    tp += kHT * kHT;
+    const uint32_t c0 = J * kHT + lane * 2;
+    const double2 xj0 = ld_masked(X + d.x_off, c0, d.m), xj1 = ld_masked(X + d.x_off, c0 + 1, d.m);
+#pragma unroll
+    for (int k = 0; k < kHRows; ++k) {
+      cmac(accN[k], h[k][0], xj0);
+      cmac(accN[k], h[k][1], xj1);
+    }
+    if (J < I) {  // H part of an off-diagonal tile: y_J += K_IJ^H r_I
+      double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int k = 0; k < kHRows; ++k) {
+        cmac_conj(a0, h[k][0], xI[k]);
+        cmac_conj(a1, h[k][1], xI[k]);
+      }
+      hbuf[par][warp][lane * 2] = a0;
+      hbuf[par][warp][lane * 2 + 1] = a1;
+      __syncthreads();
+      if (threadIdx.x < kHT) {
+        double2 s = hbuf[par][0][threadIdx.x];
+#pragma unroll
+        for (int w = 1; w < kCtaWarps; ++w) s = cadd(s, hbuf[par][w][threadIdx.x]);
+        part[d.part_off + ((uint64_t)d.n_units + u) * kHT + threadIdx.x] = s;
+      }
+      par ^= 1u;  // the next tile writes the other buffer; this one is reused after a barrier
+    }
+    ++x;
+    const bool row_end = (J == I);
+    if (row_end || x == xe) {  // flush the N partial of this tile-row segment
+      const uint32_t urow = I * (I + 1) / 2;  // unit of (I, 0)
+      const uint64_t seg = p - sk_owner(d.unit0 + urow, U, P);
+      // reduce-scatter the 8 row partials over the 32 lanes: lane l ends with row (l >> 2)
+#pragma unroll
+      for (int o = 16, nv = kHRows / 2; o >= 4; o >>= 1, nv >>= 1) {
+        const bool hi = (lane & o) != 0;
+#pragma unroll
+        for (int k = 0; k < nv; ++k) {
+          double2 send = hi ? accN[k] : accN[k + nv];
+          const double2 keep = hi ? accN[k + nv] : accN[k];
+          send.x = __shfl_xor_sync(0xffffffffu, send.x, o);
+          send.y = __shfl_xor_sync(0xffffffffu, send.y, o);
+          accN[k] = cadd(keep, send);
+        }
+      }
+      double2 a = accN[0];
+#pragma unroll
+      for (int o = 2; o >= 1; o >>= 1) {
+        a.x += __shfl_xor_sync(0xffffffffu, a.x, o);
+        a.y += __shfl_xor_sync(0xffffffffu, a.y, o);
+      }
+      if ((lane & 3) == 0)
+        part[d.part_off + (uint64_t)(urow + seg) * kHT + warp * kHRows + (lane >> 2)] = a;
+#pragma unroll
+      for (int k = 0; k < kHRows; ++k) accN[k] = make_double2(0.0, 0.0);
+    }
+    if (x == xe) break;
+    if (kPrefetch) {
+#pragma unroll
+      for (int k = 0; k < kHRows; ++k) h[k][0] = hn[k][0], h[k][1] = hn[k][1];
+    }
+    ++u;
+    if (row_end) {
+      J = 0;
+      if (++I == d.nT) {
+        d = hd[++b];
+        u = 0;
+        I = 0;
+      }
+      load_xI();
+    } else {
+      ++J;
+    }
+  }
+}
+
+// q = K r from the partials (tile-row N segments in CTA order, then the H parts of the
+// tiles below the diagonal in ascending tile-row order), ghat = g_ij - rho q
+// (the kQ stage of rows_finalize_kernel).
+__global__ void __launch_bounds__(kCtaThreads)
+hemv_finalize_kernel(RowVecs rv, const double2* __restrict__ part, const HemvDesc* __restrict__ hd, uint64_t U,
+                     uint64_t P, const Params* __restrict__ prm) {
+  const HemvDesc d = hd[blockIdx.y];
+  const uint32_t row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= d.m) return;
+  const uint32_t I = row / kHT, r = row % kHT;
+  const uint32_t urow = I * (I + 1) / 2;
+  const uint32_t nseg = seg_count(d.unit0 + urow, I + 1, U, P);
+  const double2* np = part + d.part_off + (uint64_t)urow * kHT + r;
+  double2 s = np[0];
+  for (uint32_t k = 1; k < nseg; ++k) s = cadd(s, np[(uint64_t)k * kHT]);
+  const double2* hp = part + d.part_off + (uint64_t)d.n_units * kHT + r;
+  for (uint32_t I2 = I + 1; I2 < d.nT; ++I2) s = cadd(s, hp[(uint64_t)(I2 * (I2 + 1) / 2 + I) * kHT]);
+  const uint32_t o = d.x_off + row;
+  rv.q[o] = s;
+  rv.ghat[o] = csub(rv.gij[o], cscale(s, prm->rho));
+}
+
+// Packed tiles from the dense FP64 inverse (GramDesc a_off, m x m): tile (I, J), I >= J.
+template <typename S>
+__global__ void k_pack_kernel(const double2* __restrict__ Aar, uint64_t a_off, uint32_t m, uint32_t nT,
+                              S* __restrict__ Kp) {
+  const uint64_t total = (uint64_t)nT * (nT + 1) / 2 * kHT * kHT;
+  for (uint64_t idx = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t u = (uint32_t)(idx / (kHT * kHT)), e = (uint32_t)(idx % (kHT * kHT));
+    uint32_t I = 0;
+    while ((I + 1) * (I + 2) / 2 <= u) ++I;
+    const uint32_t J = u - I * (I + 1) / 2;
+    const uint32_t row = I * kHT + e / kHT, col = J * kHT + e % kHT;
+    const double2 v = (row < m && col < m) ? Aar[a_off + (uint64_t)row * m + col] : make_double2(0.0, 0.0);
+    Kp[idx] = Store<S>::narrow(v);
+  }
+}
+
+}  // namespace admm

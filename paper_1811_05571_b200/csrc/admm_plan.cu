@@ -28,6 +28,7 @@
 #include "admm_setup.cuh"
 #include "admm_sweep.cuh"
 #include "admm_tile.cuh"
+#include "admm_hemv.cuh"
 #include "admm_batched.cuh"
 
 using namespace admm;
@@ -169,6 +170,12 @@ struct admm_plan {
   uint32_t tile_ns = 0;     // its SMEM ring slots (32-row tasks)
   int tile_cps = 1;         // its CTAs per SM
   DevBuf dHt;               // strip-major copy of H for sweep_tile_kernel
+  bool kpacked = false;     // K applied from the packed Hermitian tiles (hemv_kernel)
+  bool kkeep = false;       // ... with an L2 evict_last policy (ADMM_B200_KKEEP)
+  int hemv_occ = 1;         // hemv_kernel CTAs per SM (1: register prefetch of the next tile)
+  std::vector<HemvDesc> hv;
+  DevBuf dKp, dhv, dkppart;
+  Geom gP;
   DevBuf dtrace_tile;       // ADMM_B200_TILE_TRACE: per-strip phase timestamps
   DevBuf dtmaps;            // one CUtensorMap per local block
   std::vector<SweepDesc> segs;
@@ -602,6 +609,33 @@ void factor_blocks(admm_plan* p) {
   p->dK.alloc(p->k_elems * sizeof(S));
   k_store_kernel<S><<<dim3(gx, p->max_m, (unsigned)nb), 256, 0, p->stream>>>(
       A.as<double2>(), p->dgram.as<GramDesc>(), p->dK.as<S>(), flag.as<unsigned>());
+  if (p->kpacked) {  // packed Hermitian tiles of the same inverse
+    uint64_t koff = 0, u0 = 0, po = 0;
+    p->hv.assign(nb, HemvDesc{});
+    for (uint64_t b = 0; b < nb; ++b) {
+      HemvDesc& h = p->hv[b];
+      h.m = p->blocks[b].rows;
+      h.nT = (uint32_t)cdiv(h.m, kHT);
+      h.n_units = h.nT * (h.nT + 1) / 2;
+      h.k_off = koff;
+      h.unit0 = u0;
+      h.part_off = po;
+      h.x_off = p->blocks[b].mvec_off;
+      koff += (uint64_t)h.n_units * kHT * kHT;
+      u0 += h.n_units;
+      po += 2ull * h.n_units * kHT;
+    }
+    p->dKp.alloc(koff * sizeof(S));
+    for (uint64_t b = 0; b < nb; ++b)
+      k_pack_kernel<S><<<p->num_sms * 4, 256, 0, p->stream>>>(A.as<double2>(), p->gram[b].a_off, p->hv[b].m,
+                                                             p->hv[b].nT, p->dKp.as<S>() + p->hv[b].k_off);
+    upload_desc(p->dhv, p->hv.data(), nb * sizeof(HemvDesc));
+    p->dkppart.alloc(po * sizeof(double2));
+    p->gP.U = u0;
+    if (const char* e = std::getenv("ADMM_B200_HEMV_OCC")) p->hemv_occ = std::atoi(e) == 2 ? 2 : 1;
+    p->gP.P = p->hemv_occ == 2 ? grid_for<S>(hemv_kernel<S, 2>, u0, p->num_sms)
+                               : grid_for<S>(hemv_kernel<S, 1>, u0, p->num_sms);
+  }
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(&hf, flag.p, 4, cudaMemcpyDeviceToHost, p->stream));
   CK(cudaStreamSynchronize(p->stream));
@@ -634,6 +668,34 @@ ColVecs col_vecs(admm_plan* p) {
                  p->dvprev.as<double2>()};
 }
 
+// q = K r and ghat = g_ij - rho q for every local block: packed Hermitian K (half the
+// bytes) unless disabled, else the dense K through gemv_n.
+// `mid` runs between the two launches (profiling events).
+template <typename S, typename Mid>
+void enqueue_kapply(admm_plan* p, cudaStream_t s, Mid mid) {
+  const int nb = (int)p->blocks.size();
+  if (p->kpacked) {
+    auto fn = p->hemv_occ == 2 ? hemv_kernel<S, 2> : hemv_kernel<S, 1>;
+    fn<<<(unsigned)p->gP.P, kCtaThreads, 0, s>>>(p->dKp.as<S>(), p->dr.as<double2>(), p->dkppart.as<double2>(),
+                                                 p->dhv.as<HemvDesc>(), nb, p->gP.U, p->kkeep ? 1 : 0);
+    mid();
+    hemv_finalize_kernel<<<dim3(p->rgx, nb), kCtaThreads, 0, s>>>(row_vecs(p), p->dkppart.as<double2>(),
+                                                                   p->dhv.as<HemvDesc>(), p->gP.U, p->gP.P,
+                                                                   p->dparams.as<Params>());
+    return;
+  }
+  gemv_n_kernel<S, kVN, kEvictNormal><<<(unsigned)p->gK.P, kCtaThreads, 0, s>>>(
+      p->dK.as<S>(), p->dr.as<double2>(), p->dqpart.as<double2>(), p->dkN.as<MatDesc>(), nb, p->gK.U);
+  mid();
+  rows_finalize_kernel<kQ><<<dim3(p->rgx, nb), kCtaThreads, 0, s>>>(
+      row_vecs(p), p->dqpart.as<double2>(), p->dkN.as<MatDesc>(), p->dblocks.as<BlockDesc>(),
+      p->dgblocks.as<BlockDesc>(), (uint32_t)p->N, p->gK.U, p->gK.P, p->dparams.as<Params>());
+}
+template <typename S>
+void enqueue_kapply(admm_plan* p, cudaStream_t s) {
+  enqueue_kapply<S>(p, s, [] {});
+}
+
 // Launch list of one iteration (the order of solvers.hpp's phases).
 template <typename S>
 void enqueue_iteration_twopass(admm_plan* p, cudaStream_t s, bool with_objective, std::vector<cudaEvent_t>* ev) {
@@ -652,13 +714,7 @@ void enqueue_iteration_twopass(admm_plan* p, cudaStream_t s, bool with_objective
       p->dgblocks.as<BlockDesc>(), (uint32_t)p->N, p->gN.U,
       p->gN.P, p->dparams.as<Params>());
   mark(2);
-  gemv_n_kernel<S, kVN, kEvictNormal><<<(unsigned)p->gK.P, kCtaThreads, 0, s>>>(
-      p->dK.as<S>(), p->dr.as<double2>(), p->dqpart.as<double2>(), p->dkN.as<MatDesc>(), nb, p->gK.U);
-  mark(3);
-  rows_finalize_kernel<kQ><<<dim3(p->rgx, nb), kCtaThreads, 0, s>>>(
-      row_vecs(p), p->dqpart.as<double2>(), p->dkN.as<MatDesc>(), p->dblocks.as<BlockDesc>(),
-      p->dgblocks.as<BlockDesc>(), (uint32_t)p->N, p->gK.U,
-      p->gK.P, p->dparams.as<Params>());
+  enqueue_kapply<S>(p, s, [&] { mark(3); });
   mark(4);
   gemv_h_kernel<S, kVH, kEvictNormal><<<(unsigned)p->gH.P, kCtaThreads, 0, s>>>(
       p->dH.as<S>(), p->dq.as<double2>(), p->dzpart.as<double2>(), p->dhH.as<MatDesc>(), nb, p->gH.U);
@@ -689,12 +745,7 @@ void enqueue_sweep_prologue(admm_plan* p, cudaStream_t s) {
       row_vecs(p), p->dwpart_s.as<double2>(), p->dsegs.as<SweepDesc>(), p->dblocks.as<BlockDesc>(),
       p->dgblocks.as<BlockDesc>(), (uint32_t)p->N, (uint32_t)p->n_meas, p->gS.U, p->gS.P, 1, 0, p->dred.as<double>(),
       p->dparams.as<Params>(), p->dtrace.as<double>(), p->trace_cap, p->dstate.as<IterState>(), nullptr);
-  gemv_n_kernel<S, kVN, kEvictNormal><<<(unsigned)p->gK.P, kCtaThreads, 0, s>>>(
-      p->dK.as<S>(), p->dr.as<double2>(), p->dqpart.as<double2>(), p->dkN.as<MatDesc>(), nb, p->gK.U);
-  rows_finalize_kernel<kQ><<<dim3(p->rgx, nb), kCtaThreads, 0, s>>>(
-      row_vecs(p), p->dqpart.as<double2>(), p->dkN.as<MatDesc>(), p->dblocks.as<BlockDesc>(),
-      p->dgblocks.as<BlockDesc>(), (uint32_t)p->N,
-      p->gK.U, p->gK.P, p->dparams.as<Params>());
+  enqueue_kapply<S>(p, s);
   CK(cudaGetLastError());
 }
 
@@ -769,13 +820,7 @@ void enqueue_iteration_sweep(admm_plan* p, cudaStream_t s, bool with_objective, 
                                                      p->no, p->dparams.as<Params>(), p->dtrace.as<double>(),
                                                      p->trace_cap, p->dstate.as<IterState>());
   }
-  gemv_n_kernel<S, kVN, kEvictNormal><<<(unsigned)p->gK.P, kCtaThreads, 0, s>>>(
-      p->dK.as<S>(), p->dr.as<double2>(), p->dqpart.as<double2>(), p->dkN.as<MatDesc>(), nb, p->gK.U);
-  mark(3);
-  rows_finalize_kernel<kQ><<<dim3(p->rgx, nb), kCtaThreads, 0, s>>>(
-      row_vecs(p), p->dqpart.as<double2>(), p->dkN.as<MatDesc>(), p->dblocks.as<BlockDesc>(),
-      p->dgblocks.as<BlockDesc>(), (uint32_t)p->N,
-      p->gK.U, p->gK.P, p->dparams.as<Params>());
+  enqueue_kapply<S>(p, s, [&] { mark(3); });
   mark(4);
   CK(cudaGetLastError());
 }
@@ -1220,6 +1265,12 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
   p->ghat_ptr = p->dghat.as<double2>();
   p->outbox_ptr = p->doutbox.as<double2>();
   p->fused_scal = p->Pr == 1 && p->Pc > 1 && p->schedule == 2;
+  {  // packed Hermitian K for the per-iteration K apply (the batched schedule uses bgemm)
+    const char* e = std::getenv("ADMM_B200_KPACK");
+    p->kpacked = p->batch == 1 && !(e && e[0] == '0');
+    const char* e2 = std::getenv("ADMM_B200_KKEEP");
+    p->kkeep = e2 && e2[0] == '1';
+  }
   p->scal_ptr = p->fused_scal ? reinterpret_cast<double*>(p->ghat_ptr + p->Mr * p->Nc * p->mpad)
                               : p->dscal.as<double>();
   for (DevBuf* d : {&p->du, &p->ds, &p->dc}) d->alloc(p->vec_total * 16 * p->batch);
@@ -1438,12 +1489,18 @@ admm_status admm_plan_profile(admm_plan* p, uint64_t iters, const char** names, 
   static const char* kNames2[7] = {"gemv_n(H,c)", "rows_finalize(rhs)", "gemv_n(K,r)", "rows_finalize(q)",
                                    "gemv_h(H,q)", "zupdate", "finalize"};
   static const char* kNamesS[4] = {"sweep(H)", "rows_finalize(rhs)+finalize", "gemv_n(K,r)", "rows_finalize(q)"};
+  static const char* kNames2P[7] = {"gemv_n(H,c)", "rows_finalize(rhs)", "hemv(Kpacked,r)", "hemv_finalize(q)",
+                                    "gemv_h(H,q)", "zupdate", "finalize"};
+  static const char* kNamesSP[4] = {"sweep(H)", "rows_finalize(rhs)+finalize", "hemv(Kpacked,r)",
+                                    "hemv_finalize(q)"};
   static const char* kNamesB[7] = {"bgemm(H,C)", "brows(rhs)", "bgemm(K,R)", "brows(q)", "bgemm_adj(H,Q)",
                                    "bzupdate", "bfinalize"};
   return run_guarded([&] {
     check_plan(p);
     const int nk = (int)admm_plan_kernel_count(p);
-    const char* const* kn = p->schedule == 2 ? kNamesS : p->schedule == 3 ? kNamesB : kNames2;
+    const char* const* kn = p->schedule == 2   ? (p->kpacked ? kNamesSP : kNamesS)
+                            : p->schedule == 3 ? kNamesB
+                                               : (p->kpacked ? kNames2P : kNames2);
     std::vector<cudaEvent_t> ev(nk + 1);
     for (auto& e : ev) CK(cudaEventCreate(&e));
     std::vector<double> acc(nk, 0.0);
@@ -1475,10 +1532,15 @@ admm_status admm_plan_get_info(const admm_plan* p, admm_plan_info* info) {
       kb += (uint64_t)b.rows * b.rows * p->elem;
       vb += (uint64_t)b.cols * 16 * 6 + (uint64_t)b.rows * 16 * 8;
     }
+    const uint64_t kb_dense = kb;
+    if (p->kpacked) {  // the packed Hermitian tiles actually streamed per iteration
+      kb = 0;
+      for (const auto& h : p->hv) kb += (uint64_t)h.n_units * kHT * kHT * p->elem;
+    }
     r.h_bytes = hb;
     r.k_bytes = kb;
     r.h_stream_bytes_per_iter = 2 * hb;
-    r.bytes_per_iter = 2 * hb + kb + vb;  // two-pass algorithmic bytes
+    r.bytes_per_iter = 2 * hb + kb_dense + vb;  // two-pass algorithmic bytes
     r.launches_per_iter = p->schedule == 3 ? 7 : p->schedule == 2 ? (p->trace_obj ? 7 : 4) : (p->trace_obj ? 9 : 7);
     r.schedule = (uint64_t)p->schedule;
     r.grid_sweep = p->gS.P;
@@ -1660,11 +1722,7 @@ void enqueue_phase(admm_plan* p, int phase) {
           row_vecs(p), p->dwpart.as<double2>(), p->dhN.as<MatDesc>(), p->dblocks.as<BlockDesc>(),
           p->dgblocks.as<BlockDesc>(), (uint32_t)p->N, p->gN.U, p->gN.P, p->dparams.as<Params>());
     }
-    gemv_n_kernel<S, kVN, kEvictNormal><<<(unsigned)p->gK.P, kCtaThreads, 0, s>>>(
-        p->dK.as<S>(), p->dr.as<double2>(), p->dqpart.as<double2>(), p->dkN.as<MatDesc>(), nb, p->gK.U);
-    rows_finalize_kernel<kQ><<<dim3(p->rgx, nb), kCtaThreads, 0, s>>>(
-        row_vecs(p), p->dqpart.as<double2>(), p->dkN.as<MatDesc>(), p->dblocks.as<BlockDesc>(),
-        p->dgblocks.as<BlockDesc>(), (uint32_t)p->N, p->gK.U, p->gK.P, p->dparams.as<Params>());
+    enqueue_kapply<S>(p, s);
   } else if (phase == 2) {
     if (p->schedule == 2) throw Fail{ADMM_E_STATE, "phase 2 belongs to the two-pass schedule"};
     gemv_h_kernel<S, kVH, kEvictNormal><<<(unsigned)p->gH.P, kCtaThreads, 0, s>>>(
