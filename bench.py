@@ -353,7 +353,8 @@ def bench_ours(args, cfg):
     hb, kb = info["h_bytes"], info["k_bytes"]
     # algorithmic HBM bytes per launch: each H pass / the sweep streams H once from HBM
     # (the sweep's second, L2-resident read of each strip is not HBM traffic), K once.
-    algo = {"gemv_n(H,c)": hb, "gemv_h(H,q)": hb, "gemv_n(K,r)": kb, "hemv(Kpacked,r)": kb, "sweep(H)": hb}
+    algo = {"gemv_n(H,c)": hb, "gemv_h(H,q)": hb, "gemv_n(K,r)": kb, "hemv(Kpacked,r)": kb,
+            "hemv(Kpacked,r)+finalize": kb, "sweep(H)": hb}
     algo = {k: v for k, v in algo.items() if k in kern}
     if plan.batch > 1:  # config 5: FP64 SIMT compute-bound skinny GEMMs (8 flop per complex MAC)
         rows, cols = problem.h.shape

@@ -158,4 +158,12 @@ __device__ __forceinline__ void cpa_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// Programmatic dependent launch: wait until the preceding grid in the stream has
+// completed (its writes visible), then allow the next grid to be launched while this one
+// runs.  A no-op when the launch carried no programmatic dependency.  Call first thing.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 }  // namespace admm

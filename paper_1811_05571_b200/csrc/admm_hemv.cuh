@@ -30,7 +30,55 @@ struct HemvDesc {       // one per local block
   uint32_t nT;          // tile rows
   uint32_t x_off;       // offset of r / q / ghat / gij (the block's mvec_off)
   uint32_t n_units;     // nT (nT + 1) / 2
+  uint32_t cnt_off;     // first of the block's nT tile-row completion counters
+  uint32_t pad_;
 };
+
+// (K r)[row] from the partials of row r of tile-row I: the N segments in CTA order, then
+// the H parts of the tiles below the diagonal in ascending tile-row order.  Loads are
+// issued 8 at a time (independent) and added in that fixed order; L1 bypassed (the
+// partials come from other SMs).
+__device__ __forceinline__ double2 hemv_sum_row(const double2* __restrict__ part, const HemvDesc& d, uint32_t I,
+                                                uint32_t r, uint64_t U, uint64_t P) {
+  const uint32_t urow = I * (I + 1) / 2;
+  const uint32_t nseg = seg_count(d.unit0 + urow, I + 1, U, P);
+  const uint32_t nh = d.nT - 1 - I;
+  const double2* np = part + d.part_off + (uint64_t)urow * kHT + r;
+  const double2* hp = part + d.part_off + (uint64_t)d.n_units * kHT + r;
+  const uint32_t n = nseg + nh;
+  double2 s = make_double2(0.0, 0.0);
+  for (uint32_t k0 = 0; k0 < n; k0 += 8) {
+    double2 v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const uint32_t k = k0 + e;
+      if (k < nseg) {
+        v[e] = __ldcg(np + (uint64_t)k * kHT);
+      } else if (k < n) {
+        const uint32_t I2 = I + 1 + (k - nseg);
+        v[e] = __ldcg(hp + (uint64_t)(I2 * (I2 + 1) / 2 + I) * kHT);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      if (k0 + e < n) s = k0 + e == 0 ? v[e] : cadd(s, v[e]);
+  }
+  return s;
+}
+
+// q = K r and ghat = g_ij - rho q on the 64 rows of tile-row I (one warp).
+__device__ __forceinline__ void hemv_finalize_rows(RowVecs rv, const double2* __restrict__ part, const HemvDesc& d,
+                                                   uint32_t I, uint64_t U, uint64_t P, double rho, int lane) {
+#pragma unroll
+  for (int h = 0; h < kHT / kWarp; ++h) {
+    const uint32_t r = h * kWarp + lane, row = I * kHT + r;
+    if (row >= d.m) continue;
+    const double2 s = hemv_sum_row(part, d, I, r, U, P);
+    const uint32_t o = d.x_off + row;
+    rv.q[o] = s;
+    rv.ghat[o] = csub(rv.gij[o], cscale(s, rho));
+  }
+}
 
 // Two complex elements of a tile row, widened to FP64 (c128: one 32-byte load; c64:
 // one 16-byte load), L1 no-allocate, L2 policy `pol` (createpolicy).
@@ -59,11 +107,16 @@ __device__ __forceinline__ double2 ld_masked(const double2* x, uint32_t i, uint3
 
 // keep: K fits in L2 next to the sweep's open strips -> evict_last (re-read next
 // iteration), else evict_first.
-template <typename S, int OCC>
+template <typename S, int OCC, bool FUSE>
 __global__ void __launch_bounds__(kCtaThreads, OCC)
 hemv_kernel(const S* __restrict__ Kp, const double2* __restrict__ X, double2* __restrict__ part,
-            const HemvDesc* __restrict__ hd, int nb, uint64_t U, int keep) {
+            const HemvDesc* __restrict__ hd, int nb, uint64_t U, int keep, unsigned* __restrict__ cnt,
+            RowVecs rv, const Params* __restrict__ prm) {
+  // FUSE: fused finalize.  Every contribution to tile-row I (an N segment of each
+  // warp, the H part of each tile (I2, I) below the diagonal) bumps cnt[I] after its
+  // partial is stored; the warp that completes the count finalizes the 64 rows.
   constexpr bool kPrefetch = OCC == 1;  // two tiles in registers only at one CTA per SM
+  pdl_enter();
   __shared__ double2 hbuf[2][kCtaWarps][kHT];
   uint64_t pol;
   if (keep)
@@ -92,6 +145,21 @@ hemv_kernel(const S* __restrict__ Kp, const double2* __restrict__ X, double2* __
   for (int k = 0; k < kHRows; ++k) accN[k] = make_double2(0.0, 0.0);
   load_xI();
   uint32_t par = 0;
+  auto contribute = [&](uint32_t Ir) {  // warp-uniform: this warp's partial for tile-row Ir is stored
+    __threadfence();  // every lane's partial stores are visible device-wide before the count
+    __syncwarp();
+    unsigned last = 0;
+    if (lane == 0) {
+      const uint32_t urow = Ir * (Ir + 1) / 2;
+      const unsigned expect = kCtaWarps * seg_count(d.unit0 + urow, Ir + 1, U, P) + (d.nT - 1 - Ir);
+      last = atomicAdd(&cnt[d.cnt_off + Ir], 1u) == expect - 1;
+    }
+    if (__shfl_sync(0xffffffffu, last, 0)) {
+      __threadfence();
+      hemv_finalize_rows(rv, part, d, Ir, U, P, prm->rho, lane);
+      if (lane == 0) cnt[d.cnt_off + Ir] = 0;  // ready for the next iteration's launch
+    }
+  };
   // Tiles of all blocks are contiguous in unit order (k_off = unit0 * 64 * 64), so unit
   // x + 1 is the next 64 x 64 tile: its rows are loaded before tile x is reduced.
   const S* tp = Kp + x * (uint64_t)(kHT * kHT) + (uint64_t)(warp * kHRows) * kHT + lane * 2;
@@ -128,11 +196,16 @@ hemv_kernel(const S* __restrict__ Kp, const double2* __restrict__ X, double2* __
       hbuf[par][warp][lane * 2] = a0;
       hbuf[par][warp][lane * 2 + 1] = a1;
       __syncthreads();
-      if (threadIdx.x < kHT) {
-        double2 s = hbuf[par][0][threadIdx.x];
+      if (warp == 0) {
 #pragma unroll
-        for (int w = 1; w < kCtaWarps; ++w) s = cadd(s, hbuf[par][w][threadIdx.x]);
-        part[d.part_off + ((uint64_t)d.n_units + u) * kHT + threadIdx.x] = s;
+        for (int e = 0; e < 2; ++e) {
+          const int c = lane * 2 + e;
+          double2 s = hbuf[par][0][c];
+#pragma unroll
+          for (int w = 1; w < kCtaWarps; ++w) s = cadd(s, hbuf[par][w][c]);
+          part[d.part_off + ((uint64_t)d.n_units + u) * kHT + c] = s;
+        }
+        if (FUSE) contribute(J);
       }
       par ^= 1u;  // the next tile writes the other buffer; this one is reused after a barrier
     }
@@ -162,6 +235,7 @@ hemv_kernel(const S* __restrict__ Kp, const double2* __restrict__ X, double2* __
       }
       if ((lane & 3) == 0)
         part[d.part_off + (uint64_t)(urow + seg) * kHT + warp * kHRows + (lane >> 2)] = a;
+      if (FUSE) contribute(I);
 #pragma unroll
       for (int k = 0; k < kHRows; ++k) accN[k] = make_double2(0.0, 0.0);
     }
@@ -188,20 +262,17 @@ hemv_kernel(const S* __restrict__ Kp, const double2* __restrict__ X, double2* __
 // q = K r from the partials (tile-row N segments in CTA order, then the H parts of the
 // tiles below the diagonal in ascending tile-row order), ghat = g_ij - rho q
 // (the kQ stage of rows_finalize_kernel).
-__global__ void __launch_bounds__(kCtaThreads)
+// Unfused variant (default; ADMM_B200_HEMV_FUSE=1 finalizes inside hemv_kernel).
+// Grid: (cdiv(max rows, kHFinRows), blocks).
+constexpr int kHFinRows = 64;
+__global__ void __launch_bounds__(kHFinRows)
 hemv_finalize_kernel(RowVecs rv, const double2* __restrict__ part, const HemvDesc* __restrict__ hd, uint64_t U,
                      uint64_t P, const Params* __restrict__ prm) {
+  pdl_enter();
   const HemvDesc d = hd[blockIdx.y];
   const uint32_t row = blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= d.m) return;
-  const uint32_t I = row / kHT, r = row % kHT;
-  const uint32_t urow = I * (I + 1) / 2;
-  const uint32_t nseg = seg_count(d.unit0 + urow, I + 1, U, P);
-  const double2* np = part + d.part_off + (uint64_t)urow * kHT + r;
-  double2 s = np[0];
-  for (uint32_t k = 1; k < nseg; ++k) s = cadd(s, np[(uint64_t)k * kHT]);
-  const double2* hp = part + d.part_off + (uint64_t)d.n_units * kHT + r;
-  for (uint32_t I2 = I + 1; I2 < d.nT; ++I2) s = cadd(s, hp[(uint64_t)(I2 * (I2 + 1) / 2 + I) * kHT]);
+  const double2 s = hemv_sum_row(part, d, row / kHT, row % kHT, U, P);
   const uint32_t o = d.x_off + row;
   rv.q[o] = s;
   rv.ghat[o] = csub(rv.gij[o], cscale(s, prm->rho));

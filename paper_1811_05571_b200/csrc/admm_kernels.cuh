@@ -297,6 +297,28 @@ struct RowVecs {
 // kQ:   q_b = sum(partials of K_b r_b), ghat_b = g_ij - rho q_b.
 enum RowStage { kRhs = 0, kQ = 1 };
 
+// g_ij[row] = g_i - sum_{q != j} ghat_iq in ascending q (solvers.hpp:378-384); the ghat
+// loads are issued 8 at a time (independent), the subtractions stay in order.
+// gblocks: the global block table (a sharded plan's peers too).
+__device__ __forceinline__ double2 gij_row(const RowVecs& rv, const BlockDesc* __restrict__ gblocks,
+                                           const BlockDesc& bd, uint32_t N, uint32_t row) {
+  double2 gij = rv.g[bd.row0 + row];
+  for (uint32_t q0 = 0; q0 < N; q0 += 8) {
+    double2 v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const uint32_t qj = q0 + e;
+      if (qj < N && qj != bd.j) v[e] = rv.ghat[gblocks[bd.i * N + qj].mvec_off + row];
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const uint32_t qj = q0 + e;
+      if (qj < N && qj != bd.j) gij = csub(gij, v[e]);
+    }
+  }
+  return gij;
+}
+
 template <int Stage>
 __global__ void __launch_bounds__(kCtaThreads)
 rows_finalize_kernel(RowVecs rv, const double2* __restrict__ part, const MatDesc* __restrict__ mats,
@@ -310,11 +332,7 @@ rows_finalize_kernel(RowVecs rv, const double2* __restrict__ part, const MatDesc
   const double2 s = sum_rows_part(part, md, row, U, P);
   const uint32_t o = bd.mvec_off + row;
   if constexpr (Stage == kRhs) {
-    double2 gij = rv.g[bd.row0 + row];
-    for (uint32_t qj = 0; qj < N; ++qj) {
-      if (qj == bd.j) continue;
-      gij = csub(gij, rv.ghat[gblocks[bd.i * N + qj].mvec_off + row]);  // global table: peers too
-    }
+    const double2 gij = gij_row(rv, gblocks, bd, N, row);
     rv.gij[o] = gij;
     rv.r[o] = csub(gij, s);
   } else {

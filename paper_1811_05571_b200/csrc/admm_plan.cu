@@ -173,6 +173,8 @@ struct admm_plan {
   bool kpacked = false;     // K applied from the packed Hermitian tiles (hemv_kernel)
   bool kkeep = false;       // ... with an L2 evict_last policy (ADMM_B200_KKEEP)
   int hemv_occ = 1;         // hemv_kernel CTAs per SM (1: register prefetch of the next tile)
+  bool hemv_fuse = false;   // q / ghat finalized inside hemv_kernel (tile-row completion counters)
+  DevBuf dkcnt;
   std::vector<HemvDesc> hv;
   DevBuf dKp, dhv, dkppart;
   Geom gP;
@@ -207,6 +209,32 @@ uint64_t grid_for(K kernel, uint64_t U, int sms, size_t smem = 0) {
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kCtaThreads, smem));
   occ = std::max(occ, 1);
   return std::max<uint64_t>(1, std::min<uint64_t>(U, (uint64_t)sms * occ));
+}
+
+// Launch with programmatic stream serialization (PDL): the kernel may be scheduled
+// while its predecessor runs; it must call pdl_enter() before touching the
+// predecessor's output (sweep_kernel, rows_finalize_sweep_kernel, hemv_kernel,
+// hemv_finalize_kernel do).  ADMM_B200_PDL=0 launches plainly.
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("ADMM_B200_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  CK(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
 }
 
 template <typename S>
@@ -610,7 +638,7 @@ void factor_blocks(admm_plan* p) {
   k_store_kernel<S><<<dim3(gx, p->max_m, (unsigned)nb), 256, 0, p->stream>>>(
       A.as<double2>(), p->dgram.as<GramDesc>(), p->dK.as<S>(), flag.as<unsigned>());
   if (p->kpacked) {  // packed Hermitian tiles of the same inverse
-    uint64_t koff = 0, u0 = 0, po = 0;
+    uint64_t koff = 0, u0 = 0, po = 0, co = 0;
     p->hv.assign(nb, HemvDesc{});
     for (uint64_t b = 0; b < nb; ++b) {
       HemvDesc& h = p->hv[b];
@@ -621,6 +649,8 @@ void factor_blocks(admm_plan* p) {
       h.unit0 = u0;
       h.part_off = po;
       h.x_off = p->blocks[b].mvec_off;
+      h.cnt_off = (uint32_t)co;
+      co += h.nT;
       koff += (uint64_t)h.n_units * kHT * kHT;
       u0 += h.n_units;
       po += 2ull * h.n_units * kHT;
@@ -631,10 +661,13 @@ void factor_blocks(admm_plan* p) {
                                                              p->hv[b].nT, p->dKp.as<S>() + p->hv[b].k_off);
     upload_desc(p->dhv, p->hv.data(), nb * sizeof(HemvDesc));
     p->dkppart.alloc(po * sizeof(double2));
+    p->dkcnt.alloc(std::max<uint64_t>(co, 1) * sizeof(unsigned));
+    CK(cudaMemset(p->dkcnt.p, 0, std::max<uint64_t>(co, 1) * sizeof(unsigned)));
+    if (const char* e = std::getenv("ADMM_B200_HEMV_FUSE")) p->hemv_fuse = e[0] == '1';
     p->gP.U = u0;
     if (const char* e = std::getenv("ADMM_B200_HEMV_OCC")) p->hemv_occ = std::atoi(e) == 2 ? 2 : 1;
-    p->gP.P = p->hemv_occ == 2 ? grid_for<S>(hemv_kernel<S, 2>, u0, p->num_sms)
-                               : grid_for<S>(hemv_kernel<S, 1>, u0, p->num_sms);
+    p->gP.P = p->hemv_occ == 2 ? grid_for<S>(hemv_kernel<S, 2, false>, u0, p->num_sms)
+                               : grid_for<S>(hemv_kernel<S, 1, false>, u0, p->num_sms);
   }
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(&hf, flag.p, 4, cudaMemcpyDeviceToHost, p->stream));
@@ -675,13 +708,15 @@ template <typename S, typename Mid>
 void enqueue_kapply(admm_plan* p, cudaStream_t s, Mid mid) {
   const int nb = (int)p->blocks.size();
   if (p->kpacked) {
-    auto fn = p->hemv_occ == 2 ? hemv_kernel<S, 2> : hemv_kernel<S, 1>;
-    fn<<<(unsigned)p->gP.P, kCtaThreads, 0, s>>>(p->dKp.as<S>(), p->dr.as<double2>(), p->dkppart.as<double2>(),
-                                                 p->dhv.as<HemvDesc>(), nb, p->gP.U, p->kkeep ? 1 : 0);
+    auto fn = p->hemv_fuse ? hemv_kernel<S, 1, true> : p->hemv_occ == 2 ? hemv_kernel<S, 2, false> : hemv_kernel<S, 1, false>;
+    launch_pdl(fn, dim3((unsigned)p->gP.P), dim3(kCtaThreads), 0, s, p->dKp.as<S>(), p->dr.as<double2>(),
+               p->dkppart.as<double2>(), p->dhv.as<HemvDesc>(), nb, p->gP.U, p->kkeep ? 1 : 0,
+               p->hemv_fuse ? p->dkcnt.as<unsigned>() : nullptr, row_vecs(p), p->dparams.as<Params>());
     mid();
-    hemv_finalize_kernel<<<dim3(p->rgx, nb), kCtaThreads, 0, s>>>(row_vecs(p), p->dkppart.as<double2>(),
-                                                                   p->dhv.as<HemvDesc>(), p->gP.U, p->gP.P,
-                                                                   p->dparams.as<Params>());
+    if (!p->hemv_fuse)
+      launch_pdl(hemv_finalize_kernel, dim3((unsigned)cdiv(p->max_rows, kHFinRows), nb), dim3(kHFinRows), 0, s,
+                 row_vecs(p), p->dkppart.as<double2>(), p->dhv.as<HemvDesc>(), p->gP.U, p->gP.P,
+                 p->dparams.as<Params>());
     return;
   }
   gemv_n_kernel<S, kVN, kEvictNormal><<<(unsigned)p->gK.P, kCtaThreads, 0, s>>>(
@@ -753,7 +788,7 @@ template <typename S, int LPR>
 void launch_sweep_lpr(admm_plan* p, cudaStream_t s) {
   if constexpr (LPR >= 4) {
     if (p->sweep_bulk) {
-      sweep_bulk_kernel<S, LPR><<<(unsigned)p->gS.P, kSweepThreads, p->sweep_smem, s>>>(
+      sweep_bulk_kernel<S, LPR><<<(unsigned)p->gS.P, kBulkThreads, p->sweep_smem, s>>>(
           p->dH.as<S>(), p->dhN.as<MatDesc>(), p->dblocks.as<BlockDesc>(), p->dsegs.as<SweepDesc>(), (uint32_t)p->Mr,
           (uint32_t)p->Nc, (uint32_t)p->n_meas, p->gS.U, p->dq.as<double2>(), col_vecs(p), p->dwpart_s.as<double2>(),
           p->dparams.as<Params>(), p->dred.as<double>(), p->dstate.as<IterState>(), p->dtmaps.as<unsigned char>());
@@ -761,10 +796,10 @@ void launch_sweep_lpr(admm_plan* p, cudaStream_t s) {
     }
   }
   auto fn = p->keep_l2 ? sweep_kernel<S, LPR, true> : sweep_kernel<S, LPR, false>;
-  fn<<<(unsigned)p->gS.P, kSweepThreads, p->sweep_smem, s>>>(
-      p->dH.as<S>(), p->dhN.as<MatDesc>(), p->dblocks.as<BlockDesc>(), p->dsegs.as<SweepDesc>(), (uint32_t)p->Mr,
-      (uint32_t)p->Nc, (uint32_t)p->n_meas, p->gS.U, p->dq.as<double2>(), col_vecs(p), p->dwpart_s.as<double2>(),
-      p->dparams.as<Params>(), p->dred.as<double>(), p->dstate.as<IterState>());
+  launch_pdl(fn, dim3((unsigned)p->gS.P), dim3(kSweepThreads), p->sweep_smem, s, p->dH.as<S>(),
+             p->dhN.as<MatDesc>(), p->dblocks.as<BlockDesc>(), p->dsegs.as<SweepDesc>(), (uint32_t)p->Mr,
+             (uint32_t)p->Nc, (uint32_t)p->n_meas, p->gS.U, p->dq.as<double2>(), col_vecs(p),
+             p->dwpart_s.as<double2>(), p->dparams.as<Params>(), p->dred.as<double>(), p->dstate.as<IterState>());
 }
 
 template <typename S, int RB>
@@ -810,10 +845,11 @@ void enqueue_iteration_sweep(admm_plan* p, cudaStream_t s, bool with_objective, 
         p->dg.as<double2>(), p->dopart.as<double2>(), p->dhNv.as<MatDesc>(), p->dblocks.as<BlockDesc>(),
         (uint32_t)p->Nc, p->gO.U, p->gO.P, p->dored.as<double>());
   }
-  rows_finalize_sweep_kernel<<<dim3(p->rgx_s, nb), kCtaThreads, 0, s>>>(
-      row_vecs(p), p->dwpart_s.as<double2>(), p->dsegs.as<SweepDesc>(), p->dblocks.as<BlockDesc>(),
-      p->dgblocks.as<BlockDesc>(), (uint32_t)p->N, (uint32_t)p->n_meas, p->gS.U, p->gS.P, 0, 1, p->dred.as<double>(),
-      p->dparams.as<Params>(), p->dtrace.as<double>(), p->trace_cap, p->dstate.as<IterState>(), nullptr);
+  launch_pdl(rows_finalize_sweep_kernel, dim3(p->rgx_s, nb), dim3(kCtaThreads), 0, s, row_vecs(p),
+             p->dwpart_s.as<double2>(), p->dsegs.as<SweepDesc>(), p->dblocks.as<BlockDesc>(),
+             p->dgblocks.as<BlockDesc>(), (uint32_t)p->N, (uint32_t)p->n_meas, p->gS.U, p->gS.P, 0, 1,
+             p->dred.as<double>(), p->dparams.as<Params>(), p->dtrace.as<double>(), p->trace_cap,
+             p->dstate.as<IterState>(), (double*)nullptr);
   mark(2);
   if (with_objective) {  // the sweep's finalize wrote NaN: fill the objective of this iteration
     objective_trace_kernel<<<1, kCtaThreads, 0, s>>>(p->dred.as<double>(), (uint32_t)p->gS.P, p->dored.as<double>(),
@@ -1493,14 +1529,19 @@ admm_status admm_plan_profile(admm_plan* p, uint64_t iters, const char** names, 
                                     "gemv_h(H,q)", "zupdate", "finalize"};
   static const char* kNamesSP[4] = {"sweep(H)", "rows_finalize(rhs)+finalize", "hemv(Kpacked,r)",
                                     "hemv_finalize(q)"};
+  static const char* kNamesSF[4] = {"sweep(H)", "rows_finalize(rhs)+finalize", "hemv(Kpacked,r)+finalize",
+                                    "(none)"};
+  static const char* kNames2F[7] = {"gemv_n(H,c)", "rows_finalize(rhs)", "hemv(Kpacked,r)+finalize", "(none)",
+                                    "gemv_h(H,q)", "zupdate", "finalize"};
   static const char* kNamesB[7] = {"bgemm(H,C)", "brows(rhs)", "bgemm(K,R)", "brows(q)", "bgemm_adj(H,Q)",
                                    "bzupdate", "bfinalize"};
   return run_guarded([&] {
     check_plan(p);
     const int nk = (int)admm_plan_kernel_count(p);
-    const char* const* kn = p->schedule == 2   ? (p->kpacked ? kNamesSP : kNamesS)
+    const bool fused = p->kpacked && p->hemv_fuse;
+    const char* const* kn = p->schedule == 2   ? (fused ? kNamesSF : p->kpacked ? kNamesSP : kNamesS)
                             : p->schedule == 3 ? kNamesB
-                                               : (p->kpacked ? kNames2P : kNames2);
+                                               : (fused ? kNames2F : p->kpacked ? kNames2P : kNames2);
     std::vector<cudaEvent_t> ev(nk + 1);
     for (auto& e : ev) CK(cudaEventCreate(&e));
     std::vector<double> acc(nk, 0.0);
@@ -1542,6 +1583,7 @@ admm_status admm_plan_get_info(const admm_plan* p, admm_plan_info* info) {
     r.h_stream_bytes_per_iter = 2 * hb;
     r.bytes_per_iter = 2 * hb + kb_dense + vb;  // two-pass algorithmic bytes
     r.launches_per_iter = p->schedule == 3 ? 7 : p->schedule == 2 ? (p->trace_obj ? 7 : 4) : (p->trace_obj ? 9 : 7);
+    if (p->schedule != 3 && p->kpacked && p->hemv_fuse) r.launches_per_iter -= 1;  // finalize inside hemv
     r.schedule = (uint64_t)p->schedule;
     r.grid_sweep = p->gS.P;
     r.hbm_bytes_per_iter = (p->schedule == 2 ? hb : 2 * hb) + kb + vb;

@@ -31,13 +31,15 @@ struct SweepDesc {    // one per segment j
 };
 
 constexpr int kSweepU = 8;   // producer: row-instructions in flight per lane
+
 constexpr int kSweepUA = 8;  // consumer (L2 re-read): row-instructions in flight per lane
 
 // Named barriers (id 0 is __syncthreads).
 __device__ __forceinline__ void nb_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void nb_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-constexpr int kSweepThreads = 512;           // 16 warps
+constexpr int kSweepThreads = 512;           // 16 warps (8 producers with kSweepU = 16 and 4
+                                             // consumers at 384 threads measured 191 vs 126 us)
 constexpr int kProdWarps = 8;                // (C) HBM stream
 constexpr int kConsWarps = 8;                // (D) column update + (A) L2 re-read
 constexpr int kConsThreads = kConsWarps * kWarp;
@@ -56,6 +58,7 @@ sweep_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const Bloc
              const SweepDesc* __restrict__ segs, uint32_t M, uint32_t N, uint32_t n_meas, uint64_t Utot,
              const double2* __restrict__ q, ColVecs cv, double2* __restrict__ wpart,
              const Params* __restrict__ prm, double* __restrict__ red, IterState* st) {
+  pdl_enter();
   constexpr int PV = Store<S>::kPerVec;
   constexpr int W = LPR * PV;            // columns per strip
   constexpr int RPI = kWarp / LPR;       // rows per warp instruction
@@ -274,6 +277,7 @@ constexpr int kBulkRI = 2;            // row-instructions per compute warp per s
 constexpr int kBulkCompute = 8;       // compute warps (warps 1..8)
 constexpr int kBulkCons = 7;          // consumer warps (warps 9..15)
 constexpr int kBulkHandoff = (kBulkCompute + kBulkCons) * kWarp;  // FULL/EMPTY participants
+constexpr int kBulkThreads = 512;                                  // loader + compute + consumer warps
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
@@ -311,7 +315,7 @@ __device__ __forceinline__ void tma_2d(uint32_t dst, const void* tmap, int c0, i
 // tmaps: one 128-byte CUtensorMap per local block (H_b viewed as rows x 2*ld reals),
 // box = {ROWB / sizeof(real), R}; rows past the block and columns past ld are zero-filled.
 template <typename S, int LPR>
-__global__ void __launch_bounds__(kSweepThreads, 1)
+__global__ void __launch_bounds__(kBulkThreads, 1)
 sweep_bulk_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const BlockDesc* __restrict__ blocks,
                   const SweepDesc* __restrict__ segs, uint32_t M, uint32_t N, uint32_t n_meas, uint64_t Utot,
                   const double2* __restrict__ q, ColVecs cv, double2* __restrict__ wpart,
@@ -333,7 +337,7 @@ sweep_bulk_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const
   double2* us = zbuf + 2 * (size_t)kBulkCompute * M * W;
   double2* cs = us + (size_t)M * W;
   double2* pre = cs + (size_t)M * W;
-  __shared__ double sm_red[kSweepThreads / kWarp];
+  __shared__ double sm_red[kBulkThreads / kWarp];
 
   const uint64_t P = gridDim.x, p = blockIdx.x;
   const uint64_t x0 = sk_lo(p, Utot, P);
@@ -544,11 +548,11 @@ sweep_bulk_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const
     }
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) st->nonfinite = 1u;
-  double r = block_sum<kSweepThreads>(rp2, sm_red);
+  double r = block_sum<kBulkThreads>(rp2, sm_red);
   if (threadIdx.x == 0) red[p] = r;
-  r = block_sum<kSweepThreads>(rd2, sm_red);
+  r = block_sum<kBulkThreads>(rd2, sm_red);
   if (threadIdx.x == 0) red[P + p] = r;
-  r = block_sum<kSweepThreads>(l1, sm_red);
+  r = block_sum<kBulkThreads>(l1, sm_red);
   if (threadIdx.x == 0) red[2 * P + p] = r;
 }
 
@@ -569,6 +573,7 @@ rows_finalize_sweep_kernel(RowVecs rv, const double2* __restrict__ wpart, const 
                            const double* __restrict__ red, const Params* __restrict__ prm,
                            double* __restrict__ trace, uint64_t trace_cap, IterState* st,
                            double* __restrict__ slot) {
+  pdl_enter();
   __shared__ double sm[kCtaWarps];
   __shared__ double2 gsum[kRfGroups][kRfRows];
   const uint32_t b = blockIdx.y;
@@ -588,11 +593,7 @@ rows_finalize_sweep_kernel(RowVecs rv, const double2* __restrict__ wpart, const 
     __syncthreads();
     if (grp == 0 && row < bd.rows) {
       for (int g2 = 1; g2 < kRfGroups; ++g2) w = cadd(w, gsum[g2][tr]);
-      double2 gij = rv.g[bd.row0 + row];
-      for (uint32_t qj = 0; qj < N; ++qj) {
-        if (qj == bd.j) continue;
-        gij = csub(gij, rv.ghat[gblocks[bd.i * N + qj].mvec_off + row]);  // global table: peers too
-      }
+      const double2 gij = gij_row(rv, gblocks, bd, N, row);
       const uint32_t o = bd.mvec_off + row;
       rv.gij[o] = gij;
       rv.r[o] = csub(gij, w);
