@@ -28,6 +28,7 @@
 #include "admm_setup.cuh"
 #include "admm_sweep.cuh"
 #include "admm_tile.cuh"
+#include "admm_slab.cuh"
 #include "admm_hemv.cuh"
 #include "admm_batched.cuh"
 
@@ -170,6 +171,10 @@ struct admm_plan {
   uint32_t tile_ns = 0;     // its SMEM ring slots (32-row tasks)
   int tile_cps = 1;         // its CTAs per SM
   DevBuf dHt;               // strip-major copy of H for sweep_tile_kernel
+  int slab_rpl = 0;         // > 0: per-warp slab sweep (sweep_slab_kernel), rows per lane
+  uint32_t slab_C = 1, slab_nw = 0, slab_ns = 0, slab_Ns = 0;  // cluster size, compute warps, stages, slabs
+  std::vector<SlabDesc> slabs;
+  DevBuf dHs, dslabs;       // slab-major copy of H, slab table
   bool kpacked = false;     // K applied from the packed Hermitian tiles (hemv_kernel)
   bool kkeep = false;       // ... with an L2 evict_last policy (ADMM_B200_KKEEP)
   int hemv_occ = 1;         // hemv_kernel CTAs per SM (1: register prefetch of the next tile)
@@ -505,11 +510,115 @@ bool try_tile(admm_plan* p) {
   return true;
 }
 
+// Per-warp slab sweep (admm_slab.cuh): rows of every strip cut into RPW-row slabs (each
+// inside one replica), C x NW slabs per cluster; NS ring stages of NW slabs per CTA.
+// Chosen to avoid padding rows (padding is streamed from HBM), then the smallest
+// cluster with >= 3 stages.  ADMM_B200_SLAB_C / ADMM_B200_SLAB_RPW force a geometry.
+template <typename S>
+bool try_slab(admm_plan* p) {
+  constexpr uint32_t W = kSlabNSL * (16 / sizeof(S));
+  if (p->Pr != 1) return false;  // the replica mean needs every row block of a strip
+  if (const char* env = std::getenv("ADMM_B200_SWEEP"))
+    if (std::strcmp(env, "slab") != 0) return false;  // another sweep variant requested
+  const uint32_t M = (uint32_t)p->Mr, N = (uint32_t)p->Nc;
+  if (M * W > kWarp) return false;  // the D warp maps (replica, column) onto lanes
+  int fC = 0, fR = 0;
+  if (const char* e = std::getenv("ADMM_B200_SLAB_C")) fC = std::atoi(e);
+  if (const char* e = std::getenv("ADMM_B200_SLAB_RPW")) fR = std::atoi(e);
+  const size_t cap = 227 * 1024;
+  struct Cand { uint32_t rpl, C, nw, ns, Ns; uint64_t pad; };
+  bool have = false;
+  Cand best{};
+  for (uint32_t rpl : {2u, 1u, 4u}) {
+    const uint32_t rpw = rpl * kWarp;
+    if (fR && (uint32_t)fR != rpw) continue;
+    uint32_t Ns = 0;
+    uint64_t pad = 0;
+    for (uint32_t i = 0; i < M; ++i) {
+      const uint32_t R = p->blocks[(size_t)i * N].rows;
+      Ns += (uint32_t)cdiv(R, rpw);
+      pad += cdiv(R, rpw) * rpw - R;
+    }
+    for (uint32_t C : {1u, 2u, 4u, 8u}) {
+      if (fC && (uint32_t)fC != C) continue;
+      const uint32_t nw = (uint32_t)cdiv(Ns, C);
+      if (nw > (uint32_t)kSlabMaxW || (C > 1 && nw * (C - 1) >= Ns)) continue;  // no empty rank
+      const size_t fixed = slab_smem_bytes(0, nw, rpw, C, M, W);
+      const size_t per = (size_t)nw * rpw * kSlabRB + nw * sizeof(uint64_t);
+      const uint32_t ns = (uint32_t)std::min<size_t>((cap - fixed) / per, 8);
+      if (ns < 3) continue;
+      Cand c{rpl, C, nw, ns, Ns, pad};
+      const bool better = !have || c.pad < best.pad || (c.pad == best.pad && c.C < best.C);
+      if (better) best = c, have = true;
+    }
+  }
+  if (!have) return false;
+  const size_t smem = slab_smem_bytes(best.ns, best.nw, best.rpl * kWarp, best.C, M, W);
+  auto fn = best.rpl == 1 ? sweep_slab_kernel<S, 1> : best.rpl == 2 ? sweep_slab_kernel<S, 2> : sweep_slab_kernel<S, 4>;
+  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  std::vector<SweepDesc> segs(N);
+  uint64_t u = 0;
+  for (uint32_t j = 0; j < N; ++j) {
+    const uint32_t cols = p->blocks[j].cols;
+    segs[j] = SweepDesc{u, 0, (uint32_t)cdiv(cols, W), cols};
+    u += segs[j].n_strips;
+  }
+  // co-resident clusters (one CTA per SM)
+  uint64_t ncl = (uint64_t)p->num_sms / best.C;
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(ncl * best.C));
+    cfg.blockDim = dim3((best.nw + 1) * kWarp);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = best.C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, fn, &cfg) != cudaSuccess || nc < 1) {
+      cudaGetLastError();
+      return false;
+    }
+    ncl = std::min<uint64_t>(ncl, (uint64_t)nc);
+  }
+  const uint64_t P = std::min<uint64_t>(u, ncl);
+  uint64_t po = 0;
+  for (auto& sd : segs) {  // one partial slot per cluster overlapping the segment
+    sd.part_off = po;
+    po += (uint64_t)seg_count(sd.unit0, sd.n_strips, u, P) * p->n_meas;
+  }
+  std::vector<SlabDesc> slabs;
+  const uint32_t rpw = best.rpl * kWarp;
+  for (uint32_t i = 0; i < M; ++i) {
+    const BlockDesc& b = p->blocks[(size_t)i * N];
+    for (uint32_t r = 0; r < b.rows; r += rpw) slabs.push_back(SlabDesc{i, r, b.row0 + r, std::min(rpw, b.rows - r)});
+  }
+  p->segs = segs;
+  p->slabs = slabs;
+  p->gS.U = u;
+  p->gS.P = P;
+  p->slab_rpl = (int)best.rpl;
+  p->slab_C = best.C;
+  p->slab_nw = best.nw;
+  p->slab_ns = best.ns;
+  p->slab_Ns = best.Ns;
+  p->sweep_smem = smem;
+  p->sweep_bulk = false;
+  p->dwpart_s.alloc(po * sizeof(double2));
+  upload_desc(p->dsegs, segs.data(), segs.size() * sizeof(SweepDesc));
+  upload_desc(p->dslabs, slabs.data(), slabs.size() * sizeof(SlabDesc));
+  p->dHs.alloc(u * best.Ns * (uint64_t)rpw * kSlabRB);
+  return true;
+}
+
 template <typename S>
 void choose_schedule(admm_plan* p, int requested) {
   p->schedule = 1;
   if (requested == 1) return;
-  if (try_tile<S, 128>(p) || try_tile<S, 64>(p)) {
+  if (try_slab<S>(p) || try_tile<S, 128>(p) || try_tile<S, 64>(p)) {
     p->schedule = 2;
     return;
   }
@@ -596,6 +705,18 @@ void build_tile(admm_plan* p) {
                                                           p->dblocks.as<BlockDesc>(), p->dsegs.as<SweepDesc>(),
                                                           (uint32_t)p->Mr, (uint32_t)p->Nc, (uint32_t)p->n_meas, W,
                                                           total, p->dHt.as<S>());
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(p->stream));
+}
+
+// Slab-major copy of the (scaled) H for sweep_slab_kernel.
+template <typename S>
+void build_slab(admm_plan* p) {
+  const uint64_t chunks = p->gS.U * p->slab_Ns * (uint64_t)p->slab_rpl * kWarp * kSlabNSL;
+  slab_h_kernel<S><<<p->num_sms * 8, 256, 0, p->stream>>>(p->dH.as<S>(), p->dhN.as<MatDesc>(),
+                                                          p->dsegs.as<SweepDesc>(), p->dslabs.as<SlabDesc>(),
+                                                          (uint32_t)p->Nc, p->slab_Ns, (uint32_t)p->slab_rpl * kWarp,
+                                                          chunks, p->dHs.as<S>());
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(p->stream));
 }
@@ -813,8 +934,38 @@ void launch_tile_rb(admm_plan* p, cudaStream_t s) {
       p->dtrace_tile.p ? p->dtrace_tile.as<unsigned long long>() : nullptr);
 }
 
+template <typename S, int RPL>
+void launch_slab_rpl(admm_plan* p, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(p->gS.P * p->slab_C));
+  cfg.blockDim = dim3((p->slab_nw + 1) * kWarp);
+  cfg.dynamicSmemBytes = p->sweep_smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = p->slab_C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  CK(cudaLaunchKernelEx(&cfg, sweep_slab_kernel<S, RPL>, (const S*)p->dHs.as<S>(),
+                        (const SlabDesc*)p->dslabs.as<SlabDesc>(), (const BlockDesc*)p->dblocks.as<BlockDesc>(),
+                        (const SweepDesc*)p->dsegs.as<SweepDesc>(), (uint32_t)p->Mr, (uint32_t)p->Nc,
+                        (uint32_t)p->n_meas, p->gS.U, p->slab_ns, p->slab_Ns, (const double2*)p->dq.as<double2>(),
+                        col_vecs(p), p->dwpart_s.as<double2>(), (const Params*)p->dparams.as<Params>(),
+                        p->dred.as<double>(), p->dstate.as<IterState>()));
+}
+
 template <typename S>
 void launch_sweep(admm_plan* p, cudaStream_t s) {
+  if (p->slab_rpl == 1)
+    return launch_slab_rpl<S, 1>(p, s);
+  if (p->slab_rpl == 2)
+    return launch_slab_rpl<S, 2>(p, s);
+  if (p->slab_rpl == 4)
+    return launch_slab_rpl<S, 4>(p, s);
   if (p->tile_rb == 128)
     launch_tile_rb<S, 128>(p, s);
   else if (p->tile_rb == 64)
@@ -1328,10 +1479,12 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
   if (p->dtype == ADMM_C128) {
     upload_h<double2>(p.get(), h, h_dtype);
     if (p->tile_rb) build_tile<double2>(p.get());
+    if (p->slab_rpl) build_slab<double2>(p.get());
     factor_blocks<double2>(p.get());
   } else {
     upload_h<float2>(p.get(), h, h_dtype);
     if (p->tile_rb) build_tile<float2>(p.get());
+    if (p->slab_rpl) build_slab<float2>(p.get());
     factor_blocks<float2>(p.get());
   }
   if (p->batch > 1) {
