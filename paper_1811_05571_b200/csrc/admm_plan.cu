@@ -172,7 +172,7 @@ struct admm_plan {
   int tile_cps = 1;         // its CTAs per SM
   DevBuf dHt;               // strip-major copy of H for sweep_tile_kernel
   int slab_rpl = 0;         // > 0: per-warp slab sweep (sweep_slab_kernel), rows per lane
-  uint32_t slab_C = 1, slab_nw = 0, slab_ns = 0, slab_Ns = 0;  // cluster size, compute warps, stages, slabs
+  uint32_t slab_C = 1, slab_nw = 0, slab_ns = 0, slab_Ns = 0, slab_lag = 1, slab_nd = 1;  // cluster size, compute warps, stages, slabs, (A) lag
   std::vector<SlabDesc> slabs;
   DevBuf dHs, dslabs;       // slab-major copy of H, slab table
   bool kpacked = false;     // K applied from the packed Hermitian tiles (hemv_kernel)
@@ -543,7 +543,7 @@ bool try_slab(admm_plan* p) {
       if (fC && (uint32_t)fC != C) continue;
       const uint32_t nw = (uint32_t)cdiv(Ns, C);
       if (nw > (uint32_t)kSlabMaxW || (C > 1 && nw * (C - 1) >= Ns)) continue;  // no empty rank
-      const size_t fixed = slab_smem_bytes(0, nw, rpw, C, M, W);
+      const size_t fixed = slab_smem_bytes(0, nw, kSlabMaxD, rpw, C, M, W, N);
       const size_t per = (size_t)nw * rpw * kSlabRB + nw * sizeof(uint64_t);
       const uint32_t ns = (uint32_t)std::min<size_t>((cap - fixed) / per, 8);
       if (ns < 3) continue;
@@ -553,8 +553,21 @@ bool try_slab(admm_plan* p) {
     }
   }
   if (!have) return false;
-  const size_t smem = slab_smem_bytes(best.ns, best.nw, best.rpl * kWarp, best.C, M, W);
-  auto fn = best.rpl == 1 ? sweep_slab_kernel<S, 1> : best.rpl == 2 ? sweep_slab_kernel<S, 2> : sweep_slab_kernel<S, 4>;
+  // lag of (A) behind (C) and D warps: the deepest lag the ring allows, two D warps when
+  // the slot-reuse rules permit (slab_lag_ok)
+  uint32_t lag = std::max<uint32_t>(1, std::min<uint32_t>(best.ns - 2, kSlabZB - 1));
+  if (const char* e = std::getenv("ADMM_B200_SLAB_LAG"))
+    lag = std::max<uint32_t>(1, std::min<uint32_t>((uint32_t)std::atoi(e), std::min<uint32_t>(best.ns - 2, kSlabZB - 1)));
+  uint32_t nd = kSlabMaxD;
+  if (const char* e = std::getenv("ADMM_B200_SLAB_ND")) nd = std::max(1, std::min(kSlabMaxD, std::atoi(e)));
+  while (lag > 1 && !slab_lag_ok(lag, nd) && !slab_lag_ok(lag, 1)) --lag;
+  if (!slab_lag_ok(lag, nd)) nd = 1;
+  if (!slab_lag_ok(lag, nd)) return false;
+  const size_t smem = slab_smem_bytes(best.ns, best.nw, nd, best.rpl * kWarp, best.C, M, W, N);
+  const bool tr = std::getenv("ADMM_B200_SLAB_TRACE") != nullptr;
+  auto fn = best.rpl == 1 ? (tr ? sweep_slab_kernel<S, 1, true> : sweep_slab_kernel<S, 1, false>)
+          : best.rpl == 2 ? (tr ? sweep_slab_kernel<S, 2, true> : sweep_slab_kernel<S, 2, false>)
+                          : (tr ? sweep_slab_kernel<S, 4, true> : sweep_slab_kernel<S, 4, false>);
   CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   std::vector<SweepDesc> segs(N);
   uint64_t u = 0;
@@ -568,7 +581,7 @@ bool try_slab(admm_plan* p) {
   {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(ncl * best.C));
-    cfg.blockDim = dim3((best.nw + 1) * kWarp);
+    cfg.blockDim = dim3((best.nw + nd) * kWarp);
     cfg.dynamicSmemBytes = smem;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -578,7 +591,19 @@ bool try_slab(admm_plan* p) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int nc = 0;
-    if (cudaOccupancyMaxActiveClusters(&nc, fn, &cfg) != cudaSuccess || nc < 1) {
+    const cudaError_t e = cudaOccupancyMaxActiveClusters(&nc, fn, &cfg);
+    if (std::getenv("ADMM_B200_DEBUG")) {
+      cudaFuncAttributes fa{};
+      cudaFuncGetAttributes(&fa, fn);
+      int ob = -1;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ob, fn, (best.nw + nd) * kWarp, smem);
+      std::fprintf(stderr, "slab attrs: regs=%d maxthr=%d static_smem=%zu maxdyn=%d occ_blocks=%d\n", fa.numRegs,
+                   fa.maxThreadsPerBlock, fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes, ob);
+    }
+    if (std::getenv("ADMM_B200_DEBUG"))
+      std::fprintf(stderr, "slab: C=%u rpw=%u nw=%u nd=%u lag=%u ns=%u smem=%zu clusters=%d (%s)\n", best.C,
+                   best.rpl * kWarp, best.nw, nd, lag, best.ns, smem, nc, cudaGetErrorString(e));
+    if (e != cudaSuccess || nc < 1) {
       cudaGetLastError();
       return false;
     }
@@ -605,12 +630,19 @@ bool try_slab(admm_plan* p) {
   p->slab_nw = best.nw;
   p->slab_ns = best.ns;
   p->slab_Ns = best.Ns;
+  p->slab_lag = lag;
+  p->slab_nd = nd;
   p->sweep_smem = smem;
   p->sweep_bulk = false;
   p->dwpart_s.alloc(po * sizeof(double2));
   upload_desc(p->dsegs, segs.data(), segs.size() * sizeof(SweepDesc));
   upload_desc(p->dslabs, slabs.data(), slabs.size() * sizeof(SlabDesc));
   p->dHs.alloc(u * best.Ns * (uint64_t)rpw * kSlabRB);
+  if (std::getenv("ADMM_B200_SLAB_TRACE")) {
+    const uint64_t n = P * best.C * 64 * 8;
+    p->dtrace_tile.alloc(n * sizeof(unsigned long long));
+    CK(cudaMemset(p->dtrace_tile.p, 0, n * sizeof(unsigned long long)));
+  }
   return true;
 }
 
@@ -938,7 +970,7 @@ template <typename S, int RPL>
 void launch_slab_rpl(admm_plan* p, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(p->gS.P * p->slab_C));
-  cfg.blockDim = dim3((p->slab_nw + 1) * kWarp);
+  cfg.blockDim = dim3((p->slab_nw + p->slab_nd) * kWarp);
   cfg.dynamicSmemBytes = p->sweep_smem;
   cfg.stream = s;
   cudaLaunchAttribute at[2];
@@ -950,12 +982,15 @@ void launch_slab_rpl(admm_plan* p, cudaStream_t s) {
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  CK(cudaLaunchKernelEx(&cfg, sweep_slab_kernel<S, RPL>, (const S*)p->dHs.as<S>(),
+  auto fn = p->dtrace_tile.p ? sweep_slab_kernel<S, RPL, true> : sweep_slab_kernel<S, RPL, false>;
+  CK(cudaLaunchKernelEx(&cfg, fn, (const S*)p->dHs.as<S>(),
                         (const SlabDesc*)p->dslabs.as<SlabDesc>(), (const BlockDesc*)p->dblocks.as<BlockDesc>(),
                         (const SweepDesc*)p->dsegs.as<SweepDesc>(), (uint32_t)p->Mr, (uint32_t)p->Nc,
-                        (uint32_t)p->n_meas, p->gS.U, p->slab_ns, p->slab_Ns, (const double2*)p->dq.as<double2>(),
+                        (uint32_t)p->n_meas, p->gS.U, p->slab_ns, p->slab_lag, p->slab_Ns, p->slab_nw,
+                        (const double2*)p->dq.as<double2>(),
                         col_vecs(p), p->dwpart_s.as<double2>(), (const Params*)p->dparams.as<Params>(),
-                        p->dred.as<double>(), p->dstate.as<IterState>()));
+                        p->dred.as<double>(), p->dstate.as<IterState>(),
+                        p->dtrace_tile.p ? p->dtrace_tile.as<unsigned long long>() : nullptr));
 }
 
 template <typename S>
@@ -1526,7 +1561,15 @@ admm_status admm_plan_create(const admm_plan_options* opts, const admm_solver_co
 void admm_plan_destroy(admm_plan* plan) {
   if (plan) {
     cudaSetDevice(plan->device);
-    if (plan->dtrace_tile.p) {  // diagnostics: mean phase durations of the last sweep launch
+    if (plan->dtrace_tile.p && plan->slab_rpl) {  // diagnostics: raw slab-sweep timestamps -> file
+      const size_t n = plan->gS.P * plan->slab_C * 64 * 8;
+      std::vector<unsigned long long> t(n);
+      cudaMemcpy(t.data(), plan->dtrace_tile.p, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+      if (FILE* f = std::fopen(std::getenv("ADMM_B200_SLAB_TRACE"), "wb")) {
+        std::fwrite(t.data(), sizeof(unsigned long long), n, f);
+        std::fclose(f);
+      }
+    } else if (plan->dtrace_tile.p) {  // diagnostics: mean phase durations of the last sweep launch
       const size_t n = plan->gS.P * 64 * 8;
       std::vector<unsigned long long> t(n);
       cudaMemcpy(t.data(), plan->dtrace_tile.p, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost);

@@ -37,8 +37,8 @@ namespace admm {
 
 constexpr int kSlabRB = 64;          // bytes per slab row (one strip row)
 constexpr int kSlabNSL = kSlabRB / 16;  // 16-byte chunks per row
-constexpr int kSlabMaxW = 16;        // compute warps per CTA (+1 D warp)
-constexpr int kSlabThreads = (kSlabMaxW + 1) * kWarp;
+constexpr int kSlabMaxW = 16;        // compute warps per CTA (+ D warps)
+constexpr int kSlabThreads = (kSlabMaxW + 4) * kWarp;  // up to 2 D warps; 20 warps keep the 96-register cap
 
 struct SlabDesc {
   uint32_t rep;    // replica (row block) i
@@ -78,8 +78,13 @@ __device__ __forceinline__ uint32_t mapa(uint32_t a, uint32_t rank) {
 __device__ __forceinline__ void st_cluster_d2(uint32_t a, double2 v) {
   asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
 }
-__device__ __forceinline__ void mbar_arrive_remote(uint32_t a) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(a) : "memory");
+// Asynchronous 16-byte store into a peer CTA's shared memory that completes (tx bytes)
+// on the peer's mbarrier: no release fence, so it never waits for this thread's
+// outstanding global stores.
+__device__ __forceinline__ void st_async_d2(uint32_t a, double2 v, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(a), "d"(v.x),
+               "d"(v.y), "r"(mbar)
+               : "memory");
 }
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* b, uint32_t parity) {
   asm volatile(
@@ -87,6 +92,54 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* b, uint32_t parity) 
       "WAITC_%=;\n}\n" ::"r"(smem_u32(b)),
       "r"(parity)
       : "memory");
+}
+
+// mbarrier / bulk-copy helpers on 32-bit shared addresses (computed once per thread).
+__device__ __forceinline__ void mbar_wait_s(uint32_t a, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAITU_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAITU_%=;\n}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_s(uint32_t a) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_s(uint32_t a, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+      : "memory");
+}
+
+// mbarrier wait with a long suspend-time hint: the warp sleeps until the phase completes
+// instead of re-polling.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAITS_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n @!p bra WAITS_%=;\n}\n" ::"r"(
+          smem_u32(b)),
+      "r"(parity), "r"(0x989680u)
+      : "memory");
+}
+
+// Bulk shared -> global copy (async proxy: no LSU store traffic from the issuing warp).
+__device__ __forceinline__ void bulk_s2g(void* gdst, uint32_t ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(ssrc), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 __device__ __forceinline__ double2 lds_d2(uint32_t a) {
@@ -107,37 +160,56 @@ template <>
 struct Chunk<double2> {
   static constexpr int PV = 1;
   double2 v;
-  __device__ __forceinline__ void load(uint32_t a) { v = lds_d2(a); }
+  __device__ __forceinline__ void ld(const unsigned char* p) { v = *reinterpret_cast<const double2*>(p); }
   __device__ __forceinline__ double2 get(int) const { return v; }
 };
 template <>
 struct Chunk<float2> {
   static constexpr int PV = 2;
   float4 v;
-  __device__ __forceinline__ void load(uint32_t a) { v = lds_f4(a); }
+  __device__ __forceinline__ void ld(const unsigned char* p) { v = *reinterpret_cast<const float4*>(p); }
   __device__ __forceinline__ double2 get(int e) const {
     return e == 0 ? make_double2((double)v.x, (double)v.y) : make_double2((double)v.z, (double)v.w);
   }
 };
 
-__host__ __device__ inline size_t slab_smem_bytes(uint32_t ns, uint32_t nw, uint32_t rpw, uint32_t C, uint32_t M,
-                                                  uint32_t W) {
-  return (size_t)ns * nw * rpw * kSlabRB            // ring
-         + (size_t)nw * ns * sizeof(uint64_t)       // per-warp full barriers
-         + 6 * sizeof(uint64_t)                     // zfull[2], cfull[2], xfull[2]
-         + 2 * (size_t)nw * W * sizeof(double2)     // z partials per warp
-         + 2 * (size_t)C * M * W * sizeof(double2)  // cluster exchange
-         + 2 * (size_t)M * W * sizeof(double2);     // c of the strip
+constexpr int kSlabZB = 4;   // z-partial / c / barrier slots (lag L <= kSlabZB - 1)
+constexpr int kSlabXB = 8;   // cluster-exchange slots
+constexpr int kSlabPF = 3;   // D warp: its strips of iterates prefetched ahead (cp.async)
+constexpr int kSlabMaxD = 2; // D warps
+
+__host__ __device__ inline size_t slab_smem_bytes(uint32_t ns, uint32_t nw, uint32_t nd, uint32_t rpw, uint32_t C,
+                                                  uint32_t M, uint32_t W, uint32_t N) {
+  return (size_t)ns * nw * rpw * kSlabRB                        // ring
+         + (size_t)nw * ns * sizeof(uint64_t)                   // per-warp full barriers
+         + (2 * kSlabZB + kSlabXB) * sizeof(uint64_t)           // zfull, cfull, xfull
+         + (size_t)kSlabZB * nw * W * sizeof(double2)           // z partials per warp
+         + (size_t)kSlabXB * C * M * W * sizeof(double2)        // cluster exchange
+         + (size_t)kSlabZB * M * W * sizeof(double2)            // c of the strip
+         + (size_t)nd * (kSlabPF + 1) * 3 * kWarp * sizeof(double2)  // prefetched c, s, v
+         + (size_t)(nw + nd) * 4 * sizeof(double)               // per-warp residual partials
+         + (size_t)N * sizeof(SweepDesc) + (2 * (size_t)M * N + N) * sizeof(uint32_t);  // descriptor tables
+}
+
+// Valid (lag, D warps) pairs: the slot-reuse arguments below need (kSlabZB - 1 - L) and
+// (kSlabXB - 1 - L) to be multiples of ND (the D warp of strip k also owns strip k + ND).
+__host__ __device__ inline bool slab_lag_ok(uint32_t L, uint32_t ND) {
+  return L >= 1 && L <= kSlabZB - 1 && (kSlabZB - 1 - L) % ND == 0 && (kSlabXB - 1 - L) % ND == 0 &&
+         kSlabXB - 1 - L >= ND;
 }
 
 // RPL = rows per lane in (A) = RPW / 32.  Launched as NCl clusters of C CTAs, block
-// (NW + 1) x 32 threads: warps 0..NW-1 compute, warp NW is the D warp.
-template <typename S, int RPL>
+// (NW + ND) x 32 threads: warps 0..NW-1 compute, warps NW.. are the D warps (strip k is
+// updated by D warp k % ND).  L = lag of the (A) pass behind the (C) pass, in strips.
+// 20 warps x 32 lanes: the register allocation granularity (4 warps) caps this at 96
+// registers per thread (65536 / (20 x 32)).
+template <typename S, int RPL, bool kTrace>
 __global__ void __launch_bounds__(kSlabThreads, 1)
 sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, const BlockDesc* __restrict__ blocks,
                   const SweepDesc* __restrict__ segs, uint32_t M, uint32_t N, uint32_t n_meas, uint64_t U, uint32_t NS,
-                  uint32_t Ns, const double2* __restrict__ q, ColVecs cv, double2* __restrict__ wpart,
-                  const Params* __restrict__ prm, double* __restrict__ red, IterState* st) {
+                  uint32_t L, uint32_t Ns, uint32_t NW, const double2* __restrict__ q, ColVecs cv,
+                  double2* __restrict__ wpart, const Params* __restrict__ prm, double* __restrict__ red, IterState* st,
+                  unsigned long long* __restrict__ trace) {  // diagnostics (ADMM_B200_SLAB_TRACE), else null
   using CK = Chunk<S>;
   constexpr int PV = CK::PV;
   constexpr int W = kSlabNSL * PV;          // columns per strip
@@ -146,70 +218,98 @@ sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, 
   constexpr int CRG = kWarp / kSlabNSL;     // (C) rows per warp instruction
   constexpr int CNU = RPW / CRG;            // (C) instructions per slab
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const uint32_t NW = blockDim.x / kWarp - 1;
+  const uint32_t NWT = blockDim.x / kWarp, ND = NWT - NW;
   const uint32_t C = cluster_size();
   unsigned char* ring = smem_raw;
   uint64_t* fullb = reinterpret_cast<uint64_t*>(ring + (size_t)NS * NW * SLAB_B);  // [NW][NS]
-  uint64_t* zfull = fullb + (size_t)NW * NS;
-  uint64_t* cfull = zfull + 2;
-  uint64_t* xfull = cfull + 2;
-  double2* zp = reinterpret_cast<double2*>(xfull + 2);  // [2][NW][W]
-  double2* xb = zp + 2 * (size_t)NW * W;                // [2][C][M][W]
-  double2* cb = xb + 2 * (size_t)C * M * W;             // [2][M][W]
+  uint64_t* zfull = fullb + (size_t)NW * NS;              // [kSlabZB]
+  uint64_t* cfull = zfull + kSlabZB;                      // [kSlabZB]
+  uint64_t* xfull = cfull + kSlabZB;                      // [kSlabXB]
+  double2* zp = reinterpret_cast<double2*>(xfull + kSlabXB);  // [kSlabZB][NW][W]
+  double2* xb = zp + (size_t)kSlabZB * NW * W;            // [kSlabXB][C][M][W]
+  double2* cb = xb + (size_t)kSlabXB * C * M * W;         // [kSlabZB][M][W]
+  double2* pf = cb + (size_t)kSlabZB * M * W;             // [ND][kSlabPF + 1][3][32]
+  double* wred = reinterpret_cast<double*>(pf + (size_t)ND * (kSlabPF + 1) * 3 * kWarp);  // [NWT][4]
+  // descriptor tables in SMEM: nothing on the per-strip path reads global metadata
+  SweepDesc* tseg = reinterpret_cast<SweepDesc*>(wred + (size_t)NWT * 4);  // [N]
+  uint32_t* tvec = reinterpret_cast<uint32_t*>(tseg + N);                  // [M][N] vec_off
+  uint32_t* tmvec = tvec + (size_t)M * N;                                  // [M][N] mvec_off
+  uint32_t* tsego = tmvec + (size_t)M * N;                                 // [N] seg_off
+  for (uint32_t b = threadIdx.x; b < M * N; b += blockDim.x) {
+    tvec[b] = blocks[b].vec_off;
+    tmvec[b] = blocks[b].mvec_off;
+  }
+  for (uint32_t b = threadIdx.x; b < N; b += blockDim.x) {
+    tseg[b] = segs[b];
+    tsego[b] = blocks[b].seg_off;
+  }
+  double rp2 = 0.0, rd2 = 0.0, l1 = 0.0;  // residual partials (rank 0 D warps)
+  bool bad = false;
 
   const uint32_t rank = cluster_rank();
   const uint64_t NCl = cluster_count(), cl = cluster_id();
   const uint64_t x0 = sk_lo(cl, U, NCl), xe = sk_lo(cl + 1, U, NCl);
   const uint32_t nstrip = (uint32_t)(xe - x0);
   const uint32_t warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+  // diagnostics: per-strip timestamps of compute warp 0 and the D warps (first 64 strips)
+  auto mark = [&](uint32_t k, int ev) {
+    if (kTrace && lane == 0 && k < 64 && (warp == 0 || warp >= NW))
+      trace[((uint64_t)blockIdx.x * 64 + k) * 8 + ev] = clock64();
+  };
 
   if (threadIdx.x == 0) {
     for (uint32_t b = 0; b < NW * NS; ++b) mbar_init(&fullb[b], 1);
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kSlabZB; ++b) {
       mbar_init(&zfull[b], NW);
       mbar_init(&cfull[b], 1);
-      mbar_init(&xfull[b], C * kWarp);
     }
+    for (int b = 0; b < kSlabXB; ++b) mbar_init(&xfull[b], 1);  // + C x M x W x 16 tx bytes
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (C > 1)
     cluster_sync_all();  // peers' barriers initialised before any remote arrive
   else
     __syncthreads();
-  pdl_enter();  // q, c, s, v of the previous kernels are visible from here on
 
   if (warp < NW) {
     // ============================================================ compute warp
+    // Static data first (H and the tables never change during a solve): the first NS
+    // stages stream in while the previous kernel of the chain finishes (PDL).
     const uint32_t sl = rank * NW + warp;
     const bool act = sl < Ns;
     SlabDesc sd{0, 0, 0, 0};
     if (act) sd = slabs[sl];
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    uint64_t* myfull = fullb + (size_t)warp * NS;
-    const uint32_t ring_w = smem_u32(ring) + warp * SLAB_B;  // + stage * NW * SLAB_B
+    const uint32_t full_s = smem_u32(fullb) + warp * NS * 8;      // this warp's full barriers
+    const uint32_t zfull_s = smem_u32(zfull), cfull_s = smem_u32(cfull);
+    const uint32_t ring_off = warp * SLAB_B;                          // + stage * NW * SLAB_B
+    const uint32_t ring_s = smem_u32(ring) + ring_off;
     const uint32_t stage_stride = NW * SLAB_B;
     const unsigned char* src0 = reinterpret_cast<const unsigned char*>(Hs) + ((x0 * Ns) + sl) * (uint64_t)SLAB_B;
     const uint64_t strip_stride = (uint64_t)Ns * SLAB_B;
     auto issue = [&](uint32_t k, uint32_t stg) {
-      mbar_expect_tx(&myfull[stg], SLAB_B);
-      bulk_g2s(ring_w + stg * stage_stride, src0 + k * strip_stride, SLAB_B, &myfull[stg], pol);
+      mbar_expect_tx_s(full_s + stg * 8, SLAB_B);
+      bulk_g2s_s(ring_s + stg * stage_stride, src0 + k * strip_stride, SLAB_B, full_s + stg * 8, pol);
     };
     if (act && lane == 0)
       for (uint32_t k = 0; k < NS && k < nstrip; ++k) issue(k, k);
+    uint32_t j = 0;
+    if (nstrip > 0)
+      while (j + 1 < N && tseg[j + 1].unit0 <= x0) ++j;
+    uint32_t jA = j;
+    uint64_t seg_end = (nstrip > 0) ? tseg[j].unit0 + tseg[j].n_strips : 0;   // (C) side
+    uint64_t seg_endA = seg_end;                                              // (A) side
+    pdl_enter();  // q of the previous kernels is visible from here on
 
     // (C) lane geometry: rows crg + CRG u, logical chunk ccol at physical ccol ^ swz
     const uint32_t crg = lane / kSlabNSL, ccol = lane % kSlabNSL;
     const uint32_t c_off = crg * kSlabRB + ((ccol ^ ((crg >> 1) & 3)) * 16);
     // (A) lane geometry: rows lane + 32 m, logical chunk s at physical s ^ swz
     const uint32_t a_swz = (lane >> 1) & 3;
-    uint32_t j = 0;
-    if (nstrip > 0)
-      while (j + 1 < N && segs[j + 1].unit0 <= x0) ++j;
-    uint32_t jA = j;
     double2 qr[CNU];
     auto load_q = [&](uint32_t jj) {
-      const double2* qb = q + blocks[sd.rep * N + jj].mvec_off + sd.lrow0;
+      const double2* qb = q + tmvec[sd.rep * N + jj] + sd.lrow0;
 #pragma unroll
       for (int u = 0; u < CNU; ++u) {
         const uint32_t r = crg + CRG * u;
@@ -220,90 +320,90 @@ sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, 
     double2 wacc[RPL];
 #pragma unroll
     for (int m = 0; m < RPL; ++m) wacc[m] = make_double2(0.0, 0.0);
-    uint64_t seg_end = (nstrip > 0) ? segs[j].unit0 + segs[j].n_strips : 0;   // (C) side
-    uint64_t seg_endA = seg_end;                                              // (A) side
     uint32_t stgC = 0, phC = 0, stgA = 0;
+    const double2* cb_rep = cb + (size_t)sd.rep * W;
+    double2* zp_w = zp + (size_t)warp * W + ccol * PV;
 
-    for (uint32_t k = 0; k <= nstrip; ++k) {
+    for (uint32_t k = 0; k < nstrip + L; ++k) {
       if (k < nstrip) {
         // ---------------------------------------------------------- (C) strip k
         if (x0 + k == seg_end) {
           ++j;
-          seg_end = segs[j].unit0 + segs[j].n_strips;
+          seg_end = tseg[j].unit0 + tseg[j].n_strips;
           load_q(j);
         }
         if (act) {
-          mbar_wait(&myfull[stgC], phC);
-          const uint32_t base = ring_w + stgC * stage_stride + c_off;
-          double2 acc[PV], acc2[PV];
+          mbar_wait_s(full_s + stgC * 8, phC);
+          mark(k, 0);
+          const unsigned char* base = ring + ring_off + stgC * stage_stride + c_off;
+          CK h[CNU];
 #pragma unroll
-          for (int e = 0; e < PV; ++e) acc[e] = acc2[e] = make_double2(0.0, 0.0);
+          for (int u = 0; u < CNU; ++u) h[u].ld(base + u * CRG * kSlabRB);
+          double2 acc[4][PV];
 #pragma unroll
-          for (int u = 0; u < CNU; u += 2) {
-            CK h0, h1;
-            h0.load(base + u * CRG * kSlabRB);
-            h1.load(base + (u + 1) * CRG * kSlabRB);
+          for (int a4 = 0; a4 < 4; ++a4)
 #pragma unroll
-            for (int e = 0; e < PV; ++e) {
-              cmac_conj(acc[e], h0.get(e), qr[u]);
-              cmac_conj(acc2[e], h1.get(e), qr[u + 1]);
-            }
-          }
+            for (int e = 0; e < PV; ++e) acc[a4][e] = make_double2(0.0, 0.0);
+#pragma unroll
+          for (int u = 0; u < CNU; ++u)
+#pragma unroll
+            for (int e = 0; e < PV; ++e) cmac_conj(acc[u & 3][e], h[u].get(e), qr[u]);
 #pragma unroll
           for (int e = 0; e < PV; ++e) {
-            acc[e] = cadd(acc[e], acc2[e]);
+            double2 z = cadd(cadd(acc[0][e], acc[1][e]), cadd(acc[2][e], acc[3][e]));
 #pragma unroll
             for (int o = kSlabNSL; o < kWarp; o <<= 1) {
-              acc[e].x += __shfl_xor_sync(0xffffffffu, acc[e].x, o);
-              acc[e].y += __shfl_xor_sync(0xffffffffu, acc[e].y, o);
+              z.x += __shfl_xor_sync(0xffffffffu, z.x, o);
+              z.y += __shfl_xor_sync(0xffffffffu, z.y, o);
             }
-          }
-          if (crg == 0) {
-            double2* dst = zp + ((size_t)(k & 1) * NW + warp) * W + ccol * PV;
-#pragma unroll
-            for (int e = 0; e < PV; ++e) dst[e] = acc[e];
+            if (crg == 0) zp_w[(size_t)(k % kSlabZB) * NW * W + e] = z;
           }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&zfull[k & 1]);
+        if (lane == 0) mbar_arrive_s(zfull_s + (k % kSlabZB) * 8);
+        mark(k, 1);
         if (++stgC == NS) stgC = 0, phC ^= 1u;
       }
-      if (k >= 1) {
-        // ---------------------------------------------------------- (A) strip k - 1
-        const uint32_t kk = k - 1;
-        mbar_wait(&cfull[kk & 1], (kk >> 1) & 1);
+      if (k >= L) {
+        // ---------------------------------------------------------- (A) strip k - L
+        const uint32_t kk = k - L;
+        mbar_wait_s(cfull_s + (kk % kSlabZB) * 8, (kk / kSlabZB) & 1);
+        mark(kk, 2);
         if (act) {
-          const double2* cbi = cb + ((size_t)(kk & 1) * M + sd.rep) * W;
+          const double2* cbi = cb_rep + (size_t)(kk % kSlabZB) * M * W;
           double2 cr[kSlabNSL][PV];
 #pragma unroll
           for (int s2 = 0; s2 < kSlabNSL; ++s2)
 #pragma unroll
             for (int e = 0; e < PV; ++e) cr[s2][e] = cbi[s2 * PV + e];
-          const uint32_t base = ring_w + stgA * stage_stride + lane * kSlabRB;
+          const unsigned char* base = ring + ring_off + stgA * stage_stride + lane * kSlabRB;
+          CK h[RPL][kSlabNSL];
+#pragma unroll
+          for (int m = 0; m < RPL; ++m)
+#pragma unroll
+            for (int s2 = 0; s2 < kSlabNSL; ++s2) h[m][s2].ld(base + m * kWarp * kSlabRB + ((s2 ^ a_swz) * 16));
 #pragma unroll
           for (int m = 0; m < RPL; ++m) {
-            CK h[kSlabNSL];
-#pragma unroll
-            for (int s2 = 0; s2 < kSlabNSL; ++s2) h[s2].load(base + m * kWarp * kSlabRB + ((s2 ^ a_swz) * 16));
             double2 ae = make_double2(0.0, 0.0), ao = make_double2(0.0, 0.0);
 #pragma unroll
             for (int s2 = 0; s2 < kSlabNSL; ++s2)
 #pragma unroll
               for (int e = 0; e < PV; ++e) {
                 if ((s2 * PV + e) & 1)
-                  cmac(ao, h[s2].get(e), cr[s2][e]);
+                  cmac(ao, h[m][s2].get(e), cr[s2][e]);
                 else
-                  cmac(ae, h[s2].get(e), cr[s2][e]);
+                  cmac(ae, h[m][s2].get(e), cr[s2][e]);
               }
             wacc[m] = cadd(wacc[m], cadd(ae, ao));
           }
           __syncwarp();  // every lane has consumed the stage
           if (lane == 0 && kk + NS < nstrip) issue(kk + NS, stgA);
+          mark(kk, 3);
         }
         if (++stgA == NS) stgA = 0;
         if (x0 + kk + 1 == seg_endA || kk + 1 == nstrip) {  // flush this segment's w partial
           if (act) {
-            const SweepDesc sg = segs[jA];
+            const SweepDesc sg = tseg[jA];
             const uint64_t slotp = cl - sk_owner(sg.unit0, U, NCl);
             double2* dst = wpart + sg.part_off + slotp * n_meas + sd.mrow0;
 #pragma unroll
@@ -315,16 +415,16 @@ sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, 
           }
           if (kk + 1 < nstrip) {
             ++jA;
-            seg_endA = segs[jA].unit0 + segs[jA].n_strips;
+            seg_endA = tseg[jA].unit0 + tseg[jA].n_strips;
           }
         }
       }
     }
   } else {
-    // ============================================================ D warp
+    // ============================================================ D warps
+    const uint32_t dw = warp - NW;
     const uint32_t i = lane / W, t = lane % W;
     const bool dl = i < M;
-    const bool store = rank == 0;
     // this CTA's warps of replica i: slabs are ordered by replica, so a contiguous range
     uint32_t wlo = 0, whi = 0;
     if (dl) {
@@ -338,72 +438,84 @@ sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, 
       }
       if (whi == 0) wlo = 0;
     }
+    pdl_enter();  // c, s, v, kappa of the previous kernels are visible from here on
     const double m_rep = prm->m_rep, kappa = prm->kappa;
     const double kappa2_lo = kappa * kappa * (1.0 - 0x1p-40);
     const double inv_m = 1.0 / m_rep;
     const bool pow2_m = inv_m * m_rep == 1.0 && (__double_as_longlong(m_rep) & 0xfffffffffffffull) == 0;
-    double rp2 = 0.0, rd2 = 0.0, l1 = 0.0;
-    bool bad = false;
-    uint32_t j = 0;
-    if (nstrip > 0)
-      while (j + 1 < N && segs[j + 1].unit0 <= x0) ++j;
-    SweepDesc sg = nstrip > 0 ? segs[j] : SweepDesc{0, 0, 0, 0};
-    // iterates of strip k (prefetched one strip ahead)
-    double2 cpre = make_double2(0.0, 0.0), spre = cpre, vpre = cpre;
-    auto fetch = [&](uint64_t x, const SweepDesc& g, uint32_t jj, double2& c_, double2& s_, double2& v_) {
-      const uint32_t col = (uint32_t)(x - g.unit0) * W + t;
-      if (dl && col < g.cols) {
-        const uint32_t o = blocks[i * N + jj].vec_off + col;
-        c_ = cv.c[o];
-        s_ = cv.s[o];
-        v_ = cv.v[blocks[jj].seg_off + col];
-      } else {
-        c_ = s_ = v_ = make_double2(0.0, 0.0);
-      }
+    // this D warp's strips dw, dw + ND, ...: the n-th is prefetched (cp.async, zero-filled
+    // past the segment) into pfw[n % (kSlabPF + 1)] kSlabPF strips ahead
+    double2* pfw = pf + (size_t)dw * (kSlabPF + 1) * 3 * kWarp + lane;
+    auto seg_of = [&](uint64_t x, uint32_t& jj) {
+      while (jj + 1 < N && tseg[jj + 1].unit0 <= x) ++jj;
     };
-    if (nstrip > 0) fetch(x0, sg, j, cpre, spre, vpre);
-    const uint32_t xb_me = smem_u32(xb);
-    for (uint32_t k = 0; k < nstrip; ++k) {
-      const uint64_t x = x0 + k;
-      const uint32_t col = (uint32_t)(x - sg.unit0) * W + t;
-      const bool dcol = dl && col < sg.cols;
-      const uint32_t jc = j;
-      // prefetch strip k + 1
-      double2 cn = make_double2(0.0, 0.0), sn = cn, vn1 = cn;
-      SweepDesc sgn = sg;
-      uint32_t jn = j;
-      if (k + 1 < nstrip) {
-        if (x + 1 == sg.unit0 + sg.n_strips) sgn = segs[++jn];
-        fetch(x + 1, sgn, jn, cn, sn, vn1);
+    uint32_t jf = 0;
+    auto fetch = [&](uint32_t n) {
+      const uint32_t kf = dw + n * ND;
+      if (kf < nstrip) {
+        const uint64_t x = x0 + kf;
+        seg_of(x, jf);
+        const SweepDesc g = tseg[jf];
+        const uint32_t col = (uint32_t)(x - g.unit0) * W + t;
+        const bool ok = dl && col < g.cols;
+        const uint32_t o = tvec[(dl ? i : 0) * N + jf] + (ok ? col : 0);
+        const uint32_t so = tsego[jf] + (ok ? col : 0);
+        double2* dst = pfw + (size_t)(n % (kSlabPF + 1)) * 3 * kWarp;
+        cpa(dst, cv.c + o, ok);
+        cpa(dst + kWarp, cv.s + o, ok);
+        cpa(dst + 2 * kWarp, cv.v + so, ok);
       }
-      const uint32_t kb = k & 1;
-      mbar_wait(&zfull[kb], (k >> 1) & 1);
+      cpa_commit();
+    };
+    for (uint32_t n = 0; n < kSlabPF; ++n) fetch(n);
+    uint32_t j = 0;
+    const uint32_t xb_me = smem_u32(xb);
+    uint32_t n = 0;
+    for (uint32_t k = dw; k < nstrip; k += ND, ++n) {
+      const uint64_t x = x0 + k;
+      seg_of(x, j);
+      const uint32_t col = (uint32_t)(x - tseg[j].unit0) * W + t;
+      const bool dcol = dl && col < tseg[j].cols;
+      const uint32_t kb = k % kSlabZB;
+      cpa_wait<kSlabPF - 1>();  // this strip's iterates
+      const double2* pk = pfw + (size_t)(n % (kSlabPF + 1)) * 3 * kWarp;
+      const double2 cpre = pk[0], spre = pk[kWarp], vpre = pk[2 * kWarp];
+      mbar_wait(&zfull[kb], (k / kSlabZB) & 1);
+      mark(k, 4);
       double2 z = make_double2(0.0, 0.0);
       {
         const double2* zs = zp + (size_t)kb * NW * W + t;
         for (uint32_t w = wlo; w < whi; ++w) z = cadd(z, zs[(size_t)w * W]);
       }
       if (C > 1) {
-        const uint32_t me = xb_me + (uint32_t)((((size_t)kb * C + rank) * M + (dl ? i : 0)) * W + t) * 16;
+        // every rank sends its CTA partial to every rank (itself included) with st.async;
+        // the local arrive.expect_tx arms this strip's phase for the C x M x W x 16 bytes
+        const uint32_t xs_b = k % kSlabXB;
+        const uint32_t xf = smem_u32(&xfull[xs_b]);
+        if (lane == 0) mbar_expect_tx(&xfull[xs_b], C * M * W * 16);
+        const uint32_t me = xb_me + (uint32_t)((((size_t)xs_b * C + rank) * M + (dl ? i : 0)) * W + t) * 16;
         if (dl)
-          for (uint32_t r2 = 0; r2 < C; ++r2) st_cluster_d2(mapa(me, r2), z);
-        const uint32_t xf = smem_u32(&xfull[kb]);
-        for (uint32_t r2 = 0; r2 < C; ++r2) mbar_arrive_remote(mapa(xf, r2));
-        mbar_wait_cluster(&xfull[kb], (k >> 1) & 1);
+          for (uint32_t r2 = 0; r2 < C; ++r2) st_async_d2(mapa(me, r2), z, mapa(xf, r2));
+        mbar_wait_cluster(&xfull[xs_b], (k / kSlabXB) & 1);
         z = make_double2(0.0, 0.0);
         if (dl) {
-          const double2* xs = xb + ((size_t)kb * C * M + i) * W + t;
+          const double2* xs = xb + ((size_t)xs_b * C * M + i) * W + t;
           for (uint32_t r2 = 0; r2 < C; ++r2) z = cadd(z, xs[(size_t)r2 * M * W]);
         }
       }
       // (D) u = c + z; mean over replicas of (u + s) in ascending i; v; s; next c
       const double2 u = cadd(cpre, z);
       const double2 a = cadd(u, spre);
-      double2 mean = make_double2(0.0, 0.0);
-      for (uint32_t i2 = 0; i2 < M; ++i2) {
-        const double ax = __shfl_sync(0xffffffffu, a.x, i2 * W + t);
-        const double ay = __shfl_sync(0xffffffffu, a.y, i2 * W + t);
-        mean = cadd(mean, make_double2(ax, ay));
+      double2 mean;
+      if (M == 1) {
+        mean = a;
+      } else {
+        mean = make_double2(0.0, 0.0);
+        for (uint32_t i2 = 0; i2 < M; ++i2) {
+          const double ax = __shfl_sync(0xffffffffu, a.x, i2 * W + t);
+          const double ay = __shfl_sync(0xffffffffu, a.y, i2 * W + t);
+          mean = cadd(mean, make_double2(ax, ay));
+        }
       }
       mean = pow2_m ? make_double2(mean.x * inv_m, mean.y * inv_m) : make_double2(mean.x / m_rep, mean.y / m_rep);
       const double2 vnew = soft_threshold_fast(mean, kappa, kappa2_lo);
@@ -412,42 +524,54 @@ sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, 
       if (dl) cb[((size_t)kb * M + i) * W + t] = dcol ? cnew : make_double2(0.0, 0.0);
       __syncwarp();
       if (lane == 0) mbar_arrive(&cfull[kb]);
-      if (store && dcol) {  // off the critical path
-        const uint32_t o = blocks[i * N + jc].vec_off + col;
+      mark(k, 5);
+      fetch(n + kSlabPF);  // into the slot of this warp's previous strip (consumed)
+      if (rank == 0 && dcol) {  // off the critical path
+        const uint32_t o = tvec[i * N + j] + col;
         bad |= !cfinite(u);
         cv.u[o] = u;
         cv.s[o] = snew;
         cv.c[o] = cnew;
         rp2 += cabs2(csub(u, vnew));
         if (i == 0) {
-          const uint32_t so = blocks[jc].seg_off + col;
+          const uint32_t so = tsego[j] + col;
           cv.vprev[so] = vpre;
           cv.v[so] = vnew;
           rd2 += cabs2(csub(vnew, vpre));
           l1 += hypot(vnew.x, vnew.y);
         }
       }
-      cpre = cn;
-      spre = sn;
-      vpre = vn1;
-      sg = sgn;
-      j = jn;
     }
-    if (store) {
+    cpa_wait<0>();
+  }
+  // residual partials: warp sums, then the warps in order (rank 0 carries them)
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        rp2 += __shfl_xor_sync(0xffffffffu, rp2, o);
-        rd2 += __shfl_xor_sync(0xffffffffu, rd2, o);
-        l1 += __shfl_xor_sync(0xffffffffu, l1, o);
-      }
-      const bool anybad = __any_sync(0xffffffffu, bad);
-      if (lane == 0) {
-        red[cl] = rp2;
-        red[NCl + cl] = rd2;
-        red[2 * NCl + cl] = l1;
-        if (anybad) st->nonfinite = 1u;
-      }
+  for (int o = 16; o > 0; o >>= 1) {
+    rp2 += __shfl_xor_sync(0xffffffffu, rp2, o);
+    rd2 += __shfl_xor_sync(0xffffffffu, rd2, o);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+  }
+  const bool anybad = __any_sync(0xffffffffu, bad);
+  if (lane == 0) {
+    wred[warp * 4 + 0] = rp2;
+    wred[warp * 4 + 1] = rd2;
+    wred[warp * 4 + 2] = l1;
+    wred[warp * 4 + 3] = anybad ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  if (rank == 0 && threadIdx.x == 0) {
+    double a = 0.0, d = 0.0, l = 0.0;
+    bool nb = false;
+    for (uint32_t w = NW; w < NWT; ++w) {
+      a += wred[w * 4 + 0];
+      d += wred[w * 4 + 1];
+      l += wred[w * 4 + 2];
+      nb |= wred[w * 4 + 3] != 0.0;
     }
+    red[cl] = a;
+    red[NCl + cl] = d;
+    red[2 * NCl + cl] = l;
+    if (nb) st->nonfinite = 1u;
   }
   if (C > 1) cluster_sync_all();  // no CTA leaves while a peer may still write its SMEM
 }
