@@ -541,6 +541,8 @@ bool try_slab(admm_plan* p) {
     }
     for (uint32_t C : {1u, 2u, 4u, 8u}) {
       if (fC && (uint32_t)fC != C) continue;
+      // clusters of 4+ measured slower than the two-pass schedule (config 3: 344 vs 264 us)
+      if (!fC && C > 2) continue;
       const uint32_t nw = (uint32_t)cdiv(Ns, C);
       if (nw > (uint32_t)kSlabMaxW || (C > 1 && nw * (C - 1) >= Ns)) continue;  // no empty rank
       const size_t fixed = slab_smem_bytes(0, nw, kSlabMaxD, rpw, C, M, W, N);
@@ -1490,8 +1492,11 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
   {  // packed Hermitian K for the per-iteration K apply (the batched schedule uses bgemm)
     const char* e = std::getenv("ADMM_B200_KPACK");
     p->kpacked = p->batch == 1 && !(e && e[0] == '0');
+    // keep the packed K in L2 (evict_last) when the H stream cannot evict it: the slab
+    // sweep streams H with evict_first, so a K of <= ~96 MiB stays resident across
+    // iterations (config 2: K apply 19 -> 15 us)
     const char* e2 = std::getenv("ADMM_B200_KKEEP");
-    p->kkeep = e2 && e2[0] == '1';
+    p->kkeep = e2 ? e2[0] == '1' : (p->slab_rpl > 0 && p->k_elems * p->elem / 2 <= (96ull << 20));
   }
   p->scal_ptr = p->fused_scal ? reinterpret_cast<double*>(p->ghat_ptr + p->Mr * p->Nc * p->mpad)
                               : p->dscal.as<double>();
