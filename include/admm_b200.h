@@ -189,6 +189,10 @@ typedef struct {
   uint64_t schedule;            /* 1 two-pass, 2 sweep */
   uint64_t grid_sweep;
   uint64_t hbm_bytes_per_iter;  /* compulsory HBM bytes of the chosen schedule */
+  uint64_t sweep_variant;       /* schedule 2 kernel: 1 L2 re-read sweep, 2 strip-major tile, 3 slab */
+  uint64_t slab_cluster;        /* slab sweep: thread-block cluster size (CTAs per strip) */
+  uint64_t slab_row_bytes;      /* slab sweep: bytes per strip row (64 or 32) */
+  uint64_t slab_rows;           /* slab sweep: rows per warp slab */
 } admm_plan_info;
 admm_status admm_plan_get_info(const admm_plan* plan, admm_plan_info* info);
 

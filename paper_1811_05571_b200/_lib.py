@@ -42,7 +42,8 @@ class PlanInfoC(ctypes.Structure):
                 ("h_stream_bytes_per_iter", _u64), ("bytes_per_iter", _u64),
                 ("launches_per_iter", _u64), ("grid_gemv_n", _u64), ("grid_gemv_h", _u64),
                 ("setup_seconds", _dbl), ("inner_dim_max", _u64), ("schedule", _u64),
-                ("grid_sweep", _u64), ("hbm_bytes_per_iter", _u64)]
+                ("grid_sweep", _u64), ("hbm_bytes_per_iter", _u64), ("sweep_variant", _u64),
+                ("slab_cluster", _u64), ("slab_row_bytes", _u64), ("slab_rows", _u64)]
 
 
 class ShardC(ctypes.Structure):

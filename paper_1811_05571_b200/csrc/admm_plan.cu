@@ -172,7 +172,7 @@ struct admm_plan {
   int tile_cps = 1;         // its CTAs per SM
   DevBuf dHt;               // strip-major copy of H for sweep_tile_kernel
   int slab_rpl = 0;         // > 0: per-warp slab sweep (sweep_slab_kernel), rows per lane
-  uint32_t slab_C = 1, slab_nw = 0, slab_ns = 0, slab_Ns = 0, slab_lag = 1, slab_nd = 1;  // cluster size, compute warps, stages, slabs, (A) lag
+  uint32_t slab_C = 1, slab_nw = 0, slab_ns = 0, slab_Ns = 0, slab_lag = 1, slab_nd = 1, slab_rb = 64;  // cluster size, compute warps, stages, slabs, (A) lag
   std::vector<SlabDesc> slabs;
   DevBuf dHs, dslabs;       // slab-major copy of H, slab table
   bool kpacked = false;     // K applied from the packed Hermitian tiles (hemv_kernel)
@@ -510,51 +510,74 @@ bool try_tile(admm_plan* p) {
   return true;
 }
 
+template <typename S>
+using SlabFn = void (*)(const S*, const SlabDesc*, const BlockDesc*, const SweepDesc*, uint32_t, uint32_t, uint32_t,
+                        uint64_t, uint32_t, uint32_t, uint32_t, uint32_t, const double2*, ColVecs, double2*,
+                        const Params*, double*, IterState*, unsigned long long*);
+template <typename S, int RB>
+SlabFn<S> slab_fn_rb(int rpl, bool tr) {
+  if (rpl == 1) return tr ? sweep_slab_kernel<S, 1, RB, true> : sweep_slab_kernel<S, 1, RB, false>;
+  if (rpl == 2) return tr ? sweep_slab_kernel<S, 2, RB, true> : sweep_slab_kernel<S, 2, RB, false>;
+  return tr ? sweep_slab_kernel<S, 4, RB, true> : sweep_slab_kernel<S, 4, RB, false>;
+}
+template <typename S>
+SlabFn<S> slab_fn(int rpl, uint32_t rb, bool tr) {
+  return rb == 32 ? slab_fn_rb<S, 32>(rpl, tr) : slab_fn_rb<S, 64>(rpl, tr);
+}
+
 // Per-warp slab sweep (admm_slab.cuh): rows of every strip cut into RPW-row slabs (each
 // inside one replica), C x NW slabs per cluster; NS ring stages of NW slabs per CTA.
 // Chosen to avoid padding rows (padding is streamed from HBM), then the smallest
 // cluster with >= 3 stages.  ADMM_B200_SLAB_C / ADMM_B200_SLAB_RPW force a geometry.
 template <typename S>
 bool try_slab(admm_plan* p) {
-  constexpr uint32_t W = kSlabNSL * (16 / sizeof(S));
   if (p->Pr != 1) return false;  // the replica mean needs every row block of a strip
   if (const char* env = std::getenv("ADMM_B200_SWEEP"))
     if (std::strcmp(env, "slab") != 0) return false;  // another sweep variant requested
   const uint32_t M = (uint32_t)p->Mr, N = (uint32_t)p->Nc;
-  if (M * W > kWarp) return false;  // the D warp maps (replica, column) onto lanes
-  int fC = 0, fR = 0;
+  int fC = 0, fR = 0, fB = 0;
   if (const char* e = std::getenv("ADMM_B200_SLAB_C")) fC = std::atoi(e);
   if (const char* e = std::getenv("ADMM_B200_SLAB_RPW")) fR = std::atoi(e);
+  if (const char* e = std::getenv("ADMM_B200_SLAB_RB")) fB = std::atoi(e);
   const size_t cap = 227 * 1024;
-  struct Cand { uint32_t rpl, C, nw, ns, Ns; uint64_t pad; };
+  struct Cand { uint32_t rb, rpl, C, nw, ns, Ns; uint64_t pad; };
   bool have = false;
   Cand best{};
-  for (uint32_t rpl : {2u, 1u, 4u}) {
-    const uint32_t rpw = rpl * kWarp;
-    if (fR && (uint32_t)fR != rpw) continue;
-    uint32_t Ns = 0;
-    uint64_t pad = 0;
-    for (uint32_t i = 0; i < M; ++i) {
-      const uint32_t R = p->blocks[(size_t)i * N].rows;
-      Ns += (uint32_t)cdiv(R, rpw);
-      pad += cdiv(R, rpw) * rpw - R;
-    }
-    for (uint32_t C : {1u, 2u, 4u, 8u}) {
-      if (fC && (uint32_t)fC != C) continue;
-      // clusters of 4+ measured slower than the two-pass schedule (config 3: 344 vs 264 us)
-      if (!fC && C > 2) continue;
-      const uint32_t nw = (uint32_t)cdiv(Ns, C);
-      if (nw > (uint32_t)kSlabMaxW || (C > 1 && nw * (C - 1) >= Ns)) continue;  // no empty rank
-      const size_t fixed = slab_smem_bytes(0, nw, kSlabMaxD, rpw, C, M, W, N);
-      const size_t per = (size_t)nw * rpw * kSlabRB + nw * sizeof(uint64_t);
-      const uint32_t ns = (uint32_t)std::min<size_t>((cap - fixed) / per, 8);
-      if (ns < 3) continue;
-      Cand c{rpl, C, nw, ns, Ns, pad};
-      const bool better = !have || c.pad < best.pad || (c.pad == best.pad && c.C < best.C);
-      if (better) best = c, have = true;
+  for (uint32_t rb : {64u, 32u}) {
+    if (fB && (uint32_t)fB != rb) continue;
+    const uint32_t W = rb / 16 * (16 / sizeof(S));
+    if (M * W > kWarp) continue;  // the D warp maps (replica, column) onto lanes
+    for (uint32_t rpl : {2u, 1u, 4u}) {
+      const uint32_t rpw = rpl * kWarp;
+      if (fR && (uint32_t)fR != rpw) continue;
+      uint32_t Ns = 0;
+      uint64_t pad = 0;
+      for (uint32_t i = 0; i < M; ++i) {
+        const uint32_t R = p->blocks[(size_t)i * N].rows;
+        Ns += (uint32_t)cdiv(R, rpw);
+        pad += cdiv(R, rpw) * rpw - R;
+      }
+      for (uint32_t C : {1u, 2u, 4u, 8u}) {
+        if (fC && (uint32_t)fC != C) continue;
+        // clusters of 4+ measured slower than the two-pass schedule (config 3: 344 vs 264 us)
+        if (!fC && C > 2) continue;
+        const uint32_t nw = (uint32_t)cdiv(Ns, C);
+        if (nw > (uint32_t)kSlabMaxW || (C > 1 && nw * (C - 1) >= Ns)) continue;  // no empty rank
+        const size_t fixed = slab_smem_bytes(0, nw, kSlabMaxD, rpw, rb, C, M, W, N);
+        const size_t per = (size_t)nw * rpw * rb + nw * sizeof(uint64_t);
+        const uint32_t ns = (uint32_t)std::min<size_t>((cap - fixed) / per, 8);
+        if (ns < 3) continue;
+        Cand c{rb, rpl, C, nw, ns, Ns, pad};
+        // fewest padding rows (they are streamed), then the smallest cluster, then the
+        // widest rows (fewer strips, fewer per-strip overheads)
+        const bool better = !have || c.pad < best.pad || (c.pad == best.pad && c.C < best.C) ||
+                            (c.pad == best.pad && c.C == best.C && c.rb > best.rb);
+        if (better) best = c, have = true;
+      }
     }
   }
   if (!have) return false;
+  const uint32_t W = best.rb / 16 * (16 / sizeof(S));
   // lag of (A) behind (C) and D warps: the deepest lag the ring allows, two D warps when
   // the slot-reuse rules permit (slab_lag_ok)
   uint32_t lag = std::max<uint32_t>(1, std::min<uint32_t>(best.ns - 2, kSlabZB - 1));
@@ -565,11 +588,8 @@ bool try_slab(admm_plan* p) {
   while (lag > 1 && !slab_lag_ok(lag, nd) && !slab_lag_ok(lag, 1)) --lag;
   if (!slab_lag_ok(lag, nd)) nd = 1;
   if (!slab_lag_ok(lag, nd)) return false;
-  const size_t smem = slab_smem_bytes(best.ns, best.nw, nd, best.rpl * kWarp, best.C, M, W, N);
-  const bool tr = std::getenv("ADMM_B200_SLAB_TRACE") != nullptr;
-  auto fn = best.rpl == 1 ? (tr ? sweep_slab_kernel<S, 1, true> : sweep_slab_kernel<S, 1, false>)
-          : best.rpl == 2 ? (tr ? sweep_slab_kernel<S, 2, true> : sweep_slab_kernel<S, 2, false>)
-                          : (tr ? sweep_slab_kernel<S, 4, true> : sweep_slab_kernel<S, 4, false>);
+  const size_t smem = slab_smem_bytes(best.ns, best.nw, nd, best.rpl * kWarp, best.rb, best.C, M, W, N);
+  const auto fn = slab_fn<S>(best.rpl, best.rb, std::getenv("ADMM_B200_SLAB_TRACE") != nullptr);
   CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   std::vector<SweepDesc> segs(N);
   uint64_t u = 0;
@@ -603,7 +623,7 @@ bool try_slab(admm_plan* p) {
                    fa.maxThreadsPerBlock, fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes, ob);
     }
     if (std::getenv("ADMM_B200_DEBUG"))
-      std::fprintf(stderr, "slab: C=%u rpw=%u nw=%u nd=%u lag=%u ns=%u smem=%zu clusters=%d (%s)\n", best.C,
+      std::fprintf(stderr, "slab: rb=%u C=%u rpw=%u nw=%u nd=%u lag=%u ns=%u smem=%zu clusters=%d (%s)\n", best.rb, best.C,
                    best.rpl * kWarp, best.nw, nd, lag, best.ns, smem, nc, cudaGetErrorString(e));
     if (e != cudaSuccess || nc < 1) {
       cudaGetLastError();
@@ -639,7 +659,8 @@ bool try_slab(admm_plan* p) {
   p->dwpart_s.alloc(po * sizeof(double2));
   upload_desc(p->dsegs, segs.data(), segs.size() * sizeof(SweepDesc));
   upload_desc(p->dslabs, slabs.data(), slabs.size() * sizeof(SlabDesc));
-  p->dHs.alloc(u * best.Ns * (uint64_t)rpw * kSlabRB);
+  p->dHs.alloc(u * best.Ns * (uint64_t)rpw * best.rb);
+  p->slab_rb = best.rb;
   if (std::getenv("ADMM_B200_SLAB_TRACE")) {
     const uint64_t n = P * best.C * 64 * 8;
     p->dtrace_tile.alloc(n * sizeof(unsigned long long));
@@ -746,8 +767,9 @@ void build_tile(admm_plan* p) {
 // Slab-major copy of the (scaled) H for sweep_slab_kernel.
 template <typename S>
 void build_slab(admm_plan* p) {
-  const uint64_t chunks = p->gS.U * p->slab_Ns * (uint64_t)p->slab_rpl * kWarp * kSlabNSL;
-  slab_h_kernel<S><<<p->num_sms * 8, 256, 0, p->stream>>>(p->dH.as<S>(), p->dhN.as<MatDesc>(),
+  const uint64_t chunks = p->gS.U * p->slab_Ns * (uint64_t)p->slab_rpl * kWarp * (p->slab_rb / 16);
+  auto kern = p->slab_rb == 32 ? slab_h_kernel<S, 32> : slab_h_kernel<S, 64>;
+  kern<<<p->num_sms * 8, 256, 0, p->stream>>>(p->dH.as<S>(), p->dhN.as<MatDesc>(),
                                                           p->dsegs.as<SweepDesc>(), p->dslabs.as<SlabDesc>(),
                                                           (uint32_t)p->Nc, p->slab_Ns, (uint32_t)p->slab_rpl * kWarp,
                                                           chunks, p->dHs.as<S>());
@@ -968,8 +990,8 @@ void launch_tile_rb(admm_plan* p, cudaStream_t s) {
       p->dtrace_tile.p ? p->dtrace_tile.as<unsigned long long>() : nullptr);
 }
 
-template <typename S, int RPL>
-void launch_slab_rpl(admm_plan* p, cudaStream_t s) {
+template <typename S>
+void launch_slab(admm_plan* p, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(p->gS.P * p->slab_C));
   cfg.blockDim = dim3((p->slab_nw + p->slab_nd) * kWarp);
@@ -984,25 +1006,19 @@ void launch_slab_rpl(admm_plan* p, cudaStream_t s) {
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  auto fn = p->dtrace_tile.p ? sweep_slab_kernel<S, RPL, true> : sweep_slab_kernel<S, RPL, false>;
-  CK(cudaLaunchKernelEx(&cfg, fn, (const S*)p->dHs.as<S>(),
-                        (const SlabDesc*)p->dslabs.as<SlabDesc>(), (const BlockDesc*)p->dblocks.as<BlockDesc>(),
-                        (const SweepDesc*)p->dsegs.as<SweepDesc>(), (uint32_t)p->Mr, (uint32_t)p->Nc,
-                        (uint32_t)p->n_meas, p->gS.U, p->slab_ns, p->slab_lag, p->slab_Ns, p->slab_nw,
-                        (const double2*)p->dq.as<double2>(),
-                        col_vecs(p), p->dwpart_s.as<double2>(), (const Params*)p->dparams.as<Params>(),
-                        p->dred.as<double>(), p->dstate.as<IterState>(),
+  const auto fn = slab_fn<S>(p->slab_rpl, p->slab_rb, p->dtrace_tile.p != nullptr);
+  CK(cudaLaunchKernelEx(&cfg, fn, (const S*)p->dHs.as<S>(), (const SlabDesc*)p->dslabs.as<SlabDesc>(),
+                        (const BlockDesc*)p->dblocks.as<BlockDesc>(), (const SweepDesc*)p->dsegs.as<SweepDesc>(),
+                        (uint32_t)p->Mr, (uint32_t)p->Nc, (uint32_t)p->n_meas, p->gS.U, p->slab_ns, p->slab_lag,
+                        p->slab_Ns, p->slab_nw, (const double2*)p->dq.as<double2>(), col_vecs(p),
+                        p->dwpart_s.as<double2>(), (const Params*)p->dparams.as<Params>(), p->dred.as<double>(),
+                        p->dstate.as<IterState>(),
                         p->dtrace_tile.p ? p->dtrace_tile.as<unsigned long long>() : nullptr));
 }
 
 template <typename S>
 void launch_sweep(admm_plan* p, cudaStream_t s) {
-  if (p->slab_rpl == 1)
-    return launch_slab_rpl<S, 1>(p, s);
-  if (p->slab_rpl == 2)
-    return launch_slab_rpl<S, 2>(p, s);
-  if (p->slab_rpl == 4)
-    return launch_slab_rpl<S, 4>(p, s);
+  if (p->slab_rpl) return launch_slab<S>(p, s);
   if (p->tile_rb == 128)
     launch_tile_rb<S, 128>(p, s);
   else if (p->tile_rb == 64)
@@ -1788,6 +1804,10 @@ admm_status admm_plan_get_info(const admm_plan* p, admm_plan_info* info) {
     r.schedule = (uint64_t)p->schedule;
     r.grid_sweep = p->gS.P;
     r.hbm_bytes_per_iter = (p->schedule == 2 ? hb : 2 * hb) + kb + vb;
+    r.sweep_variant = p->schedule != 2 ? 0 : p->slab_rpl ? 3 : p->tile_rb ? 2 : 1;
+    r.slab_cluster = p->slab_rpl ? p->slab_C : 0;
+    r.slab_row_bytes = p->slab_rpl ? p->slab_rb : 0;
+    r.slab_rows = p->slab_rpl ? (uint64_t)p->slab_rpl * kWarp : 0;
     r.grid_gemv_n = p->gN.P;
     r.grid_gemv_h = p->gH.P;
     r.setup_seconds = p->setup_s;

@@ -35,8 +35,13 @@
 
 namespace admm {
 
-constexpr int kSlabRB = 64;          // bytes per slab row (one strip row)
-constexpr int kSlabNSL = kSlabRB / 16;  // 16-byte chunks per row
+// Slab row width RB (bytes of one strip row): 64 (4 c128 / 8 c64 columns per strip) or
+// 32 (half the strip, for blocks with many rows).  16-byte chunk c of row r is stored at
+// position c ^ slab_swz<RB>(r): both SMEM access patterns below are then conflict-free.
+template <int RB>
+__host__ __device__ constexpr uint32_t slab_swz(uint32_t row) {
+  return (row / (128 / RB)) % (RB / 16);
+}
 constexpr int kSlabMaxW = 16;        // compute warps per CTA (+ D warps)
 constexpr int kSlabThreads = (kSlabMaxW + 4) * kWarp;  // up to 2 D warps; 20 warps keep the 96-register cap
 
@@ -178,9 +183,9 @@ constexpr int kSlabXB = 8;   // cluster-exchange slots
 constexpr int kSlabPF = 3;   // D warp: its strips of iterates prefetched ahead (cp.async)
 constexpr int kSlabMaxD = 2; // D warps
 
-__host__ __device__ inline size_t slab_smem_bytes(uint32_t ns, uint32_t nw, uint32_t nd, uint32_t rpw, uint32_t C,
-                                                  uint32_t M, uint32_t W, uint32_t N) {
-  return (size_t)ns * nw * rpw * kSlabRB                        // ring
+__host__ __device__ inline size_t slab_smem_bytes(uint32_t ns, uint32_t nw, uint32_t nd, uint32_t rpw, uint32_t rb,
+                                                  uint32_t C, uint32_t M, uint32_t W, uint32_t N) {
+  return (size_t)ns * nw * rpw * rb                             // ring
          + (size_t)nw * ns * sizeof(uint64_t)                   // per-warp full barriers
          + (2 * kSlabZB + kSlabXB) * sizeof(uint64_t)           // zfull, cfull, xfull
          + (size_t)kSlabZB * nw * W * sizeof(double2)           // z partials per warp
@@ -203,7 +208,7 @@ __host__ __device__ inline bool slab_lag_ok(uint32_t L, uint32_t ND) {
 // updated by D warp k % ND).  L = lag of the (A) pass behind the (C) pass, in strips.
 // 20 warps x 32 lanes: the register allocation granularity (4 warps) caps this at 96
 // registers per thread (65536 / (20 x 32)).
-template <typename S, int RPL, bool kTrace>
+template <typename S, int RPL, int RB, bool kTrace>
 __global__ void __launch_bounds__(kSlabThreads, 1)
 sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, const BlockDesc* __restrict__ blocks,
                   const SweepDesc* __restrict__ segs, uint32_t M, uint32_t N, uint32_t n_meas, uint64_t U, uint32_t NS,
@@ -212,10 +217,11 @@ sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, 
                   unsigned long long* __restrict__ trace) {  // diagnostics (ADMM_B200_SLAB_TRACE), else null
   using CK = Chunk<S>;
   constexpr int PV = CK::PV;
-  constexpr int W = kSlabNSL * PV;          // columns per strip
+  constexpr int NSL = RB / 16;              // 16-byte chunks per row
+  constexpr int W = NSL * PV;               // columns per strip
   constexpr int RPW = RPL * kWarp;          // rows per slab
-  constexpr int SLAB_B = RPW * kSlabRB;     // bytes per slab
-  constexpr int CRG = kWarp / kSlabNSL;     // (C) rows per warp instruction
+  constexpr int SLAB_B = RPW * RB;          // bytes per slab
+  constexpr int CRG = kWarp / NSL;          // (C) rows per warp instruction
   constexpr int CNU = RPW / CRG;            // (C) instructions per slab
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const uint32_t NWT = blockDim.x / kWarp, ND = NWT - NW;
@@ -303,10 +309,10 @@ sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, 
     pdl_enter();  // q of the previous kernels is visible from here on
 
     // (C) lane geometry: rows crg + CRG u, logical chunk ccol at physical ccol ^ swz
-    const uint32_t crg = lane / kSlabNSL, ccol = lane % kSlabNSL;
-    const uint32_t c_off = crg * kSlabRB + ((ccol ^ ((crg >> 1) & 3)) * 16);
+    const uint32_t crg = lane / NSL, ccol = lane % NSL;
+    const uint32_t c_off = crg * RB + ((ccol ^ slab_swz<RB>(crg)) * 16);  // swz(crg + CRG u) = swz(crg)
     // (A) lane geometry: rows lane + 32 m, logical chunk s at physical s ^ swz
-    const uint32_t a_swz = (lane >> 1) & 3;
+    const uint32_t a_swz = slab_swz<RB>(lane);  // = swz(lane + 32 m)
     double2 qr[CNU];
     auto load_q = [&](uint32_t jj) {
       const double2* qb = q + tmvec[sd.rep * N + jj] + sd.lrow0;
@@ -338,7 +344,7 @@ sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, 
           const unsigned char* base = ring + ring_off + stgC * stage_stride + c_off;
           CK h[CNU];
 #pragma unroll
-          for (int u = 0; u < CNU; ++u) h[u].ld(base + u * CRG * kSlabRB);
+          for (int u = 0; u < CNU; ++u) h[u].ld(base + u * CRG * RB);
           double2 acc[4][PV];
 #pragma unroll
           for (int a4 = 0; a4 < 4; ++a4)
@@ -352,7 +358,7 @@ sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, 
           for (int e = 0; e < PV; ++e) {
             double2 z = cadd(cadd(acc[0][e], acc[1][e]), cadd(acc[2][e], acc[3][e]));
 #pragma unroll
-            for (int o = kSlabNSL; o < kWarp; o <<= 1) {
+            for (int o = NSL; o < kWarp; o <<= 1) {
               z.x += __shfl_xor_sync(0xffffffffu, z.x, o);
               z.y += __shfl_xor_sync(0xffffffffu, z.y, o);
             }
@@ -371,22 +377,22 @@ sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, 
         mark(kk, 2);
         if (act) {
           const double2* cbi = cb_rep + (size_t)(kk % kSlabZB) * M * W;
-          double2 cr[kSlabNSL][PV];
+          double2 cr[NSL][PV];
 #pragma unroll
-          for (int s2 = 0; s2 < kSlabNSL; ++s2)
+          for (int s2 = 0; s2 < NSL; ++s2)
 #pragma unroll
             for (int e = 0; e < PV; ++e) cr[s2][e] = cbi[s2 * PV + e];
-          const unsigned char* base = ring + ring_off + stgA * stage_stride + lane * kSlabRB;
-          CK h[RPL][kSlabNSL];
+          const unsigned char* base = ring + ring_off + stgA * stage_stride + lane * RB;
+          CK h[RPL][NSL];
 #pragma unroll
           for (int m = 0; m < RPL; ++m)
 #pragma unroll
-            for (int s2 = 0; s2 < kSlabNSL; ++s2) h[m][s2].ld(base + m * kWarp * kSlabRB + ((s2 ^ a_swz) * 16));
+            for (int s2 = 0; s2 < NSL; ++s2) h[m][s2].ld(base + m * kWarp * RB + ((s2 ^ a_swz) * 16));
 #pragma unroll
           for (int m = 0; m < RPL; ++m) {
             double2 ae = make_double2(0.0, 0.0), ao = make_double2(0.0, 0.0);
 #pragma unroll
-            for (int s2 = 0; s2 < kSlabNSL; ++s2)
+            for (int s2 = 0; s2 < NSL; ++s2)
 #pragma unroll
               for (int e = 0; e < PV; ++e) {
                 if ((s2 * PV + e) & 1)
@@ -577,23 +583,24 @@ sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, 
 }
 
 // One-time re-layout into slabs: Hs[x][sl][rr][pc] (16-byte chunks) holds logical chunk
-// pc ^ ((rr >> 1) & 3) of row lrow0(sl) + rr of block (rep(sl), j(x)), strip x; zero past
+// pc ^ slab_swz(rr) of row lrow0(sl) + rr of block (rep(sl), j(x)), strip x; zero past
 // the slab's valid rows or the segment's last column.  Setup only.
-template <typename S>
+template <typename S, int RB>
 __global__ void slab_h_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const SweepDesc* __restrict__ segs,
                               const SlabDesc* __restrict__ slabs, uint32_t N, uint32_t Ns, uint32_t RPW,
                               uint64_t total_chunks, S* __restrict__ Hs) {
   constexpr int PV = 16 / (int)sizeof(S);
-  constexpr int W = kSlabNSL * PV;
+  constexpr int NSL = RB / 16;
+  constexpr int W = NSL * PV;
   for (uint64_t idx = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; idx < total_chunks;
        idx += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t pc = (uint32_t)(idx % kSlabNSL);
-    const uint64_t r1 = idx / kSlabNSL;
+    const uint32_t pc = (uint32_t)(idx % NSL);
+    const uint64_t r1 = idx / NSL;
     const uint32_t rr = (uint32_t)(r1 % RPW);
     const uint64_t r2 = r1 / RPW;
     const uint32_t sl = (uint32_t)(r2 % Ns);
     const uint64_t x = r2 / Ns;
-    const uint32_t lc = pc ^ ((rr >> 1) & 3);
+    const uint32_t lc = pc ^ slab_swz<RB>(rr);
     uint32_t j = 0;
     while (j + 1 < N && segs[j + 1].unit0 <= x) ++j;
     const SlabDesc sd = slabs[sl];

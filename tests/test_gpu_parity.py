@@ -323,3 +323,44 @@ def test_sweep_schedule_equals_twopass(shape, method, M, N, ragged, dtype):
     assert rel(s.solution, t.solution) <= 1e-12
     assert rel(s.trace.dual, t.trace.dual) <= 1e-10
     assert abs(s.objective - t.objective) <= 1e-12 * abs(t.objective)
+
+
+@pytest.mark.parametrize("geom", [
+    {},                                                             # automatic (C=1, 64-byte rows)
+    {"ADMM_B200_SLAB_C": "2", "ADMM_B200_SLAB_RPW": "32"},          # cluster pair, st.async exchange
+    {"ADMM_B200_SLAB_C": "2", "ADMM_B200_SLAB_RB": "32"},           # half-width strips
+    {"ADMM_B200_SLAB_C": "4", "ADMM_B200_SLAB_RB": "32", "ADMM_B200_SLAB_RPW": "64"},
+    {"ADMM_B200_SLAB_ND": "1", "ADMM_B200_SLAB_LAG": "1"},          # one D warp
+])
+@pytest.mark.parametrize("shape,method,M,N,dtype", [
+    ((512, 4096), "sectioning", 1, 4, "c128"),
+    ((512, 3072), "hybrid", 2, 3, "c64"),
+    ((256, 1536), "consensus", 2, 1, "c128"),
+])
+def test_slab_geometries_equal_twopass(monkeypatch, geom, shape, method, M, N, dtype):
+    """Every slab-sweep geometry (clusters with the DSMEM z exchange, 32/64-byte strip rows,
+    one or two D warps, lag 1..3) computes the two-pass iterates up to summation order."""
+    a = admm()
+    p = a.gen_problem(shape[0], shape[1], 12, 30.0, 23, dtype=dtype)
+    lam = 0.05 * float(np.max(np.abs(orc.adjoint_matvec(p.h.astype(np.complex128), p.g))))
+    cfg = a.SolverConfig(rho=1.0, lambda_=lam, max_iters=30)
+    outs = {}
+    for sched in ("twopass", "sweep"):
+        with monkeypatch.context() as mp:
+            if sched == "sweep":
+                for k, v in geom.items():
+                    mp.setenv(k, v)
+            opts = a.SolveOptions(dtype=dtype, schedule=sched)
+            with a.AdmmPlan(p, cfg, method, M, N, opts) as plan:
+                info = plan.info()
+                if sched == "sweep":
+                    assert info["sweep_variant"] == 3, info
+                    if "ADMM_B200_SLAB_C" in geom:
+                        assert info["slab_cluster"] == int(geom["ADMM_B200_SLAB_C"])
+                    if "ADMM_B200_SLAB_RB" in geom:
+                        assert info["slab_row_bytes"] == int(geom["ADMM_B200_SLAB_RB"])
+                outs[sched] = plan.solve()
+    t, s = outs["twopass"], outs["sweep"]
+    assert rel(s.solution, t.solution) <= 1e-12
+    assert rel(s.trace.primal, t.trace.primal) <= 1e-10
+    assert rel(s.trace.dual, t.trace.dual) <= 1e-10
