@@ -196,11 +196,15 @@ __host__ __device__ inline size_t slab_smem_bytes(uint32_t ns, uint32_t nw, uint
          + (size_t)N * sizeof(SweepDesc) + (2 * (size_t)M * N + N) * sizeof(uint32_t);  // descriptor tables
 }
 
-// Valid (lag, D warps) pairs: the slot-reuse arguments below need (kSlabZB - 1 - L) and
-// (kSlabXB - 1 - L) to be multiples of ND (the D warp of strip k also owns strip k + ND).
+// Valid (lag, D warps) pairs.  Slot reuse: a compute warp writes z partials of strip
+// k + kSlabZB only after it has waited for c of every strip <= k + kSlabZB - 1 - L, so the
+// D warp of strip k has read them (kSlabZB >= L + 1), and a D warp overwrites c of strip k
+// only after every compute warp has passed (A) of strip k (same bound).  A peer's D warp
+// writes exchange slot k % kSlabXB for strip k + kSlabXB only after this CTA sent its
+// partials for some strip j in (k, k + kSlabXB - 1 - L] owned by the same D warp as k,
+// i.e. after that D warp finished strip k: kSlabXB - 1 - L >= ND.
 __host__ __device__ inline bool slab_lag_ok(uint32_t L, uint32_t ND) {
-  return L >= 1 && L <= kSlabZB - 1 && (kSlabZB - 1 - L) % ND == 0 && (kSlabXB - 1 - L) % ND == 0 &&
-         kSlabXB - 1 - L >= ND;
+  return L >= 1 && L <= kSlabZB - 1 && kSlabXB - 1 - L >= ND;
 }
 
 // RPL = rows per lane in (A) = RPW / 32.  Launched as NCl clusters of C CTAs, block
