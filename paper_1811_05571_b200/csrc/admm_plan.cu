@@ -559,8 +559,10 @@ bool try_slab(admm_plan* p) {
       }
       for (uint32_t C : {1u, 2u, 4u, 8u}) {
         if (fC && (uint32_t)fC != C) continue;
-        // clusters of 4+ measured slower than the two-pass schedule (config 3: 344 vs 264 us)
-        if (!fC && C > 2) continue;
+        // clusters only on request: every cluster geometry measured so far loses to the
+        // single-CTA slab (config 2: 120 vs 96 us) or to two-pass (config 3: 276-362 us vs
+        // 265 us) -- the per-strip DSMEM exchange sits on the D warps' critical path
+        if (!fC && C > 1) continue;
         const uint32_t nw = (uint32_t)cdiv(Ns, C);
         if (nw > (uint32_t)kSlabMaxW || (C > 1 && nw * (C - 1) >= Ns)) continue;  // no empty rank
         const size_t fixed = slab_smem_bytes(0, nw, kSlabMaxD, rpw, rb, C, M, W, N);
