@@ -43,7 +43,7 @@ __host__ __device__ constexpr uint32_t slab_swz(uint32_t row) {
   return (row / (128 / RB)) % (RB / 16);
 }
 constexpr int kSlabMaxW = 16;        // compute warps per CTA (+ D warps)
-constexpr int kSlabThreads = (kSlabMaxW + 4) * kWarp;  // up to 2 D warps; 20 warps keep the 96-register cap
+constexpr int kSlabThreads = (kSlabMaxW + 4) * kWarp;  // + up to 4 D warps; 20 warps keep the 96-register cap
 
 struct SlabDesc {
   uint32_t rep;    // replica (row block) i
@@ -181,7 +181,7 @@ struct Chunk<float2> {
 constexpr int kSlabZB = 4;   // z-partial / c / barrier slots (lag L <= kSlabZB - 1)
 constexpr int kSlabXB = 8;   // cluster-exchange slots
 constexpr int kSlabPF = 3;   // D warp: its strips of iterates prefetched ahead (cp.async)
-constexpr int kSlabMaxD = 2; // D warps
+constexpr int kSlabMaxD = 4; // D warps (config 2: 4 -> 94.8 us, 2 -> 97.1 us, 1 -> 103 us)
 
 __host__ __device__ inline size_t slab_smem_bytes(uint32_t ns, uint32_t nw, uint32_t nd, uint32_t rpw, uint32_t rb,
                                                   uint32_t C, uint32_t M, uint32_t W, uint32_t N) {
