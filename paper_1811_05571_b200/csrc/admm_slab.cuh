@@ -267,6 +267,7 @@ sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, 
       trace[((uint64_t)blockIdx.x * 64 + k) * 8 + ev] = clock64();
   };
 
+  if (kTrace && threadIdx.x == 0) trace[((uint64_t)blockIdx.x * 64) * 8 + 6] = clock64();  // kernel entry
   if (threadIdx.x == 0) {
     for (uint32_t b = 0; b < NW * NS; ++b) mbar_init(&fullb[b], 1);
     for (int b = 0; b < kSlabZB; ++b) {
@@ -311,6 +312,7 @@ sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, 
     uint64_t seg_end = (nstrip > 0) ? tseg[j].unit0 + tseg[j].n_strips : 0;   // (C) side
     uint64_t seg_endA = seg_end;                                              // (A) side
     pdl_enter();  // q of the previous kernels is visible from here on
+    if (kTrace && warp == 0 && lane == 0) trace[((uint64_t)blockIdx.x * 64 + 1) * 8 + 6] = clock64();
 
     // (C) lane geometry: rows crg + CRG u, logical chunk ccol at physical ccol ^ swz
     const uint32_t crg = lane / NSL, ccol = lane % NSL;
@@ -554,6 +556,7 @@ sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, 
     }
     cpa_wait<0>();
   }
+  if (kTrace && warp == 0 && lane == 0) trace[((uint64_t)blockIdx.x * 64 + 1) * 8 + 7] = clock64();
   // residual partials: warp sums, then the warps in order (rank 0 carries them)
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -584,6 +587,7 @@ sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, 
     if (nb) st->nonfinite = 1u;
   }
   if (C > 1) cluster_sync_all();  // no CTA leaves while a peer may still write its SMEM
+  if (kTrace && threadIdx.x == 0) trace[((uint64_t)blockIdx.x * 64) * 8 + 7] = clock64();  // kernel exit
 }
 
 // One-time re-layout into slabs: Hs[x][sl][rr][pc] (16-byte chunks) holds logical chunk
