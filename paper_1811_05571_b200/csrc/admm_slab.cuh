@@ -309,8 +309,10 @@ sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, 
     if (nstrip > 0)
       while (j + 1 < N && tseg[j + 1].unit0 <= x0) ++j;
     uint32_t jA = j;
-    uint64_t seg_end = (nstrip > 0) ? tseg[j].unit0 + tseg[j].n_strips : 0;   // (C) side
-    uint64_t seg_endA = seg_end;                                              // (A) side
+    // local strip index where the current segment ends, (C) side and (A) side (32-bit:
+    // the strip loop runs at the 96-register cap)
+    uint32_t kend = (nstrip > 0) ? (uint32_t)(tseg[j].unit0 + tseg[j].n_strips - x0) : 0;
+    uint32_t kendA = kend;
     pdl_enter();  // q of the previous kernels is visible from here on
     if (kTrace && warp == 0 && lane == 0) trace[((uint64_t)blockIdx.x * 64 + 1) * 8 + 6] = clock64();
 
@@ -339,27 +341,31 @@ sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, 
     for (uint32_t k = 0; k < nstrip + L; ++k) {
       if (k < nstrip) {
         // ---------------------------------------------------------- (C) strip k
-        if (x0 + k == seg_end) {
+        if (k == kend) {
           ++j;
-          seg_end = tseg[j].unit0 + tseg[j].n_strips;
+          kend = (uint32_t)(tseg[j].unit0 + tseg[j].n_strips - x0);
           load_q(j);
         }
         if (act) {
           mbar_wait_s(full_s + stgC * 8, phC);
           mark(k, 0);
           const unsigned char* base = ring + ring_off + stgC * stage_stride + c_off;
-          CK h[CNU];
-#pragma unroll
-          for (int u = 0; u < CNU; ++u) h[u].ld(base + u * CRG * RB);
           double2 acc[4][PV];
 #pragma unroll
           for (int a4 = 0; a4 < 4; ++a4)
 #pragma unroll
             for (int e = 0; e < PV; ++e) acc[a4][e] = make_double2(0.0, 0.0);
+          constexpr int CB = CNU > 4 ? 4 : CNU;  // loads in flight per batch (register cap)
 #pragma unroll
-          for (int u = 0; u < CNU; ++u)
+          for (int u0 = 0; u0 < CNU; u0 += CB) {
+            CK h[CB];
 #pragma unroll
-            for (int e = 0; e < PV; ++e) cmac_conj(acc[u & 3][e], h[u].get(e), qr[u]);
+            for (int u = 0; u < CB; ++u) h[u].ld(base + (u0 + u) * CRG * RB);
+#pragma unroll
+            for (int u = 0; u < CB; ++u)
+#pragma unroll
+              for (int e = 0; e < PV; ++e) cmac_conj(acc[u & 3][e], h[u].get(e), qr[u0 + u]);
+          }
 #pragma unroll
           for (int e = 0; e < PV; ++e) {
             double2 z = cadd(cadd(acc[0][e], acc[1][e]), cadd(acc[2][e], acc[3][e]));
@@ -413,7 +419,7 @@ sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, 
           mark(kk, 3);
         }
         if (++stgA == NS) stgA = 0;
-        if (x0 + kk + 1 == seg_endA || kk + 1 == nstrip) {  // flush this segment's w partial
+        if (kk + 1 == kendA || kk + 1 == nstrip) {  // flush this segment's w partial
           if (act) {
             const SweepDesc sg = tseg[jA];
             const uint64_t slotp = cl - sk_owner(sg.unit0, U, NCl);
@@ -427,7 +433,7 @@ sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, 
           }
           if (kk + 1 < nstrip) {
             ++jA;
-            seg_endA = tseg[jA].unit0 + tseg[jA].n_strips;
+            kendA = (uint32_t)(tseg[jA].unit0 + tseg[jA].n_strips - x0);
           }
         }
       }
