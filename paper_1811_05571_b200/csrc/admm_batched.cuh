@@ -7,7 +7,7 @@
 // (tensor cores are reserved for setup by the north star).  Register-tiled FP64 SIMT:
 // a 256-thread CTA owns a 64 x 64 output tile (64 rows or columns x up to 64 scenes),
 // each thread a 4 x 4 complex sub-tile (rows ty + 16q, scenes tx + 16w: both SMEM
-// operand reads are conflict-free); A and X stream through SMEM in k-chunks of 32.
+// operand reads are conflict-free); A and X stream through SMEM in k-chunks of 16.
 // Vectors are [row][scene] (scene fastest), FP64 like the single-scene engine.
 #pragma once
 
@@ -173,8 +173,10 @@ brows_kernel(BRowVecs rv, const double2* __restrict__ part, uint64_t part_stride
 // Per (segment column t, scene): u_i = c_i + z_i for all replicas i, the replica mean,
 // v = S_{kappa_scene}(mean), residual partials per scene, dual update, next c.
 // Threads: scene = tid % 64 group of 4 columns; grid-stride over the segment columns.
+// z holds zsplit split-K slices (zstride apart), summed in slice order.
 __global__ void __launch_bounds__(kCtaThreads)
-bzupdate_kernel(ColVecs cv, const double2* __restrict__ z, const BlockDesc* __restrict__ blocks, uint32_t M,
+bzupdate_kernel(ColVecs cv, const double2* __restrict__ z, uint32_t zsplit, uint64_t zstride,
+                const BlockDesc* __restrict__ blocks, uint32_t M,
                 uint32_t N, uint32_t B, const double* __restrict__ kappa, double* __restrict__ red,
                 IterState* st) {
   __shared__ double sred[3][4][kBB];
@@ -190,7 +192,9 @@ bzupdate_kernel(ColVecs cv, const double2* __restrict__ z, const BlockDesc* __re
         double2 mean = make_double2(0.0, 0.0);
         for (uint32_t i = 0; i < M; ++i) {
           const uint64_t o = ((uint64_t)blocks[i * N + j].vec_off + t) * B + sc;
-          const double2 u = cadd(cv.c[o], z[o]);
+          double2 zo = z[o];  // split-K slices of Z = H^H Q, fixed order
+          for (uint32_t k = 1; k < zsplit; ++k) zo = cadd(zo, z[(uint64_t)k * zstride + o]);
+          const double2 u = cadd(cv.c[o], zo);
           bad |= !cfinite(u);
           cv.u[o] = u;
           mean = cadd(mean, cadd(u, cv.s[o]));

@@ -161,7 +161,7 @@ struct admm_plan {
   uint64_t batch = 1;
   std::vector<BTile> tN, tK, tH, tG;
   DevBuf dtN, dtK, dtH, dtG, dz, dkappa, dbred;
-  uint32_t splitN = 1, splitK = 1, pz = 1;
+  uint32_t splitN = 1, splitK = 1, splitH = 1, pz = 1;
   std::vector<double> lambdas;
   // sweep schedule (admm_sweep.cuh)
   int schedule = 1;             // 1 two-pass, 2 single-HBM-pass sweep
@@ -1105,6 +1105,21 @@ void bgemm_attrs() {
                           (int)bgemm_smem<S, true>()));
 }
 
+// Split-K count s in [1, smax] (and at most kmax) whose tiles*s work units fill the
+// `slots` resident CTAs in the most nearly whole waves; each extra split costs a
+// partial slice, so ties go to the smaller s.
+uint32_t wave_split(uint64_t tiles, uint64_t slots, uint32_t smax, uint64_t kmax) {
+  smax = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(smax, kmax));
+  double best = -1.0;
+  uint32_t bs = 1;
+  for (uint32_t sp = 1; sp <= smax; ++sp) {
+    const double waves = (double)(tiles * sp) / (double)slots;
+    const double score = waves / std::ceil(waves) - 0.01 * (sp - 1);
+    if (score > best + 1e-12) best = score, bs = sp;
+  }
+  return bs;
+}
+
 void build_batched(admm_plan* p) {
   const uint64_t B = p->batch;
   if (p->dtype == ADMM_C128)
@@ -1112,12 +1127,26 @@ void build_batched(admm_plan* p) {
   else
     bgemm_attrs<float2>();
   const uint64_t nb = p->blocks.size();
-  uint64_t rtiles = 0;
-  for (auto& b : p->blocks) rtiles += cdiv(b.rows, kBT);
-  const uint64_t target = 4ull * p->num_sms;  // split-K until the N-GEMMs have ~4 waves
-  p->splitN = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(16, cdiv(target, rtiles)));
-  p->splitK = p->splitN;
+  uint64_t rtiles = 0, ctiles = 0;
+  for (auto& b : p->blocks) rtiles += cdiv(b.rows, kBT), ctiles += cdiv(b.cols, kBT);
+  // split-K counts chosen for whole waves over the resident CTA slots (bgemm runs 2 CTAs
+  // per SM): config 5 has 192 row tiles (x3 -> 1.95 waves) and 1024 column tiles
+  // (x2 -> 6.9 waves) instead of 2.6 / 3.5 waves
+  int occ = 0;
+  if (p->dtype == ADMM_C128)
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bgemm_kernel<double2, false>, 256, bgemm_smem<double2, false>()));
+  else
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bgemm_kernel<float2, false>, 256, bgemm_smem<float2, false>()));
+  const uint64_t slots = (uint64_t)std::max(1, occ) * p->num_sms;
+  p->splitN = wave_split(rtiles, slots, 16, p->max_seg / (4 * kBK));
+  p->splitK = wave_split(rtiles, slots, 16, p->max_rows / (4 * kBK));
+  p->splitH = wave_split(ctiles, slots, 4, p->max_rows / (4 * kBK));
+  if (const char* e = std::getenv("ADMM_B200_BSPLIT")) {  // diagnostics: "N,K,H"
+    unsigned a = 0, b = 0, c = 0;
+    if (std::sscanf(e, "%u,%u,%u", &a, &b, &c) == 3 && a && b && c) p->splitN = a, p->splitK = b, p->splitH = c;
+  }
   const uint64_t stride = p->mvec_total * B;
+  const uint64_t zstride = p->vec_total * B;
   p->tN.clear();
   p->tK.clear();
   p->tH.clear();
@@ -1140,9 +1169,12 @@ void build_batched(admm_plan* p) {
                 bd.rows, t0, std::min(bd.rows, sp * kcK), std::min(bd.rows, (sp + 1) * kcK)};
         p->tK.push_back(t);
       }
+    const uint32_t kcH = (uint32_t)round_up(cdiv(bd.rows, p->splitH), kBK);
+    for (uint32_t t0 = 0; t0 < bd.cols; t0 += kBT)
+      for (uint32_t sp = 0; sp < p->splitH; ++sp)
+        p->tH.push_back(BTile{hn.a_off, (uint64_t)bd.mvec_off * B, sp * zstride + (uint64_t)bd.vec_off * B, hn.ld,
+                              bd.rows, bd.cols, t0, std::min(bd.rows, sp * kcH), std::min(bd.rows, (sp + 1) * kcH)});
     for (uint32_t t0 = 0; t0 < bd.cols; t0 += kBT) {
-      p->tH.push_back(BTile{hn.a_off, (uint64_t)bd.mvec_off * B, (uint64_t)bd.vec_off * B, hn.ld, bd.rows,
-                            bd.cols, t0, 0, bd.rows});
       p->tG.push_back(BTile{hn.a_off, (uint64_t)bd.row0 * B, (uint64_t)bd.vec_off * B, hn.ld, bd.rows, bd.cols, t0,
                             0, bd.rows});
     }
@@ -1153,7 +1185,7 @@ void build_batched(admm_plan* p) {
   upload_desc(p->dtG, p->tG.data(), p->tG.size() * sizeof(BTile));
   p->dwpart.alloc((size_t)p->splitN * stride * 16);
   p->dqpart.alloc((size_t)p->splitK * stride * 16);
-  p->dz.alloc(p->vec_total * B * 16);
+  p->dz.alloc((size_t)p->splitH * p->vec_total * B * 16);
   p->dkappa.alloc(B * sizeof(double));
   p->pz = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(4ull * p->num_sms, cdiv(p->max_seg, 4)));
   p->dbred.alloc((size_t)3 * p->pz * kBB * sizeof(double));
@@ -1189,7 +1221,8 @@ void enqueue_iteration_batched(admm_plan* p, cudaStream_t s, std::vector<cudaEve
   bgemm_kernel<S, true><<<(unsigned)p->tH.size(), 256, bgemm_smem<S, true>(), s>>>(p->dH.as<S>(), p->dtH.as<BTile>(), p->dq.as<double2>(),
                                                                  p->dz.as<double2>(), B);
   mark(5);
-  bzupdate_kernel<<<p->pz, kCtaThreads, 0, s>>>(col_vecs(p), p->dz.as<double2>(), p->dblocks.as<BlockDesc>(),
+  bzupdate_kernel<<<p->pz, kCtaThreads, 0, s>>>(col_vecs(p), p->dz.as<double2>(), p->splitH, p->vec_total * B,
+                                                p->dblocks.as<BlockDesc>(),
                                                 (uint32_t)p->Mr, (uint32_t)p->Nc, B, p->dkappa.as<double>(),
                                                 p->dbred.as<double>(), p->dstate.as<IterState>());
   mark(6);

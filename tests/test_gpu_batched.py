@@ -18,9 +18,14 @@ def support(v):
     return np.abs(v) > 1e-3 * np.max(np.abs(v))
 
 
-@pytest.mark.parametrize("dtype,B", [("c64", 8), ("c128", 5), ("c64", 64)])
-def test_batched_scenes_match_independent_solves(dtype, B):
+@pytest.mark.parametrize("dtype,B,split", [("c64", 8, None), ("c128", 5, None), ("c64", 64, None),
+                                            ("c64", 8, "3,2,3"), ("c128", 3, "2,3,4")])
+def test_batched_scenes_match_independent_solves(dtype, B, split, monkeypatch):
+    """split: forced split-K counts "N,K,H" of the three skinny GEMMs (the automatic
+    choice follows the wave count and is 1 at this size)."""
     import paper_1811_05571_b200 as admm
+    if split:
+        monkeypatch.setenv("ADMM_B200_BSPLIT", split)
     h = admm.cra_matrix(seed=5, dtype=dtype, n_tx=6, n_freq=32, grid=16)  # 192 x 4096
     g, truth = admm.cra_scenes(h, B, seed=5, lo=20, hi=60, grid=16)
     iters = 60
