@@ -42,7 +42,9 @@ typedef enum {
   ADMM_E_PARTITION = 5,   /* PartitionError   errors.hpp:54 */
   ADMM_E_PARAMETER = 6,   /* ParameterError   errors.hpp:60 */
   ADMM_E_CUDA = 7,        /* device / driver failure (no reference counterpart) */
-  ADMM_E_STATE = 8        /* API misuse (null pointer, wrong plan state) */
+  ADMM_E_STATE = 8,       /* API misuse (null pointer, wrong plan state) */
+  ADMM_E_FORMAT = 9,      /* FormatError      errors.hpp:64 (byte offset: admm_cmat_error_offset) */
+  ADMM_E_IO = 10          /* IoError          errors.hpp:75 */
 } admm_status;
 
 /* The four solver entry points (reference.hpp:27, solvers.hpp:74,179,306). */
@@ -227,6 +229,22 @@ admm_status admm_gen_problem(uint64_t n_meas, uint64_t n_pix, uint64_t k, double
 admm_status admm_gen_cra(uint64_t n_tx, uint64_t n_freq, uint64_t grid, double spacing, double z0,
                          double aperture, double f0, double f1, uint64_t n_facets, uint64_t seed,
                          void* h, admm_dtype h_dtype);
+
+/* ---- CMAT file I/O (cmat_io.hpp; host, not the hot path) -------------------------
+ * "CMX1": the reference format (cmat_io.hpp:18-24), binary64 (re, im) pairs, <= 2^32
+ * entries.  "CMF1": the same layout with binary32 pairs (complex64 storage of the c64
+ * plans; <= 2^36 entries).  Reads convert to dst_dtype on the fly (round / widen) and
+ * validate exactly as read_cmat (cmat_io.hpp:57-105): IoError, FormatError with the
+ * byte offset of the defect (admm_cmat_error_offset()).  A vector is a cols == 1 file
+ * (read_cvec / write_cvec, cmat_io.hpp:108-125). */
+admm_status admm_cmat_info(const char* path, uint64_t* rows, uint64_t* cols, admm_dtype* file_dtype);
+/* read_cmat (cmat_io.hpp:57): dst holds capacity_entries complex values of dst_dtype. */
+admm_status admm_cmat_read(const char* path, void* dst, uint64_t capacity_entries, admm_dtype dst_dtype);
+/* write_cmat (cmat_io.hpp:44): src is rows x cols of src_dtype; file_dtype picks CMX1/CMF1. */
+admm_status admm_cmat_write(const char* path, const void* src, uint64_t rows, uint64_t cols, admm_dtype src_dtype,
+                            admm_dtype file_dtype);
+/* FormatError::byte_offset (errors.hpp:64-73) of the calling thread's last failure. */
+uint64_t admm_cmat_error_offset(void);
 
 const char* admm_last_error(void);
 uint64_t admm_last_good_iteration(void);

@@ -11,6 +11,7 @@
 //   SolverConfig admm_core.hpp:17   SensingProblem problem.hpp:25   SolveOptions report.hpp:42
 //   SolveReport report.hpp:16   IterateSnapshot report.hpp:28   CommLedger comm.hpp:45
 //   errors errors.hpp:10-81   GramSolver gram.hpp:26   matvec/adjoint_matvec linalg.hpp:97/114
+//   read_cmat/write_cmat/read_cvec/write_cvec cmat_io.hpp:44-125
 #pragma once
 
 #include <algorithm>
@@ -50,6 +51,14 @@ class SingularityError : public Error { public: using Error::Error; };
 class PartitionError : public Error { public: using Error::Error; };
 class ParameterError : public Error { public: using Error::Error; };
 class MetricsError : public Error { public: using Error::Error; };
+class FormatError : public Error {
+ public:
+  explicit FormatError(const std::string& what, std::size_t byte_offset = 0) : Error(what), offset_(byte_offset) {}
+  std::size_t byte_offset() const { return offset_; }
+ private:
+  std::size_t offset_ = 0;
+};
+class IoError : public Error { public: using Error::Error; };
 class DeviceError : public Error { public: using Error::Error; };  // ADMM_E_CUDA
 
 inline void check(admm_status st) {
@@ -63,6 +72,8 @@ inline void check(admm_status st) {
     case ADMM_E_PARTITION: throw PartitionError(msg);
     case ADMM_E_PARAMETER: throw ParameterError(msg);
     case ADMM_E_CUDA: throw DeviceError(msg);
+    case ADMM_E_FORMAT: throw FormatError(msg, admm_cmat_error_offset());
+    case ADMM_E_IO: throw IoError(msg);
     default: throw Error(msg);
   }
 }
@@ -409,5 +420,38 @@ class GramSolver {
   int device_;
   Strategy strategy_;
 };
+
+// ---- cmat_io.hpp:44-125 (host file I/O; CMX1 = the reference format) ----------------
+// Same names, checks and exceptions as the reference.  write_cmat's `c64` flag writes the
+// complex64 "CMF1" variant; read_cmat reads either (CMF1 widens exactly).  To feed a c64
+// plan without an FP64 host copy call admm_cmat_read(path, float buffer, n, ADMM_C64).
+inline void write_cmat(const std::string& path, const CMatrix& a, bool c64 = false) {
+  if (a.empty()) throw ParameterError("write_cmat: empty matrix");
+  check(admm_cmat_write(path.c_str(), a.data(), a.rows(), a.cols(), ADMM_C128, c64 ? ADMM_C64 : ADMM_C128));
+}
+inline CMatrix read_cmat(const std::string& path) {
+  uint64_t rows = 0, cols = 0;
+  admm_dtype t = ADMM_C128;
+  check(admm_cmat_info(path.c_str(), &rows, &cols, &t));
+  CMatrix a(rows, cols);
+  check(admm_cmat_read(path.c_str(), a.data(), rows * cols, ADMM_C128));
+  return a;
+}
+inline void write_cvec(const std::string& path, const CVector& v, bool c64 = false) {
+  if (v.empty()) throw ParameterError("write_cvec: empty vector");
+  check(admm_cmat_write(path.c_str(), v.data(), v.size(), 1, ADMM_C128, c64 ? ADMM_C64 : ADMM_C128));
+}
+inline CVector read_cvec(const std::string& path) {
+  uint64_t rows = 0, cols = 0;
+  admm_dtype t = ADMM_C128;
+  check(admm_cmat_info(path.c_str(), &rows, &cols, &t));
+  if (cols != 1)
+    throw FormatError("read_cvec: " + path + " holds a " + std::to_string(rows) + "x" + std::to_string(cols) +
+                          " matrix, expected a column vector",
+                      12);
+  CVector v(rows);
+  check(admm_cmat_read(path.c_str(), v.data(), rows, ADMM_C128));
+  return v;
+}
 
 }  // namespace admmgpu

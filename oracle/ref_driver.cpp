@@ -20,6 +20,8 @@
 //
 // Usage (key=value arguments):
 //   admmsplit_ref gen   out=DIR m=ROWS n=COLS k=SPARSITY snr=DB|inf seed=S kind=cg|rp
+//   admmsplit_ref cmat  in=FILE [vec=0|1]   read_cmat / read_cvec (cmat_io.hpp:57,116):
+//                       prints "ok ROWS COLS FNV64" or "error CLASS OFFSET"
 //   admmsplit_ref solve in=DIR out=DIR method=reference|consensus|sectioning|hybrid
 //                       M=.. N=.. rho=.. lambda=.. [lambda_rel=0|1] scl=.. iters=..
 //                       eps_pri=.. eps_dual=.. threads=.. ragged=0|1 snapshots=0|1
@@ -225,6 +227,31 @@ int cmd_solve(const std::map<std::string, std::string>& kv) {
   return 0;
 }
 
+// FNV-1a over the payload bytes of a read matrix (what read_cmat returned).
+int cmd_cmat(const std::map<std::string, std::string>& kv) {
+  const fs::path in = kv.at("in");
+  const bool vec = kv.count("vec") && kv.at("vec") == "1";
+  try {
+    CMatrix a = vec ? CMatrix(1, 1) : read_cmat(in);
+    if (vec) {
+      const CVector v = read_cvec(in);
+      a = CMatrix(v.size(), 1);
+      for (std::size_t i = 0; i < v.size(); ++i) a(i, 0) = v[i];
+    }
+    std::uint64_t h = 0xcbf29ce484222325ULL;
+    const unsigned char* b = reinterpret_cast<const unsigned char*>(a.data());
+    for (std::size_t i = 0; i < a.size() * sizeof(Complex); ++i) h = (h ^ b[i]) * 0x100000001b3ULL;
+    std::printf("ok %zu %zu %016llx\n", a.rows(), a.cols(), static_cast<unsigned long long>(h));
+  } catch (const FormatError& e) {
+    std::printf("error FormatError %zu\n", e.byte_offset());
+  } catch (const IoError&) {
+    std::printf("error IoError 0\n");
+  } catch (const Error& e) {
+    std::printf("error Error 0 %s\n", e.what());
+  }
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -236,6 +263,7 @@ int main(int argc, char** argv) {
   const std::string cmd = argv[1];
   if (cmd == "gen") return cmd_gen(kv);
   if (cmd == "solve") return cmd_solve(kv);
+  if (cmd == "cmat") return cmd_cmat(kv);
   std::fprintf(stderr, "unknown command %s\n", cmd.c_str());
   return 2;
 }

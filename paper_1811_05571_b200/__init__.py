@@ -3,8 +3,10 @@
 Drop-in for the reference admmsplit solver entry points; all arithmetic runs in the
 sm_100a kernels of libadmm_b200.so.
 """
-from .errors import (DeviceError, DimensionError, Error, IndexError, MetricsError,  # noqa: F401
-                     NumericalError, ParameterError, PartitionError, SingularityError, StateError)
+from .errors import (DeviceError, DimensionError, Error, FormatError, IndexError, IoError,  # noqa: F401
+                     MetricsError, NumericalError, ParameterError, PartitionError, SingularityError,
+                     StateError)
+from .cmat import cmat_info, read_cmat, read_cvec, write_cmat, write_cvec  # noqa: F401
 from .comm import CommLedger, Convention, Method, per_node_elements, reduction_vs_consensus  # noqa: F401
 from .solvers import (AdmmPlan, GramSolver, IterateSnapshot, PartitionSpec, ProblemKind,  # noqa: F401
                       RecoveryMetrics, ResidualTrace, SensingProblem, SolveOptions, SolveReport,

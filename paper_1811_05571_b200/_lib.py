@@ -89,6 +89,10 @@ _SIGS = {
     "admm_soft_threshold": ([_ptr, _u64, _dbl, _ptr, _i32], _i32),
     "admm_gram_solve": ([_ptr, _u64, _u64, _dbl, _ptr, _ptr, _i32], _i32),
     "admm_gen_problem": ([_u64, _u64, _u64, _dbl, _u64, _i32, _ptr, _i32, _ptr, _ptr, _ptr], _i32),
+    "admm_cmat_info": ([ctypes.c_char_p, ctypes.POINTER(_u64), ctypes.POINTER(_u64), ctypes.POINTER(_i32)], _i32),
+    "admm_cmat_read": ([ctypes.c_char_p, _ptr, _u64, _i32], _i32),
+    "admm_cmat_write": ([ctypes.c_char_p, _ptr, _u64, _u64, _i32, _i32], _i32),
+    "admm_cmat_error_offset": ([], _u64),
     "admm_gen_cra": ([_u64, _u64, _u64, _dbl, _dbl, _dbl, _dbl, _dbl, _u64, _u64, _ptr, _i32], _i32),
 }
 for _name, (_args, _res) in _SIGS.items():

@@ -31,6 +31,7 @@
 #include "admm_slab.cuh"
 #include "admm_hemv.cuh"
 #include "admm_batched.cuh"
+#include "admm_host.h"
 
 using namespace admm;
 
@@ -38,6 +39,7 @@ namespace {
 
 thread_local std::string g_last_error;
 thread_local uint64_t g_last_good = 0;
+thread_local uint64_t g_last_offset = 0;
 
 struct Fail {
   admm_status st;
@@ -126,6 +128,11 @@ struct Geom {
 };
 
 }  // namespace
+
+void admm_host_set_error(const char* msg, uint64_t byte_offset) {
+  g_last_error = msg ? msg : "";
+  g_last_offset = byte_offset;
+}
 
 struct admm_plan {
   int device = 0;
@@ -1632,6 +1639,7 @@ extern "C" {
 
 int admm_abi_version(void) { return ADMM_B200_ABI_VERSION; }
 const char* admm_last_error(void) { return g_last_error.c_str(); }
+uint64_t admm_cmat_error_offset(void) { return g_last_offset; }
 uint64_t admm_last_good_iteration(void) { return g_last_good; }
 
 admm_status admm_plan_create(const admm_plan_options* opts, const admm_solver_config* cfg, uint64_t n_meas,

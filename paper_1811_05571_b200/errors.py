@@ -37,6 +37,21 @@ class ParameterError(Error):
     """errors.hpp:60 — invalid scalar parameter."""
 
 
+class FormatError(Error):
+    """errors.hpp:64 — malformed file contents; carries the byte offset of the defect."""
+
+    def __init__(self, what: str, byte_offset: int = 0):
+        super().__init__(what)
+        self._offset = int(byte_offset)
+
+    def byte_offset(self) -> int:
+        return self._offset
+
+
+class IoError(Error):
+    """errors.hpp:75 — underlying I/O failure (open/read/write)."""
+
+
 class MetricsError(Error):
     """errors.hpp:78 — recovery metrics undefined."""
 
@@ -50,7 +65,8 @@ class StateError(Error):
 
 
 STATUS = {1: DimensionError, 2: IndexError, 3: NumericalError, 4: SingularityError,
-          5: PartitionError, 6: ParameterError, 7: DeviceError, 8: StateError}
+          5: PartitionError, 6: ParameterError, 7: DeviceError, 8: StateError, 9: FormatError,
+          10: IoError}
 
 
 def check(status: int) -> None:
@@ -62,4 +78,6 @@ def check(status: int) -> None:
     cls = STATUS.get(status, Error)
     if cls is NumericalError:
         raise NumericalError(msg, _lib.lib.admm_last_good_iteration())
+    if cls is FormatError:
+        raise FormatError(msg, _lib.lib.admm_cmat_error_offset())
     raise cls(msg)

@@ -4,8 +4,11 @@
 // not in this image, so a ten-line harness stands in for TEST_CASE / CHECK.
 // Inputs come from the product generator (bit-identical to the reference's gen_problem),
 // the expected values from the test-only C oracle (oracle/liboracle.so).
+#include <unistd.h>
+
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <limits>
 #include <string>
 #include <vector>
@@ -156,8 +159,51 @@ TEST_CASE(errors_follow_reference) {  // test_solvers.cpp:221-243, test_referenc
   CHECK_THROWS_AS(consensus_solve(p, bad, 2), ParameterError);
 }
 
-int main() {
+TEST_CASE(cmat_round_trip_and_malformed) {  // test_problem_gen.cpp:105-164 (host only)
+  const std::string dir = "/tmp/admmgpu_shim_cmat_" + std::to_string(::getpid());
+  std::system(("mkdir -p " + dir).c_str());
+  const SensingProblem p = desk_problem(7, 5, 2, 33);
+  write_cmat(dir + "/roundtrip.cmat", p.h);
+  const CMatrix back = read_cmat(dir + "/roundtrip.cmat");
+  bool same = back.rows() == 7 && back.cols() == 5;
+  for (std::size_t i = 0; same && i < back.size(); ++i) same = back.data()[i] == p.h.data()[i];
+  CHECK(same);
+  write_cvec(dir + "/v.cmat", p.g);
+  CHECK(read_cvec(dir + "/v.cmat") == p.g);
+  write_cmat(dir + "/h64.cmat", p.h, /*c64=*/true);
+  const CMatrix h64 = read_cmat(dir + "/h64.cmat");
+  bool rounded = true;
+  for (std::size_t i = 0; i < h64.size(); ++i)
+    rounded = rounded && h64.data()[i] == Complex((float)p.h.data()[i].real(), (float)p.h.data()[i].imag());
+  CHECK(rounded);
+  std::FILE* f = std::fopen((dir + "/empty.cmat").c_str(), "wb");
+  std::fclose(f);
+  CHECK_THROWS_AS(read_cmat(dir + "/empty.cmat"), FormatError);
+  std::system(("truncate -s 68 " + dir + "/roundtrip.cmat").c_str());
+  try {
+    read_cmat(dir + "/roundtrip.cmat");
+    CHECK(false);
+  } catch (const FormatError& e) {
+    CHECK(e.byte_offset() == 20 + 3 * sizeof(Complex));
+  }
+  CHECK_THROWS_AS(read_cvec(dir + "/h64.cmat"), FormatError);
+  CHECK_THROWS_AS(read_cmat(dir + "/does_not_exist.cmat"), IoError);
+  CHECK_THROWS_AS(write_cvec(dir + "/e.cmat", CVector{}), ParameterError);
+  CMatrix bad(1, 1);
+  bad(0, 0) = Complex(std::numeric_limits<double>::infinity(), 0.0);
+  CHECK_THROWS_AS(write_cmat(dir + "/inf.cmat", bad), NumericalError);
+  std::system(("rm -rf " + dir).c_str());
+}
+
+int main(int argc, char** argv) {
+  if (argc > 1 && std::string(argv[1]) == "host") {  // cases that need no device
+    cmat_round_trip_and_malformed();
+    std::printf("%s cmat_round_trip_and_malformed\n%d checks, %d failures\n", g_fail ? "FAIL" : "PASS", g_checks,
+                g_fail);
+    return g_fail ? 1 : 0;
+  }
   struct { const char* name; void (*fn)(); } cases[] = {
+      {"cmat_round_trip_and_malformed", cmat_round_trip_and_malformed},
       {"matvec_known_answers", matvec_known_answers}, {"prox_known_answers", prox_known_answers},
       {"gram_solver", gram_solver}, {"degeneracy_lattice", degeneracy_lattice},
       {"oracle_parity_and_ledger", oracle_parity_and_ledger}, {"errors_follow_reference", errors_follow_reference}};

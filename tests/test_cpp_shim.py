@@ -22,6 +22,13 @@ def test_cpp_shim_compiles():
     assert os.path.exists(BIN)
 
 
+def test_cpp_shim_host_cases():
+    """CMAT I/O through the shim (cmat_io.hpp names and exceptions) needs no device."""
+    build()
+    r = subprocess.run([BIN, "host"], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "0 failures" in r.stdout, r.stdout + r.stderr
+
+
 @pytest.mark.gpu
 def test_cpp_shim_reference_cases_on_device():
     build()
