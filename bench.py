@@ -312,7 +312,7 @@ def bench_ours(args, cfg):
     method, m, n, k, snr, seed, kind, M, N, lr, iters, dtype = cfg
     problem = make_problem(cfg)
     scfg = admm.SolverConfig(rho=1.0, lambda_=1.0, max_iters=iters)
-    opts = admm.SolveOptions(dtype=dtype, device=dev, trace_objective=False)
+    opts = admm.SolveOptions(dtype=dtype, device=dev, trace_objective=args.trace_objective)
     plan = admm.AdmmPlan(problem, scfg, method, M, N, opts)
     if plan.batch > 1:  # per-scene lambda_b = c max|H^H g_b|
         lams = lr * plan.max_abs_adjoint_batched()
@@ -412,7 +412,7 @@ def bench_ours(args, cfg):
         "config": {"workload": f"config {args.config}: {describe(cfg)}",
                    "l2": f"inputs larger than L2 (H {hb / 2**20:.0f} MiB per replica)",
                    "parallelism": "replicas" if ws > 1 else "single GPU, all blocks",
-                   "lambda": lam},
+                   "lambda": lam, "trace_objective": bool(args.trace_objective)},
         "h_stream_gbs": h_stream_gbs, "h_stream_frac_of_peak": h_stream_gbs / peak,
         "hbm_compulsory_gbs": info["hbm_bytes_per_iter"] / (ms_per_step / 1000.0) / 1e9,
         "schedule": {1: "two-pass", 2: "single-HBM-pass sweep", 3: "batched scenes (FP64 SIMT GEMMs)"}[
@@ -447,6 +447,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-trace-objective", dest="trace_objective", action="store_false",
+                    help="drop the per-iteration objective from the trace (default: on, as the "
+                         "reference evaluates it every iteration, solvers.hpp:146; here by the "
+                         "H-pass-free recurrence, DESIGN.md §2)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":

@@ -425,6 +425,38 @@ objective_rows_kernel(const double2* __restrict__ g, const double2* __restrict__
   if (threadIdx.x == 0) red[blockIdx.y * gridDim.x + blockIdx.x] = r;
 }
 
+// Per-iteration objective (admm_core.hpp:60-64) WITHOUT a pass over H.  For block b
+// let a_b = H_b v and h_b = H_b s_b (this iteration's v and s).  Two products the
+// iteration already has pin them: w' = H_b c' with c' = v - s_b (the next w, read back as
+// g_ij - r after rows_finalize), and ghat_b = H_b u_b (still in the ghat buffer).  The
+// dual update s_b = s_b,prev + u_b - v (admm_core.hpp:87-89) gives
+//     h_b = h_b,prev + ghat_b - a_b,   a_b - h_b = w'   =>   a_b = (w' + h_b,prev + ghat_b) / 2,
+// with h_b = 0 before the first iteration (s = 0).  Row r of row block i:
+// (H v)_r = sum_j a_ij,r (ascending j).  Writes per-CTA partials of |Hv - g|^2; skipped
+// (zero partials, h untouched) while st->iter < min_iter.
+__global__ void __launch_bounds__(kCtaThreads)
+objective_rec_kernel(RowVecs rv, double2* __restrict__ hs, const BlockDesc* __restrict__ blocks, uint32_t N,
+                     double* __restrict__ red, const IterState* st, uint64_t min_iter) {
+  __shared__ double sm[kCtaWarps];
+  const uint32_t i = blockIdx.y;
+  const BlockDesc b0 = blocks[i * N];
+  const uint32_t row = blockIdx.x * blockDim.x + threadIdx.x;
+  double q = 0.0;
+  if (row < b0.rows && st->iter >= min_iter) {
+    double2 hv = make_double2(0.0, 0.0);
+    for (uint32_t j = 0; j < N; ++j) {
+      const uint64_t o = (uint64_t)blocks[i * N + j].mvec_off + row;
+      const double2 w = csub(rv.gij[o], rv.r[o]);
+      const double2 a = cscale(cadd(cadd(w, hs[o]), rv.ghat[o]), 0.5);
+      hs[o] = csub(a, w);
+      hv = cadd(hv, a);
+    }
+    q = cabs2(csub(hv, rv.g[b0.row0 + row]));
+  }
+  const double r = block_sum<kCtaThreads>(q, sm);
+  if (threadIdx.x == 0) red[blockIdx.y * gridDim.x + blockIdx.x] = r;
+}
+
 // Single-CTA epilogue of an iteration: fixed-order sums of the per-CTA
 // partials, trace[k] = (sqrt(rp2), sqrt(rho*rho*M*rd2), objective), and the
 // non-finite bookkeeping behind NumericalError(last_good_iteration).

@@ -152,7 +152,7 @@ struct admm_plan {
   bool fused_scal = false;   // Pr == 1, Pc > 1: scalars ride in the ghat all-gather slot
   uint64_t gslot = 0;        // ghat slot per rank (complex elements)
   bool keep_l2 = false;      // local H + K fit in L2: keep H resident across iterations
-  bool ragged = false, trace_obj = false;
+  bool ragged = false, trace_obj = false, obj_pass = false;  // obj_pass: objective by an extra H pass
   admm_solver_config cfg{};
   std::vector<uint64_t> rb, cb;
   std::vector<BlockDesc> blocks;
@@ -161,7 +161,7 @@ struct admm_plan {
   uint64_t mvec_total = 0, vec_total = 0, seg_total = 0, h_elems = 0, k_elems = 0, a_elems = 0;
   uint32_t max_rows = 0, max_seg = 0, max_rowblock = 0, max_m = 0;
   DevBuf dH, dK, dg, dghat, dgij, dr, dq, du, ds, dc, dv, dvprev;
-  DevBuf dwpart, dqpart, dzpart, dopart, dgpart;
+  DevBuf dwpart, dqpart, dzpart, dopart, dgpart, dhs;  // dhs: H_b s_b per block (objective recurrence)
   DevBuf dred, dored, dtrace, dstate, dparams, dblocks, dhN, dhNv, dkN, dhH, dhHg, dgram, dobj;
   Geom gN, gK, gH, gO, gG;
   // batched scenes (admm_batched.cuh): B right-hand sides sharing H and the factors
@@ -963,6 +963,14 @@ void enqueue_iteration_twopass(admm_plan* p, cudaStream_t s, bool with_objective
       row_vecs(p), p->dwpart.as<double2>(), p->dhN.as<MatDesc>(), p->dblocks.as<BlockDesc>(),
       p->dgblocks.as<BlockDesc>(), (uint32_t)p->N, p->gN.U,
       p->gN.P, p->dparams.as<Params>());
+  if (with_objective && !p->obj_pass) {  // trace[k-1].objective from this iteration's w = H c
+    objective_rec_kernel<<<dim3(p->ogx, M), kCtaThreads, 0, s>>>(row_vecs(p), p->dhs.as<double2>(),
+                                                                p->dblocks.as<BlockDesc>(), N, p->dored.as<double>(),
+                                                                p->dstate.as<IterState>(), 1);
+    objective_trace_kernel<<<1, kCtaThreads, 0, s>>>(p->dred.as<double>(), p->nz, p->dored.as<double>(), p->no,
+                                                     p->dparams.as<Params>(), p->dtrace.as<double>(), p->trace_cap,
+                                                     p->dstate.as<IterState>());
+  }
   mark(2);
   enqueue_kapply<S>(p, s, [&] { mark(3); });
   mark(4);
@@ -973,7 +981,8 @@ void enqueue_iteration_twopass(admm_plan* p, cudaStream_t s, bool with_objective
       col_vecs(p), p->dzpart.as<double2>(), p->dhH.as<MatDesc>(), p->dblocks.as<BlockDesc>(), M, N, p->gH.U,
       p->gH.P, p->dparams.as<Params>(), p->dred.as<double>(), p->dstate.as<IterState>());
   mark(6);
-  if (with_objective) {
+  const bool pass = with_objective && p->obj_pass;
+  if (pass) {
     gemv_n_kernel<S, kVN, kEvictNormal><<<(unsigned)p->gO.P, kCtaThreads, 0, s>>>(
         p->dH.as<S>(), p->dv.as<double2>(), p->dopart.as<double2>(), p->dhNv.as<MatDesc>(), nb, p->gO.U);
     objective_rows_kernel<<<dim3(p->ogx, M), kCtaThreads, 0, s>>>(
@@ -981,7 +990,7 @@ void enqueue_iteration_twopass(admm_plan* p, cudaStream_t s, bool with_objective
         p->gO.U, p->gO.P, p->dored.as<double>());
   }
   finalize_kernel<<<1, kCtaThreads, 0, s>>>(p->dred.as<double>(), p->nz, p->dored.as<double>(),
-                                            with_objective ? p->no : 0, p->dparams.as<Params>(),
+                                            pass ? p->no : 0, p->dparams.as<Params>(),
                                             p->dtrace.as<double>(), p->trace_cap, p->dstate.as<IterState>());
   mark(7);
   CK(cudaGetLastError());
@@ -1080,7 +1089,7 @@ void enqueue_iteration_sweep(admm_plan* p, cudaStream_t s, bool with_objective, 
   mark(0);
   launch_sweep<S>(p, s);
   mark(1);
-  if (with_objective) {
+  if (with_objective && p->obj_pass) {
     gemv_n_kernel<S, kVN, kEvictNormal><<<(unsigned)p->gO.P, kCtaThreads, 0, s>>>(
         p->dH.as<S>(), p->dv.as<double2>(), p->dopart.as<double2>(), p->dhNv.as<MatDesc>(), nb, p->gO.U);
     objective_rows_kernel<<<dim3(p->ogx, (uint32_t)p->Mr), kCtaThreads, 0, s>>>(
@@ -1093,6 +1102,10 @@ void enqueue_iteration_sweep(admm_plan* p, cudaStream_t s, bool with_objective, 
              p->dred.as<double>(), p->dparams.as<Params>(), p->dtrace.as<double>(), p->trace_cap,
              p->dstate.as<IterState>(), (double*)nullptr);
   mark(2);
+  if (with_objective && !p->obj_pass)  // this iteration's a_b from the sweep's next w (no H pass)
+    objective_rec_kernel<<<dim3(p->ogx, (uint32_t)p->Mr), kCtaThreads, 0, s>>>(
+        row_vecs(p), p->dhs.as<double2>(), p->dblocks.as<BlockDesc>(), (uint32_t)p->Nc, p->dored.as<double>(),
+        p->dstate.as<IterState>(), 0);
   if (with_objective) {  // the sweep's finalize wrote NaN: fill the objective of this iteration
     objective_trace_kernel<<<1, kCtaThreads, 0, s>>>(p->dred.as<double>(), (uint32_t)p->gS.P, p->dored.as<double>(),
                                                      p->no, p->dparams.as<Params>(), p->dtrace.as<double>(),
@@ -1341,8 +1354,8 @@ void upload_g(admm_plan* p, const double* g) {
 
 void reset_state(admm_plan* p) {
   cudaStream_t s = p->stream;
-  for (DevBuf* d : {&p->du, &p->ds, &p->dc, &p->dv, &p->dvprev, &p->dgij, &p->dr, &p->dq})
-    CK(cudaMemsetAsync(d->p, 0, d->bytes, s));
+  for (DevBuf* d : {&p->du, &p->ds, &p->dc, &p->dv, &p->dvprev, &p->dgij, &p->dr, &p->dq, &p->dhs})
+    if (d->p) CK(cudaMemsetAsync(d->p, 0, d->bytes, s));
   CK(cudaMemsetAsync(p->ghat_ptr, 0, p->mvec_total * 16 * p->batch, s));
   CK(cudaMemsetAsync(p->outbox_ptr, 0, p->outbox_total * 16, s));
   IterState st{0, ~0ull, 0u, 0u};
@@ -1601,6 +1614,8 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
   p->no = p->ogx * (uint32_t)p->Mr;
   p->dred.alloc((size_t)3 * std::max<uint64_t>(p->nz, p->gS.P) * sizeof(double));
   p->dored.alloc((size_t)std::max<uint32_t>(p->no, p->zgx * (uint32_t)p->Nc) * sizeof(double));
+  if (const char* e = std::getenv("ADMM_B200_OBJ")) p->obj_pass = !std::strcmp(e, "pass");
+  if (p->trace_obj && !p->obj_pass) p->dhs.alloc(p->mvec_total * sizeof(double2));
   ensure_trace(p.get(), std::max<uint64_t>(cfg.max_iters, 1));
 
   if (p->dtype == ADMM_C128) {
@@ -1873,7 +1888,7 @@ admm_status admm_plan_get_info(const admm_plan* p, admm_plan_info* info) {
     r.k_bytes = kb;
     r.h_stream_bytes_per_iter = 2 * hb;
     r.bytes_per_iter = 2 * hb + kb_dense + vb;  // two-pass algorithmic bytes
-    r.launches_per_iter = p->schedule == 3 ? 7 : p->schedule == 2 ? (p->trace_obj ? 7 : 4) : (p->trace_obj ? 9 : 7);
+    r.launches_per_iter = p->schedule == 3 ? 7 : p->schedule == 2 ? (p->trace_obj ? (p->obj_pass ? 7 : 6) : 4) : (p->trace_obj ? 9 : 7);
     if (p->schedule != 3 && p->kpacked && p->hemv_fuse) r.launches_per_iter -= 1;  // finalize inside hemv
     r.schedule = (uint64_t)p->schedule;
     r.grid_sweep = p->gS.P;
@@ -2011,10 +2026,10 @@ admm_status admm_plan_solve(admm_plan* p, double* solution, double* trace, uint6
       if (solution) read_segments(p, p->dv, solution);
       return;
     }
-    if (p->trace_obj) {
+    if (p->trace_obj && p->obj_pass) {  // the last iteration's pass already is the final objective
       CK(cudaMemcpyAsync(&obj, p->dtrace.as<double>() + 3 * (done - 1) + 2, 8, cudaMemcpyDeviceToHost, p->stream));
       CK(cudaStreamSynchronize(p->stream));
-    } else {
+    } else {  // one exact pass over H for SolveReport::objective (solvers.hpp:163)
       if (p->dtype == ADMM_C128)
         enqueue_objective<double2>(p, p->stream);
       else
@@ -2026,7 +2041,9 @@ admm_status admm_plan_solve(admm_plan* p, double* solution, double* trace, uint6
     if (trace) {
       CK(cudaMemcpyAsync(trace, p->dtrace.p, done * 3 * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
       CK(cudaStreamSynchronize(p->stream));
-      if (!p->trace_obj) trace[3 * (done - 1) + 2] = obj;
+      // the recurrence fills entry k-1 during iteration k (two-pass) / k (sweep): the last
+      // entry is the exact pass either way
+      trace[3 * (done - 1) + 2] = obj;
     }
     if (solution) read_segments(p, p->dv, solution);
   });
