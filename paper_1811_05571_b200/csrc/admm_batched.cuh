@@ -18,6 +18,10 @@ namespace admm {
 constexpr int kBT = 64;   // output tile: rows (N) or columns (adjoint)
 constexpr int kBB = 64;   // scenes per tile
 constexpr int kBK = 16;   // k-chunk
+// k-steps unrolled per chunk: 4 for W = H C (2.23 vs 2.29 ms on config 5), 2 for the
+// adjoint (2.27 vs 2.31 ms; 4 spills there at the 128-register cap)
+template <bool ADJ>
+constexpr int kBUnroll = ADJ ? 2 : 4;
 
 struct BTile {
   uint64_t a_off;   // matrix in the storage arena
@@ -92,7 +96,7 @@ bgemm_kernel(const S* __restrict__ A, const BTile* __restrict__ tiles, const dou
       __syncthreads();
       ad = Ad;
     }
-#pragma unroll 4
+#pragma unroll kBUnroll<ADJ>
     for (int kk = 0; kk < kBK; ++kk) {
       double2 av[4], xv[4];
 #pragma unroll
@@ -103,13 +107,17 @@ bgemm_kernel(const S* __restrict__ A, const BTile* __restrict__ tiles, const dou
           av[q] = ad[o];
         else
           av[q] = Store<S>::widen(as[o]);
-        if (ADJ) av[q].y = -av[q].y;
         xv[q] = xs[kk * (kBB + 1) + tx + 16 * q];
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q)
 #pragma unroll
-        for (int w = 0; w < 4; ++w) cmac(acc[q][w], av[q], xv[w]);
+        for (int w = 0; w < 4; ++w) {
+          if (ADJ)
+            cmac_conj(acc[q][w], av[q], xv[w]);
+          else
+            cmac(acc[q][w], av[q], xv[w]);
+        }
     }
     __syncthreads();
     buf ^= 1;
