@@ -16,6 +16,7 @@
 #pragma once
 
 #include "admm_kernels.cuh"
+#include "admm_slab.cuh"  // mbarrier / bulk-copy helpers
 
 namespace admm {
 
@@ -251,6 +252,190 @@ hemv_kernel(const S* __restrict__ Kp, const double2* __restrict__ X, double2* __
         d = hd[++b];
         u = 0;
         I = 0;
+      }
+      load_xI();
+    } else {
+      ++J;
+    }
+  }
+}
+
+// Bulk-copy variant (default): the packed tiles are contiguous 64 x 64 blocks (32 KiB
+// c64, 64 KiB c128), so each tile is ONE cp.async.bulk into an NS-deep SMEM ring
+// (mbarrier complete_tx), issued by one thread as soon as all warps have read the stage
+// it replaces.  NS tiles in flight per SM (192 KiB) instead of the register variant's one
+// or two — that variant measured ~2 us per tile, latency-bound (2.2 TB/s on config 3).
+// K does not depend on the previous kernel, so the first NS tiles are requested BEFORE
+// the PDL wait and stream while rows_finalize is still finishing r.  Same tile/lane
+// mapping, arithmetic order and partial layout as hemv_kernel (identical bits).
+// OCC CTAs per SM: 1 -> NS = 5 (c64) / 2 (c128) stages; 2 -> NS = 2 per CTA.
+template <typename S, int OCC>
+struct HemvRing {
+  static constexpr int NS = OCC == 2 ? 2 : sizeof(S) == 16 ? 2 : 5;
+  static_assert(NS * sizeof(uint64_t) <= 128, "barrier area");
+  static constexpr uint32_t TB = kHT * kHT * sizeof(S);
+};
+// ring + H-part buffers + barriers + the block's r (max_m complex)
+template <typename S, int OCC>
+constexpr size_t hemv_bulk_smem_fixed() {
+  return (size_t)HemvRing<S, OCC>::NS * HemvRing<S, OCC>::TB + 2 * kCtaWarps * kHT * sizeof(double2) +
+         128;  // NS barriers, padded so the r buffer behind them stays 16-byte aligned
+}
+template <typename S, int OCC>
+size_t hemv_bulk_smem(uint32_t max_m) {
+  return hemv_bulk_smem_fixed<S, OCC>() + (size_t)((max_m + kHT - 1) / kHT * kHT) * sizeof(double2);
+}
+
+template <typename S, int OCC>
+__global__ void __launch_bounds__(kCtaThreads, OCC)
+hemv_bulk_kernel(const S* __restrict__ Kp, const double2* __restrict__ X, double2* __restrict__ part,
+                 const HemvDesc* __restrict__ hd, int nb, uint64_t U, int keep) {
+  constexpr int NS = HemvRing<S, OCC>::NS;
+  constexpr uint32_t TB = HemvRing<S, OCC>::TB;
+  extern __shared__ __align__(128) unsigned char hsm[];
+  const S* ring = reinterpret_cast<const S*>(hsm);
+  double2(*hbuf)[kCtaWarps][kHT] = reinterpret_cast<double2(*)[kCtaWarps][kHT]>(hsm + NS * TB);
+  uint64_t* full = reinterpret_cast<uint64_t*>(hsm + NS * TB + 2 * kCtaWarps * kHT * sizeof(double2));
+  double2* xs = reinterpret_cast<double2*>(hsm + hemv_bulk_smem_fixed<S, OCC>());  // r of the current block
+  uint64_t pol;
+  if (keep)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  const uint64_t P = gridDim.x, p = blockIdx.x;
+  uint64_t x = sk_lo(p, U, P);
+  const uint64_t x0 = x, xe = sk_lo(p + 1, U, P);
+  if (x >= xe) {
+    pdl_enter();
+    return;
+  }
+  const uint32_t ring_s = smem_u32(hsm), full_s = smem_u32(full);
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < NS; ++st) mbar_init(&full[st], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (uint64_t t = 0; t < (uint64_t)NS && x0 + t < xe; ++t) {  // K is ready before the PDL wait
+      mbar_expect_tx_s(full_s + 8 * (uint32_t)t, TB);
+      bulk_g2s_s(ring_s + (uint32_t)t * TB, Kp + (x0 + t) * (uint64_t)(kHT * kHT), TB, full_s + 8 * (uint32_t)t, pol);
+    }
+  }
+  __syncthreads();
+  pdl_enter();  // r (rows_finalize) visible from here on
+  const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+  int b = 0;
+  while (b + 1 < nb && hd[b + 1].unit0 <= x) ++b;
+  HemvDesc d = hd[b];
+  uint32_t u = (uint32_t)(x - d.unit0);
+  uint32_t I = 0;
+  while ((I + 1) * (I + 2) / 2 <= u) ++I;
+  uint32_t J = u - I * (I + 1) / 2;
+  double2 accN[kHRows];
+  double2 xI[kHRows];
+  // the block's r, zero-padded to whole tiles, staged once per block: every X read of
+  // the tile loop is an SMEM read (no L2 round trip on the per-tile critical path)
+  auto stage_r = [&]() {
+    const uint32_t mp = d.nT * kHT;
+    for (uint32_t e = threadIdx.x; e < mp; e += kCtaThreads) xs[e] = ld_masked(X + d.x_off, e, d.m);
+    __syncthreads();
+  };
+  auto load_xI = [&]() {
+#pragma unroll
+    for (int k = 0; k < kHRows; ++k) xI[k] = xs[I * kHT + warp * kHRows + k];
+  };
+#pragma unroll
+  for (int k = 0; k < kHRows; ++k) accN[k] = make_double2(0.0, 0.0);
+  stage_r();
+  load_xI();
+  uint32_t par = 0;
+  for (uint64_t t = 0;; ++t) {
+    const int st = (int)(t % NS);
+    const uint32_t c0 = J * kHT + lane * 2;
+    const double2 xj0 = xs[c0], xj1 = xs[c0 + 1];
+    mbar_wait_s(full_s + 8 * st, (uint32_t)(t / NS) & 1u);
+    double2 h[kHRows][2];
+    const S* ts = ring + (size_t)st * (kHT * kHT) + (warp * kHRows) * kHT + lane * 2;
+#pragma unroll
+    for (int k = 0; k < kHRows; ++k) {
+      if constexpr (sizeof(S) == 16) {
+        h[k][0] = ts[k * kHT];
+        h[k][1] = ts[k * kHT + 1];
+      } else {
+        const float4 f = *reinterpret_cast<const float4*>(ts + k * kHT);
+        h[k][0] = make_double2(f.x, f.y);
+        h[k][1] = make_double2(f.z, f.w);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kHRows; ++k) {
+      cmac(accN[k], h[k][0], xj0);
+      cmac(accN[k], h[k][1], xj1);
+    }
+    const bool offdiag = J < I;
+    if (offdiag) {  // H part of an off-diagonal tile: y_J += K_IJ^H r_I
+      double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int k = 0; k < kHRows; ++k) {
+        cmac_conj(a0, h[k][0], xI[k]);
+        cmac_conj(a1, h[k][1], xI[k]);
+      }
+      hbuf[par][warp][lane * 2] = a0;
+      hbuf[par][warp][lane * 2 + 1] = a1;
+    }
+    __syncthreads();  // stage st read by every warp; hbuf[par] complete
+    if (threadIdx.x == 0 && x + NS < xe) {
+      mbar_expect_tx_s(full_s + 8 * st, TB);
+      bulk_g2s_s(ring_s + (uint32_t)st * TB, Kp + (x + NS) * (uint64_t)(kHT * kHT), TB, full_s + 8 * st, pol);
+    }
+    if (offdiag) {
+      if (warp == 0) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c = lane * 2 + e;
+          double2 sum = hbuf[par][0][c];
+#pragma unroll
+          for (int w = 1; w < kCtaWarps; ++w) sum = cadd(sum, hbuf[par][w][c]);
+          part[d.part_off + ((uint64_t)d.n_units + u) * kHT + c] = sum;
+        }
+      }
+      par ^= 1u;
+    }
+    ++x;
+    const bool row_end = (J == I);
+    if (row_end || x == xe) {  // flush the N partial of this tile-row segment (as hemv_kernel)
+      const uint32_t urow = I * (I + 1) / 2;
+      const uint64_t seg = p - sk_owner(d.unit0 + urow, U, P);
+#pragma unroll
+      for (int o = 16, nv = kHRows / 2; o >= 4; o >>= 1, nv >>= 1) {
+        const bool hi = (lane & o) != 0;
+#pragma unroll
+        for (int k = 0; k < nv; ++k) {
+          double2 send = hi ? accN[k] : accN[k + nv];
+          const double2 kp = hi ? accN[k + nv] : accN[k];
+          send.x = __shfl_xor_sync(0xffffffffu, send.x, o);
+          send.y = __shfl_xor_sync(0xffffffffu, send.y, o);
+          accN[k] = cadd(kp, send);
+        }
+      }
+      double2 a = accN[0];
+#pragma unroll
+      for (int o = 2; o >= 1; o >>= 1) {
+        a.x += __shfl_xor_sync(0xffffffffu, a.x, o);
+        a.y += __shfl_xor_sync(0xffffffffu, a.y, o);
+      }
+      if ((lane & 3) == 0)
+        part[d.part_off + (uint64_t)(urow + seg) * kHT + warp * kHRows + (lane >> 2)] = a;
+#pragma unroll
+      for (int k = 0; k < kHRows; ++k) accN[k] = make_double2(0.0, 0.0);
+    }
+    if (x == xe) break;
+    ++u;
+    if (row_end) {
+      J = 0;
+      if (++I == d.nT) {
+        d = hd[++b];
+        u = 0;
+        I = 0;
+        __syncthreads();  // every warp is done with the previous block's r
+        stage_r();
       }
       load_xI();
     } else {

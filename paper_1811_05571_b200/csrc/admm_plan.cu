@@ -186,6 +186,7 @@ struct admm_plan {
   bool kkeep = false;       // ... with an L2 evict_last policy (ADMM_B200_KKEEP)
   int hemv_occ = 1;         // hemv_kernel CTAs per SM (1: register prefetch of the next tile)
   bool hemv_fuse = false;   // q / ghat finalized inside hemv_kernel (tile-row completion counters)
+  int hemv_bulk = 0;        // hemv_bulk_kernel CTAs per SM (0: register variant hemv_kernel)
   DevBuf dkcnt;
   std::vector<HemvDesc> hv;
   DevBuf dKp, dhv, dkppart;
@@ -883,6 +884,19 @@ void factor_blocks(admm_plan* p) {
     if (const char* e = std::getenv("ADMM_B200_HEMV_OCC")) p->hemv_occ = std::atoi(e) == 2 ? 2 : 1;
     p->gP.P = p->hemv_occ == 2 ? grid_for<S>(hemv_kernel<S, 2, false>, u0, p->num_sms)
                                : grid_for<S>(hemv_kernel<S, 1, false>, u0, p->num_sms);
+    // bulk-copy ring variant unless the register variants are requested (same P: one CTA per SM)
+    const char* hv = std::getenv("ADMM_B200_HEMV");
+    // default for complex64 K (streamed from HBM: configs 3/4, 35 -> 2x us); complex128 K
+    // on config 2 is L2-resident and the register variant is faster there (15.0 vs 18.4 us)
+    const bool want = hv ? !std::strcmp(hv, "bulk") : sizeof(S) == 8;
+    const int bocc = std::getenv("ADMM_B200_HEMV_BOCC") ? std::atoi(std::getenv("ADMM_B200_HEMV_BOCC")) : 1;
+    const size_t bsm = bocc == 2 ? hemv_bulk_smem<S, 2>(p->max_rows) : hemv_bulk_smem<S, 1>(p->max_rows);
+    p->hemv_bulk = want && !p->hemv_fuse && p->hemv_occ == 1 && bsm * bocc <= 227 * 1024 ? bocc : 0;
+    if (p->hemv_bulk) {
+      CK(cudaFuncSetAttribute(p->hemv_bulk == 2 ? hemv_bulk_kernel<S, 2> : hemv_bulk_kernel<S, 1>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
+      p->gP.P = std::max<uint64_t>(1, std::min<uint64_t>(u0, (uint64_t)p->num_sms * p->hemv_bulk));
+    }
   }
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(&hf, flag.p, 4, cudaMemcpyDeviceToHost, p->stream));
@@ -923,6 +937,18 @@ template <typename S, typename Mid>
 void enqueue_kapply(admm_plan* p, cudaStream_t s, Mid mid) {
   const int nb = (int)p->blocks.size();
   if (p->kpacked) {
+    if (p->hemv_bulk) {
+      auto fb = p->hemv_bulk == 2 ? hemv_bulk_kernel<S, 2> : hemv_bulk_kernel<S, 1>;
+      const size_t sm = p->hemv_bulk == 2 ? hemv_bulk_smem<S, 2>(p->max_rows) : hemv_bulk_smem<S, 1>(p->max_rows);
+      launch_pdl(fb, dim3((unsigned)p->gP.P), dim3(kCtaThreads), sm, s,
+                 p->dKp.as<S>(), p->dr.as<double2>(), p->dkppart.as<double2>(), p->dhv.as<HemvDesc>(), nb, p->gP.U,
+                 p->kkeep ? 1 : 0);
+      mid();
+      launch_pdl(hemv_finalize_kernel, dim3((unsigned)cdiv(p->max_rows, kHFinRows), nb), dim3(kHFinRows), 0, s,
+                 row_vecs(p), p->dkppart.as<double2>(), p->dhv.as<HemvDesc>(), p->gP.U, p->gP.P,
+                 p->dparams.as<Params>());
+      return;
+    }
     auto fn = p->hemv_fuse ? hemv_kernel<S, 1, true> : p->hemv_occ == 2 ? hemv_kernel<S, 2, false> : hemv_kernel<S, 1, false>;
     launch_pdl(fn, dim3((unsigned)p->gP.P), dim3(kCtaThreads), 0, s, p->dKp.as<S>(), p->dr.as<double2>(),
                p->dkppart.as<double2>(), p->dhv.as<HemvDesc>(), nb, p->gP.U, p->kkeep ? 1 : 0,
