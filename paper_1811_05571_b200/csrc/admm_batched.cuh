@@ -265,6 +265,55 @@ __global__ void bfinalize_kernel(const double* __restrict__ red, uint32_t nct, u
   }
 }
 
+// Per-scene objective (admm_core.hpp:60-64) by the recurrence of objective_rec_kernel:
+// a_b = (w' + h_b,prev + ghat_b) / 2, h_b = a_b - w', w' = G_ij - R after brows<kRhs>.
+// Grid (gx, row blocks), 256 threads: scene = tid % 64, rows tid / 64 + 4 k.  Per-CTA,
+// per-scene partials of |Hv - g|^2 (fixed order); skipped while st->iter < min_iter.
+__global__ void __launch_bounds__(kCtaThreads)
+bobjective_rec_kernel(BRowVecs rv, double2* __restrict__ hs, const BlockDesc* __restrict__ blocks, uint32_t N,
+                      uint32_t B, double* __restrict__ ored, const IterState* st, uint64_t min_iter) {
+  __shared__ double sm[kCtaThreads / kBB][kBB];
+  const uint32_t i = blockIdx.y;
+  const BlockDesc b0 = blocks[i * N];
+  const uint32_t sc = threadIdx.x % kBB, grp = threadIdx.x / kBB;
+  constexpr uint32_t G = kCtaThreads / kBB;
+  double q = 0.0;
+  if (sc < B && st->iter >= min_iter) {
+    for (uint32_t row = blockIdx.x * G + grp; row < b0.rows; row += gridDim.x * G) {
+      double2 hv = make_double2(0.0, 0.0);
+      for (uint32_t j = 0; j < N; ++j) {
+        const uint64_t o = ((uint64_t)blocks[i * N + j].mvec_off + row) * B + sc;
+        const double2 w = csub(rv.gij[o], rv.r[o]);
+        const double2 a = cscale(cadd(cadd(w, hs[o]), rv.ghat[o]), 0.5);
+        hs[o] = csub(a, w);
+        hv = cadd(hv, a);
+      }
+      q += cabs2(csub(hv, rv.g[((uint64_t)b0.row0 + row) * B + sc]));
+    }
+  }
+  sm[grp][sc] = q;
+  __syncthreads();
+  if (threadIdx.x < kBB) {
+    double a = sm[0][threadIdx.x];
+    for (uint32_t g = 1; g < G; ++g) a += sm[g][threadIdx.x];
+    ored[((uint64_t)blockIdx.y * gridDim.x + blockIdx.x) * kBB + threadIdx.x] = a;
+  }
+}
+
+// trace[iter - 1][scene].objective = 0.5 sum |Hv - g|^2 + lambda_b ||v_b||_1 (the l1
+// partials of bzupdate, red[2][pz][64]); one thread per scene, fixed order.
+__global__ void bobjective_trace_kernel(const double* __restrict__ red, uint32_t pz, const double* __restrict__ ored,
+                                        uint32_t no, const double* __restrict__ lam, uint32_t B,
+                                        double* __restrict__ trace, uint64_t trace_cap, const IterState* st) {
+  const uint32_t sc = threadIdx.x;
+  const uint64_t k = st->iter - 1;
+  if (sc >= B || st->iter == 0 || k >= trace_cap) return;
+  double o = 0.0, l = 0.0;
+  for (uint32_t c = 0; c < no; ++c) o += ored[(uint64_t)c * kBB + sc];
+  for (uint32_t c = 0; c < pz; ++c) l += red[((uint64_t)2 * pz + c) * kBB + sc];
+  trace[(k * B + sc) * 3 + 2] = 0.5 * o + lam[sc] * l;
+}
+
 // max_t |(H^H g_b)_t| per scene from Z = H^H G (segment sums over the row blocks).
 __global__ void babsmax_kernel(const double2* __restrict__ z, const BlockDesc* __restrict__ blocks, uint32_t M,
                                uint32_t N, uint32_t B, double* __restrict__ out) {

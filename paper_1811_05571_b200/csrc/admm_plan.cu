@@ -167,7 +167,8 @@ struct admm_plan {
   // batched scenes (admm_batched.cuh): B right-hand sides sharing H and the factors
   uint64_t batch = 1;
   std::vector<BTile> tN, tK, tH, tG;
-  DevBuf dtN, dtK, dtH, dtG, dz, dkappa, dbred;
+  DevBuf dtN, dtK, dtH, dtG, dz, dkappa, dbred, dblam, dbored;  // dblam: lambda_b; dbored: objective partials
+  uint32_t bogx = 1;  // bobjective_rec_kernel grid x
   uint32_t splitN = 1, splitK = 1, splitH = 1, pz = 1;
   std::vector<double> lambdas;
   // sweep schedule (admm_sweep.cuh)
@@ -1235,10 +1236,40 @@ void build_batched(admm_plan* p) {
   p->dkappa.alloc(B * sizeof(double));
   p->pz = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(4ull * p->num_sms, cdiv(p->max_seg, 4)));
   p->dbred.alloc((size_t)3 * p->pz * kBB * sizeof(double));
+  p->dblam.alloc(B * sizeof(double));
+  p->bogx = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(2ull * p->num_sms / std::max<uint64_t>(1, p->Mr),
+                                                                cdiv(p->max_rows, kCtaThreads / kBB)));
+  p->dbored.alloc((size_t)p->bogx * p->Mr * kBB * sizeof(double));
 }
 
 BRowVecs brow_vecs(admm_plan* p) {
   return BRowVecs{p->dg.as<double2>(), p->ghat_ptr, p->dgij.as<double2>(), p->dr.as<double2>(), p->dq.as<double2>()};
+}
+
+void enqueue_bobjective(admm_plan* p, cudaStream_t s) {
+  const uint32_t B = (uint32_t)p->batch;
+  bobjective_rec_kernel<<<dim3(p->bogx, (unsigned)p->Mr), kCtaThreads, 0, s>>>(
+      brow_vecs(p), p->dhs.as<double2>(), p->dblocks.as<BlockDesc>(), (uint32_t)p->Nc, B, p->dbored.as<double>(),
+      p->dstate.as<IterState>(), 1);
+  bobjective_trace_kernel<<<1, kBB, 0, s>>>(p->dbred.as<double>(), p->pz, p->dbored.as<double>(),
+                                            p->bogx * (uint32_t)p->Mr, p->dblam.as<double>(), B,
+                                            p->dtrace.as<double>(), p->trace_cap, p->dstate.as<IterState>());
+}
+
+// After the last iteration: w = H c of the would-be next iteration (bgemm + brows<kRhs>),
+// then the recurrence fills the last trace entry.  Leaves the iterates untouched.
+template <typename S>
+void enqueue_bobjective_last(admm_plan* p, cudaStream_t s) {
+  const uint32_t B = (uint32_t)p->batch, nb = (uint32_t)p->blocks.size();
+  const uint64_t stride = p->mvec_total * B;
+  const unsigned rgx = (unsigned)cdiv((uint64_t)p->max_rows * B, kCtaThreads);
+  bgemm_kernel<S, false><<<(unsigned)p->tN.size(), 256, bgemm_smem<S, false>(), s>>>(p->dH.as<S>(), p->dtN.as<BTile>(),
+                                                                  p->dc.as<double2>(), p->dwpart.as<double2>(), B);
+  brows_kernel<kRhs><<<dim3(rgx, nb), kCtaThreads, 0, s>>>(brow_vecs(p), p->dwpart.as<double2>(), stride, p->splitN,
+                                                          p->dblocks.as<BlockDesc>(), (uint32_t)p->Nc, B,
+                                                          p->dparams.as<Params>());
+  enqueue_bobjective(p, s);
+  CK(cudaGetLastError());
 }
 
 template <typename S>
@@ -1256,6 +1287,7 @@ void enqueue_iteration_batched(admm_plan* p, cudaStream_t s, std::vector<cudaEve
   brows_kernel<kRhs><<<dim3(rgx, nb), kCtaThreads, 0, s>>>(brow_vecs(p), p->dwpart.as<double2>(), stride, p->splitN,
                                                           p->dblocks.as<BlockDesc>(), (uint32_t)p->Nc, B,
                                                           p->dparams.as<Params>());
+  if (p->trace_obj) enqueue_bobjective(p, s);  // trace[k-1].objective per scene (w = H c of this iteration)
   mark(2);
   bgemm_kernel<S, false><<<(unsigned)p->tK.size(), 256, bgemm_smem<S, false>(), s>>>(p->dK.as<S>(), p->dtK.as<BTile>(),
                                                                   p->dr.as<double2>(), p->dqpart.as<double2>(), B);
@@ -1366,6 +1398,8 @@ void set_params(admm_plan* p) {
     std::vector<double> k(p->batch);
     for (uint64_t b = 0; b < p->batch; ++b) k[b] = p->params.kappa * (p->lambdas[b] / p->cfg.lambda);
     CK(cudaMemcpyAsync(p->dkappa.p, k.data(), k.size() * 8, cudaMemcpyHostToDevice, p->stream));
+    if (p->dblam.p)
+      CK(cudaMemcpyAsync(p->dblam.p, p->lambdas.data(), p->batch * 8, cudaMemcpyHostToDevice, p->stream));
     CK(cudaStreamSynchronize(p->stream));
   }
 }
@@ -1641,7 +1675,7 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
   p->dred.alloc((size_t)3 * std::max<uint64_t>(p->nz, p->gS.P) * sizeof(double));
   p->dored.alloc((size_t)std::max<uint32_t>(p->no, p->zgx * (uint32_t)p->Nc) * sizeof(double));
   if (const char* e = std::getenv("ADMM_B200_OBJ")) p->obj_pass = !std::strcmp(e, "pass");
-  if (p->trace_obj && !p->obj_pass) p->dhs.alloc(p->mvec_total * sizeof(double2));
+  if (p->trace_obj && !p->obj_pass) p->dhs.alloc(p->mvec_total * std::max<uint64_t>(1, p->batch) * sizeof(double2));
   ensure_trace(p.get(), std::max<uint64_t>(cfg.max_iters, 1));
 
   if (p->dtype == ADMM_C128) {
@@ -2041,9 +2075,15 @@ admm_status admm_plan_solve(admm_plan* p, double* solution, double* trace, uint6
     }
     if (iterations_run) *iterations_run = done;
     double obj = 0.0;
-    if (p->batch > 1) {  // per-scene objective is not computed for batched plans
+    if (p->batch > 1) {  // per-scene objectives live in the trace; SolveReport.objective is a scalar
       obj = std::numeric_limits<double>::quiet_NaN();
       if (objective) *objective = obj;
+      if (trace && p->trace_obj && done > 0) {
+        if (p->dtype == ADMM_C128)
+          enqueue_bobjective_last<double2>(p, p->stream);
+        else
+          enqueue_bobjective_last<float2>(p, p->stream);
+      }
       if (trace) {
         CK(cudaMemcpyAsync(trace, p->dtrace.p, done * 3 * p->batch * sizeof(double), cudaMemcpyDeviceToHost,
                            p->stream));

@@ -50,3 +50,26 @@ def test_batched_scenes_match_independent_solves(dtype, B, split, monkeypatch):
         ref = orc.solve("hybrid", h128, g[:, b], M=2, N=4, lam=float(lams[b]), iters=iters)
         err = rel(rep.solution[:, b], ref["solution"])
         assert err <= 1e-4 and np.array_equal(support(rep.solution[:, b]), support(ref["solution"]))
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_batched_objective_trace(dtype):
+    """Per-scene objective trace of a batched plan (the recurrence of the single-scene
+    engine, per scene; the last entry from one extra w = H c) against the oracle."""
+    import paper_1811_05571_b200 as admm
+    h = admm.cra_matrix(seed=6, dtype=dtype, n_tx=6, n_freq=32, grid=16)  # 192 x 4096
+    B = 6
+    g, _ = admm.cra_scenes(h, B, seed=6, lo=20, hi=60, grid=16)
+    iters = 40
+    p = admm.SensingProblem(h, g)
+    cfg = admm.SolverConfig(rho=1.0, lambda_=1.0, max_iters=iters)
+    with admm.AdmmPlan(p, cfg, "hybrid", 2, 4, admm.SolveOptions(dtype=dtype, trace_objective=True)) as plan:
+        lams = 0.03 * plan.max_abs_adjoint_batched()
+        plan.set_lambdas(lams)
+        rep = plan.solve()
+    h128 = h.astype(np.complex128)
+    for b in range(B):
+        ref = orc.solve("hybrid", h128, g[:, b], M=2, N=4, lam=float(lams[b]), iters=iters)
+        want = ref["trace"][:, 2]
+        assert np.all(np.isfinite(rep.trace.objective[:, b]))
+        np.testing.assert_allclose(rep.trace.objective[:, b], want, rtol=1e-9 if dtype == "c128" else 1e-5)
