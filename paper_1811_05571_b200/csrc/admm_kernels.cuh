@@ -434,23 +434,33 @@ objective_rows_kernel(const double2* __restrict__ g, const double2* __restrict__
 // with h_b = 0 before the first iteration (s = 0).  Row r of row block i:
 // (H v)_r = sum_j a_ij,r (ascending j).  Writes per-CTA partials of |Hv - g|^2; skipped
 // (zero partials, h untouched) while st->iter < min_iter.
+// Parallel over (row, column block): 256 threads = RT rows x NP lanes (NP = 2^np_log2 >=
+// N), so a sectioning row block of 1024 rows and N = 8 spreads over 32 CTAs instead of 4.
+// Each lane updates one a_ij / h_ij; lane 0 of each row sums the row's a_ij in ascending j.
 __global__ void __launch_bounds__(kCtaThreads)
 objective_rec_kernel(RowVecs rv, double2* __restrict__ hs, const BlockDesc* __restrict__ blocks, uint32_t N,
-                     double* __restrict__ red, const IterState* st, uint64_t min_iter) {
+                     uint32_t np_log2, double* __restrict__ red, const IterState* st, uint64_t min_iter) {
+  pdl_enter();
+  __shared__ double2 sa[kCtaThreads];
   __shared__ double sm[kCtaWarps];
   const uint32_t i = blockIdx.y;
   const BlockDesc b0 = blocks[i * N];
-  const uint32_t row = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t NP = 1u << np_log2, j = threadIdx.x & (NP - 1), rl = threadIdx.x >> np_log2;
+  const uint32_t row = blockIdx.x * (kCtaThreads >> np_log2) + rl;
+  const bool on = st->iter >= min_iter && row < b0.rows;
+  double2 a = make_double2(0.0, 0.0);
+  if (on && j < N) {
+    const uint64_t o = (uint64_t)blocks[i * N + j].mvec_off + row;
+    const double2 w = csub(rv.gij[o], rv.r[o]);
+    a = cscale(cadd(cadd(w, hs[o]), rv.ghat[o]), 0.5);
+    hs[o] = csub(a, w);
+  }
+  sa[threadIdx.x] = a;
+  __syncthreads();
   double q = 0.0;
-  if (row < b0.rows && st->iter >= min_iter) {
+  if (on && j == 0) {
     double2 hv = make_double2(0.0, 0.0);
-    for (uint32_t j = 0; j < N; ++j) {
-      const uint64_t o = (uint64_t)blocks[i * N + j].mvec_off + row;
-      const double2 w = csub(rv.gij[o], rv.r[o]);
-      const double2 a = cscale(cadd(cadd(w, hs[o]), rv.ghat[o]), 0.5);
-      hs[o] = csub(a, w);
-      hv = cadd(hv, a);
-    }
+    for (uint32_t jj = 0; jj < N; ++jj) hv = cadd(hv, sa[rl * NP + jj]);
     q = cabs2(csub(hv, rv.g[b0.row0 + row]));
   }
   const double r = block_sum<kCtaThreads>(q, sm);

@@ -199,6 +199,8 @@ struct admm_plan {
   Geom gS;
   size_t sweep_smem = 0;
   uint32_t zgx = 0, rgx = 0, rgx_s = 0, ogx = 0, nz = 0, no = 0;
+  uint32_t orgx = 1, onp = 0, nor = 1;  // objective_rec_kernel: grid x, log2 lanes per row, partials
+  DevBuf drored;
   uint64_t trace_cap = 0;
   cudaGraphExec_t exec = nullptr;
   uint64_t graph_iters = 0;
@@ -910,6 +912,7 @@ void factor_blocks(admm_plan* p) {
 __global__ void objective_trace_kernel(const double* __restrict__ red, uint32_t P, const double* __restrict__ ored,
                                        uint32_t no, const Params* __restrict__ prm, double* __restrict__ trace,
                                        uint64_t trace_cap, const IterState* st) {
+  pdl_enter();
   __shared__ double sm[kCtaWarps];
   double l = 0.0, o = 0.0;
   for (uint32_t k = threadIdx.x; k < P; k += kCtaThreads) l += red[2 * P + k];
@@ -991,12 +994,12 @@ void enqueue_iteration_twopass(admm_plan* p, cudaStream_t s, bool with_objective
       p->dgblocks.as<BlockDesc>(), (uint32_t)p->N, p->gN.U,
       p->gN.P, p->dparams.as<Params>());
   if (with_objective && !p->obj_pass) {  // trace[k-1].objective from this iteration's w = H c
-    objective_rec_kernel<<<dim3(p->ogx, M), kCtaThreads, 0, s>>>(row_vecs(p), p->dhs.as<double2>(),
-                                                                p->dblocks.as<BlockDesc>(), N, p->dored.as<double>(),
-                                                                p->dstate.as<IterState>(), 1);
-    objective_trace_kernel<<<1, kCtaThreads, 0, s>>>(p->dred.as<double>(), p->nz, p->dored.as<double>(), p->no,
-                                                     p->dparams.as<Params>(), p->dtrace.as<double>(), p->trace_cap,
-                                                     p->dstate.as<IterState>());
+    launch_pdl(objective_rec_kernel, dim3(p->orgx, M), dim3(kCtaThreads), 0, s, row_vecs(p), p->dhs.as<double2>(),
+               p->dblocks.as<BlockDesc>(), N, p->onp, p->drored.as<double>(), (const IterState*)p->dstate.as<IterState>(),
+               (uint64_t)1);
+    launch_pdl(objective_trace_kernel, dim3(1), dim3(kCtaThreads), 0, s, (const double*)p->dred.as<double>(), p->nz,
+               (const double*)p->drored.as<double>(), p->nor, (const Params*)p->dparams.as<Params>(),
+               p->dtrace.as<double>(), p->trace_cap, (const IterState*)p->dstate.as<IterState>());
   }
   mark(2);
   enqueue_kapply<S>(p, s, [&] { mark(3); });
@@ -1130,13 +1133,15 @@ void enqueue_iteration_sweep(admm_plan* p, cudaStream_t s, bool with_objective, 
              p->dstate.as<IterState>(), (double*)nullptr);
   mark(2);
   if (with_objective && !p->obj_pass)  // this iteration's a_b from the sweep's next w (no H pass)
-    objective_rec_kernel<<<dim3(p->ogx, (uint32_t)p->Mr), kCtaThreads, 0, s>>>(
-        row_vecs(p), p->dhs.as<double2>(), p->dblocks.as<BlockDesc>(), (uint32_t)p->Nc, p->dored.as<double>(),
-        p->dstate.as<IterState>(), 0);
+    launch_pdl(objective_rec_kernel, dim3(p->orgx, (uint32_t)p->Mr), dim3(kCtaThreads), 0, s, row_vecs(p),
+               p->dhs.as<double2>(), p->dblocks.as<BlockDesc>(), (uint32_t)p->Nc, p->onp, p->drored.as<double>(),
+               (const IterState*)p->dstate.as<IterState>(), (uint64_t)0);
   if (with_objective) {  // the sweep's finalize wrote NaN: fill the objective of this iteration
-    objective_trace_kernel<<<1, kCtaThreads, 0, s>>>(p->dred.as<double>(), (uint32_t)p->gS.P, p->dored.as<double>(),
-                                                     p->no, p->dparams.as<Params>(), p->dtrace.as<double>(),
-                                                     p->trace_cap, p->dstate.as<IterState>());
+    const bool rec = !p->obj_pass;
+    launch_pdl(objective_trace_kernel, dim3(1), dim3(kCtaThreads), 0, s, (const double*)p->dred.as<double>(),
+               (uint32_t)p->gS.P, (const double*)(rec ? p->drored.as<double>() : p->dored.as<double>()),
+               rec ? p->nor : p->no, (const Params*)p->dparams.as<Params>(), p->dtrace.as<double>(), p->trace_cap,
+               (const IterState*)p->dstate.as<IterState>());
   }
   enqueue_kapply<S>(p, s, [&] { mark(3); });
   mark(4);
@@ -1273,7 +1278,7 @@ void enqueue_bobjective_last(admm_plan* p, cudaStream_t s) {
 }
 
 template <typename S>
-void enqueue_iteration_batched(admm_plan* p, cudaStream_t s, std::vector<cudaEvent_t>* ev) {
+void enqueue_iteration_batched(admm_plan* p, cudaStream_t s, bool with_objective, std::vector<cudaEvent_t>* ev) {
   const uint32_t B = (uint32_t)p->batch, nb = (uint32_t)p->blocks.size();
   const uint64_t stride = p->mvec_total * B;
   const unsigned rgx = (unsigned)cdiv((uint64_t)p->max_rows * B, kCtaThreads);
@@ -1287,7 +1292,7 @@ void enqueue_iteration_batched(admm_plan* p, cudaStream_t s, std::vector<cudaEve
   brows_kernel<kRhs><<<dim3(rgx, nb), kCtaThreads, 0, s>>>(brow_vecs(p), p->dwpart.as<double2>(), stride, p->splitN,
                                                           p->dblocks.as<BlockDesc>(), (uint32_t)p->Nc, B,
                                                           p->dparams.as<Params>());
-  if (p->trace_obj) enqueue_bobjective(p, s);  // trace[k-1].objective per scene (w = H c of this iteration)
+  if (with_objective) enqueue_bobjective(p, s);  // trace[k-1].objective per scene (w = H c of this iteration)
   mark(2);
   bgemm_kernel<S, false><<<(unsigned)p->tK.size(), 256, bgemm_smem<S, false>(), s>>>(p->dK.as<S>(), p->dtK.as<BTile>(),
                                                                   p->dr.as<double2>(), p->dqpart.as<double2>(), B);
@@ -1313,9 +1318,9 @@ void enqueue_iteration_batched(admm_plan* p, cudaStream_t s, std::vector<cudaEve
 void enqueue_iteration_any(admm_plan* p, cudaStream_t s, bool obj, std::vector<cudaEvent_t>* ev) {
   if (p->batch > 1) {
     if (p->dtype == ADMM_C128)
-      enqueue_iteration_batched<double2>(p, s, ev);
+      enqueue_iteration_batched<double2>(p, s, obj, ev);
     else
-      enqueue_iteration_batched<float2>(p, s, ev);
+      enqueue_iteration_batched<float2>(p, s, obj, ev);
     return;
   }
   if (p->schedule == 2) {
@@ -1675,7 +1680,14 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
   p->dred.alloc((size_t)3 * std::max<uint64_t>(p->nz, p->gS.P) * sizeof(double));
   p->dored.alloc((size_t)std::max<uint32_t>(p->no, p->zgx * (uint32_t)p->Nc) * sizeof(double));
   if (const char* e = std::getenv("ADMM_B200_OBJ")) p->obj_pass = !std::strcmp(e, "pass");
-  if (p->trace_obj && !p->obj_pass) p->dhs.alloc(p->mvec_total * std::max<uint64_t>(1, p->batch) * sizeof(double2));
+  if (p->Nc > kCtaThreads) p->obj_pass = true;  // the recurrence kernel spreads at most 256 column blocks
+  if (p->trace_obj && !p->obj_pass) {
+    p->dhs.alloc(p->mvec_total * std::max<uint64_t>(1, p->batch) * sizeof(double2));
+    while ((1u << p->onp) < p->Nc) ++p->onp;
+    p->orgx = (uint32_t)std::max<uint64_t>(1, cdiv(p->max_rowblock, kCtaThreads >> p->onp));
+    p->nor = p->orgx * (uint32_t)p->Mr;
+    p->drored.alloc((size_t)p->nor * sizeof(double));
+  }
   ensure_trace(p.get(), std::max<uint64_t>(cfg.max_iters, 1));
 
   if (p->dtype == ADMM_C128) {
