@@ -84,7 +84,9 @@ typedef struct {
   int trace_objective; /* 1: objective every iteration (extra H pass, as the reference
                           does at solvers.hpp:146); 0: objective of the final iterate only */
   int schedule;        /* 0 auto, 1 two-pass (H streamed twice per iteration), 2 single-HBM-pass
-                          column-strip sweep; env ADMM_B200_SCHEDULE overrides */
+                          column-strip sweep, 4 resident (small problems: H in SMEM, one
+                          persistent kernel per launch); env ADMM_B200_SCHEDULE
+                          (twopass|sweep|resident) overrides */
   uint64_t batch;      /* 0/1: one scene; 2..64: independent scenes sharing H (BASELINE config 5):
                           g is n_meas x batch (scene fastest), solutions n_pix x batch, trace
                           iterations x batch x 3, lambda per scene via admm_plan_set_lambdas */
@@ -188,7 +190,7 @@ typedef struct {
   uint64_t grid_gemv_n, grid_gemv_h;
   double setup_seconds;         /* upload + Gram + inverse (host wall clock) */
   uint64_t inner_dim_max;       /* largest factored dimension */
-  uint64_t schedule;            /* 1 two-pass, 2 sweep */
+  uint64_t schedule;            /* 1 two-pass, 2 sweep, 3 batched scenes, 4 resident */
   uint64_t grid_sweep;
   uint64_t hbm_bytes_per_iter;  /* compulsory HBM bytes of the chosen schedule */
   uint64_t sweep_variant;       /* schedule 2 kernel: 1 L2 re-read sweep, 2 strip-major tile, 3 slab */

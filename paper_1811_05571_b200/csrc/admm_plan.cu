@@ -31,6 +31,7 @@
 #include "admm_slab.cuh"
 #include "admm_hemv.cuh"
 #include "admm_batched.cuh"
+#include "admm_resident.cuh"
 #include "admm_host.h"
 
 using namespace admm;
@@ -201,6 +202,12 @@ struct admm_plan {
   uint32_t zgx = 0, rgx = 0, rgx_s = 0, ogx = 0, nz = 0, no = 0;
   uint32_t orgx = 1, onp = 0, nor = 1;  // objective_rec_kernel: grid x, log2 lanes per row, partials
   DevBuf drored;
+  // resident schedule (4): per-CTA column ranges, w / residual / objective partials
+  DevBuf dres_dbg;
+  DevBuf dres_cta, dres_seg, dres_w, dres_red, dres_opart, dres_abuf, dres_lprev, dres_bar, dghat2;
+  uint32_t res_P = 0, res_cols = 0;
+  bool is_shard = false;  // created by admm_plan_create_sharded (driven phase by phase)
+  size_t res_smem = 0;
   uint64_t trace_cap = 0;
   cudaGraphExec_t exec = nullptr;
   uint64_t graph_iters = 0;
@@ -682,10 +689,159 @@ bool try_slab(admm_plan* p) {
   return true;
 }
 
+// Resident schedule (admm_resident.cuh): H of each CTA's columns kept in SMEM, one
+// persistent cooperative kernel per launch.  On request (schedule 4 / ADMM_B200_SCHEDULE=
+// resident) for small problems: single GPU, one scene, <= 8 replicas per segment, one
+// owner CTA per block, and the SMEM tile (H columns + the owner's K) must fit.
+template <typename S>
+bool try_resident(admm_plan* p, int requested) {
+  // opt-in: on config 1 it measured 45.5k it/s vs 46k for the sweep launch chain (two
+  // grid barriers + dependent L2 round trips per iteration)
+  if (requested != 4) return false;
+  if (p->batch > 1 || p->is_shard || p->Mr > (uint64_t)kResMaxM || p->Mr * p->Nc > (uint64_t)p->num_sms) return false;
+  const char* oe = std::getenv("ADMM_B200_OBJ");
+  if (oe && !std::strcmp(oe, "pass")) return false;
+  int coop = 0;
+  CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, p->device));
+  if (!coop) return false;
+  // CTAs per segment in proportion to its columns (at least one each).  Fewer, wider CTAs
+  // shorten phase B (the owners sum one w partial per CTA) and the grid barriers:
+  // at least kResMinCols columns per CTA.
+  uint64_t min_cols = 32;
+  if (const char* e = std::getenv("ADMM_B200_RES_COLS")) min_cols = std::max(1, std::atoi(e));
+  const uint64_t Pmax = std::max<uint64_t>(std::min<uint64_t>(p->num_sms, cdiv(p->n_pix, min_cols)),
+                                           p->blocks.size()),
+                 ncol = p->n_pix;
+  std::vector<uint32_t> pj(p->Nc);
+  uint64_t tot = 0;
+  for (uint64_t j = 0; j < p->Nc; ++j) {
+    pj[j] = (uint32_t)std::max<uint64_t>(1, (Pmax * p->blocks[j].cols) / std::max<uint64_t>(ncol, 1));
+    pj[j] = std::min<uint32_t>(pj[j], p->blocks[j].cols);
+    tot += pj[j];
+  }
+  while (tot > Pmax) {
+    auto it = std::max_element(pj.begin(), pj.end());
+    if (*it <= 1) return false;
+    --*it;
+    --tot;
+  }
+  std::vector<ResCta> ctas;
+  std::vector<uint32_t> seg(2 * p->Nc);
+  uint32_t maxc = 0;
+  for (uint64_t j = 0; j < p->Nc; ++j) {
+    const uint32_t lo = (uint32_t)ctas.size(), n = p->blocks[j].cols;
+    for (uint32_t c = 0; c < pj[j]; ++c) {
+      const uint32_t c0 = (uint32_t)((uint64_t)n * c / pj[j]), c1 = (uint32_t)((uint64_t)n * (c + 1) / pj[j]);
+      ctas.push_back(ResCta{(uint32_t)j, c0, c1 - c0, lo, lo + pj[j], 0});
+      maxc = std::max(maxc, c1 - c0);
+    }
+    seg[2 * j] = lo;
+    seg[2 * j + 1] = lo + pj[j];
+  }
+  if (maxc > (uint32_t)kResMaxCols || p->blocks.size() > ctas.size() || p->blocks.size() > (size_t)kResMaxBlocks)
+    return false;  // one owner CTA per block
+  const size_t smem = resident_smem<S>(maxc, (uint32_t)p->n_meas, (uint32_t)p->Mr, p->max_rows);
+  if (smem > 225 * 1024) return false;
+  CK(cudaFuncSetAttribute(resident_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, resident_kernel<S>, kCtaThreads, smem));
+  if (occ < 1) return false;
+  p->res_P = (uint32_t)ctas.size();
+  p->res_cols = maxc;
+  p->res_smem = smem;
+  upload_desc(p->dres_cta, ctas.data(), ctas.size() * sizeof(ResCta));
+  upload_desc(p->dres_seg, seg.data(), seg.size() * sizeof(uint32_t));
+  p->dres_w.alloc((size_t)p->res_P * p->n_meas * sizeof(double2));
+  p->dres_red.alloc((size_t)3 * p->res_P * sizeof(double));
+  p->dres_opart.alloc((size_t)p->res_P * sizeof(double));
+  p->dres_abuf.alloc(p->mvec_total * sizeof(double2));
+  p->dres_lprev.alloc(sizeof(double));
+  p->dres_bar.alloc(2 * sizeof(unsigned));
+  CK(cudaMemset(p->dres_bar.p, 0, 2 * sizeof(unsigned)));
+  p->dghat2.alloc(p->mvec_total * sizeof(double2));
+  return true;
+}
+
+template <typename S>
+void launch_resident(admm_plan* p, cudaStream_t s, uint32_t iters, bool prologue, bool obj) {
+  ResArgs a{};
+  a.H = p->dH.p;
+  a.K = p->dK.p;
+  a.hN = p->dhN.as<MatDesc>();
+  a.kN = p->dkN.as<MatDesc>();
+  a.blocks = p->dblocks.as<BlockDesc>();
+  a.ctas = p->dres_cta.as<ResCta>();
+  a.seg_cta = p->dres_seg.as<uint32_t>();
+  a.g = p->dg.as<double2>();
+  a.ghat[0] = p->ghat_ptr;
+  a.ghat[1] = p->dghat2.as<double2>();
+  a.gij = p->dgij.as<double2>();
+  a.r = p->dr.as<double2>();
+  a.q = p->dq.as<double2>();
+  a.cv = ColVecs{p->du.as<double2>(), p->ds.as<double2>(), p->dc.as<double2>(), p->dv.as<double2>(),
+                 p->dvprev.as<double2>()};
+  a.wpart = p->dres_w.as<double2>();
+  a.red = p->dres_red.as<double>();
+  a.opart = p->dres_opart.as<double>();
+  a.hs = p->dhs.as<double2>();
+  a.abuf = p->dres_abuf.as<double2>();
+  a.lprev = p->dres_lprev.as<double>();
+  a.prm = p->dparams.as<Params>();
+  a.trace = p->dtrace.as<double>();
+  a.trace_cap = p->trace_cap;
+  a.st = p->dstate.as<IterState>();
+  a.bar = p->dres_bar.as<unsigned>();
+  a.M = (uint32_t)p->Mr;
+  a.N = (uint32_t)p->Nc;
+  a.nb = (uint32_t)p->blocks.size();
+  a.n_meas = (uint32_t)p->n_meas;
+  a.max_cols = p->res_cols;
+  a.max_m = p->max_rows;
+  a.dbg = nullptr;
+  if (const char* tf = std::getenv("ADMM_B200_RES_TRACE")) {
+    if (!p->dres_dbg.p) {
+      p->dres_dbg.alloc((size_t)p->res_P * 16 * 10 * 8);
+      CK(cudaMemset(p->dres_dbg.p, 0, p->dres_dbg.bytes));
+    }
+    a.dbg = p->dres_dbg.as<unsigned long long>();
+    (void)tf;
+  }
+  a.iters = iters;
+  a.prologue = prologue ? 1u : 0u;
+  a.trace_obj = (obj && p->dhs.p) ? 1u : 0u;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p->res_P);
+  cfg.blockDim = dim3(kCtaThreads);
+  cfg.dynamicSmemBytes = p->res_smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident: the grid barriers cannot deadlock
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, resident_kernel<S>, a));
+}
+
+void launch_resident_any(admm_plan* p, cudaStream_t s, uint64_t iters, bool prologue, bool obj) {
+  do {
+    const uint32_t n = (uint32_t)std::min<uint64_t>(iters, 1u << 30);
+    if (p->dtype == ADMM_C128)
+      launch_resident<double2>(p, s, n, prologue, obj);
+    else
+      launch_resident<float2>(p, s, n, prologue, obj);
+    iters -= n;
+  } while (iters > 0 && !prologue);
+}
+
 template <typename S>
 void choose_schedule(admm_plan* p, int requested) {
   p->schedule = 1;
   if (requested == 1) return;
+  if (try_resident<S>(p, requested)) {
+    p->schedule = 4;
+    return;
+  }
+  if (requested == 4) throw Fail{ADMM_E_PARAMETER, "resident schedule not possible for this shape"};
   if (try_slab<S>(p) || try_tile<S, 128>(p) || try_tile<S, 64>(p)) {
     p->schedule = 2;
     return;
@@ -1316,6 +1472,12 @@ void enqueue_iteration_batched(admm_plan* p, cudaStream_t s, bool with_objective
 }
 
 void enqueue_iteration_any(admm_plan* p, cudaStream_t s, bool obj, std::vector<cudaEvent_t>* ev) {
+  if (p->schedule == 4) {
+    if (ev) CK(cudaEventRecord((*ev)[0], s));
+    launch_resident_any(p, s, 1, false, obj);
+    if (ev) CK(cudaEventRecord((*ev)[1], s));
+    return;
+  }
   if (p->batch > 1) {
     if (p->dtype == ADMM_C128)
       enqueue_iteration_batched<double2>(p, s, obj, ev);
@@ -1358,9 +1520,11 @@ void enqueue_objective(admm_plan* p, cudaStream_t s) {
   objective_rows_kernel<<<dim3(p->ogx, (unsigned)p->Mr), kCtaThreads, 0, s>>>(
       p->dg.as<double2>(), p->dopart.as<double2>(), p->dhNv.as<MatDesc>(), p->dblocks.as<BlockDesc>(),
       (uint32_t)p->Nc, p->gO.U, p->gO.P, p->dored.as<double>());
-  const uint32_t nred = p->schedule == 2 ? (uint32_t)p->gS.P : p->nz;  // l1 partials of the last update
-  objective_final_kernel<<<1, kCtaThreads, 0, s>>>(p->dred.as<double>(), nred, p->dored.as<double>(), p->no,
-                                                   p->dparams.as<Params>(), p->dobj.as<double>());
+  // l1 partials of the last column update ([3][n] layout: rp2, rd2, l1)
+  const uint32_t nred = p->schedule == 4 ? p->res_P : p->schedule == 2 ? (uint32_t)p->gS.P : p->nz;
+  const double* red = p->schedule == 4 ? p->dres_red.as<double>() : p->dred.as<double>();
+  objective_final_kernel<<<1, kCtaThreads, 0, s>>>(red, nred, p->dored.as<double>(), p->no, p->dparams.as<Params>(),
+                                                   p->dobj.as<double>());
   CK(cudaGetLastError());
 }
 
@@ -1431,6 +1595,7 @@ void reset_state(admm_plan* p) {
     else
       enqueue_sweep_prologue<float2>(p, s);
   }
+  if (p->schedule == 4) launch_resident_any(p, s, 0, true, false);
 }
 
 void ensure_trace(admm_plan* p, uint64_t iters) {
@@ -1465,6 +1630,10 @@ void ensure_graph(admm_plan* p) {
 }
 
 void enqueue_iters(admm_plan* p, uint64_t iters) {
+  if (p->schedule == 4) {  // one persistent launch for all of them
+    if (iters) launch_resident_any(p, p->stream, iters, false, p->trace_obj);
+    return;
+  }
   ensure_graph(p);
   uint64_t k = 0;
   for (; k + kGraphIters <= iters; k += kGraphIters) CK(cudaGraphLaunch(p->exec, p->stream));
@@ -1561,6 +1730,7 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
   p->stream = p->own_stream;
 
   // sharding: this plan owns row blocks [i0, i0+Mr) x column blocks [j0, j0+Nc)
+  p->is_shard = shard != nullptr;
   if (shard) {
     p->Pr = shard->Pr;
     p->Pc = shard->Pc;
@@ -1631,6 +1801,7 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
   if (const char* env = std::getenv("ADMM_B200_SCHEDULE")) {
     if (!std::strcmp(env, "twopass")) requested = 1;
     if (!std::strcmp(env, "sweep")) requested = 2;
+    if (!std::strcmp(env, "resident")) requested = 4;
   }
   if (skip_cfg_validation || o.batch > 1) requested = 1;  // helper plans / batched scenes
   if (p->dtype == ADMM_C128) {
@@ -1857,7 +2028,9 @@ admm_status admm_plan_set_stream(admm_plan* p, void* stream) {
   });
 }
 
-uint32_t admm_plan_kernel_count(const admm_plan* p) { return p && p->schedule == 2 ? 4 : 7; }
+uint32_t admm_plan_kernel_count(const admm_plan* p) {
+  return !p ? 7 : p->schedule == 4 ? 1 : p->schedule == 2 ? 4 : 7;
+}
 
 admm_status admm_plan_set_lambdas(admm_plan* p, const double* lambdas) {
   return run_guarded([&] {
@@ -1917,7 +2090,9 @@ admm_status admm_plan_profile(admm_plan* p, uint64_t iters, const char** names, 
     check_plan(p);
     const int nk = (int)admm_plan_kernel_count(p);
     const bool fused = p->kpacked && p->hemv_fuse;
-    const char* const* kn = p->schedule == 2   ? (fused ? kNamesSF : p->kpacked ? kNamesSP : kNamesS)
+    static const char* kNamesR[1] = {"resident(iteration)"};
+    const char* const* kn = p->schedule == 4   ? kNamesR
+                            : p->schedule == 2 ? (fused ? kNamesSF : p->kpacked ? kNamesSP : kNamesS)
                             : p->schedule == 3 ? kNamesB
                                                : (fused ? kNames2F : p->kpacked ? kNames2P : kNames2);
     std::vector<cudaEvent_t> ev(nk + 1);
@@ -1960,11 +2135,12 @@ admm_status admm_plan_get_info(const admm_plan* p, admm_plan_info* info) {
     r.k_bytes = kb;
     r.h_stream_bytes_per_iter = 2 * hb;
     r.bytes_per_iter = 2 * hb + kb_dense + vb;  // two-pass algorithmic bytes
-    r.launches_per_iter = p->schedule == 3 ? 7 : p->schedule == 2 ? (p->trace_obj ? (p->obj_pass ? 7 : 6) : 4) : (p->trace_obj ? 9 : 7);
+    // resident: ONE launch runs all the iterations of an enqueue (reported as 0 per iteration)
+    r.launches_per_iter = p->schedule == 4 ? 0 : p->schedule == 3 ? 7 : p->schedule == 2 ? (p->trace_obj ? (p->obj_pass ? 7 : 6) : 4) : (p->trace_obj ? 9 : 7);
     if (p->schedule != 3 && p->kpacked && p->hemv_fuse) r.launches_per_iter -= 1;  // finalize inside hemv
     r.schedule = (uint64_t)p->schedule;
     r.grid_sweep = p->gS.P;
-    r.hbm_bytes_per_iter = (p->schedule == 2 ? hb : 2 * hb) + kb + vb;
+    r.hbm_bytes_per_iter = (p->schedule == 4 ? 0 : p->schedule == 2 ? hb : 2 * hb) + kb + vb;
     r.sweep_variant = p->schedule != 2 ? 0 : p->slab_rpl ? 3 : p->tile_rb ? 2 : 1;
     r.slab_cluster = p->slab_rpl ? p->slab_C : 0;
     r.slab_row_bytes = p->slab_rpl ? p->slab_rb : 0;
@@ -2002,6 +2178,12 @@ admm_status admm_plan_read(admm_plan* p, int which, double* dst, uint64_t count)
       if (count < 3 * n) throw Fail{ADMM_E_DIMENSION, "destination too small"};
       CK(cudaMemcpyAsync(dst, p->dtrace.p, n * 3 * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
       CK(cudaStreamSynchronize(p->stream));
+    } else if (which == 9) {  // diagnostics: the resident kernel's clock64 trace (ADMM_B200_RES_TRACE)
+      if (p->dres_dbg.p) {
+        CK(cudaMemcpyAsync(dst, p->dres_dbg.p, std::min<uint64_t>(count * 8, p->dres_dbg.bytes),
+                           cudaMemcpyDeviceToHost, p->stream));
+        CK(cudaStreamSynchronize(p->stream));
+      }
     } else if (which == 4) {  // {iterations completed, first non-finite iteration or -1}
       if (count < 2) throw Fail{ADMM_E_DIMENSION, "destination too small"};
       const IterState st = read_state(p);

@@ -22,7 +22,7 @@ def solve(p, method, M, N, lam, iters, dtype, schedule):
         return plan.solve()
 
 
-@pytest.mark.parametrize("schedule", ["auto", "twopass"])
+@pytest.mark.parametrize("schedule", ["auto", "twopass", "resident"])
 @pytest.mark.parametrize("method,M,N", CASES)
 def test_objective_recurrence_matches_pass_and_oracle(method, M, N, schedule, monkeypatch):
     import paper_1811_05571_b200 as admm
@@ -31,14 +31,16 @@ def test_objective_recurrence_matches_pass_and_oracle(method, M, N, schedule, mo
     iters = 150
     rec = solve(p, method, M, N, lam, iters, "c128", schedule)
     monkeypatch.setenv("ADMM_B200_OBJ", "pass")
-    ps = solve(p, method, M, N, lam, iters, "c128", schedule)
+    ps = solve(p, method, M, N, lam, iters, "c128", "auto" if schedule == "resident" else schedule)
     ref = orc.solve(method if method != "reference" else "reference", p.h, p.g, M=M, N=N, lam=lam, iters=iters)
     assert ref["error"] == "none"
     o_rec, o_pass, o_ref = rec.trace.objective, ps.trace.objective, ref["trace"][:, 2]
     assert np.all(np.isfinite(o_rec))
     np.testing.assert_allclose(o_pass, o_ref, rtol=1e-10)
     np.testing.assert_allclose(o_rec, o_ref, rtol=1e-9)
-    assert rec.objective == ps.objective  # SolveReport.objective: one exact pass either way
+    # SolveReport.objective: one exact pass either way (ADMM_B200_OBJ=pass also moves small
+    # problems off the resident schedule, so the iterates may differ in the last bit)
+    assert abs(rec.objective - ps.objective) <= 1e-13 * abs(ps.objective)
 
 
 def test_objective_recurrence_c64_and_ragged():
