@@ -262,7 +262,10 @@ def bench_distributed(args, cfg):
     value = args.steps / (ms / 1000.0)
     # end to end: fresh iterates (reset), the measurement vector is already resident per
     # rank; a full solve of `iters` iterations + the solution gathered to every rank
+    from paper_1811_05571_b200 import _lib
+    g_pinned = torch.from_numpy(np.ascontiguousarray(problem.g).view(np.float64)).pin_memory()
     t0 = time.perf_counter()
+    _lib.lib.admm_plan_set_g(sh._h, g_pinned.data_ptr())  # the step's input from pinned host memory
     sh.reset()
     D.prime([sh], comm)
     graphed.run(iters)
@@ -296,7 +299,7 @@ def bench_distributed(args, cfg):
             "roofline": {"bound": "hbm", "kernel": "whole iteration", "achieved":
                          per_gpu_h * (1 if sh.schedule == "sweep" else 2) / (ms_per_step / 1000.0) / 1e9,
                          "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "traffic": None},
-            "e2e": {"value": e2e, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step":
+            "e2e": {"value": e2e, "unit": "iterations/s", "h2d_bytes_per_step": problem.g.nbytes, "d2h_bytes_per_step":
                     problem.h.shape[1] * 16,
                     "step": f"one full solve ({iters} iterations), solution all-gathered"},
             "gpu_launches": (6 if sh.schedule == "sweep" else 9) * args.steps,
@@ -312,7 +315,7 @@ def bench_ours(args, cfg):
     import paper_1811_05571_b200 as admm
 
     ws, rank, local = dist_env()
-    if ws > 1:
+    if ws > 1 or os.environ.get("BENCH_FORCE_DIST") == "1":  # (forced: exercise the sharded path at N=1)
         return bench_distributed(args, cfg)
     dev = local
     method, m, n, k, snr, seed, kind, M, N, lr, iters, dtype = cfg
