@@ -306,6 +306,14 @@ def bench_distributed(args, cfg):
             "clocks": clk.summary(),
         }
         line["roofline"]["frac"] = line["roofline"]["achieved"] / peak
+        # NVLink term of the exchanges: bytes each rank receives per iteration from its peers
+        # (all-gathers: (group - 1) / group of each buffer) against the nominal 900 GB/s per
+        # direction of NVLink 5; these exchanges are latency-, not bandwidth-bound
+        group = {0: Pc, 1: Pr, 2: Pr * Pc}
+        rx = sum(x_bytes[w] * (group[w] - 1) / group[w] for w in x_bytes)
+        line["nvlink"] = {"rx_bytes_per_iter_per_rank": rx, "achieved_gbs": rx / (ms_per_step / 1000.0) / 1e9,
+                          "peak_gbs": 900.0, "peak_kind": "nominal NVLink 5 per direction",
+                          "frac": rx / (ms_per_step / 1000.0) / 1e9 / 900.0}
         print(json.dumps(line))
     dist.destroy_process_group()
 
