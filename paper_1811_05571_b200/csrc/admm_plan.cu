@@ -185,6 +185,7 @@ struct admm_plan {
   std::vector<SlabDesc> slabs;
   DevBuf dHs, dslabs;       // slab-major copy of H, slab table
   bool kpacked = false;     // K applied from the packed Hermitian tiles (hemv_kernel)
+  bool h_evict_first = false;  // two-pass GEMVs stream H with L2 evict_first
   bool kkeep = false;       // ... with an L2 evict_last policy (ADMM_B200_KKEEP)
   int hemv_occ = 1;         // hemv_kernel CTAs per SM (1: register prefetch of the next tile)
   bool hemv_fuse = false;   // q / ghat finalized inside hemv_kernel (tile-row completion counters)
@@ -1142,8 +1143,11 @@ void enqueue_iteration_twopass(admm_plan* p, cudaStream_t s, bool with_objective
     if (ev) CK(cudaEventRecord((*ev)[k], s));
   };
   mark(0);
-  gemv_n_kernel<S, kVN, kEvictNormal><<<(unsigned)p->gN.P, kCtaThreads, 0, s>>>(
-      p->dH.as<S>(), p->dc.as<double2>(), p->dwpart.as<double2>(), p->dhN.as<MatDesc>(), nb, p->gN.U);
+  // H streams through L2 (evict_first) so the packed K, re-read every iteration, can stay
+  auto gn = p->h_evict_first ? gemv_n_kernel<S, kVN, kEvictFirst> : gemv_n_kernel<S, kVN, kEvictNormal>;
+  auto gh = p->h_evict_first ? gemv_h_kernel<S, kVH, kEvictFirst> : gemv_h_kernel<S, kVH, kEvictNormal>;
+  gn<<<(unsigned)p->gN.P, kCtaThreads, 0, s>>>(p->dH.as<S>(), p->dc.as<double2>(), p->dwpart.as<double2>(),
+                                               p->dhN.as<MatDesc>(), nb, p->gN.U);
   mark(1);
   rows_finalize_kernel<kRhs><<<dim3(p->rgx, nb), kCtaThreads, 0, s>>>(
       row_vecs(p), p->dwpart.as<double2>(), p->dhN.as<MatDesc>(), p->dblocks.as<BlockDesc>(),
@@ -1160,8 +1164,8 @@ void enqueue_iteration_twopass(admm_plan* p, cudaStream_t s, bool with_objective
   mark(2);
   enqueue_kapply<S>(p, s, [&] { mark(3); });
   mark(4);
-  gemv_h_kernel<S, kVH, kEvictNormal><<<(unsigned)p->gH.P, kCtaThreads, 0, s>>>(
-      p->dH.as<S>(), p->dq.as<double2>(), p->dzpart.as<double2>(), p->dhH.as<MatDesc>(), nb, p->gH.U);
+  gh<<<(unsigned)p->gH.P, kCtaThreads, 0, s>>>(p->dH.as<S>(), p->dq.as<double2>(), p->dzpart.as<double2>(),
+                                               p->dhH.as<MatDesc>(), nb, p->gH.U);
   mark(5);
   zupdate_kernel<CH><<<dim3(p->zgx, N), kCtaThreads, 0, s>>>(
       col_vecs(p), p->dzpart.as<double2>(), p->dhH.as<MatDesc>(), p->dblocks.as<BlockDesc>(), M, N, p->gH.U,
@@ -1833,6 +1837,10 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
     // iterations (config 2: K apply 19 -> 15 us)
     const char* e2 = std::getenv("ADMM_B200_KKEEP");
     p->kkeep = e2 ? e2[0] == '1' : (p->slab_rpl > 0 && p->k_elems * p->elem / 2 <= (96ull << 20));
+    // two-pass: H evict_first and the packed K evict_last when K fits next to the stream
+    const char* e3 = std::getenv("ADMM_B200_HFIRST");
+    p->h_evict_first = e3 ? e3[0] == '1' : (p->schedule == 1 && p->k_elems * p->elem / 2 <= (96ull << 20));
+    if (p->schedule == 1 && p->h_evict_first && !e2) p->kkeep = true;
   }
   p->scal_ptr = p->fused_scal ? reinterpret_cast<double*>(p->ghat_ptr + p->Mr * p->Nc * p->mpad)
                               : p->dscal.as<double>();
