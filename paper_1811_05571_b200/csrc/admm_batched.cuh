@@ -30,6 +30,8 @@ struct BTile {
   uint32_t ld, rows, cols;
   uint32_t t0;      // first output row (N) / column (adjoint)
   uint32_t k0, k1;  // k range of this unit (split-K)
+  uint32_t s0;      // first scene of this unit (scene tiles of SB)
+  uint32_t pad_;
 };
 
 // out[t0 + i][b] = sum_{k in [k0,k1)} op(A)[t0 + i][k] X[k][b]
@@ -37,24 +39,27 @@ struct BTile {
 //   ADJ = true:  op(A)[i][k] = conj(A[k][i])    (Z = H^H Q)
 // A (storage precision) and X are staged by cp.async into double-buffered SMEM in the
 // layout their global rows arrive in (no transposing stores); A is widened at read time.
-template <typename S, bool ADJ>
-__global__ void __launch_bounds__(256, 2)
+// SB scenes per CTA tile: 64 (4 x 4 complex per thread, 2 CTAs/SM) or 32 (4 x 2, 3 CTAs/SM:
+// more warps to keep the FP64 pipe fed, A staged twice as often).
+template <typename S, bool ADJ, int SB>
+__global__ void __launch_bounds__(256, SB == 64 ? 2 : 3)
 bgemm_kernel(const S* __restrict__ A, const BTile* __restrict__ tiles, const double2* __restrict__ X,
              double2* __restrict__ out, uint32_t B) {
+  constexpr int NW = SB / 16;  // scenes per thread
   constexpr int AR = ADJ ? kBK : kBT;      // As[2][AR][AC + 1]
   constexpr int AC = ADJ ? kBT : kBK;
   extern __shared__ __align__(16) unsigned char bsm[];
   S* As = reinterpret_cast<S*>(bsm);                                           // 2 x AR x (AC+1)
   constexpr size_t kAsBytes = (2 * AR * (AC + 1) * sizeof(S) + 15) & ~(size_t)15;
-  double2* Xs = reinterpret_cast<double2*>(bsm + kAsBytes);  // 2 x kBK x (kBB+1)
-  double2* Ad = Xs + 2 * kBK * (kBB + 1);                     // AR x (AC+1) FP64 (complex64 only)
+  double2* Xs = reinterpret_cast<double2*>(bsm + kAsBytes);  // 2 x kBK x (SB+1)
+  double2* Ad = Xs + 2 * kBK * (SB + 1);                      // AR x (AC+1) FP64 (complex64 only)
   const BTile t = tiles[blockIdx.x];
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
   const S* a = A + t.a_off;
   const uint32_t nout = ADJ ? t.cols : t.rows;
   auto stage = [&](int buf, uint32_t k0) {
     S* as = As + (size_t)buf * AR * (AC + 1);
-    double2* xs = Xs + (size_t)buf * kBK * (kBB + 1);
+    double2* xs = Xs + (size_t)buf * kBK * (SB + 1);
     for (int e = threadIdx.x; e < kBT * kBK; e += 256) {
       const int r = e / AC, c = e % AC;  // consecutive threads -> consecutive global and SMEM
       const uint32_t oi = t.t0 + (ADJ ? c : r), k = k0 + (ADJ ? r : c);
@@ -65,19 +70,19 @@ bgemm_kernel(const S* __restrict__ A, const BTile* __restrict__ tiles, const dou
       else
         cpa8(as + r * (AC + 1) + c, src, ok);
     }
-    for (int e = threadIdx.x; e < kBK * kBB; e += 256) {
-      const int kk = e / kBB, b = e % kBB;
+    for (int e = threadIdx.x; e < kBK * SB; e += 256) {
+      const int kk = e / SB, b = e % SB;
       const uint32_t k = k0 + kk;
-      const bool ok = k < t.k1 && (uint32_t)b < B;
-      cpa(xs + kk * (kBB + 1) + b, ok ? X + t.x_off + (uint64_t)k * B + b : X, ok);
+      const bool ok = k < t.k1 && t.s0 + b < B;
+      cpa(xs + kk * (SB + 1) + b, ok ? X + t.x_off + (uint64_t)k * B + t.s0 + b : X, ok);
     }
     cpa_commit();
   };
-  double2 acc[4][4];
+  double2 acc[4][NW];
 #pragma unroll
   for (int q = 0; q < 4; ++q)
 #pragma unroll
-    for (int w = 0; w < 4; ++w) acc[q][w] = make_double2(0.0, 0.0);
+    for (int w = 0; w < NW; ++w) acc[q][w] = make_double2(0.0, 0.0);
   int buf = 0;
   stage(0, t.k0);
   for (uint32_t k0 = t.k0; k0 < t.k1; k0 += kBK) {
@@ -89,7 +94,7 @@ bgemm_kernel(const S* __restrict__ A, const BTile* __restrict__ tiles, const dou
     }
     __syncthreads();
     const S* as = As + (size_t)buf * AR * (AC + 1);
-    const double2* xs = Xs + (size_t)buf * kBK * (kBB + 1);
+    const double2* xs = Xs + (size_t)buf * kBK * (SB + 1);
     const double2* ad = nullptr;  // complex64: the chunk widened once (not once per reader)
     if constexpr (sizeof(S) == 8) {
       for (int e = threadIdx.x; e < AR * (AC + 1); e += 256) Ad[e] = Store<S>::widen(as[e]);
@@ -98,7 +103,7 @@ bgemm_kernel(const S* __restrict__ A, const BTile* __restrict__ tiles, const dou
     }
 #pragma unroll kBUnroll<ADJ>
     for (int kk = 0; kk < kBK; ++kk) {
-      double2 av[4], xv[4];
+      double2 av[4], xv[NW];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int i = ty + 16 * q;
@@ -107,12 +112,13 @@ bgemm_kernel(const S* __restrict__ A, const BTile* __restrict__ tiles, const dou
           av[q] = ad[o];
         else
           av[q] = Store<S>::widen(as[o]);
-        xv[q] = xs[kk * (kBB + 1) + tx + 16 * q];
       }
+#pragma unroll
+      for (int w = 0; w < NW; ++w) xv[w] = xs[kk * (SB + 1) + tx + 16 * w];
 #pragma unroll
       for (int q = 0; q < 4; ++q)
 #pragma unroll
-        for (int w = 0; w < 4; ++w) {
+        for (int w = 0; w < NW; ++w) {
           if (ADJ)
             cmac_conj(acc[q][w], av[q], xv[w]);
           else
@@ -127,18 +133,18 @@ bgemm_kernel(const S* __restrict__ A, const BTile* __restrict__ tiles, const dou
     const uint32_t oi = t.t0 + ty + 16 * q;
     if (oi >= nout) continue;
 #pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const uint32_t b = tx + 16 * w;
+    for (int w = 0; w < NW; ++w) {
+      const uint32_t b = t.s0 + tx + 16 * w;
       if (b < B) out[t.o_off + (uint64_t)oi * B + b] = acc[q][w];
     }
   }
 }
 
-template <typename S, bool ADJ>
+template <typename S, bool ADJ, int SB>
 constexpr size_t bgemm_smem() {
   constexpr int AR = ADJ ? kBK : kBT;
   constexpr int AC = ADJ ? kBT : kBK;
-  return ((2 * AR * (AC + 1) * sizeof(S) + 15) & ~(size_t)15) + 2 * kBK * (kBB + 1) * sizeof(double2) +
+  return ((2 * AR * (AC + 1) * sizeof(S) + 15) & ~(size_t)15) + 2 * kBK * (SB + 1) * sizeof(double2) +
          (sizeof(S) == 8 ? AR * (AC + 1) * sizeof(double2) : 0);
 }
 

@@ -171,6 +171,7 @@ struct admm_plan {
   DevBuf dtN, dtK, dtH, dtG, dz, dkappa, dbred, dblam, dbored;  // dblam: lambda_b; dbored: objective partials
   uint32_t bogx = 1;  // bobjective_rec_kernel grid x
   uint32_t splitN = 1, splitK = 1, splitH = 1, pz = 1;
+  uint32_t bsb = 64;  // scenes per bgemm CTA tile (64 or 32)
   std::vector<double> lambdas;
   // sweep schedule (admm_sweep.cuh)
   int schedule = 1;             // 1 two-pass, 2 single-HBM-pass sweep
@@ -1311,10 +1312,24 @@ void enqueue_iteration_sweep(admm_plan* p, cudaStream_t s, bool with_objective, 
 // ---- batched scenes (config 5) ----------------------------------------------------
 template <typename S>
 void bgemm_attrs() {
-  CK(cudaFuncSetAttribute(bgemm_kernel<S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)bgemm_smem<S, false>()));
-  CK(cudaFuncSetAttribute(bgemm_kernel<S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)bgemm_smem<S, true>()));
+  CK(cudaFuncSetAttribute(bgemm_kernel<S, false, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)bgemm_smem<S, false, 64>()));
+  CK(cudaFuncSetAttribute(bgemm_kernel<S, true, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)bgemm_smem<S, true, 64>()));
+  CK(cudaFuncSetAttribute(bgemm_kernel<S, false, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)bgemm_smem<S, false, 32>()));
+  CK(cudaFuncSetAttribute(bgemm_kernel<S, true, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)bgemm_smem<S, true, 32>()));
+}
+
+// One skinny GEMM launch over a tile list, in the plan's scene-tile width.
+template <typename S, bool ADJ>
+void launch_bgemm(const admm_plan* p, cudaStream_t s, size_t ntiles, const S* A, const BTile* tiles,
+                  const double2* X, double2* out, uint32_t B) {
+  if (p->bsb == 32)
+    bgemm_kernel<S, ADJ, 32><<<(unsigned)ntiles, 256, bgemm_smem<S, ADJ, 32>(), s>>>(A, tiles, X, out, B);
+  else
+    bgemm_kernel<S, ADJ, 64><<<(unsigned)ntiles, 256, bgemm_smem<S, ADJ, 64>(), s>>>(A, tiles, X, out, B);
 }
 
 // Split-K count s in [1, smax] (and at most kmax) whose tiles*s work units fill the
@@ -1345,10 +1360,17 @@ void build_batched(admm_plan* p) {
   // per SM): config 5 has 192 row tiles (x3 -> 1.95 waves) and 1024 column tiles
   // (x2 -> 6.9 waves) instead of 2.6 / 3.5 waves
   int occ = 0;
+  p->bsb = 64;
+  if (const char* e = std::getenv("ADMM_B200_BSB")) p->bsb = std::atoi(e) == 32 ? 32 : 64;
   if (p->dtype == ADMM_C128)
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bgemm_kernel<double2, false>, 256, bgemm_smem<double2, false>()));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, p->bsb == 32 ? bgemm_kernel<double2, false, 32> : bgemm_kernel<double2, false, 64>, 256,
+                                                     p->bsb == 32 ? bgemm_smem<double2, false, 32>() : bgemm_smem<double2, false, 64>()));
   else
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bgemm_kernel<float2, false>, 256, bgemm_smem<float2, false>()));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, p->bsb == 32 ? bgemm_kernel<float2, false, 32> : bgemm_kernel<float2, false, 64>, 256,
+                                                     p->bsb == 32 ? bgemm_smem<float2, false, 32>() : bgemm_smem<float2, false, 64>()));
+  const uint64_t nsc = cdiv(B, (uint64_t)p->bsb);  // scene tiles
+  rtiles *= nsc;
+  ctiles *= nsc;
   const uint64_t slots = (uint64_t)std::max(1, occ) * p->num_sms;
   p->splitN = wave_split(rtiles, slots, 16, p->max_seg / (4 * kBK));
   p->splitK = wave_split(rtiles, slots, 16, p->max_rows / (4 * kBK));
@@ -1363,34 +1385,33 @@ void build_batched(admm_plan* p) {
   p->tK.clear();
   p->tH.clear();
   p->tG.clear();
-  for (uint64_t b = 0; b < nb; ++b) {
-    const BlockDesc& bd = p->blocks[b];
-    const MatDesc& hn = p->hN[b];
-    const MatDesc& kn = p->kN[b];
-    const uint32_t kcN = (uint32_t)round_up(cdiv(bd.cols, p->splitN), kBK);
-    const uint32_t kcK = (uint32_t)round_up(cdiv(bd.rows, p->splitK), kBK);
-    for (uint32_t t0 = 0; t0 < bd.rows; t0 += kBT)
-      for (uint32_t sp = 0; sp < p->splitN; ++sp) {
-        BTile t{hn.a_off, (uint64_t)bd.vec_off * B, sp * stride + (uint64_t)bd.mvec_off * B, hn.ld, bd.rows,
-                bd.cols, t0, std::min(bd.cols, sp * kcN), std::min(bd.cols, (sp + 1) * kcN)};
-        p->tN.push_back(t);
-      }
-    for (uint32_t t0 = 0; t0 < bd.rows; t0 += kBT)
-      for (uint32_t sp = 0; sp < p->splitK; ++sp) {
-        BTile t{kn.a_off, (uint64_t)bd.mvec_off * B, sp * stride + (uint64_t)bd.mvec_off * B, kn.ld, bd.rows,
-                bd.rows, t0, std::min(bd.rows, sp * kcK), std::min(bd.rows, (sp + 1) * kcK)};
-        p->tK.push_back(t);
-      }
-    const uint32_t kcH = (uint32_t)round_up(cdiv(bd.rows, p->splitH), kBK);
-    for (uint32_t t0 = 0; t0 < bd.cols; t0 += kBT)
-      for (uint32_t sp = 0; sp < p->splitH; ++sp)
-        p->tH.push_back(BTile{hn.a_off, (uint64_t)bd.mvec_off * B, sp * zstride + (uint64_t)bd.vec_off * B, hn.ld,
-                              bd.rows, bd.cols, t0, std::min(bd.rows, sp * kcH), std::min(bd.rows, (sp + 1) * kcH)});
-    for (uint32_t t0 = 0; t0 < bd.cols; t0 += kBT) {
-      p->tG.push_back(BTile{hn.a_off, (uint64_t)bd.row0 * B, (uint64_t)bd.vec_off * B, hn.ld, bd.rows, bd.cols, t0,
-                            0, bd.rows});
+  for (uint32_t s0 = 0; s0 < B; s0 += p->bsb)  // scene tiles outermost: a wave streams each A tile once per scene tile
+    for (uint64_t b = 0; b < nb; ++b) {
+      const BlockDesc& bd = p->blocks[b];
+      const MatDesc& hn = p->hN[b];
+      const MatDesc& kn = p->kN[b];
+      const uint32_t kcN = (uint32_t)round_up(cdiv(bd.cols, p->splitN), kBK);
+      const uint32_t kcK = (uint32_t)round_up(cdiv(bd.rows, p->splitK), kBK);
+      for (uint32_t t0 = 0; t0 < bd.rows; t0 += kBT)
+        for (uint32_t sp = 0; sp < p->splitN; ++sp)
+          p->tN.push_back(BTile{hn.a_off, (uint64_t)bd.vec_off * B, sp * stride + (uint64_t)bd.mvec_off * B, hn.ld,
+                                bd.rows, bd.cols, t0, std::min(bd.cols, sp * kcN), std::min(bd.cols, (sp + 1) * kcN),
+                                s0, 0});
+      for (uint32_t t0 = 0; t0 < bd.rows; t0 += kBT)
+        for (uint32_t sp = 0; sp < p->splitK; ++sp)
+          p->tK.push_back(BTile{kn.a_off, (uint64_t)bd.mvec_off * B, sp * stride + (uint64_t)bd.mvec_off * B, kn.ld,
+                                bd.rows, bd.rows, t0, std::min(bd.rows, sp * kcK), std::min(bd.rows, (sp + 1) * kcK),
+                                s0, 0});
+      const uint32_t kcH = (uint32_t)round_up(cdiv(bd.rows, p->splitH), kBK);
+      for (uint32_t t0 = 0; t0 < bd.cols; t0 += kBT)
+        for (uint32_t sp = 0; sp < p->splitH; ++sp)
+          p->tH.push_back(BTile{hn.a_off, (uint64_t)bd.mvec_off * B, sp * zstride + (uint64_t)bd.vec_off * B, hn.ld,
+                                bd.rows, bd.cols, t0, std::min(bd.rows, sp * kcH), std::min(bd.rows, (sp + 1) * kcH),
+                                s0, 0});
+      for (uint32_t t0 = 0; t0 < bd.cols; t0 += kBT)
+        p->tG.push_back(BTile{hn.a_off, (uint64_t)bd.row0 * B, (uint64_t)bd.vec_off * B, hn.ld, bd.rows, bd.cols, t0,
+                              0, bd.rows, s0, 0});
     }
-  }
   upload_desc(p->dtN, p->tN.data(), p->tN.size() * sizeof(BTile));
   upload_desc(p->dtK, p->tK.data(), p->tK.size() * sizeof(BTile));
   upload_desc(p->dtH, p->tH.data(), p->tH.size() * sizeof(BTile));
@@ -1428,7 +1449,7 @@ void enqueue_bobjective_last(admm_plan* p, cudaStream_t s) {
   const uint32_t B = (uint32_t)p->batch, nb = (uint32_t)p->blocks.size();
   const uint64_t stride = p->mvec_total * B;
   const unsigned rgx = (unsigned)cdiv((uint64_t)p->max_rows * B, kCtaThreads);
-  bgemm_kernel<S, false><<<(unsigned)p->tN.size(), 256, bgemm_smem<S, false>(), s>>>(p->dH.as<S>(), p->dtN.as<BTile>(),
+  launch_bgemm<S, false>(p, s, p->tN.size(), p->dH.as<S>(), p->dtN.as<BTile>(),
                                                                   p->dc.as<double2>(), p->dwpart.as<double2>(), B);
   brows_kernel<kRhs><<<dim3(rgx, nb), kCtaThreads, 0, s>>>(brow_vecs(p), p->dwpart.as<double2>(), stride, p->splitN,
                                                           p->dblocks.as<BlockDesc>(), (uint32_t)p->Nc, B,
@@ -1446,7 +1467,7 @@ void enqueue_iteration_batched(admm_plan* p, cudaStream_t s, bool with_objective
     if (ev) CK(cudaEventRecord((*ev)[k], s));
   };
   mark(0);
-  bgemm_kernel<S, false><<<(unsigned)p->tN.size(), 256, bgemm_smem<S, false>(), s>>>(p->dH.as<S>(), p->dtN.as<BTile>(),
+  launch_bgemm<S, false>(p, s, p->tN.size(), p->dH.as<S>(), p->dtN.as<BTile>(),
                                                                   p->dc.as<double2>(), p->dwpart.as<double2>(), B);
   mark(1);
   brows_kernel<kRhs><<<dim3(rgx, nb), kCtaThreads, 0, s>>>(brow_vecs(p), p->dwpart.as<double2>(), stride, p->splitN,
@@ -1454,14 +1475,14 @@ void enqueue_iteration_batched(admm_plan* p, cudaStream_t s, bool with_objective
                                                           p->dparams.as<Params>());
   if (with_objective) enqueue_bobjective(p, s);  // trace[k-1].objective per scene (w = H c of this iteration)
   mark(2);
-  bgemm_kernel<S, false><<<(unsigned)p->tK.size(), 256, bgemm_smem<S, false>(), s>>>(p->dK.as<S>(), p->dtK.as<BTile>(),
+  launch_bgemm<S, false>(p, s, p->tK.size(), p->dK.as<S>(), p->dtK.as<BTile>(),
                                                                   p->dr.as<double2>(), p->dqpart.as<double2>(), B);
   mark(3);
   brows_kernel<kQ><<<dim3(rgx, nb), kCtaThreads, 0, s>>>(brow_vecs(p), p->dqpart.as<double2>(), stride, p->splitK,
                                                         p->dblocks.as<BlockDesc>(), (uint32_t)p->Nc, B,
                                                         p->dparams.as<Params>());
   mark(4);
-  bgemm_kernel<S, true><<<(unsigned)p->tH.size(), 256, bgemm_smem<S, true>(), s>>>(p->dH.as<S>(), p->dtH.as<BTile>(), p->dq.as<double2>(),
+  launch_bgemm<S, true>(p, s, p->tH.size(), p->dH.as<S>(), p->dtH.as<BTile>(), p->dq.as<double2>(),
                                                                  p->dz.as<double2>(), B);
   mark(5);
   bzupdate_kernel<<<p->pz, kCtaThreads, 0, s>>>(col_vecs(p), p->dz.as<double2>(), p->splitH, p->vec_total * B,
@@ -2058,10 +2079,10 @@ admm_status admm_plan_max_abs_adjoint_batched(admm_plan* p, double* out) {
     if (p->batch < 2) throw Fail{ADMM_E_STATE, "not a batched plan"};
     const uint32_t B = (uint32_t)p->batch;
     if (p->dtype == ADMM_C128)
-      bgemm_kernel<double2, true><<<(unsigned)p->tG.size(), 256, bgemm_smem<double2, true>(), p->stream>>>(
+      launch_bgemm<double2, true>(p, p->stream, p->tG.size(),
           p->dH.as<double2>(), p->dtG.as<BTile>(), p->dg.as<double2>(), p->dz.as<double2>(), B);
     else
-      bgemm_kernel<float2, true><<<(unsigned)p->tG.size(), 256, bgemm_smem<float2, true>(), p->stream>>>(
+      launch_bgemm<float2, true>(p, p->stream, p->tG.size(),
           p->dH.as<float2>(), p->dtG.as<BTile>(), p->dg.as<double2>(), p->dz.as<double2>(), B);
     const unsigned gx = p->pz;
     DevBuf res;
