@@ -82,3 +82,27 @@ def test_config4_scaled_vs_oracle():
     ref128 = orc.solve("consensus", p128.h, p128.g, M=8, lam=lam, iters=iters)
     assert rel(r.solution, ref128["solution"]) <= 1e-4
     assert np.array_equal(support(r.solution), support(ref128["solution"]))
+
+
+def test_cmat_input_pipeline_to_c64_plan(tmp_path):
+    """Input pipeline: a reference-format (CMX1, FP64) H file read straight into
+    complex64 plan storage, and the same H written/read as the half-size CMF1 variant, give
+    the same c64 plan and solution as rounding the in-memory matrix."""
+    import paper_1811_05571_b200 as admm
+    p = admm.gen_problem(128, 1024, 8, 30.0, 31)
+    admm.write_cmat(tmp_path / "H.cmat", p.h)
+    admm.write_cvec(tmp_path / "g.cmat", p.g)
+    h64 = admm.read_cmat(tmp_path / "H.cmat", dtype="c64")
+    admm.write_cmat(tmp_path / "H64.cmat", h64, dtype="c64")
+    assert (tmp_path / "H64.cmat").stat().st_size == 20 + 128 * 1024 * 8
+    h64b = admm.read_cmat(tmp_path / "H64.cmat", dtype="c64")
+    assert np.array_equal(h64, p.h.astype(np.complex64)) and np.array_equal(h64b, h64)
+    g = admm.read_cvec(tmp_path / "g.cmat")
+    lam = 0.05 * float(np.max(np.abs(h64.astype(np.complex128).conj().T @ g)))
+    cfg = admm.SolverConfig(rho=1.0, lambda_=lam, max_iters=80)
+    r1 = admm.hybrid_solve(admm.SensingProblem(h64b, g), cfg, 2, 4, admm.SolveOptions(dtype="c64"))
+    r2 = admm.hybrid_solve(admm.SensingProblem(p.h.astype(np.complex64), p.g), cfg, 2, 4, admm.SolveOptions(dtype="c64"))
+    assert np.array_equal(r1.solution, r2.solution)
+    ref = orc.solve("hybrid", h64.astype(np.complex128), g, M=2, N=4, lam=lam, iters=80)
+    assert rel(r1.solution, ref["solution"]) <= 1e-4
+    assert np.array_equal(support(r1.solution), support(ref["solution"]))
