@@ -47,6 +47,10 @@ def describe(cfg):
     if kind == "cra":
         return (f"{method} ADMM {dtype} CRA-like H {m}x{n} (24 tx x 128 freq, 32^3 voxels), {k}-voxel "
                 f"planar patch, {snr:g} dB seed {seed}, {grid}, rho=1, lambda={lr}*max|H^H g|, {iters} iterations")
+    if kind == "cra_batch":
+        return (f"{method} ADMM {dtype} CRA-like H {m}x{n} (config 3's generator and seed), {k} scenes of "
+                f"100-400 planar-patch voxels, {snr:g} dB seed {seed}, {grid}, rho=1, "
+                f"lambda_b={lr}*max|H^H g_b| per scene, {iters} iterations")
     return (f"{method} ADMM {dtype} H {m}x{n} CN(0,1/{m}) {k}-sparse {snr:g} dB seed {seed}, "
             f"{grid}, rho=1, lambda={lr}*max|H^H g|, {iters} iterations")
 
