@@ -60,7 +60,10 @@ bgemm_kernel(const S* __restrict__ A, const BTile* __restrict__ tiles, const dou
   auto stage = [&](int buf, uint32_t k0) {
     S* as = As + (size_t)buf * AR * (AC + 1);
     double2* xs = Xs + (size_t)buf * kBK * (SB + 1);
-    for (int e = threadIdx.x; e < kBT * kBK; e += 256) {
+    // fixed trip counts, unrolled: the index math folds to per-thread constants
+#pragma unroll
+    for (int it = 0; it < kBT * kBK / 256; ++it) {
+      const int e = (int)threadIdx.x + 256 * it;
       const int r = e / AC, c = e % AC;  // consecutive threads -> consecutive global and SMEM
       const uint32_t oi = t.t0 + (ADJ ? c : r), k = k0 + (ADJ ? r : c);
       const bool ok = oi < nout && k < t.k1;
@@ -70,7 +73,9 @@ bgemm_kernel(const S* __restrict__ A, const BTile* __restrict__ tiles, const dou
       else
         cpa8(as + r * (AC + 1) + c, src, ok);
     }
-    for (int e = threadIdx.x; e < kBK * SB; e += 256) {
+#pragma unroll
+    for (int it = 0; it < kBK * SB / 256; ++it) {
+      const int e = (int)threadIdx.x + 256 * it;
       const int kk = e / SB, b = e % SB;
       const uint32_t k = k0 + kk;
       const bool ok = k < t.k1 && t.s0 + b < B;
@@ -97,7 +102,12 @@ bgemm_kernel(const S* __restrict__ A, const BTile* __restrict__ tiles, const dou
     const double2* xs = Xs + (size_t)buf * kBK * (SB + 1);
     const double2* ad = nullptr;  // complex64: the chunk widened once (not once per reader)
     if constexpr (sizeof(S) == 8) {
-      for (int e = threadIdx.x; e < AR * (AC + 1); e += 256) Ad[e] = Store<S>::widen(as[e]);
+#pragma unroll
+      for (int it = 0; it < AR * AC / 256; ++it) {  // the pad column is never read
+        const int e = (int)threadIdx.x + 256 * it;
+        const int o = e / AC * (AC + 1) + e % AC;
+        Ad[o] = Store<S>::widen(as[o]);
+      }
       __syncthreads();
       ad = Ad;
     }
