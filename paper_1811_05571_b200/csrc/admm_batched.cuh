@@ -257,17 +257,36 @@ bzupdate_kernel(ColVecs cv, const double2* __restrict__ z, uint32_t zsplit, uint
 }
 
 // Per scene: fixed-order sums over the CTAs -> trace[k][scene] = (r_p, r_d, NaN).
-__global__ void bfinalize_kernel(const double* __restrict__ red, uint32_t nct, uint32_t B,
-                                 const Params* __restrict__ prm, double* __restrict__ trace, uint64_t trace_cap,
-                                 IterState* st) {
-  const uint32_t sc = threadIdx.x;
+// kBFinParts thread groups per scene each sum a strided subset of the CTA partials
+// (loads independent, 4 in flight per thread), then the parts are added in order:
+// a fixed association, so the trace is deterministic.  Launch: kBB * kBFinParts threads.
+constexpr int kBFinParts = 16;
+__device__ __forceinline__ double bfin_part_sum(const double* __restrict__ red, uint64_t base, uint32_t n,
+                                                uint32_t part, uint32_t sc) {
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  uint32_t c = part;
+  for (; c + 3 * kBFinParts < n; c += 4 * kBFinParts) {
+    a0 += red[(base + c) * kBB + sc];
+    a1 += red[(base + c + kBFinParts) * kBB + sc];
+    a2 += red[(base + c + 2 * kBFinParts) * kBB + sc];
+    a3 += red[(base + c + 3 * kBFinParts) * kBB + sc];
+  }
+  for (; c < n; c += kBFinParts) a0 += red[(base + c) * kBB + sc];
+  return (a0 + a1) + (a2 + a3);
+}
+
+__global__ void __launch_bounds__(kBB * kBFinParts)
+bfinalize_kernel(const double* __restrict__ red, uint32_t nct, uint32_t B, const Params* __restrict__ prm,
+                 double* __restrict__ trace, uint64_t trace_cap, IterState* st) {
+  __shared__ double sp[2][kBFinParts][kBB];
+  const uint32_t sc = threadIdx.x % kBB, part = threadIdx.x / kBB;
   const uint64_t k = st->iter;
-  if (sc < B && k < trace_cap) {
-    double a = 0.0, d = 0.0;
-    for (uint32_t c = 0; c < nct; ++c) {
-      a += red[(uint64_t)c * kBB + sc];
-      d += red[((uint64_t)nct + c) * kBB + sc];
-    }
+  sp[0][part][sc] = bfin_part_sum(red, 0, nct, part, sc);
+  sp[1][part][sc] = bfin_part_sum(red, nct, nct, part, sc);
+  __syncthreads();
+  if (part == 0 && sc < B && k < trace_cap) {
+    double a = sp[0][0][sc], d = sp[1][0][sc];
+    for (int q = 1; q < kBFinParts; ++q) a += sp[0][q][sc], d += sp[1][q][sc];
     double* tr = trace + (k * B + sc) * 3;
     tr[0] = sqrt(a);
     tr[1] = sqrt(prm->rho * prm->rho * prm->m_rep * d);
@@ -318,16 +337,22 @@ bobjective_rec_kernel(BRowVecs rv, double2* __restrict__ hs, const BlockDesc* __
 
 // trace[iter - 1][scene].objective = 0.5 sum |Hv - g|^2 + lambda_b ||v_b||_1 (the l1
 // partials of bzupdate, red[2][pz][64]); one thread per scene, fixed order.
-__global__ void bobjective_trace_kernel(const double* __restrict__ red, uint32_t pz, const double* __restrict__ ored,
-                                        uint32_t no, const double* __restrict__ lam, uint32_t B,
-                                        double* __restrict__ trace, uint64_t trace_cap, const IterState* st) {
-  const uint32_t sc = threadIdx.x;
+__global__ void __launch_bounds__(kBB * kBFinParts)
+bobjective_trace_kernel(const double* __restrict__ red, uint32_t pz, const double* __restrict__ ored, uint32_t no,
+                        const double* __restrict__ lam, uint32_t B, double* __restrict__ trace, uint64_t trace_cap,
+                        const IterState* st) {
+  __shared__ double sp[2][kBFinParts][kBB];
+  const uint32_t sc = threadIdx.x % kBB, part = threadIdx.x / kBB;
   const uint64_t k = st->iter - 1;
-  if (sc >= B || st->iter == 0 || k >= trace_cap) return;
-  double o = 0.0, l = 0.0;
-  for (uint32_t c = 0; c < no; ++c) o += ored[(uint64_t)c * kBB + sc];
-  for (uint32_t c = 0; c < pz; ++c) l += red[((uint64_t)2 * pz + c) * kBB + sc];
-  trace[(k * B + sc) * 3 + 2] = 0.5 * o + lam[sc] * l;
+  if (st->iter == 0 || k >= trace_cap) return;  // uniform over the CTA
+  sp[0][part][sc] = bfin_part_sum(ored, 0, no, part, sc);
+  sp[1][part][sc] = bfin_part_sum(red, 2 * (uint64_t)pz, pz, part, sc);
+  __syncthreads();
+  if (part == 0 && sc < B) {
+    double o = sp[0][0][sc], l = sp[1][0][sc];
+    for (int q = 1; q < kBFinParts; ++q) o += sp[0][q][sc], l += sp[1][q][sc];
+    trace[(k * B + sc) * 3 + 2] = 0.5 * o + lam[sc] * l;
+  }
 }
 
 // max_t |(H^H g_b)_t| per scene from Z = H^H G (segment sums over the row blocks).

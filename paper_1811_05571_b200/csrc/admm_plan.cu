@@ -1420,7 +1420,9 @@ void build_batched(admm_plan* p) {
   p->dqpart.alloc((size_t)p->splitK * stride * 16);
   p->dz.alloc((size_t)p->splitH * p->vec_total * B * 16);
   p->dkappa.alloc(B * sizeof(double));
-  p->pz = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(4ull * p->num_sms, cdiv(p->max_seg, 4)));
+  uint64_t pzm = 5;  // bzupdate CTAs per SM (48 registers: 5 x 256 threads fit; 127 -> 113 us on config 5)
+  if (const char* e = std::getenv("ADMM_B200_BPZ")) pzm = std::max(1, std::atoi(e));
+  p->pz = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(pzm * p->num_sms, cdiv(p->max_seg, 4)));
   p->dbred.alloc((size_t)3 * p->pz * kBB * sizeof(double));
   p->dblam.alloc(B * sizeof(double));
   p->bogx = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(2ull * p->num_sms / std::max<uint64_t>(1, p->Mr),
@@ -1437,7 +1439,7 @@ void enqueue_bobjective(admm_plan* p, cudaStream_t s) {
   bobjective_rec_kernel<<<dim3(p->bogx, (unsigned)p->Mr), kCtaThreads, 0, s>>>(
       brow_vecs(p), p->dhs.as<double2>(), p->dblocks.as<BlockDesc>(), (uint32_t)p->Nc, B, p->dbored.as<double>(),
       p->dstate.as<IterState>(), 1);
-  bobjective_trace_kernel<<<1, kBB, 0, s>>>(p->dbred.as<double>(), p->pz, p->dbored.as<double>(),
+  bobjective_trace_kernel<<<1, kBB * kBFinParts, 0, s>>>(p->dbred.as<double>(), p->pz, p->dbored.as<double>(),
                                             p->bogx * (uint32_t)p->Mr, p->dblam.as<double>(), B,
                                             p->dtrace.as<double>(), p->trace_cap, p->dstate.as<IterState>());
 }
@@ -1490,7 +1492,7 @@ void enqueue_iteration_batched(admm_plan* p, cudaStream_t s, bool with_objective
                                                 (uint32_t)p->Mr, (uint32_t)p->Nc, B, p->dkappa.as<double>(),
                                                 p->dbred.as<double>(), p->dstate.as<IterState>());
   mark(6);
-  bfinalize_kernel<<<1, kBB, 0, s>>>(p->dbred.as<double>(), p->pz, B, p->dparams.as<Params>(), p->dtrace.as<double>(),
+  bfinalize_kernel<<<1, kBB * kBFinParts, 0, s>>>(p->dbred.as<double>(), p->pz, B, p->dparams.as<Params>(), p->dtrace.as<double>(),
                                      p->trace_cap, p->dstate.as<IterState>());
   mark(7);
   CK(cudaGetLastError());
