@@ -158,6 +158,24 @@ __device__ __forceinline__ void cpa_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// Index of the last descriptor with unit0 <= x (unit0 ascending, d[0].unit0 == 0) — the
+// stream-K "which matrix does my first unit belong to" search.  The warp loads 32 unit0
+// fields at once and takes the highest matching lane, instead of one dependent global load
+// per step (7 serial L2 round trips for 8 blocks at every kernel start).  Warp-uniform:
+// call with all 32 lanes.
+template <typename D>
+__device__ __forceinline__ int find_desc(const D* __restrict__ d, int n, uint64_t x) {
+  const int lane = (int)(threadIdx.x % 32);
+  int b = 0;
+  for (int base = 0; base < n; base += 32) {
+    const bool le = base + lane < n && d[base + lane].unit0 <= x;
+    const unsigned m = __ballot_sync(0xffffffffu, le);
+    if (m) b = base + 31 - __clz(m);
+    if (m != 0xffffffffu) break;
+  }
+  return b;
+}
+
 // Programmatic dependent launch: wait until the preceding grid in the stream has
 // completed (its writes visible), then allow the next grid to be launched while this one
 // runs.  A no-op when the launch carried no programmatic dependency.  Call first thing.

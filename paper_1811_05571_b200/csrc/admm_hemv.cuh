@@ -117,7 +117,6 @@ hemv_kernel(const S* __restrict__ Kp, const double2* __restrict__ X, double2* __
   // warp, the H part of each tile (I2, I) below the diagonal) bumps cnt[I] after its
   // partial is stored; the warp that completes the count finalizes the 64 rows.
   constexpr bool kPrefetch = OCC == 1;  // two tiles in registers only at one CTA per SM
-  pdl_enter();
   __shared__ double2 hbuf[2][kCtaWarps][kHT];
   uint64_t pol;
   if (keep)
@@ -127,10 +126,14 @@ hemv_kernel(const S* __restrict__ Kp, const double2* __restrict__ X, double2* __
   const uint64_t P = gridDim.x, p = blockIdx.x;
   uint64_t x = sk_lo(p, U, P);
   const uint64_t xe = sk_lo(p + 1, U, P);
-  if (x >= xe) return;
+  if (x >= xe) {
+    pdl_enter();
+    return;
+  }
   const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
-  int b = 0;
-  while (b + 1 < nb && hd[b + 1].unit0 <= x) ++b;
+  // descriptors and K do not depend on the predecessor: located / requested before the
+  // PDL wait, r (rows_finalize) only after it
+  int b = find_desc(hd, nb, x);
   HemvDesc d = hd[b];
   uint32_t u = (uint32_t)(x - d.unit0);
   uint32_t I = 0;
@@ -144,7 +147,6 @@ hemv_kernel(const S* __restrict__ Kp, const double2* __restrict__ X, double2* __
   };
 #pragma unroll
   for (int k = 0; k < kHRows; ++k) accN[k] = make_double2(0.0, 0.0);
-  load_xI();
   uint32_t par = 0;
   auto contribute = [&](uint32_t Ir) {  // warp-uniform: this warp's partial for tile-row Ir is stored
     __threadfence();  // every lane's partial stores are visible device-wide before the count
@@ -169,6 +171,8 @@ hemv_kernel(const S* __restrict__ Kp, const double2* __restrict__ X, double2* __
 #pragma unroll
     for (int k = 0; k < kHRows; ++k) ld_pair<S>(tp + (uint64_t)k * kHT, h[k], pol);
   }
+  pdl_enter();
+  load_xI();
   for (;;) {
     if (kPrefetch) {
       if (x + 1 < xe) {
@@ -318,12 +322,11 @@ hemv_bulk_kernel(const S* __restrict__ Kp, const double2* __restrict__ X, double
       bulk_g2s_s(ring_s + (uint32_t)t * TB, Kp + (x0 + t) * (uint64_t)(kHT * kHT), TB, full_s + 8 * (uint32_t)t, pol);
     }
   }
+  const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+  int b = find_desc(hd, nb, x);  // descriptors are constant: located before the PDL wait
+  HemvDesc d = hd[b];
   __syncthreads();
   pdl_enter();  // r (rows_finalize) visible from here on
-  const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
-  int b = 0;
-  while (b + 1 < nb && hd[b + 1].unit0 <= x) ++b;
-  HemvDesc d = hd[b];
   uint32_t u = (uint32_t)(x - d.unit0);
   uint32_t I = 0;
   while ((I + 1) * (I + 2) / 2 <= u) ++I;

@@ -108,8 +108,7 @@ gemv_n_kernel(const S* __restrict__ A, const double2* __restrict__ X, double2* _
   const uint64_t xe = sk_lo(p + 1, U, P);
   if (x >= xe) return;
   const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
-  int b = 0;
-  while (b + 1 < nmats && mats[b + 1].unit0 <= x) ++b;
+  int b = find_desc(mats, nmats, x);
   MatDesc md = mats[b];
   uint64_t local = x - md.unit0;
   uint32_t rg = (uint32_t)(local / md.n_chunks), cc = (uint32_t)(local % md.n_chunks);
@@ -191,8 +190,7 @@ gemv_h_kernel(const S* __restrict__ A, const double2* __restrict__ Q, double2* _
   const uint64_t xe = sk_lo(p + 1, U, P);
   if (x >= xe) return;
   const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
-  int b = 0;
-  while (b + 1 < nmats && mats[b + 1].unit0 <= x) ++b;
+  int b = find_desc(mats, nmats, x);
   MatDesc md = mats[b];
   uint64_t local = x - md.unit0;
   uint32_t cc = (uint32_t)(local / md.n_tiles), rt = (uint32_t)(local % md.n_tiles);
