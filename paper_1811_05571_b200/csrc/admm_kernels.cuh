@@ -69,7 +69,7 @@ struct IterState {
   uint32_t pad_;
 };
 
-constexpr int kRowsPerWarpN = 4;          // gemv_n: rows per warp per unit
+constexpr int kRowsPerWarpN = 8;          // gemv_n: rows per warp per unit
 constexpr int kRowsPerGroup = kCtaWarps * kRowsPerWarpN;  // gemv_n: rows per unit
 constexpr int kRowsPerWarpH = 4;          // gemv_h: rows per warp per tile
 constexpr int kRowTileH = kCtaWarps * kRowsPerWarpH;

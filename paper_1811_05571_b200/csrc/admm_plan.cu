@@ -117,7 +117,7 @@ bool host_all_finite(const T* p, uint64_t n) {  // multi-threaded problem.valida
 }
 
 // Streaming geometry (see admm_kernels.cuh).
-constexpr int kVN = 2;  // 32-byte vectors per lane per row in gemv_n
+constexpr int kVN = 1;  // 32-byte vectors per lane per row in gemv_n
 constexpr int kVH = 2;  // 32-byte vectors per lane per row in gemv_h
 template <typename S>
 constexpr int chunk_n() { return kWarp * kVN * Store<S>::kPerVec; }
