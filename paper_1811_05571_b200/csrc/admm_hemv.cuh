@@ -456,8 +456,8 @@ constexpr int kHFinRows = 64;
 __global__ void __launch_bounds__(kHFinRows)
 hemv_finalize_kernel(RowVecs rv, const double2* __restrict__ part, const HemvDesc* __restrict__ hd, uint64_t U,
                      uint64_t P, const Params* __restrict__ prm) {
+  const HemvDesc d = hd[blockIdx.y];  // constant: read before the PDL wait
   pdl_enter();
-  const HemvDesc d = hd[blockIdx.y];
   const uint32_t row = blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= d.m) return;
   const double2 s = hemv_sum_row(part, d, row / kHT, row % kHT, U, P);

@@ -573,17 +573,17 @@ rows_finalize_sweep_kernel(RowVecs rv, const double2* __restrict__ wpart, const 
                            const double* __restrict__ red, const Params* __restrict__ prm,
                            double* __restrict__ trace, uint64_t trace_cap, IterState* st,
                            double* __restrict__ slot) {
-  pdl_enter();
   __shared__ double sm[kCtaWarps];
   __shared__ double2 gsum[kRfGroups][kRfRows];
   const uint32_t b = blockIdx.y;
-  const BlockDesc bd = blocks[b];
+  const BlockDesc bd = blocks[b];  // constant: read before the PDL wait
+  const SweepDesc sd = segs[bd.jl];
+  pdl_enter();
   const uint32_t tr = threadIdx.x % kRfRows, grp = threadIdx.x / kRfRows;
   const uint32_t row = blockIdx.x * kRfRows + tr;
   if (blockIdx.x * kRfRows < bd.rows) {  // CTA-uniform
     double2 w = make_double2(0.0, 0.0);
     if (!first && row < bd.rows) {
-      const SweepDesc sd = segs[bd.jl];
       const uint32_t ns = seg_count(sd.unit0, sd.n_strips, Utot, Psweep);
       const double2* src = wpart + sd.part_off + bd.row0 + row;
 #pragma unroll 4
