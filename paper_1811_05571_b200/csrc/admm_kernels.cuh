@@ -438,17 +438,18 @@ objective_rows_kernel(const double2* __restrict__ g, const double2* __restrict__
 __global__ void __launch_bounds__(kCtaThreads)
 objective_rec_kernel(RowVecs rv, double2* __restrict__ hs, const BlockDesc* __restrict__ blocks, uint32_t N,
                      uint32_t np_log2, double* __restrict__ red, const IterState* st, uint64_t min_iter) {
-  pdl_enter();
   __shared__ double2 sa[kCtaThreads];
   __shared__ double sm[kCtaWarps];
   const uint32_t i = blockIdx.y;
-  const BlockDesc b0 = blocks[i * N];
+  const BlockDesc b0 = blocks[i * N];  // descriptors are constant: read before the PDL wait
   const uint32_t NP = 1u << np_log2, j = threadIdx.x & (NP - 1), rl = threadIdx.x >> np_log2;
+  const uint32_t mv = j < N ? blocks[i * N + j].mvec_off : 0u;
+  pdl_enter();
   const uint32_t row = blockIdx.x * (kCtaThreads >> np_log2) + rl;
   const bool on = st->iter >= min_iter && row < b0.rows;
   double2 a = make_double2(0.0, 0.0);
   if (on && j < N) {
-    const uint64_t o = (uint64_t)blocks[i * N + j].mvec_off + row;
+    const uint64_t o = (uint64_t)mv + row;
     const double2 w = csub(rv.gij[o], rv.r[o]);
     a = cscale(cadd(cadd(w, hs[o]), rv.ghat[o]), 0.5);
     hs[o] = csub(a, w);
