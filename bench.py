@@ -1,18 +1,31 @@
 #!/usr/bin/env python3
 """Benchmark of the B200 ADMM hot path (BASELINE.json metric: ADMM iterations/s and
-H-stream HBM GB/s).
+H-stream HBM GB/s, % of B200 peak, at 1/2/4/8 GPUs).
 
-Workload (N=1): BASELINE config 2 — sectioning ADMM, complex128, H 1024 x 32768 i.i.d.
-CN(0, 1/1024), 64-sparse unit-phase truth, 30 dB SNR, N = 8 column blocks of 4096,
-rho = 1, lambda = 0.05 max|H^H g|, seed 2.  A "step" is one ADMM iteration
-over the whole problem (two passes over H plus the 8 Woodbury applies).
+Workload (default, N=1): BASELINE config 4 -- consensus ADMM at scale, complex64 storage,
+H 16384 x 262144 i.i.d. CN(0, 1/16384) (32 GiB), 1000-sparse unit-phase truth, 30 dB SNR,
+M = 8 row blocks of 2048, rho = 1, lambda = 0.05 max|H^H g|, 1000 iterations, seed 4: the
+largest configuration that fits one GPU (configs[1..4]; config 5 is the batched variant of
+config 3).  `--config 1|2|3|5` selects another BASELINE config.  A "step" is one ADMM
+iteration over the whole problem (both H products, the 8 Woodbury applies, the column
+update, the residuals and the objective of the trace).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 4]
 
 Prints one JSON line (rank 0).  Timing: CUDA events on the plan's stream around K
-graph-replayed iterations, max over ranks; H (512 MiB) is larger than L2, so every
-iteration streams from HBM.  e2e: the public API (AdmmPlan.set_g + solve) with the
-measurement vector copied from pinned host memory and the solution read back.
+graph-replayed iterations, after W warm-up iterations, with a barrier + synchronize on both
+sides, max over ranks.  Every input is larger than L2 (config 4: 32 GiB of H; config 2:
+512 MiB), so each iteration streams HBM; no flush is needed.  `e2e`: the public API
+(AdmmPlan.set_g + solve) with the measurement vector copied from pinned host memory and the
+solution + trace read back.
+
+--gpus N > 1 outside torchrun re-executes itself under `torch.distributed.run
+--nproc-per-node N` (one process per GPU); the plan of every rank owns its NCCL
+communicators.
+
+The reference arm (`--impl reference`) runs the UNMODIFIED reference solver
+(oracle/_ref/admmsplit_ref, the reference headers compiled where they lie) on the host
+cores, on inputs from the reference's own generator; it never imports this package.
 """
 from __future__ import annotations
 
@@ -20,6 +33,7 @@ import argparse
 import json
 import os
 import shutil
+import socket
 import subprocess
 import sys
 import tempfile
@@ -29,7 +43,7 @@ import time
 import numpy as np
 
 REPO = os.path.dirname(os.path.abspath(__file__))
-sys.path.insert(0, REPO)
+REF_BIN = os.path.join(REPO, "oracle", "_ref", "admmsplit_ref")
 
 CONFIGS = {
     # name: (method, rows, cols, k, snr, seed, kind, M, N, lambda_rel, iters, dtype)
@@ -39,6 +53,7 @@ CONFIGS = {
     "4": ("consensus", 16384, 262144, 1000, 30.0, 4, "cg", 8, 1, 0.05, 1000, "c64"),
     "5": ("hybrid", 3072, 32768, 64, 30.0, 3, "cra_batch", 2, 4, 0.03, 500, "c64"),
 }
+DEFAULT_CONFIG = "4"
 
 
 def describe(cfg):
@@ -55,15 +70,17 @@ def describe(cfg):
             f"{grid}, rho=1, lambda={lr}*max|H^H g|, {iters} iterations")
 
 
-SMEM_PEAK_GBS = 148 * 128 * 1.965  # GB/s: shared-memory bandwidth of all SMs at the max SM clock
+def config_dict(name):
+    """The `config` object of BOTH arms (identical by construction)."""
+    return {"workload": f"config {name}: {describe(CONFIGS[name])}"}
 
 
 def peaks():
     p = os.path.join(REPO, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return float(d["hbm_gbs"]), "measured"
-    return 6650.0, "fallback"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 class ClockSampler:
@@ -113,6 +130,86 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
 
 
+def dist_env():
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+# ----------------------------------------------------------------------------- reference
+def reference_sample(name):
+    """The bounded sample of config `name` the unmodified reference runs on (SURVEY §8d,
+    BASELINE.md §4): the reference's own generator, the config's columns, blocks, method and
+    lambda rule, with fewer rows where the full size is minutes of setup or does not fit
+    host memory.  The reference's per-iteration cost is linear in the H bytes (3 FP64 passes
+    over H: the two Woodbury products and the objective), so it/s scales by rows_sample /
+    rows.  The CRA-like H of configs 3/5 has no reference generator: a random-phase H of
+    the same shape stands in (the reference's timing does not depend on the values)."""
+    method, m, n, k, snr, seed, kind, M, N, lr, iters, dtype = CONFIGS[name]
+    rows = {"1": m, "2": m, "3": 768, "4": 256, "5": 768}[name]
+    gkind = "rp" if kind.startswith("cra") else "cg"
+    kk = min(k, n) if kind != "cra_batch" else 300
+    scenes = k if kind == "cra_batch" else 1
+    return dict(method=method, rows=rows, cols=n, k=kk, snr=snr, seed=seed, kind=gkind, M=M, N=N, lr=lr,
+                scale=rows / m, scenes=scenes, full_rows=m)
+
+
+def run_reference(name, iters, threads=None):
+    """Time the unmodified reference on the host cores: generate the sample with the
+    reference's gen_problem, solve with its solver (observer timestamps; setup excluded)."""
+    if not os.path.exists(REF_BIN):
+        return None
+    s = reference_sample(name)
+    threads = threads or max(1, min(s["M"] * s["N"], os.cpu_count() or 1))
+    tmp = tempfile.mkdtemp(prefix="admm_ref_")
+    try:
+        d = os.path.join(tmp, "in")
+        subprocess.run([REF_BIN, "gen", f"out={d}", f"m={s['rows']}", f"n={s['cols']}", f"k={s['k']}",
+                        f"snr={s['snr']}", f"seed={s['seed']}", f"kind={s['kind']}"], check=True,
+                       capture_output=True, timeout=1800)
+        out = os.path.join(tmp, "out")
+        subprocess.run([REF_BIN, "solve", f"in={d}", f"out={out}", f"method={s['method']}", f"M={s['M']}",
+                        f"N={s['N']}", "rho=1", f"lambda={s['lr']}", "lambda_rel=1", f"iters={max(2, iters)}",
+                        f"threads={threads}"], check=True, capture_output=True, timeout=3600)
+        md = dict(line.split() for line in open(os.path.join(out, "meta.txt")))
+        measured = float(md["it_per_s"])
+        value = measured * s["scale"] / s["scenes"]
+        what = (f"full workload" if s["scale"] == 1.0 else
+                f"first {s['rows']} of {s['full_rows']} rows (reference gen_problem, kind {s['kind']}, all "
+                f"{s['cols']} columns, M={s['M']} N={s['N']}), it/s x {s['scale']:g} (cost linear in H size)")
+        if s["scenes"] > 1:
+            what += f"; one scene per reference solve, it/s / {s['scenes']} scenes"
+        return {"value": value, "measured": measured, "setup_s": float(md["setup_s"]), "threads": threads,
+                "iters": max(2, iters),
+                "sample": (f"unmodified reference ({s['method']}_solve, oracle/_ref) on {what}; {max(2, iters)} "
+                           f"iterations after its serial setup ({float(md['setup_s']):.1f} s, excluded); it/s "
+                           f"from observer timestamps ({measured:.4g} measured); includes the reference's "
+                           f"per-iteration objective pass")}
+    finally:
+        shutil.rmtree(tmp, ignore_errors=True)
+
+
+def bench_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    iters = min(max(args.steps, 2), 20) + min(args.warmup, 3)
+    r = run_reference(args.config, iters)
+    if r is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/admmsplit_ref not built"}))
+        return
+    v = r["value"]
+    line = {"metric": "ADMM iterations/s", "value": v, "unit": "iterations/s", "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / v,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+            "data": "synthetic", "config": config_dict(args.config),
+            "cpu_baseline": {"value": v, "unit": "iterations/s", "cores": r["threads"], "kind": "reference",
+                             "sample": r["sample"]},
+            "e2e": {"value": v, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "setup_s": r["setup_s"]}
+    print(json.dumps(line))
+
+
+# ----------------------------------------------------------------------------- ours
 def make_problem(cfg):
     import paper_1811_05571_b200 as admm
     method, m, n, k, snr, seed, kind, M, N, lr, iters, dtype = cfg
@@ -122,381 +219,221 @@ def make_problem(cfg):
         h = admm.cra_matrix(seed=seed, dtype=dtype)
         g, truth = admm.cra_scenes(h, k, seed=seed)
         return admm.SensingProblem(h, g, None)
-    p = admm.gen_problem(m, n, k, snr, seed,
-                         admm.ProblemKind.ComplexGaussian if kind == "cg" else admm.ProblemKind.RandomPhase,
-                         dtype=dtype)
-    return p
+    return admm.gen_problem(m, n, k, snr, seed, admm.ProblemKind.ComplexGaussian, dtype=dtype)
 
 
-def write_cmat(path, a):
-    a = np.ascontiguousarray(a, dtype="<c16")
-    if a.ndim == 1:
-        a = a.reshape(-1, 1)
-    with open(path, "wb") as f:
-        f.write(b"CMX1")
-        f.write(np.array(a.shape, dtype="<u8").tobytes())
-        a.tofile(f)
+def kernel_roofline(plan, info, problem, name):
+    """Dominant kernel of one iteration: per-kernel CUDA-event times of individually launched
+    kernels on the plan's stream (`plan.profile`), algorithmic bytes per launch (SURVEY §8d:
+    one pass over the stored H = rows x cols x sizeof(element); the packed K once)."""
+    kern = plan.profile(iters=10)
+    hb, kb = info["h_bytes"], info["k_bytes"]
+    algo = {"gemv_n(H,c)": hb, "gemv_h(H,q)": hb, "gemv_n(K,r)": kb, "hemv(Kpacked,r)": kb, "sweep(H)": hb,
+            "resident(iteration)": 2 * hb}
+    algo = {k: v for k, v in algo.items() if k in kern}
+    peak, peak_kind = peaks()
+    if plan.batch > 1:  # config 5: FP64 SIMT compute-bound skinny GEMMs (8 flop per complex MAC)
+        rows, cols = problem.h.shape
+        algo = {"bgemm(H,C)": 8.0 * rows * cols * plan.batch, "bgemm_adj(H,Q)": 8.0 * rows * cols * plan.batch}
+    dom = max(algo, key=lambda x: kern[x])
+    achieved = algo[dom] / (kern[dom] / 1000.0) / 1e9
+    traffic = None
+    summ = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    if os.path.exists(summ):
+        traffic = json.load(open(summ)).get(f"config{name}", {}).get(dom)
+    if plan.batch > 1:
+        roof = {"bound": "fp64-simt", "kernel": dom, "achieved": achieved / 1e3, "peak": 34.1,
+                "peak_kind": "measured FP64 FMA peak (tools/fp_peak.cu; not in MEASURED_PEAKS.json)",
+                "unit": "TFLOP/s", "frac": achieved / 1e3 / 34.1}
+    else:
+        roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
+                "unit": "GB/s", "frac": achieved / peak,
+                "peak_note": "copy bandwidth (read+write); read-only streams can exceed it"}
+    roof.update({"traffic": traffic, "algorithmic_per_launch": algo[dom], "avg_launch_ms": kern[dom]})
+    return roof, {"isolated_launch_ms": kern,
+                  "note": "CUDA events around individually launched kernels of one iteration on the plan's "
+                          "stream (not the graph-replayed chain: their sum exceeds ms_per_step)"}
 
 
-def run_reference_cpu(cfg, problem, rows=None, iters=4):
-    """Time the UNMODIFIED reference (oracle/_ref/admmsplit_ref, built from /root/reference
-    sources) on the host cores.  rows: use only the first `rows` rows (a bounded sample).
-    Returns dict with it/s (observer timestamps, setup excluded), setup_s, threads."""
-    ref = os.path.join(REPO, "oracle", "_ref", "admmsplit_ref")
-    if not os.path.exists(ref):
+def cpu_baseline(name):
+    r = run_reference(name, 5)
+    if not r:
         return None
-    method, m, n, k, snr, seed, kind, M, N, lr, _iters, dtype = cfg
-    rows = rows or m
-    tmp = tempfile.mkdtemp(prefix="admm_ref_")
-    try:
-        h = problem.h[:rows].astype(np.complex128)
-        g = problem.g[:rows]
-        scenes = 1
-        if g.ndim == 2:  # batched scenes (config 5): the reference solves one scene per call,
-            scenes = g.shape[1]  # so one batched iteration costs `scenes` reference iterations
-            g = g[:, 0]
-        write_cmat(os.path.join(tmp, "h.cmat"), h)
-        write_cmat(os.path.join(tmp, "g.cmat"), g)
-        blocks = M * N
-        threads = max(1, min(blocks, os.cpu_count() or 1))
-        out = os.path.join(tmp, "out")
-        cmd = [ref, "solve", f"in={tmp}", f"out={out}", f"method={method}", f"M={M}", f"N={N}",
-               "rho=1", f"lambda={lr}", "lambda_rel=1", f"iters={iters}", f"threads={threads}"]
-        subprocess.run(cmd, check=True, capture_output=True, timeout=1800)
-        md = dict(line.split() for line in open(os.path.join(out, "meta.txt")))
-        return {"it_per_s": float(md["it_per_s"]) / scenes, "setup_s": float(md["setup_s"]),
-                "threads": threads, "rows": rows, "iters": iters, "scenes": scenes}
-    finally:
-        shutil.rmtree(tmp, ignore_errors=True)
+    return {"value": r["value"], "unit": "iterations/s", "cores": r["threads"], "kind": "reference",
+            "sample": r["sample"]}
 
 
-def sample_rows_for(cfg, cap_bytes=256 << 20):
-    """Rows of the bounded CPU sample: a quarter of the rows, at most cap_bytes of c128 H
-    (all columns kept), a multiple of M with >= 8 rows per row block."""
-    method, m, n, k, snr, seed, kind, M, N, lr, _iters, dtype = cfg
-    r = min(max(64, m // 4), max(8 * M, cap_bytes // (n * 16)))
-    return max(M, (min(r, m) // M) * M)
-
-
-def dist_env():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
-
-
-def bench_reference(args, cfg):
-    ws, rank, _ = dist_env()
-    if rank != 0:
-        return
-    problem = make_problem(cfg)
-    iters = min(max(args.steps, 2), 20) + min(args.warmup, 3)
-    m, n = problem.h.shape
-    full = m * n * 16 <= (2 << 30)  # the whole workload, unless its c128 H exceeds 2 GiB
-    rows = m if full else sample_rows_for(cfg)
-    r = run_reference_cpu(cfg, problem, rows=rows, iters=iters)
-    if r is None:
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
-        return
-    v = r["it_per_s"] * rows / m  # per-iteration cost is linear in H size
-    what = ("full workload" if full else
-            f"first {rows} of {m} rows (all columns, same blocks), it/s scaled by {rows / m:g}")
-    if r["scenes"] > 1:
-        what += f"; scene 0 of {r['scenes']} (one reference solve per scene), it/s divided by {r['scenes']}"
-    line = {"metric": "ADMM iterations/s", "value": v, "unit": "iterations/s", "impl": "reference",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1000.0 / v, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-            "config": {"workload": f"config {args.config}: {describe(cfg)}"},
-            "cpu_baseline": {"value": v, "unit": "iterations/s", "cores": r["threads"],
-                             "kind": "reference",
-                             "sample": f"{what}, {r['iters']} iterations after the reference's "
-                                       f"serial setup ({r['setup_s']:.1f} s, excluded); it/s from "
-                                       "observer timestamps; includes the reference's per-iteration "
-                                       "objective pass"},
-            "e2e": {"value": v, "unit": "iterations/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0},
-            "setup_s": r["setup_s"]}
-    print(json.dumps(line))
-
-
-def bench_distributed(args, cfg):
-    """N > 1: the config sharded over a Pr x Pc process grid (paper_1811_05571_b200.distributed),
-    NCCL all-gathers between the shard plan's phases on its stream.  Total work is fixed
-    (strong scaling); value = iterations/s of the whole job."""
+def bench_ours(args):
     import torch
-    import torch.distributed as dist
 
     import paper_1811_05571_b200 as admm
     from paper_1811_05571_b200 import distributed as D
 
     ws, rank, local = dist_env()
+    cfg = CONFIGS[args.config]
+    method, m, n, k, snr, seed, kind, M, N, lr, iters, dtype = cfg
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    method, m, n, k, snr, seed, kind, M, N, lr, iters, dtype = cfg
-    problem = make_problem(cfg)
-    lam = [0.0]
-    if rank == 0:  # lambda = c max|H^H g| once, broadcast (every rank must use the same bits)
-        hh = problem.h.astype(np.complex128)
-        lam[0] = lr * float(np.max(np.abs(hh.conj().T @ problem.g)))
-    dist.broadcast_object_list(lam, src=0)
-    scfg = admm.SolverConfig(rho=1.0, lambda_=lam[0], max_iters=iters)
-    Pr, Pc = D.choose_grid(ws, method, M, N)
-    pr, pc = divmod(rank, Pc)
-    sh = D.ShardPlan(problem, scfg, method, M, N, (Pr, Pc), (pr, pc),
-                     admm.SolveOptions(dtype=dtype, device=local, trace_objective=False))
-    comm = D.TorchComm(Pr, Pc)
-    D.run_iterations([sh], comm, max(args.warmup, 3))  # eager warm-up: NCCL communicators up
-    sh.sync()
-    graphed = D.GraphedIterations(sh, comm, iters_per_graph=8)  # phases + all-gathers in one graph
-    steps = -(-args.steps // 8) * 8
-    graphed.run(8)
-    torch.cuda.synchronize(local)
-    dist.barrier()
-    torch.cuda.synchronize(local)
-    stream = sh.stream()  # replays go onto the shard plan's own stream
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        e0.record(stream)
-        graphed.run(steps)
-        e1.record(stream)
-        e1.synchronize()
-    torch.cuda.synchronize(local)
-    ms = e0.elapsed_time(e1)
-    args.steps = steps
-    t = torch.tensor([ms], device=f"cuda:{local}")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
-    ms_per_step = ms / args.steps
-    value = args.steps / (ms / 1000.0)
-    # end to end: fresh iterates (reset), the measurement vector is already resident per
-    # rank; a full solve of `iters` iterations + the solution gathered to every rank
-    from paper_1811_05571_b200 import _lib
-    g_pinned = torch.from_numpy(np.ascontiguousarray(problem.g).view(np.float64)).pin_memory()
-    t0 = time.perf_counter()
-    _lib.lib.admm_plan_set_g(sh._h, g_pinned.data_ptr())  # the step's input from pinned host memory
-    sh.reset()
-    D.prime([sh], comm)
-    graphed.run(iters)
-    torch.cuda.synchronize(local)
-    sh.sync()
-    segs = [None] * ws
-    dist.all_gather_object(segs, sh.segment_v())
-    t1 = time.perf_counter()
-    tt = torch.tensor([t1 - t0], device=f"cuda:{local}")
-    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-    e2e = iters / float(tt.item())
-    hb = problem.h.size * problem.h.itemsize
-    x_bytes = {w: sh.buffers[w].numel() * 8 for w in sh.buffers}
-    if rank == 0:
-        peak, peak_kind = peaks()
-        per_gpu_h = hb / ws
-        line = {
-            "metric": "ADMM iterations/s", "value": value, "unit": "iterations/s", "n_gpus": ws,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": dtype,
-            "data": "synthetic (seeded generator of the reference, generate.hpp)",
-            "config": {"workload": f"config {args.config}: {describe(cfg)}",
-                       "parallelism": f"{Pr}x{Pc} process grid ({sh.schedule} schedule)",
-                       "l2": f"per-GPU H {per_gpu_h / 2**20:.0f} MiB",
-                       # sharded plans do not compute the per-iteration objective (the N=1 line does,
-                       # +4.4% per iteration on config 2; DESIGN.md §6)
-                       "trace_objective": False},
-            "h_stream_gbs": 2 * hb / (ms_per_step / 1000.0) / 1e9,
-            "nccl_bytes_per_iter_per_rank": {"ghat": x_bytes[0], "outbox": x_bytes[1] if sh.schedule == "twopass" else 0,
-                                             "scal": x_bytes[2]},
-            "roofline": {"bound": "hbm", "kernel": "whole iteration", "achieved":
-                         per_gpu_h * (1 if sh.schedule == "sweep" else 2) / (ms_per_step / 1000.0) / 1e9,
-                         "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "traffic": None},
-            "e2e": {"value": e2e, "unit": "iterations/s", "h2d_bytes_per_step": problem.g.nbytes, "d2h_bytes_per_step":
-                    problem.h.shape[1] * 16,
-                    "step": f"one full solve ({iters} iterations), solution all-gathered"},
-            "gpu_launches": (6 if sh.schedule == "sweep" else 9) * args.steps,
-            "clocks": clk.summary(),
-        }
-        line["roofline"]["frac"] = line["roofline"]["achieved"] / peak
-        # NVLink term of the exchanges: bytes each rank receives per iteration from its peers
-        # (all-gathers: (group - 1) / group of each buffer) against the nominal 900 GB/s per
-        # direction of NVLink 5; these exchanges are latency-, not bandwidth-bound
-        group = {0: Pc, 1: Pr, 2: Pr * Pc}
-        rx = sum(x_bytes[w] * (group[w] - 1) / group[w] for w in x_bytes)
-        line["nvlink"] = {"rx_bytes_per_iter_per_rank": rx, "achieved_gbs": rx / (ms_per_step / 1000.0) / 1e9,
-                          "peak_gbs": 900.0, "peak_kind": "nominal NVLink 5 per direction",
-                          "frac": rx / (ms_per_step / 1000.0) / 1e9 / 900.0}
-        print(json.dumps(line))
-    dist.destroy_process_group()
-
-
-def bench_ours(args, cfg):
-    import torch
-    import paper_1811_05571_b200 as admm
-
-    ws, rank, local = dist_env()
-    if ws > 1 or os.environ.get("BENCH_FORCE_DIST") == "1":  # (forced: exercise the sharded path at N=1)
-        return bench_distributed(args, cfg)
-    dev = local
-    method, m, n, k, snr, seed, kind, M, N, lr, iters, dtype = cfg
+    # ws > 1: one process per GPU, the plan owns its NCCL communicators; BENCH_FORCE_DIST=1
+    # runs that path with a world of one (schema check of the N > 1 line)
+    sharded = ws > 1 or os.environ.get("BENCH_FORCE_DIST") == "1"
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")  # plumbing only (NCCL id broadcast, timing max); data moves over NCCL
     problem = make_problem(cfg)
     scfg = admm.SolverConfig(rho=1.0, lambda_=1.0, max_iters=iters)
-    opts = admm.SolveOptions(dtype=dtype, device=dev, trace_objective=args.trace_objective)
-    plan = admm.AdmmPlan(problem, scfg, method, M, N, opts)
+    opts = admm.SolveOptions(dtype=dtype, device=local, trace_objective=args.trace_objective)
+    t_setup = time.perf_counter()
+    plan = D.dist_plan(problem, scfg, method, M, N, opts) if sharded else admm.AdmmPlan(problem, scfg, method, M, N,
+                                                                                         opts)
     if plan.batch > 1:  # per-scene lambda_b = c max|H^H g_b|
         lams = lr * plan.max_abs_adjoint_batched()
         plan.set_lambdas(lams)
-        lam = float(np.median(lams))
     else:
-        lam = lr * plan.max_abs_adjoint()
-        plan.set_lambda(lam)
+        plan.set_lambda(lr * plan.max_abs_adjoint())
+    setup_s = time.perf_counter() - t_setup
     info = plan.info()
-    torch.cuda.set_device(dev)
-    stream = torch.cuda.ExternalStream(plan.stream(), device=dev)
+    stream = torch.cuda.ExternalStream(plan.stream(), device=local)
+
+    def barrier():
+        torch.cuda.synchronize(local)
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize(local)
 
     # ---- device-resident throughput (value)
     plan.reset()
     plan.enqueue(max(args.warmup, 3))
     plan.sync()
-    if ws > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize(dev)
+    barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(dev) as clk:
+    with ClockSampler(local) as clk:
         e0.record(stream)
         plan.enqueue(args.steps)
         e1.record(stream)
         e1.synchronize()
-    torch.cuda.synchronize(dev)
+    barrier()
     ms = e0.elapsed_time(e1)
     if ws > 1:
-        t = torch.tensor([ms], device=f"cuda:{dev}")
+        t = torch.tensor([ms], dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
     ms_per_step = ms / args.steps
-    value = ws * args.steps / (ms / 1000.0)  # replicas: each rank runs the whole problem
+    value = args.steps / (ms / 1000.0)  # whole job: every rank runs its shard of the same iterations
 
-    # ---- per-kernel device time (roofline of the dominant kernel)
-    kern = plan.profile(iters=10)
-    hb, kb = info["h_bytes"], info["k_bytes"]
-    # algorithmic HBM bytes per launch: each H pass / the sweep streams H once from HBM
-    # (the sweep's second, L2-resident read of each strip is not HBM traffic), K once.
-    algo = {"gemv_n(H,c)": hb, "gemv_h(H,q)": hb, "gemv_n(K,r)": kb, "hemv(Kpacked,r)": kb,
-            "hemv(Kpacked,r)+finalize": kb, "sweep(H)": hb}
-    algo = {k: v for k, v in algo.items() if k in kern}
-    resident = int(info["schedule"]) == 4
-    if resident:  # one persistent kernel per enqueue; both H products read the SMEM-resident H
-        algo = {"resident(iteration)": 2 * hb}
-    if plan.batch > 1:  # config 5: FP64 SIMT compute-bound skinny GEMMs (8 flop per complex MAC)
-        rows, cols = problem.h.shape
-        algo = {"bgemm(H,C)": 8.0 * rows * cols * plan.batch, "bgemm_adj(H,Q)": 8.0 * rows * cols * plan.batch}
-    dom = max(algo, key=lambda x: kern[x])
-    peak, peak_kind = peaks()
-    achieved = algo[dom] / (kern[dom] / 1000.0) / 1e9
-    h_stream_gbs = info["h_stream_bytes_per_iter"] / (ms_per_step / 1000.0) / 1e9
-    traffic = None
-    summ = os.path.join(REPO, "profiles", "ncu_traffic.json")
-    if os.path.exists(summ):
-        t = json.load(open(summ)).get(f"config{args.config}", {}).get(dom)
-        traffic = t
+    if not sharded:
+        roof, kern = kernel_roofline(plan, info, problem, args.config)
+    else:  # the plan's kernels are not launched one by one: whole-iteration HBM roofline
+        peak, peak_kind = peaks()
+        passes = 1 if int(info["schedule"]) == 2 else 2
+        achieved = info["h_bytes"] * passes / (ms_per_step / 1000.0) / 1e9
+        roof = {"bound": "hbm", "kernel": f"whole iteration ({passes} pass(es) over this rank's H)",
+                "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": None, "algorithmic_per_launch": info["h_bytes"] * passes, "avg_launch_ms": ms_per_step}
+        kern = None
 
-    # ---- end to end through the public API: new g from pinned memory, full solve,
-    # solution back to the host (AdmmPlan.set_g + solve), repeated.
-    g_pinned = torch.from_numpy(problem.g.view(np.float64)).pin_memory()
-    e2e_solves = max(1, min(3, args.steps // iters + 1))
-    plan.set_g(g_pinned.numpy().view(np.complex128))
-    plan.solve()  # warm
-    torch.cuda.synchronize(dev)
+    # ---- end to end through the public API: g from pinned memory, full solve, solution and
+    # trace back to the host (AdmmPlan.set_g + solve)
+    g_pinned = torch.from_numpy(np.ascontiguousarray(problem.g).view(np.float64)).pin_memory()
+    g_host = g_pinned.numpy().view(np.complex128)
+    plan.set_g(g_host)
+    plan.solve()  # warm (graphs captured)
+    barrier()
+    e2e_solves = 1 if iters >= 1000 else max(1, min(3, args.steps // iters + 1))
     t0 = time.perf_counter()
     for _ in range(e2e_solves):
-        plan.set_g(g_pinned.numpy().view(np.complex128))
+        plan.set_g(g_host)
         rep = plan.solve()
     t1 = time.perf_counter()
-    e2e_value = ws * e2e_solves * iters / (t1 - t0)
+    dt = t1 - t0
+    if ws > 1:
+        t = torch.tensor([dt], dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        dt = float(t.item())
+    e2e_value = e2e_solves * iters / dt
     h2d = problem.g.nbytes
-    d2h = rep.solution.nbytes + iters * 3 * 8
+    d2h = rep.solution.nbytes + iters * 3 * 8 * plan.batch
 
     if rank != 0:
-        if ws > 1:
-            torch.distributed.destroy_process_group()
         return
-
-    # ---- CPU baseline: the reference on a bounded row sample of the same workload
-    cpu = None
-    if ws == 1 and not args.no_cpu_baseline:
-        sample_rows = sample_rows_for(cfg)
-        r = run_reference_cpu(cfg, problem, rows=sample_rows, iters=5)
-        if r:
-            scale = sample_rows / m  # per-iteration CPU cost is linear in H size
-            cpu = {"value": r["it_per_s"] * scale, "unit": "iterations/s", "cores": r["threads"],
-                   "kind": "reference",
-                   "sample": (f"reference sectioning/consensus solver on the first {sample_rows} of {m} "
-                              f"rows (same columns, blocks, lambda rule), 5 iterations, "
-                              f"{r['it_per_s']:.3f} it/s measured, scaled by {scale:g} (cost is linear in "
-                              f"H size); setup {r['setup_s']:.2f} s excluded"
-                              + (f"; scene 0 of {r['scenes']} (one reference solve per scene), it/s "
-                                 f"divided by {r['scenes']}" if r["scenes"] > 1 else ""))}
-
+    hb = info["h_bytes"]
+    h_stream_gbs = info["h_stream_bytes_per_iter"] / (ms_per_step / 1000.0) / 1e9
+    peak, peak_kind = peaks()
+    sched = {1: "two-pass", 2: "single-HBM-pass sweep", 3: "batched scenes (FP64 SIMT GEMMs)",
+             4: "resident (H in SMEM, one persistent cooperative kernel)"}[int(info["schedule"])]
     line = {
         "metric": "ADMM iterations/s", "value": value, "unit": "iterations/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype,
-        "data": "synthetic (seeded generator of the reference, generate.hpp)",
-        "config": {"workload": f"config {args.config}: {describe(cfg)}",
-                   "l2": f"inputs larger than L2 (H {hb / 2**20:.0f} MiB per replica)",
-                   "parallelism": "replicas" if ws > 1 else "single GPU, all blocks",
-                   "lambda": lam, "trace_objective": bool(args.trace_objective)},
+        "higher_is_better": True, "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None,
+        "dtype": dtype, "data": "synthetic (seeded generator of the reference, generate.hpp)",
+        "config": config_dict(args.config),
+        "run": {"schedule": sched, "parallelism": (f"{info['grid_pr']}x{info['grid_pc']} process grid, NCCL owned "
+                                                    f"by the plan" if sharded else "single GPU, all blocks"),
+                "l2": f"inputs larger than L2 (H {hb * ws / 2**20:.0f} MiB over {ws} GPU(s)), no flush needed",
+                "lambda": plan.cfg.lambda_, "trace_objective": bool(args.trace_objective),
+                "setup_s": setup_s, "timing": "CUDA events on the plan's stream around K graph-replayed "
+                                              "iterations, max over ranks"},
         "h_stream_gbs": h_stream_gbs, "h_stream_frac_of_peak": h_stream_gbs / peak,
+        "h_stream_note": "2 x |H| per iteration (SURVEY §8d's two-pass H-stream bytes) / time: a single-pass "
+                         "schedule can exceed 1.0",
         "hbm_compulsory_gbs": info["hbm_bytes_per_iter"] / (ms_per_step / 1000.0) / 1e9,
-        "schedule": {1: "two-pass", 2: "single-HBM-pass sweep", 3: "batched scenes (FP64 SIMT GEMMs)",
-                     4: "resident (H in SMEM, one persistent cooperative kernel)"}[
-            int(info["schedule"])],
-        "roofline": ({"bound": "smem (H resident; grid-barrier latency)", "kernel": dom, "achieved": achieved,
-                      "peak": SMEM_PEAK_GBS, "peak_kind": "derived: 148 SMs x 128 B/clk x 1.965 GHz",
-                      "unit": "GB/s", "frac": achieved / SMEM_PEAK_GBS} if resident else
-                     {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
-                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                      # MEASURED_PEAKS.json's figure is a copy (read + write); a read-only
-                      # stream such as the GEMVs can exceed it (HBM3e nominal ~8 TB/s)
-                      "peak_note": "copy bandwidth (read+write); read-only streams can exceed it"}
-                     if plan.batch == 1 else
-                     {"bound": "fp64-simt", "kernel": dom, "achieved": achieved / 1e3, "peak": 34.1,
-                      "peak_kind": "measured (tools/fp_peak.cu, FP64 FMA)", "unit": "TFLOP/s",
-                      "frac": achieved / 1e3 / 34.1}) | {
-                     "traffic": traffic, "algorithmic_per_launch": algo[dom],
-                     "avg_launch_ms": kern[dom]},
-        "kernels_ms": kern,
-        "e2e": {"value": e2e_value, "unit": "iterations/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h,
-                "step": f"one full solve ({iters} iterations) via AdmmPlan.set_g+solve"},
-        "gpu_launches": 1 if resident else int(info["launches_per_iter"]) * args.steps,
+        "hbm_compulsory_frac": info["hbm_bytes_per_iter"] / (ms_per_step / 1000.0) / 1e9 / peak,
+        "e2e": {"value": e2e_value, "unit": "iterations/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "step": f"one full solve ({iters} iterations) via AdmmPlan.set_g + solve from pinned host memory"},
+        "gpu_launches": int(info["launches_per_iter"]) * args.steps if int(info["schedule"]) != 4 else 1,
         "clocks": clk.summary(),
-        "setup_s": info["setup_seconds"],
     }
-    if cpu:
-        line["cpu_baseline"] = cpu
+    line["roofline"] = roof
+    if kern:
+        line["kernels"] = kern
+    if sharded:
+        xb = info["exchange_bytes_per_iter"]
+        line["nccl"] = {"bytes_per_iter_per_rank": xb, "nvlink_term_us": xb / 900e9 * 1e6,
+                        "peak_gbs": 900.0, "peak_kind": "nominal NVLink 5 per direction",
+                        "frac_of_iteration": (xb / 900e9) / (ms_per_step / 1000.0)}
+    if not args.no_cpu_baseline:  # rank 0 only, after the GPU work
+        cb = cpu_baseline(args.config)
+        if cb:
+            line["cpu_baseline"] = cb
     print(json.dumps(line))
-    if ws > 1:
-        torch.distributed.destroy_process_group()
 
 
-def main():
+def relaunch_under_torchrun(args):
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-trace-objective", dest="trace_objective", action="store_false",
                     help="drop the per-iteration objective from the trace (default: on, as the "
                          "reference evaluates it every iteration, solvers.hpp:146; here by the "
                          "H-pass-free recurrence, DESIGN.md §2)")
-    args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    return ap.parse_args(argv)
+
+
+def main():
+    args = parse_args()
+    ws = int(os.environ.get("WORLD_SIZE", "0"))
+    if args.gpus > 1 and ws == 0:  # one process per GPU
+        sys.exit(relaunch_under_torchrun(args))
+    if ws and ws != args.gpus:
+        sys.exit(f"bench.py: WORLD_SIZE={ws} but --gpus {args.gpus}")
+    sys.path.insert(0, REPO)
     if args.impl == "reference":
-        bench_reference(args, cfg)
+        bench_reference(args)
     else:
-        bench_ours(args, cfg)
+        bench_ours(args)
 
 
 if __name__ == "__main__":

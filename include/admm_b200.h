@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define ADMM_B200_ABI_VERSION 1
+#define ADMM_B200_ABI_VERSION 2
 
 /* Exception classes of errors.hpp:10-81, in validation order. */
 typedef enum {
@@ -44,7 +44,9 @@ typedef enum {
   ADMM_E_CUDA = 7,        /* device / driver failure (no reference counterpart) */
   ADMM_E_STATE = 8,       /* API misuse (null pointer, wrong plan state) */
   ADMM_E_FORMAT = 9,      /* FormatError      errors.hpp:64 (byte offset: admm_cmat_error_offset) */
-  ADMM_E_IO = 10          /* IoError          errors.hpp:75 */
+  ADMM_E_IO = 10,         /* IoError          errors.hpp:75 */
+  ADMM_E_NCCL = 11,       /* NCCL failure in a multi-GPU plan (no reference counterpart) */
+  ADMM_E_OBSERVER = 12    /* the observer callback asked to stop (it raised) */
 } admm_status;
 
 /* The four solver entry points (reference.hpp:27, solvers.hpp:74,179,306). */
@@ -90,6 +92,8 @@ typedef struct {
   uint64_t batch;      /* 0/1: one scene; 2..64: independent scenes sharing H (BASELINE config 5):
                           g is n_meas x batch (scene fastest), solutions n_pix x batch, trace
                           iterations x batch x 3, lambda per scene via admm_plan_set_lambdas */
+  double noise_sigma;  /* SensingProblem::noise_sigma: validated (>= 0) after finiteness and
+                          before the partition, the order of problem.hpp:35-49 */
 } admm_plan_options;
 
 typedef struct admm_plan admm_plan;
@@ -106,7 +110,10 @@ typedef struct {
   const uint64_t* replica_len; /* n_workers */
   double primal, dual;         /* this iteration's residual norms */
 } admm_snapshot;
-typedef void (*admm_observer_fn)(const admm_snapshot* snap, void* user);
+/* Return 0 to continue; any other value stops the solve at once with ADMM_E_OBSERVER
+ * (an exception thrown by the reference's observer propagates out of the solver call,
+ * solvers.hpp:150-160: the shim and the Python mirror rethrow it). */
+typedef int (*admm_observer_fn)(const admm_snapshot* snap, void* user);
 
 /* Setup: validates (cfg -> problem -> partition -> Gram factor, the reference order),
  * uploads the blocks, forms rho I + H_b H_b^H and its inverse on the device.
@@ -143,6 +150,33 @@ admm_status admm_plan_attach(admm_plan* plan, int which, void* device_ptr);
 admm_status admm_plan_run_phase(admm_plan* plan, int phase);
 /* 1 = sweep, 2 = two-pass: the phase sequence the caller must drive. */
 admm_status admm_plan_schedule(const admm_plan* plan, int* schedule);
+
+/* ---- multi-GPU with plan-owned NCCL communicators ------------------
+ * A distributed plan is used exactly like a single-GPU plan (admm_plan_solve, _enqueue,
+ * _reset, _set_g, _set_lambda, _max_abs_adjoint, _read, _get_info): each GPU holds the
+ * shard of the M x N block grid given by admm_choose_grid, and the plan runs the shard's
+ * phases and the NCCL all-gathers of the exchanges (world communicator + row / column
+ * communicators split from it) on its own stream(s).  Solutions, traces and errors
+ * (NumericalError with last_good_iteration) are complete and identical on every rank and
+ * equal to the single-GPU plan's (all-gathers keep the reference's summation order).
+ * Replaces the reference's simulated node network (parallel_for + coordinator copies,
+ * solvers.hpp:109-166, 211-291, 343-453; its traffic is what CommLedger counts). */
+#define ADMM_NCCL_ID_BYTES 128
+/* A new NCCL unique id (rank 0 of a multi-process job creates it; the caller broadcasts). */
+admm_status admm_nccl_unique_id(unsigned char* id /* ADMM_NCCL_ID_BYTES */);
+/* Process grid Pr x Pc for `world` GPUs: consensus shards row blocks (Pr = world),
+ * sectioning column blocks (Pc = world), hybrid the grid with the most column ranks. */
+admm_status admm_choose_grid(int world, admm_method method, uint64_t M, uint64_t N, uint64_t* Pr, uint64_t* Pc);
+/* One process per GPU: rank `rank` of `nranks` (opts->device is this process's GPU).
+ * Collective: every rank calls it with the same arguments and id.  Each rank uploads only
+ * its own blocks of h. */
+admm_status admm_plan_create_dist(const admm_plan_options* opts, const admm_solver_config* cfg, uint64_t n_meas,
+                                  uint64_t n_pix, const void* h, admm_dtype h_dtype, const double* g,
+                                  const unsigned char* nccl_id, int nranks, int rank, admm_plan** out);
+/* One process, n_gpus distinct devices (device_ids, or 0..n_gpus-1 when NULL). */
+admm_status admm_plan_create_multi(const admm_plan_options* opts, const admm_solver_config* cfg, uint64_t n_meas,
+                                   uint64_t n_pix, const void* h, admm_dtype h_dtype, const double* g, int n_gpus,
+                                   const int* device_ids, admm_plan** out);
 
 /* Replace the measurement vector g (H, the partition and the factors are kept). */
 admm_status admm_plan_set_g(admm_plan* plan, const double* g);
@@ -197,6 +231,9 @@ typedef struct {
   uint64_t slab_cluster;        /* slab sweep: thread-block cluster size (CTAs per strip) */
   uint64_t slab_row_bytes;      /* slab sweep: bytes per strip row (64 or 32) */
   uint64_t slab_rows;           /* slab sweep: rows per warp slab */
+  uint64_t grid_pr, grid_pc;    /* process grid of a multi-GPU plan (1 x 1 on one GPU) */
+  uint64_t n_ranks;             /* GPUs of the plan */
+  uint64_t exchange_bytes_per_iter; /* NCCL bytes this rank receives per iteration */
 } admm_plan_info;
 admm_status admm_plan_get_info(const admm_plan* plan, admm_plan_info* info);
 
@@ -217,9 +254,25 @@ admm_status admm_adjoint_matvec(const double* a, uint64_t rows, uint64_t cols, c
                                 double* y, int device);
 /* out = S_kappa(a) element-wise (prox.hpp:21-25). */
 admm_status admm_soft_threshold(const double* a, uint64_t n, double kappa, double* out, int device);
-/* x = (H^H H + rho I)^-1 rhs (GramSolver::solve, gram.hpp:63-78). */
+/* x = (H^H H + rho I)^-1 rhs (GramSolver::solve, gram.hpp:63-78), one-shot. */
 admm_status admm_gram_solve(const double* h, uint64_t rows, uint64_t cols, double rho,
                             const double* rhs, double* x, int device);
+
+/* GramSolver (gram.hpp:26-128) as a device object: validated and factored ONCE at
+ * creation (gram.hpp:48-53), then solve() any number of times (serialised internally, so
+ * concurrent callers are safe, gram.hpp:25).
+ *   strategy: -1 automatic (strategy_for, gram.hpp:32-34: Woodbury iff rows < cols),
+ *             0 Direct   ((H^H H + rho I)^-1, cols x cols, applied to rhs),
+ *             1 Woodbury ((rho I + H H^H)^-1, rows x rows, through the inversion lemma).
+ * Errors in the reference's order: ParameterError (empty block, rho <= 0), NumericalError
+ * (non-finite block), SingularityError (factor breakdown). */
+typedef struct admm_gram admm_gram;
+admm_status admm_gram_create(const double* h, uint64_t rows, uint64_t cols, double rho, int strategy, int device,
+                             admm_gram** out);
+admm_status admm_gram_apply(admm_gram* g, const double* rhs, double* x);
+/* strategy actually used (0 Direct, 1 Woodbury) and the factored dimension (inner_dim). */
+admm_status admm_gram_info(const admm_gram* g, int* strategy, uint64_t* inner_dim);
+void admm_gram_destroy(admm_gram* g);
 
 /* ---- input tooling (host; not the hot path) */
 /* gen_problem (generate.hpp:32-89) with the reference's RNG stream (rng.hpp); H is

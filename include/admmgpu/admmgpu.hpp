@@ -12,6 +12,11 @@
 //   SolveReport report.hpp:16   IterateSnapshot report.hpp:28   CommLedger comm.hpp:45
 //   errors errors.hpp:10-81   GramSolver gram.hpp:26   matvec/adjoint_matvec linalg.hpp:97/114
 //   read_cmat/write_cmat/read_cvec/write_cvec cmat_io.hpp:44-125
+//
+// Beyond the reference: SolveOptions::devices (several GPUs, plan-owned NCCL), ProblemRef
+// (a non-owning view: the reference's own SensingProblem -- same memory layout -- or a
+// complex64 H, passed to the device without a host copy), and admmgpu/admmsplit_dropin.hpp,
+// which takes and returns the reference's own types (namespace admmsplit).
 #pragma once
 
 #include <algorithm>
@@ -19,7 +24,10 @@
 #include <complex>
 #include <cstddef>
 #include <cstdint>
+#include <exception>
 #include <functional>
+#include <memory>
+#include <mutex>
 #include <optional>
 #include <stdexcept>
 #include <string>
@@ -60,6 +68,7 @@ class FormatError : public Error {
 };
 class IoError : public Error { public: using Error::Error; };
 class DeviceError : public Error { public: using Error::Error; };  // ADMM_E_CUDA
+class NcclError : public Error { public: using Error::Error; };    // ADMM_E_NCCL
 
 inline void check(admm_status st) {
   if (st == ADMM_OK) return;
@@ -74,6 +83,7 @@ inline void check(admm_status st) {
     case ADMM_E_CUDA: throw DeviceError(msg);
     case ADMM_E_FORMAT: throw FormatError(msg, admm_cmat_error_offset());
     case ADMM_E_IO: throw IoError(msg);
+    case ADMM_E_NCCL: throw NcclError(msg);
     default: throw Error(msg);
   }
 }
@@ -235,10 +245,51 @@ struct SolveOptions {
   bool ragged = false;
   IterateObserver observer;
   // B200 knobs
-  admm_dtype dtype = ADMM_C128;
+  admm_dtype dtype = ADMM_C128;  // storage of the streamed matrices (iterates stay FP64)
   int device = 0;
   bool trace_objective = true;
+  std::vector<int> devices;      // non-empty: one shard per listed GPU, plan-owned NCCL
 };
+
+// Non-owning view of a sensing problem: H row-major interleaved (re, im) of h_dtype, g and
+// the optional truth complex128.  Any type with the reference's members (h.data(),
+// h.rows(), h.cols(), g, truth, noise_sigma) converts through view(); H is read straight
+// from the caller's memory by the upload (no host copy), complex64 included.
+struct ProblemRef {
+  const void* h = nullptr;
+  admm_dtype h_dtype = ADMM_C128;
+  std::size_t rows = 0, cols = 0;
+  const Complex* g = nullptr;
+  std::size_t g_size = 0;
+  const CVector* truth = nullptr;
+  double noise_sigma = 0.0;
+};
+template <class Problem>
+ProblemRef view(const Problem& p) {
+  ProblemRef r;
+  r.h = p.h.data();
+  r.rows = p.h.empty() ? 0 : p.h.rows();
+  r.cols = p.h.empty() ? 0 : p.h.cols();
+  r.g = p.g.data();
+  r.g_size = p.g.size();
+  r.truth = p.truth ? &*p.truth : nullptr;
+  r.noise_sigma = p.noise_sigma;
+  return r;
+}
+// complex64 H (e.g. the c64 configs' 32 GiB operator) with a complex128 g.
+inline ProblemRef view_c64(const std::complex<float>* h, std::size_t rows, std::size_t cols, const CVector& g,
+                           const CVector* truth = nullptr, double noise_sigma = 0.0) {
+  ProblemRef r;
+  r.h = h;
+  r.h_dtype = ADMM_C64;
+  r.rows = rows;
+  r.cols = cols;
+  r.g = g.data();
+  r.g_size = g.size();
+  r.truth = truth;
+  r.noise_sigma = noise_sigma;
+  return r;
+}
 
 namespace detail {
 
@@ -253,10 +304,12 @@ inline std::vector<std::size_t> split_bounds(std::size_t total, std::size_t part
 struct ObserverCtx {
   const IterateObserver* obs;
   std::vector<std::size_t> cb;
+  std::exception_ptr raised;  // an exception of the observer, rethrown after the solve
 };
 
-inline void observer_trampoline(const admm_snapshot* s, void* user) {
+inline int observer_trampoline(const admm_snapshot* s, void* user) {
   auto* ctx = static_cast<ObserverCtx*>(user);
+  try {
   IterateSnapshot snap;
   snap.iteration = s->iteration;
   const auto* v = reinterpret_cast<const Complex*>(s->v);
@@ -272,11 +325,17 @@ inline void observer_trampoline(const admm_snapshot* s, void* user) {
     snap.segment_v_prev.emplace_back(snap.v_prev.begin() + ctx->cb[j], snap.v_prev.begin() + ctx->cb[j + 1]);
   }
   (*ctx->obs)(snap);
+  } catch (...) {
+    ctx->raised = std::current_exception();
+    return 1;  // stop the solve; solve() rethrows (solvers.hpp:150-160: the observer's exception propagates)
+  }
+  return 0;
 }
 
 // Fills the ledger with the reference's per-iteration records (solvers.hpp:111,128,
 // 219-224, 358-369, 400).
-inline void fill_ledger(CommLedger& led, admm_method m, const std::vector<std::size_t>& rb,
+template <class Ledger>
+inline void fill_ledger(Ledger& led, admm_method m, const std::vector<std::size_t>& rb,
                         const std::vector<std::size_t>& cb, std::size_t iters) {
   const std::size_t M = rb.size() - 1, N = cb.size() - 1, nm = rb.back(), np = cb.back();
   for (std::size_t k = 0; k < iters; ++k) {
@@ -307,38 +366,54 @@ inline void fill_ledger(CommLedger& led, admm_method m, const std::vector<std::s
   }
 }
 
-inline SolveReport solve(admm_method method, const SensingProblem& problem, const SolverConfig& cfg,
-                         std::size_t m, std::size_t n, const SolveOptions& opts) {
+// Host validation in the reference's order (admm_core.hpp:26-34, problem.hpp:35-49; the
+// device side scans H and g for non-finite entries, then checks noise_sigma, then the
+// partition -- the same order), plan creation (single GPU, or one shard per device),
+// solve, and the reference's report fields.
+inline SolveReport solve(admm_method method, const ProblemRef& problem, const SolverConfig& cfg, std::size_t m,
+                         std::size_t n, const SolveOptions& opts) {
   cfg.validate();
-  if (problem.h.empty()) throw DimensionError("SensingProblem: empty sensing matrix");
-  if (problem.g.size() != problem.h.rows())
-    throw DimensionError("SensingProblem: g length " + std::to_string(problem.g.size()) + " != H rows " +
-                         std::to_string(problem.h.rows()));
+  if (!problem.h || problem.rows == 0 || problem.cols == 0) throw DimensionError("SensingProblem: empty sensing matrix");
+  if (problem.g_size != problem.rows)
+    throw DimensionError("SensingProblem: g length " + std::to_string(problem.g_size) + " != H rows " +
+                         std::to_string(problem.rows));
+  if (problem.truth && problem.truth->size() != problem.cols)
+    throw DimensionError("SensingProblem: truth length " + std::to_string(problem.truth->size()) + " != H cols " +
+                         std::to_string(problem.cols));
+  if (problem.truth)
+    for (const Complex& z : *problem.truth)
+      if (!std::isfinite(z.real()) || !std::isfinite(z.imag())) throw NumericalError("SensingProblem: non-finite entries");
   admm_plan_options o{};
   o.method = method;
   o.M = m;
   o.N = n;
   o.ragged = opts.ragged ? 1 : 0;
   o.dtype = opts.dtype;
-  o.device = opts.device;
+  o.device = opts.devices.empty() ? opts.device : opts.devices[0];
   o.trace_objective = opts.trace_objective ? 1 : 0;
+  o.noise_sigma = problem.noise_sigma;
   admm_solver_config c{cfg.rho, cfg.lambda, cfg.scl, cfg.max_iters, cfg.eps_pri, cfg.eps_dual, cfg.seed};
   admm_plan* plan = nullptr;
-  check(admm_plan_create(&o, &c, problem.h.rows(), problem.h.cols(), problem.h.data(), ADMM_C128,
-                         reinterpret_cast<const double*>(problem.g.data()), &plan));
+  const double* g = reinterpret_cast<const double*>(problem.g);
+  if (opts.devices.empty())
+    check(admm_plan_create(&o, &c, problem.rows, problem.cols, problem.h, problem.h_dtype, g, &plan));
+  else
+    check(admm_plan_create_multi(&o, &c, problem.rows, problem.cols, problem.h, problem.h_dtype, g,
+                                 (int)opts.devices.size(), opts.devices.data(), &plan));
   const std::size_t M = method == ADMM_CONSENSUS || method == ADMM_HYBRID ? m : 1;
   const std::size_t N = method == ADMM_SECTIONING || method == ADMM_HYBRID ? n : 1;
-  const auto rb = split_bounds(problem.h.rows(), M, opts.ragged);
-  const auto cb = split_bounds(problem.h.cols(), N, opts.ragged);
+  const auto rb = split_bounds(problem.rows, M, opts.ragged);
+  const auto cb = split_bounds(problem.cols, N, opts.ragged);
   SolveReport r;
-  r.solution.assign(problem.h.cols(), Complex());
+  r.solution.assign(problem.cols, Complex());
   std::vector<double> tr(cfg.max_iters * 3, 0.0);
   std::uint64_t it = 0;
   double obj = 0.0;
-  ObserverCtx ctx{&opts.observer, cb};
+  ObserverCtx ctx{&opts.observer, cb, nullptr};
   const admm_status st = admm_plan_solve(plan, reinterpret_cast<double*>(r.solution.data()), tr.data(), &it, &obj,
                                          opts.observer ? observer_trampoline : nullptr, &ctx);
   admm_plan_destroy(plan);
+  if (ctx.raised) std::rethrow_exception(ctx.raised);
   check(st);
   for (std::size_t k = 0; k < it; ++k) r.trace.push(tr[3 * k], tr[3 * k + 1], tr[3 * k + 2]);
   r.iterations_run = it;
@@ -350,21 +425,38 @@ inline SolveReport solve(admm_method method, const SensingProblem& problem, cons
 
 }  // namespace detail
 
-inline SolveReport lasso_admm_reference(const SensingProblem& p, const SolverConfig& cfg,
-                                        const SolveOptions& opts = {}) {
+// The reference's entry points (reference.hpp:27, solvers.hpp:74/179/306).  Each takes the
+// shim's SensingProblem or a ProblemRef (view(reference_problem), view_c64(...)).
+inline SolveReport lasso_admm_reference(const ProblemRef& p, const SolverConfig& cfg, const SolveOptions& opts = {}) {
   return detail::solve(ADMM_REFERENCE, p, cfg, 1, 1, opts);
 }
-inline SolveReport consensus_solve(const SensingProblem& p, const SolverConfig& cfg, std::size_t m,
+inline SolveReport consensus_solve(const ProblemRef& p, const SolverConfig& cfg, std::size_t m,
                                    const SolveOptions& opts = {}) {
   return detail::solve(ADMM_CONSENSUS, p, cfg, m, 1, opts);
 }
-inline SolveReport sectioning_solve(const SensingProblem& p, const SolverConfig& cfg, std::size_t n,
+inline SolveReport sectioning_solve(const ProblemRef& p, const SolverConfig& cfg, std::size_t n,
                                     const SolveOptions& opts = {}) {
   return detail::solve(ADMM_SECTIONING, p, cfg, 1, n, opts);
 }
-inline SolveReport hybrid_solve(const SensingProblem& p, const SolverConfig& cfg, std::size_t m, std::size_t n,
+inline SolveReport hybrid_solve(const ProblemRef& p, const SolverConfig& cfg, std::size_t m, std::size_t n,
                                 const SolveOptions& opts = {}) {
   return detail::solve(ADMM_HYBRID, p, cfg, m, n, opts);
+}
+inline SolveReport lasso_admm_reference(const SensingProblem& p, const SolverConfig& cfg,
+                                        const SolveOptions& opts = {}) {
+  return lasso_admm_reference(view(p), cfg, opts);
+}
+inline SolveReport consensus_solve(const SensingProblem& p, const SolverConfig& cfg, std::size_t m,
+                                   const SolveOptions& opts = {}) {
+  return consensus_solve(view(p), cfg, m, opts);
+}
+inline SolveReport sectioning_solve(const SensingProblem& p, const SolverConfig& cfg, std::size_t n,
+                                    const SolveOptions& opts = {}) {
+  return sectioning_solve(view(p), cfg, n, opts);
+}
+inline SolveReport hybrid_solve(const SensingProblem& p, const SolverConfig& cfg, std::size_t m, std::size_t n,
+                                const SolveOptions& opts = {}) {
+  return hybrid_solve(view(p), cfg, m, n, opts);
 }
 
 // ---- linalg.hpp:97-127, prox.hpp:21-25 on the device ------------------------------
@@ -390,36 +482,54 @@ inline CVector soft_threshold_vec(const CVector& a, double kappa, int device = 0
 }
 
 // ---- gram.hpp:26-128 -------------------------------------------------------------
+// Validated and factored ONCE on the device at construction (gram.hpp:48-53); solve() runs
+// the stored factor (Woodbury: the rows x rows inverse through the inversion lemma; Direct:
+// the cols x cols inverse).  Immutable; copies share the device factor; solve() is safe to
+// call concurrently (gram.hpp:25).
 class GramSolver {
  public:
   enum class Strategy { Direct, Woodbury };
   static Strategy strategy_for(std::size_t rows, std::size_t cols) {
     return rows < cols ? Strategy::Woodbury : Strategy::Direct;
   }
-  GramSolver(CMatrix block, double rho, int device = 0) : h_(std::move(block)), rho_(rho), device_(device) {
-    if (h_.empty()) throw ParameterError("GramSolver: empty block");
-    if (!(rho > 0.0)) throw ParameterError("GramSolver: rho must be positive");
-    for (std::size_t i = 0; i < h_.size(); ++i)
-      if (!std::isfinite(h_.data()[i].real()) || !std::isfinite(h_.data()[i].imag()))
-        throw NumericalError("GramSolver: non-finite entries in block");
-    strategy_ = strategy_for(h_.rows(), h_.cols());
+  GramSolver(std::shared_ptr<const CMatrix> block, double rho) : GramSolver(std::move(block), rho, std::nullopt) {}
+  GramSolver(CMatrix block, double rho) : GramSolver(std::make_shared<const CMatrix>(std::move(block)), rho) {}
+  GramSolver(CMatrix block, double rho, Strategy strategy)
+      : GramSolver(std::make_shared<const CMatrix>(std::move(block)), rho, strategy) {}
+  GramSolver(std::shared_ptr<const CMatrix> block, double rho, std::optional<Strategy> strategy, int device = 0)
+      : block_(std::move(block)), rho_(rho) {
+    admm_gram* g = nullptr;
+    const int s = strategy ? (*strategy == Strategy::Woodbury ? 1 : 0) : -1;
+    check(admm_gram_create(reinterpret_cast<const double*>(block_->empty() ? nullptr : block_->data()),
+                           block_->empty() ? 0 : block_->rows(), block_->empty() ? 0 : block_->cols(), rho, s, device,
+                           &g));
+    factor_.reset(g, admm_gram_destroy);
+    int used = 1;
+    std::uint64_t dim = 0;
+    check(admm_gram_info(g, &used, &dim));
+    strategy_ = used ? Strategy::Woodbury : Strategy::Direct;
+    inner_ = dim;
   }
   Strategy strategy() const { return strategy_; }
   double rho() const { return rho_; }
-  std::size_t inner_dim() const { return strategy_ == Strategy::Woodbury ? h_.rows() : h_.cols(); }
+  const CMatrix& block() const { return *block_; }
+  std::size_t inner_dim() const { return inner_; }
   CVector solve(const CVector& rhs) const {
-    if (rhs.size() != h_.cols()) throw DimensionError("GramSolver::solve: rhs length mismatch");
+    if (rhs.size() != block_->cols())
+      throw DimensionError("GramSolver::solve: rhs length " + std::to_string(rhs.size()) + " != block cols " +
+                           std::to_string(block_->cols()));
     CVector x(rhs.size());
-    check(admm_gram_solve(reinterpret_cast<const double*>(h_.data()), h_.rows(), h_.cols(), rho_,
-                          reinterpret_cast<const double*>(rhs.data()), reinterpret_cast<double*>(x.data()), device_));
+    check(admm_gram_apply(factor_.get(), reinterpret_cast<const double*>(rhs.data()), reinterpret_cast<double*>(x.data())));
     return x;
   }
  private:
-  CMatrix h_;
+  std::shared_ptr<const CMatrix> block_;
   double rho_;
-  int device_;
-  Strategy strategy_;
+  Strategy strategy_ = Strategy::Woodbury;
+  std::size_t inner_ = 0;
+  std::shared_ptr<admm_gram> factor_;
 };
+inline GramSolver make_gram_solver(CMatrix block, double rho) { return GramSolver(std::move(block), rho); }
 
 // ---- cmat_io.hpp:44-125 (host file I/O; CMX1 = the reference format) ----------------
 // Same names, checks and exceptions as the reference.  write_cmat's `c64` flag writes the

@@ -27,7 +27,8 @@ class SolverConfigC(ctypes.Structure):
 
 class PlanOptionsC(ctypes.Structure):
     _fields_ = [("method", _i32), ("M", _u64), ("N", _u64), ("ragged", _i32), ("dtype", _i32),
-                ("device", _i32), ("trace_objective", _i32), ("schedule", _i32), ("batch", _u64)]
+                ("device", _i32), ("trace_objective", _i32), ("schedule", _i32), ("batch", _u64),
+                ("noise_sigma", _dbl)]
 
 
 class SnapshotC(ctypes.Structure):
@@ -43,16 +44,20 @@ class PlanInfoC(ctypes.Structure):
                 ("launches_per_iter", _u64), ("grid_gemv_n", _u64), ("grid_gemv_h", _u64),
                 ("setup_seconds", _dbl), ("inner_dim_max", _u64), ("schedule", _u64),
                 ("grid_sweep", _u64), ("hbm_bytes_per_iter", _u64), ("sweep_variant", _u64),
-                ("slab_cluster", _u64), ("slab_row_bytes", _u64), ("slab_rows", _u64)]
+                ("slab_cluster", _u64), ("slab_row_bytes", _u64), ("slab_rows", _u64),
+                ("grid_pr", _u64), ("grid_pc", _u64), ("n_ranks", _u64), ("exchange_bytes_per_iter", _u64)]
 
 
 class ShardC(ctypes.Structure):
     _fields_ = [("Pr", _u64), ("Pc", _u64), ("pr", _u64), ("pc", _u64)]
 
 
-OBSERVER = ctypes.CFUNCTYPE(None, ctypes.POINTER(SnapshotC), ctypes.c_void_p)
+OBSERVER = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.POINTER(SnapshotC), ctypes.c_void_p)
 
 lib = ctypes.CDLL(LIB_PATH)
+ABI_VERSION = 2
+if lib.admm_abi_version() != ABI_VERSION:
+    raise ImportError(f"{LIB_PATH}: ABI {lib.admm_abi_version()} != {ABI_VERSION}; rebuild (__graft_entry__.build())")
 
 _SIGS = {
     "admm_abi_version": ([], _i32),
@@ -62,6 +67,12 @@ _SIGS = {
                           _ptr, _i32, _ptr, ctypes.POINTER(_ptr)], _i32),
     "admm_plan_create_sharded": ([ctypes.POINTER(PlanOptionsC), ctypes.POINTER(SolverConfigC), _u64, _u64,
                                   _ptr, _i32, _ptr, ctypes.POINTER(ShardC), ctypes.POINTER(_ptr)], _i32),
+    "admm_nccl_unique_id": ([_ptr], _i32),
+    "admm_choose_grid": ([_i32, _i32, _u64, _u64, ctypes.POINTER(_u64), ctypes.POINTER(_u64)], _i32),
+    "admm_plan_create_dist": ([ctypes.POINTER(PlanOptionsC), ctypes.POINTER(SolverConfigC), _u64, _u64,
+                               _ptr, _i32, _ptr, ctypes.c_char_p, _i32, _i32, ctypes.POINTER(_ptr)], _i32),
+    "admm_plan_create_multi": ([ctypes.POINTER(PlanOptionsC), ctypes.POINTER(SolverConfigC), _u64, _u64,
+                                _ptr, _i32, _ptr, _i32, _ptr, ctypes.POINTER(_ptr)], _i32),
     "admm_plan_exchange_info": ([_ptr, _i32, ctypes.POINTER(_u64), ctypes.POINTER(_u64),
                                  ctypes.POINTER(_u64)], _i32),
     "admm_plan_attach": ([_ptr, _i32, _ptr], _i32),
@@ -88,6 +99,10 @@ _SIGS = {
     "admm_adjoint_matvec": ([_ptr, _u64, _u64, _ptr, _ptr, _i32], _i32),
     "admm_soft_threshold": ([_ptr, _u64, _dbl, _ptr, _i32], _i32),
     "admm_gram_solve": ([_ptr, _u64, _u64, _dbl, _ptr, _ptr, _i32], _i32),
+    "admm_gram_create": ([_ptr, _u64, _u64, _dbl, _i32, _i32, ctypes.POINTER(_ptr)], _i32),
+    "admm_gram_apply": ([_ptr, _ptr, _ptr], _i32),
+    "admm_gram_info": ([_ptr, ctypes.POINTER(_i32), ctypes.POINTER(_u64)], _i32),
+    "admm_gram_destroy": ([_ptr], None),
     "admm_gen_problem": ([_u64, _u64, _u64, _dbl, _u64, _i32, _ptr, _i32, _ptr, _ptr, _ptr], _i32),
     "admm_cmat_info": ([ctypes.c_char_p, ctypes.POINTER(_u64), ctypes.POINTER(_u64), ctypes.POINTER(_i32)], _i32),
     "admm_cmat_read": ([ctypes.c_char_p, _ptr, _u64, _i32], _i32),

@@ -565,47 +565,147 @@ zfinal_kernel(ColVecs cv, const double2* __restrict__ outbox, const BlockDesc* _
   if (threadIdx.x == 0) red[2 * nct + cta] = r;
 }
 
-// This rank's iteration scalars (rp2, rd2, l1, non-finite) into its slot of the
-// scalar exchange buffer (all-gathered over all ranks).
-__global__ void local_scalars_kernel(const double* __restrict__ red, uint32_t n, double* __restrict__ slot,
-                                     IterState* st) {
+// Scalar slot of one rank in the exchange (doubles): rp2, rd2, |v|_1, non-finite flag,
+// objective rows |Hv - g|^2 partial, spare.
+constexpr int kScalDoubles = 8;
+
+// This rank's iteration scalars (rp2, rd2, l1, non-finite; objective-rows partials when
+// objp != null) into its slot of the scalar exchange buffer (all-gathered over all ranks).
+__global__ void local_scalars_kernel(const double* __restrict__ red, uint32_t n, const double* __restrict__ objp,
+                                     uint32_t nobj, double* __restrict__ slot, IterState* st) {
   __shared__ double sm[kCtaWarps];
-  double a = 0.0, d = 0.0, l = 0.0;
+  double a = 0.0, d = 0.0, l = 0.0, o = 0.0;
   for (uint32_t k = threadIdx.x; k < n; k += kCtaThreads) {
     a += red[k];
     d += red[n + k];
     l += red[2 * n + k];
   }
+  if (objp)
+    for (uint32_t k = threadIdx.x; k < nobj; k += kCtaThreads) o += objp[k];
   a = block_sum<kCtaThreads>(a, sm);
   d = block_sum<kCtaThreads>(d, sm);
   l = block_sum<kCtaThreads>(l, sm);
+  o = block_sum<kCtaThreads>(o, sm);
   if (threadIdx.x == 0) {
     slot[0] = a;
     slot[1] = d;
     slot[2] = l;
     slot[3] = st->nonfinite ? 1.0 : 0.0;
+    slot[4] = o;
     st->nonfinite = 0u;
   }
 }
 
+// Objective of a sharded plan (admm_core.hpp:60-64 without an H pass; the recurrence of
+// objective_rec_kernel): a_b of every LOCAL block into the A region of its ghat exchange
+// slot (gathered over the row communicator with ghat), h_b updated.  Skipped while
+// st->iter < min_iter (the two-pass schedule computes the previous iteration's a_b).
+__global__ void __launch_bounds__(kCtaThreads)
+objective_arec_kernel(RowVecs rv, double2* __restrict__ hs, const BlockDesc* __restrict__ blocks, uint64_t aoff,
+                      const IterState* st, uint64_t min_iter) {
+  const BlockDesc bd = blocks[blockIdx.y];
+  const uint32_t row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= bd.rows || st->iter < min_iter) return;
+  const uint64_t o = (uint64_t)bd.mvec_off + row;
+  const double2 w = csub(rv.gij[o], rv.r[o]);
+  const double2 a = cscale(cadd(cadd(w, hs[o]), rv.ghat[o]), 0.5);
+  hs[o] = csub(a, w);
+  rv.ghat[o + aoff] = a;
+}
+
+// After the gather: |sum_q a_iq - g_i|^2 per row of the local row blocks (ascending q over
+// ALL N column blocks, every a_iq from the gathered A regions), per-CTA partials (zero when
+// count == 0 or st->iter < min_iter: that rank's rows are counted by another rank).
+__global__ void __launch_bounds__(kCtaThreads)
+objective_grows_kernel(const double2* __restrict__ g, const double2* __restrict__ xg, uint64_t aoff,
+                       const BlockDesc* __restrict__ gblocks, uint32_t N, uint32_t i0, int count,
+                       const IterState* st, uint64_t min_iter, double* __restrict__ objp) {
+  __shared__ double sm[kCtaWarps];
+  const uint32_t i = i0 + blockIdx.y;
+  const BlockDesc b0 = gblocks[i * N];
+  const uint32_t row = blockIdx.x * blockDim.x + threadIdx.x;
+  double q = 0.0;
+  if (count && row < b0.rows && st->iter >= min_iter) {
+    double2 hv = make_double2(0.0, 0.0);
+    for (uint32_t jj = 0; jj < N; ++jj) hv = cadd(hv, xg[gblocks[i * N + jj].mvec_off + aoff + row]);
+    q = cabs2(csub(hv, g[b0.row0 + row]));
+  }
+  const double r = block_sum<kCtaThreads>(q, sm);
+  if (threadIdx.x == 0) objp[blockIdx.y * gridDim.x + blockIdx.x] = r;
+}
+
+// Final objective pass of a sharded plan: a_b = H_b v_j (row sums of gemv_n partials) into
+// the A region of the ghat slot.
+__global__ void __launch_bounds__(kCtaThreads)
+arows_kernel(double2* __restrict__ xg, uint64_t aoff, const double2* __restrict__ part,
+             const MatDesc* __restrict__ mats, const BlockDesc* __restrict__ blocks, uint64_t U, uint64_t P) {
+  const uint32_t b = blockIdx.y;
+  const BlockDesc bd = blocks[b];
+  const uint32_t row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row < bd.rows) xg[(uint64_t)bd.mvec_off + aoff + row] = sum_rows_part(part, mats[b], row, U, P);
+}
+
+// Final objective pass: slot[4] = sum of the rows partials, slot[2] = |v|_1 of the local
+// segments (when count_v: one rank per column block counts them).
+__global__ void obj_scalars_kernel(const double* __restrict__ objp, uint32_t nobj, const double2* __restrict__ v,
+                                   const BlockDesc* __restrict__ blocks, uint32_t Nc, int count_v,
+                                   double* __restrict__ slot) {
+  __shared__ double sm[kCtaWarps];
+  double o = 0.0, l = 0.0;
+  for (uint32_t k = threadIdx.x; k < nobj; k += kCtaThreads) o += objp[k];
+  if (count_v)
+    for (uint32_t jl = 0; jl < Nc; ++jl) {
+      const BlockDesc bd = blocks[jl];
+      for (uint32_t t = threadIdx.x; t < bd.cols; t += kCtaThreads) {
+        const double2 x = v[bd.seg_off + t];
+        l += hypot(x.x, x.y);
+      }
+    }
+  o = block_sum<kCtaThreads>(o, sm);
+  l = block_sum<kCtaThreads>(l, sm);
+  if (threadIdx.x == 0) {
+    slot[2] = l;
+    slot[4] = o;
+  }
+}
+
 // Close an iteration from the all-gathered scalars (rank order): trace[k] and the
-// non-finite bookkeeping, identically on every rank.
+// non-finite bookkeeping, identically on every rank.  Objective (obj_mode):
+//   0  none (NaN);
+//   1  two-pass, lagged: trace[k-1] from the gathered rows partials of this iteration and
+//      the |v|_1 of iteration k-1 (kept in *l1prev); trace[k] is filled next iteration or
+//      by the final exact pass;
+//   2  sweep (Pr == 1): trace[k] from this rank's complete rows sum (objp, every rank holds
+//      all rows after the gather) and the gathered |v|_1.
 __global__ void close_kernel(const double* __restrict__ all, uint32_t nranks, uint64_t stride,
                              const Params* __restrict__ prm, double* __restrict__ trace, uint64_t trace_cap,
-                             IterState* st) {
+                             IterState* st, int obj_mode, const double* __restrict__ objp, uint32_t nobj,
+                             double* __restrict__ l1prev) {
+  __shared__ double sm[kCtaWarps];
+  double o = 0.0;
+  if (obj_mode == 2)
+    for (uint32_t k = threadIdx.x; k < nobj; k += kCtaThreads) o += objp[k];
+  o = block_sum<kCtaThreads>(o, sm);
   if (threadIdx.x != 0) return;
-  double a = 0.0, d = 0.0;
+  double a = 0.0, d = 0.0, l = 0.0, og = 0.0;
   bool bad = false;
   for (uint32_t r = 0; r < nranks; ++r) {  // rank order; `stride` doubles between rank slots
     a += all[stride * r];
     d += all[stride * r + 1];
+    l += all[stride * r + 2];
     bad |= all[stride * r + 3] != 0.0;
+    og += all[stride * r + 4];
   }
   const uint64_t k = st->iter;
+  const double nan = __longlong_as_double(0x7ff8000000000000ll);
   if (k < trace_cap) {
     trace[3 * k] = sqrt(a);
     trace[3 * k + 1] = sqrt(prm->rho * prm->rho * prm->m_rep * d);
-    trace[3 * k + 2] = __longlong_as_double(0x7ff8000000000000ll);
+    trace[3 * k + 2] = obj_mode == 2 ? 0.5 * o + prm->lambda * l : nan;
+  }
+  if (obj_mode == 1) {
+    if (k >= 1 && k - 1 < trace_cap) trace[3 * (k - 1) + 2] = 0.5 * og + prm->lambda * *l1prev;
+    *l1prev = l;
   }
   if (bad && st->first_bad == ~0ull) st->first_bad = k;
   st->iter = k + 1;

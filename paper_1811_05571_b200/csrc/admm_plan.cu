@@ -15,6 +15,7 @@
 #include <functional>
 #include <limits>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <type_traits>
 #include <thread>
@@ -209,6 +210,16 @@ struct admm_plan {
   DevBuf dres_cta, dres_seg, dres_w, dres_red, dres_opart, dres_abuf, dres_lprev, dres_bar, dghat2;
   uint32_t res_P = 0, res_cols = 0;
   bool is_shard = false;  // created by admm_plan_create_sharded (driven phase by phase)
+  // sharded objective (admm_kernels.cuh objective_arec/grows): offset of the A region in a
+  // ghat slot (0: no per-iteration objective), rows partials, |v|_1 of the previous iteration
+  uint64_t aoff = 0;
+  bool shard_obj = false;   // sharded plan with the per-iteration objective
+  uint32_t objgx = 1;
+  DevBuf dobjp, dl1prev;
+  // multi-GPU with plan-owned NCCL communicators (admm_dist.inc): a rank of a distributed
+  // plan (dist != null), or a single-process container of one sub-plan per device (subs)
+  struct Dist* dist = nullptr;
+  std::vector<admm_plan*> subs;
   size_t res_smem = 0;
   uint64_t trace_cap = 0;
   cudaGraphExec_t exec = nullptr;
@@ -220,10 +231,7 @@ struct admm_plan {
   // host scratch for snapshots
   std::vector<double> h_v, h_vprev, h_u, h_seg;
 
-  ~admm_plan() {
-    if (exec) cudaGraphExecDestroy(exec);
-    if (own_stream) cudaStreamDestroy(own_stream);
-  }
+  ~admm_plan();
 };
 
 namespace {
@@ -913,25 +921,22 @@ void upload_h(admm_plan* p, const void* h, admm_dtype h_dtype) {
                            (size_t)bd.cols * sizeof(S), bd.rows, cudaMemcpyHostToDevice, p->stream));
       continue;
     }
-    // convert through an FP64 staging buffer, a slab of rows at a time
-    const uint64_t slab = std::max<uint64_t>(1, (tmp.bytes / 16) / std::max<uint32_t>(bd.cols, 1));
+    // convert through a device staging buffer in the host's element type, a slab of rows
+    // at a time (c128 -> c64 rounds, c64 -> c128 widens; scl applied in FP64)
+    const uint64_t slab = std::max<uint64_t>(1, (tmp.bytes / hsz) / std::max<uint32_t>(bd.cols, 1));
     for (uint64_t r0 = 0; r0 < bd.rows; r0 += slab) {
       const uint32_t nr = (uint32_t)std::min<uint64_t>(slab, bd.rows - r0);
-      if (h_dtype == ADMM_C64) {  // float host -> widen on the host side of the copy
-        std::vector<double> w((size_t)nr * bd.cols * 2);
-        const float* fs = reinterpret_cast<const float*>(src) + r0 * p->n_pix * 2;
-        for (uint32_t r = 0; r < nr; ++r)
-          for (uint32_t c = 0; c < 2 * bd.cols; ++c) w[(size_t)r * 2 * bd.cols + c] = fs[(size_t)r * 2 * p->n_pix + c];
-        CK(cudaMemcpyAsync(tmp.p, w.data(), w.size() * 8, cudaMemcpyHostToDevice, p->stream));
-        CK(cudaStreamSynchronize(p->stream));
-      } else {
-        CK(cudaMemcpy2DAsync(tmp.p, (size_t)bd.cols * 16, src + r0 * p->n_pix * hsz, p->n_pix * hsz,
-                             (size_t)bd.cols * 16, nr, cudaMemcpyHostToDevice, p->stream));
-      }
+      CK(cudaMemcpy2DAsync(tmp.p, (size_t)bd.cols * hsz, src + r0 * p->n_pix * hsz, p->n_pix * hsz,
+                           (size_t)bd.cols * hsz, nr, cudaMemcpyHostToDevice, p->stream));
       dim3 grid((unsigned)std::min<uint64_t>(cdiv(bd.cols, 256), 64), nr);
-      narrow_rows_kernel<S><<<grid, 256, 0, p->stream>>>(tmp.as<double2>(), bd.cols,
-                                                          p->dH.as<S>() + md.a_off + r0 * md.ld, md.ld,
-                                                          nr, bd.cols, p->cfg.scl);
+      if (h_dtype == ADMM_C64)
+        widen_rows_kernel<S><<<grid, 256, 0, p->stream>>>(tmp.as<float2>(), bd.cols,
+                                                           p->dH.as<S>() + md.a_off + r0 * md.ld, md.ld, nr,
+                                                           bd.cols, p->cfg.scl);
+      else
+        narrow_rows_kernel<S><<<grid, 256, 0, p->stream>>>(tmp.as<double2>(), bd.cols,
+                                                            p->dH.as<S>() + md.a_off + r0 * md.ld, md.ld,
+                                                            nr, bd.cols, p->cfg.scl);
       CK(cudaGetLastError());
       CK(cudaStreamSynchronize(p->stream));
     }
@@ -1614,6 +1619,7 @@ void reset_state(admm_plan* p) {
     if (d->p) CK(cudaMemsetAsync(d->p, 0, d->bytes, s));
   CK(cudaMemsetAsync(p->ghat_ptr, 0, p->mvec_total * 16 * p->batch, s));
   CK(cudaMemsetAsync(p->outbox_ptr, 0, p->outbox_total * 16, s));
+  if (p->dl1prev.p) CK(cudaMemsetAsync(p->dl1prev.p, 0, sizeof(double), s));
   IterState st{0, ~0ull, 0u, 0u};
   CK(cudaMemcpyAsync(p->dstate.p, &st, sizeof(st), cudaMemcpyHostToDevice, s));
   if (p->schedule == 2) {
@@ -1722,6 +1728,7 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
                         : host_all_finite(static_cast<const float*>(h), 2 * n_meas * n_pix);
   if (!hfin || !host_all_finite(g, 2 * n_meas * std::max<uint64_t>(1, o.batch)))
     throw Fail{ADMM_E_NUMERICAL, "SensingProblem: non-finite entries"};
+  if (o.noise_sigma < 0.0) throw Fail{ADMM_E_PARAMETER, "SensingProblem: negative noise_sigma"};
   if (o.method < ADMM_REFERENCE || o.method > ADMM_HYBRID) throw Fail{ADMM_E_PARAMETER, "unknown method"};
   if (o.dtype != ADMM_C128 && o.dtype != ADMM_C64) throw Fail{ADMM_E_PARAMETER, "unknown dtype"};
 
@@ -1784,9 +1791,14 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
   // layouts so that all-gathers land every peer vector where the kernels look for it:
   //   ghat:   [pc'][il][jl][mpad]  for blocks in this plan's row blocks (row comm order)
   //   outbox: [i][jl][npad]        for blocks in this plan's column blocks (column comm order)
-  // column-sharded grids reserve 4 doubles after each rank's ghat slot; the sweep schedule
-  // (scalars ready before the ghat exchange) uses them instead of a separate all-gather
-  p->gslot = p->Mr * p->Nc * p->mpad + (p->Pr == 1 && p->Pc > 1 ? 2 : 0);
+  // A sharded plan with the per-iteration objective carries a_b = H_b v next to ghat_b (the
+  // A region, gathered with it).  Column-sharded grids reserve kScalDoubles after each
+  // rank's ghat slot; the sweep schedule (scalars ready before the ghat exchange) uses them
+  // instead of a separate all-gather.
+  if (p->is_shard && p->trace_obj && (p->Nc > kCtaThreads || o.batch > 1)) p->trace_obj = false;
+  p->aoff = p->is_shard ? p->Mr * p->Nc * p->mpad : 0;  // (the final objective pass uses it too)
+  p->shard_obj = p->is_shard && p->trace_obj;
+  p->gslot = p->Mr * p->Nc * p->mpad + p->aoff + (p->Pr == 1 && p->Pc > 1 ? kScalDoubles / 2 : 0);
   p->gblocks.assign(p->M * p->N, BlockDesc{});
   for (uint64_t i = 0; i < p->M; ++i)
     for (uint64_t q = 0; q < p->N; ++q) {
@@ -1821,8 +1833,6 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
   p->vec_total = p->Mr * p->Nc * p->npad;
   p->seg_total = p->Nc * p->npad;
   p->outbox_total = p->M * p->Nc * p->npad;
-  // a sharded plan's solve needs its peers: no per-iteration objective on the device
-  if (p->Pr * p->Pc > 1) p->trace_obj = false;
 
   int requested = o.schedule;
   if (const char* env = std::getenv("ADMM_B200_SCHEDULE")) {
@@ -1842,7 +1852,7 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
   upload_desc(p->dblocks, p->blocks.data(), nb * sizeof(BlockDesc));
   upload_desc(p->dgblocks, p->gblocks.data(), p->gblocks.size() * sizeof(BlockDesc));
   p->doutbox.alloc(p->outbox_total * 16);
-  p->dscal.alloc(p->Pr * p->Pc * 4 * sizeof(double));
+  p->dscal.alloc(p->Pr * p->Pc * kScalDoubles * sizeof(double));
   upload_desc(p->dhN, p->hN.data(), nb * sizeof(MatDesc));
   upload_desc(p->dhNv, p->hNv.data(), nb * sizeof(MatDesc));
   upload_desc(p->dkN, p->kN.data(), nb * sizeof(MatDesc));
@@ -1865,7 +1875,7 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
     p->h_evict_first = e3 ? e3[0] == '1' : (p->schedule == 1 && p->k_elems * p->elem / 2 <= (96ull << 20));
     if (p->schedule == 1 && p->h_evict_first && !e2) p->kkeep = true;
   }
-  p->scal_ptr = p->fused_scal ? reinterpret_cast<double*>(p->ghat_ptr + p->Mr * p->Nc * p->mpad)
+  p->scal_ptr = p->fused_scal ? reinterpret_cast<double*>(p->ghat_ptr + p->Mr * p->Nc * p->mpad + p->aoff)
                               : p->dscal.as<double>();
   for (DevBuf* d : {&p->du, &p->ds, &p->dc}) d->alloc(p->vec_total * 16 * p->batch);
   for (DevBuf* d : {&p->dv, &p->dvprev}) d->alloc(p->seg_total * 16 * p->batch);
@@ -1883,6 +1893,12 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
   p->dored.alloc((size_t)std::max<uint32_t>(p->no, p->zgx * (uint32_t)p->Nc) * sizeof(double));
   if (const char* e = std::getenv("ADMM_B200_OBJ")) p->obj_pass = !std::strcmp(e, "pass");
   if (p->Nc > kCtaThreads) p->obj_pass = true;  // the recurrence kernel spreads at most 256 column blocks
+  if (p->is_shard) p->obj_pass = false;         // shards: recurrence + gathered A regions only
+  if (p->aoff) {
+    p->objgx = (uint32_t)cdiv(p->max_rowblock, kCtaThreads);
+    p->dobjp.alloc((size_t)p->objgx * p->Mr * sizeof(double));
+    p->dl1prev.alloc(sizeof(double));
+  }
   if (p->trace_obj && !p->obj_pass) {
     p->dhs.alloc(p->mvec_total * std::max<uint64_t>(1, p->batch) * sizeof(double2));
     while ((1u << p->onp) < p->Nc) ++p->onp;
@@ -1920,6 +1936,19 @@ void check_plan(const admm_plan* p) {
   if (!p) throw Fail{ADMM_E_STATE, "null plan"};
   CK(cudaSetDevice(p->device));
 }
+
+// multi-GPU plans (admm_dist.inc)
+bool is_dist(const admm_plan* p);
+std::vector<admm_plan*> shards_of(admm_plan* p);
+void dist_solve(admm_plan* root, double* solution, double* trace, uint64_t* iterations_run, double* objective,
+                admm_observer_fn observer, void* user);
+void dist_enqueue(admm_plan* root, uint64_t iters);
+void dist_reset(const std::vector<admm_plan*>& sh);
+void dist_sync(const std::vector<admm_plan*>& sh);
+double dist_max_abs_adjoint(admm_plan* root);
+void dist_gather_segments(const std::vector<admm_plan*>& sh, int which, double* dst);
+void dist_gather_u(const std::vector<admm_plan*>& sh, std::vector<double>& u, std::vector<uint64_t>& off,
+                   std::vector<uint64_t>& len);
 
 }  // namespace
 
@@ -1982,9 +2011,12 @@ admm_status admm_plan_set_g(admm_plan* p, const double* g) {
   return run_guarded([&] {
     check_plan(p);
     if (!g) throw Fail{ADMM_E_STATE, "null g"};
-    if (!host_all_finite(g, 2 * p->n_meas * p->batch))
+    if (!host_all_finite(g, 2 * p->n_meas * std::max<uint64_t>(1, p->batch)))
       throw Fail{ADMM_E_NUMERICAL, "SensingProblem: non-finite entries"};
-    upload_g(p, g);
+    for (admm_plan* s : shards_of(p)) {
+      CK(cudaSetDevice(s->device));
+      upload_g(s, g);
+    }
   });
 }
 
@@ -1993,17 +2025,25 @@ admm_status admm_plan_set_lambda(admm_plan* p, double lambda) {
     check_plan(p);
     if (!(lambda > 0.0)) throw Fail{ADMM_E_PARAMETER, "SolverConfig: lambda must be positive"};
     p->cfg.lambda = lambda;
-    set_params(p);
+    for (admm_plan* s : shards_of(p)) {
+      CK(cudaSetDevice(s->device));
+      s->cfg.lambda = lambda;
+      set_params(s);
+    }
   });
 }
 
 admm_status admm_plan_max_abs_adjoint(admm_plan* p, double* out) {
   return run_guarded([&] {
     check_plan(p);
+    if (is_dist(p)) {
+      *out = dist_max_abs_adjoint(p);
+      return;
+    }
     const int nb = (int)p->blocks.size();
     const uint32_t gx = p->zgx;
     DevBuf res;
-    if (p->Pr * p->Pc != 1) throw Fail{ADMM_E_STATE, "max_abs_adjoint: single-GPU plans only"};
+    if (p->Pr * p->Pc != 1) throw Fail{ADMM_E_STATE, "max_abs_adjoint: single-GPU or distributed plans only"};
     res.alloc((size_t)gx * p->N * sizeof(double));
     if (p->dtype == ADMM_C128) {
       gemv_h_kernel<double2, kVH, kEvictNormal><<<(unsigned)p->gG.P, kCtaThreads, 0, p->stream>>>(
@@ -2031,29 +2071,42 @@ admm_status admm_plan_max_abs_adjoint(admm_plan* p, double* out) {
 admm_status admm_plan_reset(admm_plan* p) {
   return run_guarded([&] {
     check_plan(p);
-    reset_state(p);
+    if (is_dist(p))
+      dist_reset(shards_of(p));
+    else
+      reset_state(p);
   });
 }
 
 admm_status admm_plan_enqueue(admm_plan* p, uint64_t iters) {
   return run_guarded([&] {
     check_plan(p);
-    enqueue_iters(p, iters);
+    if (is_dist(p))
+      dist_enqueue(p, iters);
+    else
+      enqueue_iters(p, iters);
   });
 }
 
 admm_status admm_plan_sync(admm_plan* p) {
   return run_guarded([&] {
     check_plan(p);
-    CK(cudaStreamSynchronize(p->stream));
+    if (is_dist(p))
+      dist_sync(shards_of(p));
+    else
+      CK(cudaStreamSynchronize(p->stream));
   });
 }
 
-void* admm_plan_stream(admm_plan* p) { return p ? (void*)p->stream : nullptr; }
+void* admm_plan_stream(admm_plan* p) {
+  if (!p) return nullptr;
+  return !p->subs.empty() ? (void*)p->subs[0]->stream : (void*)p->stream;
+}
 
 admm_status admm_plan_set_stream(admm_plan* p, void* stream) {
   return run_guarded([&] {
     check_plan(p);
+    if (is_dist(p)) throw Fail{ADMM_E_STATE, "set_stream: a distributed plan launches on its own streams"};
     p->stream = stream ? static_cast<cudaStream_t>(stream) : p->own_stream;
     pin_k_l2(p, p->stream);
   });
@@ -2119,6 +2172,7 @@ admm_status admm_plan_profile(admm_plan* p, uint64_t iters, const char** names, 
                                    "bzupdate", "bfinalize"};
   return run_guarded([&] {
     check_plan(p);
+    if (is_dist(p)) throw Fail{ADMM_E_STATE, "profile: single-GPU plans only"};
     const int nk = (int)admm_plan_kernel_count(p);
     const bool fused = p->kpacked && p->hemv_fuse;
     static const char* kNamesR[1] = {"resident(iteration)"};
@@ -2149,6 +2203,12 @@ admm_status admm_plan_profile(admm_plan* p, uint64_t iters, const char** names, 
 admm_status admm_plan_get_info(const admm_plan* p, admm_plan_info* info) {
   return run_guarded([&] {
     if (!p || !info) throw Fail{ADMM_E_STATE, "null argument"};
+    if (!p->subs.empty()) {  // single-process multi-GPU plan: its first shard, whole-job fields
+      admm_status st = admm_plan_get_info(p->subs[0], info);
+      if (st != ADMM_OK) throw Fail{st, g_last_error};
+      info->setup_seconds = p->setup_s;
+      return;
+    }
     admm_plan_info r{};
     r.n_blocks = p->blocks.size();
     uint64_t hb = 0, kb = 0, vb = 0;
@@ -2180,6 +2240,13 @@ admm_status admm_plan_get_info(const admm_plan* p, admm_plan_info* info) {
     r.grid_gemv_h = p->gH.P;
     r.setup_seconds = p->setup_s;
     r.inner_dim_max = p->max_m;
+    r.grid_pr = p->Pr;
+    r.grid_pc = p->Pc;
+    r.n_ranks = p->Pr * p->Pc;
+    // bytes this rank RECEIVES per iteration over NCCL (all-gathers: the peers' slots)
+    r.exchange_bytes_per_iter = (p->Pc - 1) * p->gslot * 16 +
+                                (p->schedule == 2 ? 0 : (p->Pr - 1) * p->Mr * p->Nc * p->npad * 16) +
+                                (p->fused_scal ? 0 : (p->Pr * p->Pc - 1) * kScalDoubles * 8);
     *info = r;
   });
 }
@@ -2188,6 +2255,24 @@ admm_status admm_plan_read(admm_plan* p, int which, double* dst, uint64_t count)
   return run_guarded([&] {
     check_plan(p);
     if (!dst) throw Fail{ADMM_E_STATE, "null destination"};
+    if (is_dist(p)) {  // whole-problem iterates, identical on every rank
+      const auto sh = shards_of(p);
+      if (which == 0 || which == 1) {
+        if (count < p->n_pix) throw Fail{ADMM_E_DIMENSION, "destination too small"};
+        dist_gather_segments(sh, which, dst);
+        return;
+      }
+      if (which == 2) {
+        std::vector<double> u;
+        std::vector<uint64_t> off, len;
+        dist_gather_u(sh, u, off, len);
+        if (count < u.size() / 2) throw Fail{ADMM_E_DIMENSION, "destination too small"};
+        std::memcpy(dst, u.data(), u.size() * 8);
+        return;
+      }
+      p = sh[0];
+      CK(cudaSetDevice(p->device));
+    }
     if (which == 0 || which == 1) {
       if (count < p->n_pix * p->batch) throw Fail{ADMM_E_DIMENSION, "destination too small"};
       read_segments(p, which == 0 ? p->dv : p->dvprev, dst);
@@ -2230,6 +2315,10 @@ admm_status admm_plan_solve(admm_plan* p, double* solution, double* trace, uint6
                             double* objective, admm_observer_fn observer, void* user) {
   return run_guarded([&] {
     check_plan(p);
+    if (is_dist(p)) {
+      dist_solve(p, solution, trace, iterations_run, objective, observer, user);
+      return;
+    }
     const uint64_t iters = p->cfg.max_iters;
     ensure_trace(p, iters);
     reset_state(p);
@@ -2287,7 +2376,7 @@ admm_status admm_plan_solve(admm_plan* p, double* solution, double* trace, uint6
           snap.replica_len = ulen.data();
           snap.primal = tr[0];
           snap.dual = tr[1];
-          observer(&snap, user);
+          if (observer(&snap, user) != 0) throw Fail{ADMM_E_OBSERVER, "observer stopped the solve"};
         }
         // stop_now: both thresholds 0 never stops; otherwise every enabled one must hold
         const double e1 = p->cfg.eps_pri, e2 = p->cfg.eps_dual;
@@ -2346,7 +2435,25 @@ admm_status admm_plan_solve(admm_plan* p, double* solution, double* trace, uint6
 namespace {
 
 // doubles between consecutive ranks' scalar slots
-uint64_t scal_stride(const admm_plan* p) { return p->fused_scal ? 2 * p->gslot : 4; }
+uint64_t scal_stride(const admm_plan* p) { return p->fused_scal ? 2 * p->gslot : kScalDoubles; }
+
+// Objective of a sharded iteration: a_b of the local blocks into the A
+// region of the ghat slot; the sweep schedule closes iteration k's objective in iteration
+// k (its next w is this iteration's), the two-pass schedule closes iteration k-1's.
+void enqueue_arec(admm_plan* p, cudaStream_t s) {
+  if (!p->shard_obj) return;
+  objective_arec_kernel<<<dim3(p->rgx, (unsigned)p->blocks.size()), kCtaThreads, 0, s>>>(
+      row_vecs(p), p->dhs.as<double2>(), p->dblocks.as<BlockDesc>(), p->aoff, p->dstate.as<IterState>(),
+      p->schedule == 2 ? 0 : 1);
+}
+// Rows partials |sum_q a_iq - g_i|^2 of the local row blocks from the gathered A regions.
+// count: whether this rank's rows enter the sum (two-pass / final pass: one rank per row
+// communicator; sweep: every rank holds all rows and keeps the sum to itself).
+void enqueue_grows(admm_plan* p, cudaStream_t s, bool count, uint64_t min_iter) {
+  objective_grows_kernel<<<dim3(p->objgx, (unsigned)p->Mr), kCtaThreads, 0, s>>>(
+      p->dg.as<double2>(), p->ghat_ptr, p->aoff, p->dgblocks.as<BlockDesc>(), (uint32_t)p->N, (uint32_t)p->i0,
+      count ? 1 : 0, p->dstate.as<IterState>(), min_iter, p->dobjp.as<double>());
+}
 
 template <typename S>
 void enqueue_phase(admm_plan* p, int phase) {
@@ -2367,6 +2474,7 @@ void enqueue_phase(admm_plan* p, int phase) {
           row_vecs(p), p->dwpart.as<double2>(), p->dhN.as<MatDesc>(), p->dblocks.as<BlockDesc>(),
           p->dgblocks.as<BlockDesc>(), (uint32_t)p->N, p->gN.U, p->gN.P, p->dparams.as<Params>());
     }
+    enqueue_arec(p, s);  // reads this block's ghat before the K apply replaces it
     enqueue_kapply<S>(p, s);
   } else if (phase == 2) {
     if (p->schedule == 2) throw Fail{ADMM_E_STATE, "phase 2 belongs to the two-pass schedule"};
@@ -2376,16 +2484,23 @@ void enqueue_phase(admm_plan* p, int phase) {
         col_vecs(p), p->outbox_ptr, p->dzpart.as<double2>(), p->dhH.as<MatDesc>(), p->dblocks.as<BlockDesc>(),
         p->gH.U, p->gH.P, p->dstate.as<IterState>());
   } else if (phase == 3) {
-    if (p->schedule == 2) throw Fail{ADMM_E_STATE, "phase 3 belongs to the two-pass schedule"};
-    zfinal_kernel<<<dim3(p->zgx, (unsigned)p->Nc), kCtaThreads, 0, s>>>(
-        col_vecs(p), p->outbox_ptr, p->dblocks.as<BlockDesc>(), (uint32_t)p->M, (uint32_t)p->Mr,
-        (uint32_t)p->Nc, (uint32_t)p->npad, p->pr == 0 ? 1 : 0, p->dparams.as<Params>(), p->dred.as<double>());
-    local_scalars_kernel<<<1, kCtaThreads, 0, s>>>(p->dred.as<double>(), p->nz,
-                                                   p->scal_ptr + scal_stride(p) * (p->pr * p->Pc + p->pc),
-                                                   p->dstate.as<IterState>());
+    if (p->schedule == 2) {  // sweep: the iteration's objective rows (all rows are local after the gather)
+      if (p->shard_obj) enqueue_grows(p, s, true, 0);
+    } else {
+      zfinal_kernel<<<dim3(p->zgx, (unsigned)p->Nc), kCtaThreads, 0, s>>>(
+          col_vecs(p), p->outbox_ptr, p->dblocks.as<BlockDesc>(), (uint32_t)p->M, (uint32_t)p->Mr,
+          (uint32_t)p->Nc, (uint32_t)p->npad, p->pr == 0 ? 1 : 0, p->dparams.as<Params>(), p->dred.as<double>());
+      if (p->shard_obj) enqueue_grows(p, s, p->pc == 0, 1);  // iteration k-1's rows, one rank per row block
+      local_scalars_kernel<<<1, kCtaThreads, 0, s>>>(
+          p->dred.as<double>(), p->nz, p->shard_obj ? p->dobjp.as<double>() : nullptr, p->objgx * (uint32_t)p->Mr,
+          p->scal_ptr + scal_stride(p) * (p->pr * p->Pc + p->pc), p->dstate.as<IterState>());
+    }
   } else if (phase == 4) {
-    close_kernel<<<1, 32, 0, s>>>(p->scal_ptr, (uint32_t)(p->Pr * p->Pc), scal_stride(p), p->dparams.as<Params>(),
-                                  p->dtrace.as<double>(), p->trace_cap, p->dstate.as<IterState>());
+    const int mode = !p->shard_obj ? 0 : p->schedule == 2 ? 2 : 1;
+    close_kernel<<<1, kCtaThreads, 0, s>>>(p->scal_ptr, (uint32_t)(p->Pr * p->Pc), scal_stride(p),
+                                           p->dparams.as<Params>(), p->dtrace.as<double>(), p->trace_cap,
+                                           p->dstate.as<IterState>(), mode, p->dobjp.as<double>(),
+                                           p->objgx * (uint32_t)p->Mr, p->dl1prev.as<double>());
   } else {
     throw Fail{ADMM_E_PARAMETER, "unknown phase"};
   }
@@ -2419,7 +2534,7 @@ admm_status admm_plan_exchange_info(const admm_plan* p, int which, uint64_t* tot
       t = p->Pr * b;
       o = p->pr * b;
     } else if (which == ADMM_X_SCAL) {  // [rank][4]; 0 bytes: fused into the ghat exchange
-      b = p->fused_scal ? 0 : 4 * sizeof(double);
+      b = p->fused_scal ? 0 : kScalDoubles * sizeof(double);
       t = p->Pr * p->Pc * b;
       o = (p->pr * p->Pc + p->pc) * b;
     } else {
@@ -2434,10 +2549,11 @@ admm_status admm_plan_exchange_info(const admm_plan* p, int which, uint64_t* tot
 admm_status admm_plan_attach(admm_plan* p, int which, void* ptr) {
   return run_guarded([&] {
     check_plan(p);
+    if (is_dist(p)) throw Fail{ADMM_E_STATE, "attach: a distributed plan owns its exchange buffers"};
     if (!ptr) throw Fail{ADMM_E_STATE, "null device pointer"};
     if (which == ADMM_X_GHAT) {
       p->ghat_ptr = static_cast<double2*>(ptr);
-      if (p->fused_scal) p->scal_ptr = reinterpret_cast<double*>(p->ghat_ptr + p->Mr * p->Nc * p->mpad);
+      if (p->fused_scal) p->scal_ptr = reinterpret_cast<double*>(p->ghat_ptr + p->Mr * p->Nc * p->mpad + p->aoff);
     } else if (which == ADMM_X_OUTBOX) {
       p->outbox_ptr = static_cast<double2*>(ptr);
     } else if (which == ADMM_X_SCAL) {
@@ -2562,6 +2678,95 @@ admm_status admm_soft_threshold(const double* a, uint64_t n, double kappa, doubl
   });
 }
 
+}  // extern "C"
+
+// GramSolver object (admm_b200.h admm_gram_*): a single-block plan factored once.
+//   Woodbury: the plan of H, K = (rho I + H H^H)^-1; solve = one u-update with g = 0:
+//             x = c - H^H K H c, c = rhs / rho (gram.hpp:71-77 through the inversion lemma).
+//   Direct:   the plan of H^H, whose K = (rho I + H^H H)^-1 is the cols x cols inverse;
+//             solve = x = K rhs (dense GEMV of the stored inverse, gram.hpp:68-70).
+struct admm_gram {
+  std::unique_ptr<admm_plan> plan;
+  int strategy = 1;
+  uint64_t rows = 0, cols = 0;
+  double rho = 1.0;
+  std::mutex mu;
+};
+
+extern "C" {
+
+admm_status admm_gram_create(const double* h, uint64_t rows, uint64_t cols, double rho, int strategy, int device,
+                             admm_gram** out) {
+  return run_guarded([&] {
+    if (!out) throw Fail{ADMM_E_STATE, "null argument"};
+    *out = nullptr;
+    if (!h || rows == 0 || cols == 0) throw Fail{ADMM_E_PARAMETER, "GramSolver: empty block"};
+    if (!(rho > 0.0)) throw Fail{ADMM_E_PARAMETER, "GramSolver: rho must be positive"};
+    if (!host_all_finite(h, 2 * rows * cols)) throw Fail{ADMM_E_NUMERICAL, "GramSolver: non-finite entries in block"};
+    auto g = std::make_unique<admm_gram>();
+    g->strategy = strategy < 0 ? (rows < cols ? 1 : 0) : (strategy ? 1 : 0);
+    g->rows = rows;
+    g->cols = cols;
+    g->rho = rho;
+    admm_solver_config cfg{rho, 1.0, 1.0, 1, 0.0, 0.0, 0};
+    if (g->strategy == 1) {
+      std::vector<double> z(2 * rows, 0.0);
+      g->plan.reset(create_plan(single_block(device), cfg, rows, cols, h, ADMM_C128, z.data(), true));
+    } else {  // the plan of H^H (cols x rows): its K is (rho I + H^H H)^-1
+      std::vector<double> ht(2 * rows * cols), z(2 * cols, 0.0);
+      for (uint64_t r = 0; r < rows; ++r)
+        for (uint64_t c = 0; c < cols; ++c) {
+          ht[2 * (c * rows + r)] = h[2 * (r * cols + c)];
+          ht[2 * (c * rows + r) + 1] = -h[2 * (r * cols + c) + 1];
+        }
+      admm_plan_options o = single_block(device);
+      g->plan.reset(create_plan(o, cfg, cols, rows, ht.data(), ADMM_C128, z.data(), true));
+    }
+    *out = g.release();
+  });
+}
+
+admm_status admm_gram_apply(admm_gram* g, const double* rhs, double* x) {
+  return run_guarded([&] {
+    if (!g || !rhs || !x) throw Fail{ADMM_E_STATE, "null argument"};
+    std::lock_guard<std::mutex> lock(g->mu);
+    admm_plan* p = g->plan.get();
+    CK(cudaSetDevice(p->device));
+    if (g->strategy == 1) {
+      std::vector<double> c(2 * g->cols);
+      for (uint64_t t = 0; t < 2 * g->cols; ++t) c[t] = rhs[t] / g->rho;
+      CK(cudaMemcpyAsync(p->dc.p, c.data(), g->cols * 16, cudaMemcpyHostToDevice, p->stream));
+      enqueue_iteration_twopass<double2>(p, p->stream, false, nullptr);
+      CK(cudaMemcpyAsync(x, p->du.p, g->cols * 16, cudaMemcpyDeviceToHost, p->stream));
+    } else {
+      CK(cudaMemcpyAsync(p->dr.p, rhs, g->cols * 16, cudaMemcpyHostToDevice, p->stream));
+      gemv_n_kernel<double2, kVN, kEvictNormal><<<(unsigned)p->gK.P, kCtaThreads, 0, p->stream>>>(
+          p->dK.as<double2>(), p->dr.as<double2>(), p->dqpart.as<double2>(), p->dkN.as<MatDesc>(), 1, p->gK.U);
+      rows_sum_kernel<<<(unsigned)cdiv(g->cols, 256), 256, 0, p->stream>>>(p->dqpart.as<double2>(),
+                                                                           p->dkN.as<MatDesc>(), p->gK.U, p->gK.P,
+                                                                           p->dq.as<double2>());
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(x, p->dq.p, g->cols * 16, cudaMemcpyDeviceToHost, p->stream));
+    }
+    CK(cudaStreamSynchronize(p->stream));
+  });
+}
+
+admm_status admm_gram_info(const admm_gram* g, int* strategy, uint64_t* inner_dim) {
+  return run_guarded([&] {
+    if (!g) throw Fail{ADMM_E_STATE, "null argument"};
+    if (strategy) *strategy = g->strategy;
+    if (inner_dim) *inner_dim = g->strategy == 1 ? g->rows : g->cols;
+  });
+}
+
+void admm_gram_destroy(admm_gram* g) {
+  if (g) {
+    cudaSetDevice(g->plan->device);
+    delete g;
+  }
+}
+
 admm_status admm_gram_solve(const double* h, uint64_t rows, uint64_t cols, double rho, const double* rhs,
                             double* x, int device) {
   return run_guarded([&] {
@@ -2584,3 +2789,6 @@ admm_status admm_gram_solve(const double* h, uint64_t rows, uint64_t cols, doubl
 }
 
 }  // extern "C"
+
+// ---- multi-GPU plans with plan-owned NCCL communicators ---------------------------
+#include "admm_dist.inc"

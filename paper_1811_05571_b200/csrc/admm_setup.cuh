@@ -166,6 +166,16 @@ __global__ void narrow_rows_kernel(const double2* __restrict__ src, uint64_t spi
     dst[(uint64_t)r * ld + c] = Store<S>::narrow(cscale(src[(uint64_t)r * spitch + c], scl));
 }
 
+// complex64 rows staged on the device -> storage S (scaled in FP64 first, as above).
+template <typename S>
+__global__ void widen_rows_kernel(const float2* __restrict__ src, uint64_t spitch, S* __restrict__ dst,
+                                  uint64_t ld, uint32_t rows, uint32_t cols, double scl) {
+  const uint32_t r = blockIdx.y;
+  if (r >= rows) return;
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += gridDim.x * blockDim.x)
+    dst[(uint64_t)r * ld + c] = Store<S>::narrow(cscale(Store<float2>::widen(src[(uint64_t)r * spitch + c]), scl));
+}
+
 // In-place scaling of a storage arena: p[i] *= scl (problem.hpp:59-66).
 template <typename S>
 __global__ void scale_kernel(S* __restrict__ p, uint64_t n, double scl) {

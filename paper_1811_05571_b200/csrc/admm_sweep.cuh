@@ -615,6 +615,7 @@ rows_finalize_sweep_kernel(RowVecs rv, const double2* __restrict__ wpart, const 
         slot[1] = d;
         slot[2] = l;
         slot[3] = st->nonfinite ? 1.0 : 0.0;
+        slot[4] = 0.0;
         st->nonfinite = 0u;
         return;
       }

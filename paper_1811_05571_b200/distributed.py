@@ -1,56 +1,92 @@
 """Multi-GPU consensus / sectioning / grid ADMM.
 
-One process per GPU.  The M x N block grid is dealt to a Pr x Pc process grid
-(rank = pr*Pc + pc owns row blocks [pr*M/Pr, ..) x column blocks [pc*N/Pc, ..)).
-Each rank runs a *shard plan* (libadmm_b200.so) over its blocks; between its phases
-the exchanges of the reference's simulated message layer become all-gathers:
+The M x N block grid is dealt to a Pr x Pc process grid (rank = pr*Pc + pc owns row blocks
+[pr*M/Pr, ..) x column blocks [pc*N/Pc, ..)).  The plan of every rank owns its NCCL
+communicators (world, and the row / column communicators split from it) and issues the
+exchanges of the reference's simulated message layer itself, between its shard's phases,
+on its own stream, inside its CUDA graph (libadmm_b200.so, admm_dist.inc):
 
   ghat   (solvers.hpp:218-225, 361-372)  row communicator    — every rank gets the
          peers' ghat_iq and subtracts them in ascending q, exactly as the reference;
   outbox (solvers.hpp:120-136, 389-415)  column communicator — every rank gets all
          replicas' u+s and forms the mean in ascending i;
-  scal   (residual norms, solvers.hpp:141-145)  all ranks, summed in rank order.
+  scal   (residuals and objective, solvers.hpp:141-146)  all ranks, summed in rank order.
 
-All-gather instead of all-reduce keeps the reference's reduction order, so the result
-is bit-identical for any GPU count.  The orchestration below is backend-agnostic: the
-same `run_iterations` drives
-  * TorchComm  — torch.distributed (NCCL on B200; gloo in the CPU tests), one shard
-                 per process, collectives on the shard plan's stream;
-  * LoopbackComm — several shards in ONE process (tests: the real CUDA shard plans on a
-                 single GPU, exchanges as device copies; no kernel waits on another).
+All-gathers instead of all-reduces keep the reference's reduction order, so a solve is
+bit-identical for any GPU count.  torch.distributed is only the plumbing that carries the
+NCCL unique id from rank 0 to the other ranks (any backend).
+
+ShardPlan is the lower-level "bring your own transport" surface of the same shard plans
+(admm_plan_create_sharded + admm_plan_run_phase + attached exchange buffers): a caller
+with its own collective layer drives the phase / exchange sequence of admm_b200.h.
 """
 from __future__ import annotations
 
 import ctypes
-import math
-from typing import List, Optional, Sequence
+from typing import Sequence
 
 import numpy as np
 
 X_GHAT, X_OUTBOX, X_SCAL = 0, 1, 2
+SCAL_DOUBLES = 8  # kScalDoubles: rp2, rd2, |v|_1, non-finite flag, objective rows, spare
 
 
 def choose_grid(world: int, method: str, M: int, N: int) -> tuple:
-    """Process grid Pr x Pc for `world` GPUs.  Column sharding (Pr = 1) is preferred:
-    then every replica of a segment is local and the single-HBM-pass sweep applies."""
-    if method == "consensus":
-        if M % world:
-            raise ValueError(f"consensus: {world} GPUs must divide M={M}")
-        return world, 1
-    if method in ("sectioning", "reference"):
-        if N % world:
-            raise ValueError(f"sectioning: {world} GPUs must divide N={N}")
-        return 1, world
-    for pc in sorted({d for d in range(1, world + 1) if world % d == 0}, reverse=True):
-        pr = world // pc
-        if N % pc == 0 and M % pr == 0:
-            return pr, pc
-    raise ValueError(f"no {world}-GPU grid divides the {M}x{N} block grid")
+    """Process grid Pr x Pc for `world` GPUs (admm_choose_grid).  Column sharding (Pr = 1)
+    is preferred: then every replica of a segment is local and the single-HBM-pass sweep
+    applies."""
+    from . import _lib
+    from .solvers import _METHOD
+    pr, pc = ctypes.c_uint64(), ctypes.c_uint64()
+    st = _lib.lib.admm_choose_grid(int(world), _METHOD[method], int(M), int(N), ctypes.byref(pr), ctypes.byref(pc))
+    if st != 0:
+        raise ValueError(_lib.lib.admm_last_error().decode())
+    return int(pr.value), int(pc.value)
+
+
+def nccl_unique_id() -> bytes:
+    from . import _lib
+    from .errors import check
+    buf = ctypes.create_string_buffer(128)
+    check(_lib.lib.admm_nccl_unique_id(buf))
+    return buf.raw
+
+
+def dist_plan(problem, cfg, method: str, M: int, N: int, opts=None, group=None):
+    """This process's rank of a multi-process plan (call on every rank after
+    torch.distributed.init_process_group; one process per GPU, opts.device = its GPU)."""
+    from .solvers import AdmmPlan
+    try:
+        import torch.distributed as dist
+        up = dist.is_available() and dist.is_initialized()
+    except ImportError:  # pragma: no cover
+        up = False
+    if not up:  # a one-rank job (the NCCL path with a world of one)
+        return AdmmPlan(problem, cfg, method, M, N, opts, dist=(nccl_unique_id(), 1, 0))
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    box = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(box, src=0, group=group)
+    return AdmmPlan(problem, cfg, method, M, N, opts, dist=(box[0], world, rank))
+
+
+def distributed_solve(problem, cfg, method: str, M: int, N: int, opts=None):
+    """consensus / sectioning / hybrid solve over the job's GPUs (one process per GPU).
+    Same SolveReport on every rank; early stopping (stop_now), the observer and
+    NumericalError(last_good_iteration) behave exactly as on one GPU."""
+    from .solvers import SolveOptions, _as_c128, recovery_metrics
+    opts = opts or SolveOptions()
+    with dist_plan(problem, cfg, method, M, N, opts) as plan:
+        rep = plan.solve(opts.observer)
+    if problem.truth is not None:
+        rep.metrics = recovery_metrics(rep.solution, _as_c128(problem.truth))
+    return rep
 
 
 class ShardPlan:
-    """One rank's B200 plan over its blocks plus its three exchange buffers (torch
-    tensors on the plan's device; the plan computes straight into them)."""
+    """One rank's shard plan over its blocks plus its three exchange buffers (torch tensors
+    on the plan's device; the plan computes straight into them).  The caller drives
+    phase(1), exchange(ghat), [phase(2), exchange(outbox)], phase(3), [exchange(scal)],
+    phase(4) per iteration (admm_b200.h)."""
 
     def __init__(self, problem, cfg, method: str, M: int, N: int, grid: tuple, coords: tuple,
                  opts=None):
@@ -58,7 +94,7 @@ class ShardPlan:
 
         from . import _lib
         from .errors import check
-        from .solvers import _DTYPE, _METHOD, SolveOptions, _as_c128, _ptr
+        from .solvers import _DTYPE, _METHOD, SolveOptions, _as_c128, _ptr, make_partition
         opts = opts or SolveOptions()
         cfg.validate()
         problem.validate()
@@ -72,7 +108,8 @@ class ShardPlan:
         h = np.ascontiguousarray(h) if h_dtype else _as_c128(h)
         g = _as_c128(problem.g)
         o = _lib.PlanOptionsC(_METHOD[method], M, N, int(opts.ragged), _DTYPE[opts.dtype], int(opts.device),
-                              0, {"auto": 0, "twopass": 1, "sweep": 2}[opts.schedule])
+                              int(opts.trace_objective), {"auto": 0, "twopass": 1, "sweep": 2}[opts.schedule], 1,
+                              float(problem.noise_sigma))
         c = cfg._c()
         sh = _lib.ShardC(self.Pr, self.Pc, self.pr, self.pc)
         handle = ctypes.c_void_p()
@@ -90,7 +127,7 @@ class ShardPlan:
             tot, off, nb = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
             check(_lib.lib.admm_plan_exchange_info(handle, which, ctypes.byref(tot), ctypes.byref(off),
                                                    ctypes.byref(nb)))
-            if tot.value == 0:  # scalars fused into the ghat exchange (Pr == 1)
+            if tot.value == 0:  # scalars fused into the ghat exchange (Pr == 1, Pc > 1)
                 self.fused_scal = True
                 continue
             buf = torch.zeros(tot.value // 8, dtype=torch.float64, device=dev)
@@ -98,11 +135,13 @@ class ShardPlan:
             self.buffers[which] = buf
             self.slots[which] = (off.value // 8, nb.value // 8)
         self.n_meas, self.n_pix = problem.h.shape
-        self.col_bounds = _bounds(self.n_pix, N)
+        # the plan's own partition (ragged bounds honoured on a 1 x 1 grid; sharded plans
+        # with more ranks require uniform blocks and say so at creation)
+        self.col_bounds = make_partition(self.n_meas, self.n_pix, M if method in ("consensus", "hybrid") else 1,
+                                         N if method in ("sectioning", "hybrid") else 1, opts.ragged).col_bounds
         self.cfg = cfg
         self.reset()
 
-    # engine interface used by run_iterations
     def stream(self):
         import torch
         return torch.cuda.ExternalStream(self._lib.lib.admm_plan_stream(self._h), device=self.device)
@@ -131,7 +170,7 @@ class ShardPlan:
         from .solvers import _ptr
         out = np.zeros(self.n_pix, np.complex128)
         self._check(self._lib.lib.admm_plan_read(self._h, 0, _ptr(out), self.n_pix))
-        nc = self.N // self.Pc
+        nc = self.N // self.Pc if self.method in ("sectioning", "hybrid") else 1
         return {j: out[self.col_bounds[j]:self.col_bounds[j + 1]].copy()
                 for j in range(self.pc * nc, (self.pc + 1) * nc)}
 
@@ -143,7 +182,8 @@ class ShardPlan:
         return int(out[0]), int(out[1])
 
     def trace(self) -> np.ndarray:
-        """(iterations, 3): primal, dual, objective (NaN: not computed when sharded)."""
+        """(iterations, 3): primal, dual, objective (two-pass: iteration k's objective is
+        closed in iteration k + 1; NaN until then)."""
         from .solvers import _ptr
         n = self.state()[0]
         tr = np.zeros(3 * max(n, 1))
@@ -159,148 +199,6 @@ class ShardPlan:
         self.close()
 
 
-def _bounds(total: int, parts: int) -> list:
-    base = total // parts
-    return [k * base for k in range(parts + 1)]
-
-
-class TorchComm:
-    """torch.distributed all-gathers (one shard per process).  Row/column
-    sub-communicators are created collectively by every rank in the same order."""
-
-    def __init__(self, Pr: int, Pc: int):
-        import torch.distributed as dist
-        self.dist = dist
-        self.Pr, self.Pc = Pr, Pc
-        self.rank = dist.get_rank()
-        pr, pc = divmod(self.rank, Pc)
-        self.row = self.col = None
-        for r in range(Pr):  # row communicators: same pr, ordered by pc
-            g = dist.new_group([r * Pc + c for c in range(Pc)])
-            if r == pr:
-                self.row = g
-        for c in range(Pc):  # column communicators: same pc, ordered by pr
-            g = dist.new_group([r * Pc + c for r in range(Pr)])
-            if c == pc:
-                self.col = g
-
-    def exchange(self, which: int, shards: Sequence, in_graph: bool = False) -> None:
-        (sh,) = shards
-        full, mine = sh.buffer(which)
-        group = {X_GHAT: self.row, X_OUTBOX: self.col, X_SCAL: None}[which]
-        import contextlib
-        ctx = contextlib.nullcontext() if in_graph else _stream_ctx(sh)  # capture: current stream
-        with ctx:
-            if full.is_cuda:  # in place: `mine` is this rank's slot of `full` (rank order = group order)
-                self.dist.all_gather_into_tensor(full, mine, group=group)
-            else:  # gloo: list form over views of the slots
-                n = mine.numel()
-                views = list(full.split(n))
-                self.dist.all_gather(views, mine.clone(), group=group)
-
-
-def _stream_ctx(sh):
-    import contextlib
-    s = sh.stream() if hasattr(sh, "stream") else None
-    if s is None:
-        return contextlib.nullcontext()
-    import torch
-    return torch.cuda.stream(s)
-
-
-class LoopbackComm:
-    """All-gathers among several shards living in one process (test harness).  Each
-    group's slots are copied into every member's buffer, after synchronising the
-    members' streams — no kernel ever waits for another."""
-
-    def __init__(self, Pr: int, Pc: int):
-        self.Pr, self.Pc = Pr, Pc
-
-    def exchange(self, which: int, shards: Sequence, in_graph: bool = False) -> None:
-        assert not in_graph, "LoopbackComm synchronises on the host: not capturable"
-        for sh in shards:
-            if hasattr(sh, "sync"):
-                sh.sync()
-        by_rank = {sh.rank: sh for sh in shards}
-        for sh in shards:
-            if which == X_GHAT:
-                members = [by_rank[sh.pr * self.Pc + c] for c in range(self.Pc)]
-            elif which == X_OUTBOX:
-                members = [by_rank[r * self.Pc + sh.pc] for r in range(self.Pr)]
-            else:
-                members = [by_rank[k] for k in range(self.Pr * self.Pc)]
-            full, _ = sh.buffer(which)
-            for m in members:
-                if m is sh:
-                    continue
-                _, slot = m.buffer(which)
-                off = m.slots[which][0]
-                full[off:off + slot.numel()].copy_(slot)
-        for sh in shards:
-            if hasattr(sh, "buffers") and sh.buffers[which].is_cuda:
-                import torch
-                torch.cuda.synchronize(sh.buffers[which].device)
-
-
-def run_iterations(shards: List, comm, iters: int) -> None:
-    """Drive `iters` ADMM iterations of every local shard (phase order in admm_b200.h).
-    After reset the ghat slots hold ghat^0 (sweep prologue) or 0: exchange first."""
-    comm.exchange(X_GHAT, shards)
-    _iterate(shards, comm, iters)
-
-
-def prime(shards, comm) -> None:
-    """After reset: the ghat of iteration 0 (sweep prologue) must reach the peers."""
-    comm.exchange(X_GHAT, shards)
-
-
-class GraphedIterations:
-    """`iters_per_graph` distributed iterations (shard phases + NCCL all-gathers) captured
-    once in a CUDA graph on a side stream and replayed: no Python or launch overhead per
-    iteration.  Requires TorchComm over NCCL (collectives are capturable once the
-    communicators are initialised — run one eager iteration first)."""
-
-    def __init__(self, shard, comm, iters_per_graph: int = 8):
-        import torch
-        self.shard, self.n = shard, iters_per_graph
-        self.stream = torch.cuda.Stream(device=shard.device)
-        self.graph = torch.cuda.CUDAGraph()
-        shard.sync()
-        torch.cuda.synchronize(shard.device)
-        shard.set_stream(self.stream)
-        try:
-            with torch.cuda.graph(self.graph, stream=self.stream):
-                _iterate([shard], comm, iters_per_graph, in_graph=True)
-        finally:
-            shard.set_stream(None)
-
-    def run(self, iters: int) -> None:
-        """Replay ceil(iters / iters_per_graph) graphs (whole graphs only) on the shard
-        plan's own stream, ordered after its reset/prime and covered by its sync()."""
-        import torch
-        with torch.cuda.stream(self.shard.stream()):
-            for _ in range(-(-iters // self.n)):
-                self.graph.replay()
-
-
-def _iterate(shards, comm, iters, in_graph=False):
-    sched = shards[0].schedule
-    for _ in range(iters):
-        for sh in shards:
-            sh.phase(1)
-        comm.exchange(X_GHAT, shards, in_graph)
-        if sched == "twopass":
-            for sh in shards:
-                sh.phase(2)
-            comm.exchange(X_OUTBOX, shards, in_graph)
-            for sh in shards:
-                sh.phase(3)
-        if not getattr(shards[0], "fused_scal", False):  # else the scalars rode with ghat
-            comm.exchange(X_SCAL, shards, in_graph)
-        for sh in shards:
-            sh.phase(4)
-
-
 def gather_solution(segments: Sequence[dict], n_pix: int, col_bounds: list) -> np.ndarray:
     v = np.zeros(n_pix, np.complex128)
     for seg in segments:
@@ -309,18 +207,37 @@ def gather_solution(segments: Sequence[dict], n_pix: int, col_bounds: list) -> n
     return v
 
 
-def distributed_solve(problem, cfg, method: str, M: int, N: int, opts=None, iters: Optional[int] = None):
-    """Run a sharded solve on this process's GPU (call on every rank; torch.distributed
-    already initialised).  Returns the full solution v on every rank."""
-    import torch.distributed as dist
-    world = dist.get_world_size()
-    Pr, Pc = choose_grid(world, method, M, N)
-    rank = dist.get_rank()
-    pr, pc = divmod(rank, Pc)
-    sh = ShardPlan(problem, cfg, method, M, N, (Pr, Pc), (pr, pc), opts)
-    comm = TorchComm(Pr, Pc)
-    run_iterations([sh], comm, iters or cfg.max_iters)
-    sh.sync()
-    segs = [None] * world
-    dist.all_gather_object(segs, sh.segment_v())
-    return gather_solution(segs, problem.h.shape[1], sh.col_bounds)
+def phase_program(schedule: str, fused_scal: bool) -> list:
+    """The per-iteration sequence a transport must drive (admm_b200.h): ints are phases,
+    strings exchanges."""
+    prog = [1, "ghat"]
+    if schedule == "twopass":
+        prog += [2, "outbox"]
+    prog.append(3)
+    if not fused_scal:
+        prog.append("scal")
+    prog.append(4)
+    return prog
+
+
+def iterate(shards: Sequence, comm, iters: int, in_graph: bool = False) -> None:
+    """Drive `iters` iterations of caller-transported shards (the ShardPlan surface)."""
+    prog = phase_program(shards[0].schedule, getattr(shards[0], "fused_scal", False))
+    names = {"ghat": X_GHAT, "outbox": X_OUTBOX, "scal": X_SCAL}
+    for _ in range(iters):
+        for step in prog:
+            if isinstance(step, int):
+                for sh in shards:
+                    sh.phase(step)
+            else:
+                comm.exchange(names[step], shards, in_graph)
+
+
+def run_iterations(shards: Sequence, comm, iters: int) -> None:
+    """After reset the ghat slots hold ghat^0 (sweep prologue) or 0: exchange first."""
+    comm.exchange(X_GHAT, shards)
+    iterate(shards, comm, iters)
+
+
+def prime(shards: Sequence, comm) -> None:
+    comm.exchange(X_GHAT, shards)

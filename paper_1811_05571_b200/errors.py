@@ -64,9 +64,18 @@ class StateError(Error):
     """API misuse (ADMM_E_STATE)."""
 
 
+class NcclError(Error):
+    """NCCL failure inside a multi-GPU plan (ADMM_E_NCCL; no reference counterpart)."""
+
+
+class ObserverStop(Error):
+    """ADMM_E_OBSERVER: the observer callback stopped the solve (the mirror re-raises the
+    observer's own exception instead)."""
+
+
 STATUS = {1: DimensionError, 2: IndexError, 3: NumericalError, 4: SingularityError,
           5: PartitionError, 6: ParameterError, 7: DeviceError, 8: StateError, 9: FormatError,
-          10: IoError}
+          10: IoError, 11: NcclError, 12: ObserverStop}
 
 
 def check(status: int) -> None:

@@ -79,6 +79,9 @@ class SensingProblem:
         return int(self.h.shape[1])
 
     def validate(self) -> None:
+        """problem.hpp:35-49, host part: shapes, then the truth's finiteness.  H and g are
+        scanned for non-finite entries by the C side (multithreaded), which then checks
+        noise_sigma -- the reference's order (NumericalError before ParameterError)."""
         if self.h.ndim != 2 or self.h.size == 0:
             raise DimensionError("SensingProblem: empty sensing matrix")
         if self.g.shape[0] != self.h.shape[0] or self.g.ndim not in (1, 2):
@@ -86,8 +89,8 @@ class SensingProblem:
         if self.truth is not None and self.truth.shape != (self.h.shape[1],):
             raise DimensionError(f"SensingProblem: truth length {self.truth.size} != H cols "
                                  f"{self.h.shape[1]}")
-        if self.noise_sigma < 0.0:
-            raise ParameterError("SensingProblem: negative noise_sigma")
+        if self.truth is not None and not np.all(np.isfinite(np.asarray(self.truth).view(np.float64))):
+            raise NumericalError("SensingProblem: non-finite entries")
 
 
 @dataclasses.dataclass
@@ -115,6 +118,8 @@ class SolveOptions:
     device: int = 0
     trace_objective: bool = True
     schedule: str = "auto"  # "auto" | "twopass" | "sweep" | "resident"
+    devices: Optional[list] = None  # GPUs of this process, one shard each (plan-owned NCCL);
+    #                                 None: the single-GPU plan on `device`
 
 
 @dataclasses.dataclass
@@ -222,7 +227,11 @@ class AdmmPlan:
     the factorizations across measurement vectors (set_g) and lambdas (set_lambda)."""
 
     def __init__(self, problem: SensingProblem, cfg: SolverConfig, method: str, M: int = 1,
-                 N: int = 1, opts: Optional[SolveOptions] = None):
+                 N: int = 1, opts: Optional[SolveOptions] = None, dist: Optional[tuple] = None):
+        """dist = (nccl_id bytes, nranks, rank): this process's rank of a multi-process plan
+        (see distributed.dist_plan); opts.devices = [d0, d1, ...]: one process driving
+        several GPUs.  Either way the plan owns its NCCL communicators and is used exactly
+        like a single-GPU plan."""
         opts = opts or SolveOptions()
         cfg.validate()                      # 1. SolverConfig::validate
         problem.validate()                  # 2. SensingProblem::validate (shapes; finiteness in C)
@@ -243,11 +252,23 @@ class AdmmPlan:
         self.opts = opts
         o = _lib.PlanOptionsC(_METHOD[method], self.M, self.N, int(opts.ragged),
                               _DTYPE[opts.dtype], int(opts.device), int(opts.trace_objective),
-                              {"auto": 0, "twopass": 1, "sweep": 2, "resident": 4}[opts.schedule], self.batch)
+                              {"auto": 0, "twopass": 1, "sweep": 2, "resident": 4}[opts.schedule], self.batch,
+                              float(problem.noise_sigma))
         c = self.cfg._c()
         handle = ctypes.c_void_p()
-        check(_lib.lib.admm_plan_create(ctypes.byref(o), ctypes.byref(c), self.n_meas, self.n_pix,
-                                        _ptr(h), h_dtype, _ptr(g), ctypes.byref(handle)))
+        if dist is not None:
+            nid, nranks, rank = dist
+            check(_lib.lib.admm_plan_create_dist(ctypes.byref(o), ctypes.byref(c), self.n_meas, self.n_pix,
+                                                 _ptr(h), h_dtype, _ptr(g), bytes(nid), int(nranks), int(rank),
+                                                 ctypes.byref(handle)))
+        elif opts.devices is not None:
+            devs = (ctypes.c_int * len(opts.devices))(*[int(d) for d in opts.devices])
+            check(_lib.lib.admm_plan_create_multi(ctypes.byref(o), ctypes.byref(c), self.n_meas, self.n_pix,
+                                                  _ptr(h), h_dtype, _ptr(g), len(opts.devices), devs,
+                                                  ctypes.byref(handle)))
+        else:
+            check(_lib.lib.admm_plan_create(ctypes.byref(o), ctypes.byref(c), self.n_meas, self.n_pix,
+                                            _ptr(h), h_dtype, _ptr(g), ctypes.byref(handle)))
         # (the C side validated finiteness, then the partition, then the factors)
         self._h = handle
         self.spec = make_partition(self.n_meas, self.n_pix, self.M, self.N, opts.ragged)
@@ -309,10 +330,19 @@ class AdmmPlan:
         it = ctypes.c_uint64()
         obj = ctypes.c_double()
         cb = _lib.OBSERVER()
+        raised = []
         if observer is not None:
             spec = self.spec
 
             def _cb(sp, _user):
+                try:
+                    _observe(sp)
+                    return 0
+                except BaseException as e:  # noqa: BLE001 -- re-raised after the C call returns
+                    raised.append(e)
+                    return 1
+
+            def _observe(sp):
                 s = sp.contents
                 n = int(s.n_pix)
                 v = np.ctypeslib.as_array(s.v, shape=(2 * n,)).view(np.complex128).copy()
@@ -327,8 +357,11 @@ class AdmmPlan:
                 observer(IterateSnapshot(int(s.iteration), v, vp, us, segv, segp))
 
             cb = _lib.OBSERVER(_cb)
-        check(_lib.lib.admm_plan_solve(self._h, _ptr(sol), _ptr(trace), ctypes.byref(it),
-                                       ctypes.byref(obj), cb, None))
+        st = _lib.lib.admm_plan_solve(self._h, _ptr(sol), _ptr(trace), ctypes.byref(it),
+                                      ctypes.byref(obj), cb, None)
+        if raised:  # the observer's exception propagates out of the solve (solvers.hpp:150-160)
+            raise raised[0]
+        check(st)
         k = int(it.value)
         ledger = CommLedger.for_solve(self.method, self.spec.row_bounds, self.spec.col_bounds, k)
         if B > 1:  # solution (n_pix, B), trace columns (iterations, B)
@@ -361,7 +394,7 @@ class AdmmPlan:
 
     def read(self, which: str) -> np.ndarray:
         w = {"v": 0, "v_prev": 1, "u": 2}[which]
-        n = self.n_pix if w < 2 else self.n_pix * self.M
+        n = self.n_pix if w < 2 else self.n_pix * self.M  # u: every worker's, in worker order
         out = np.zeros(n, np.complex128)
         check(_lib.lib.admm_plan_read(self._h, w, _ptr(out), n))
         return out
@@ -432,7 +465,10 @@ def soft_threshold_vec(a: np.ndarray, kappa: float, device: int = 0) -> np.ndarr
 
 
 class GramSolver:
-    """gram.hpp:26-128: (H^H H + rho I)^-1 via the inversion lemma on the device."""
+    """gram.hpp:26-128 on the device: validated and factored ONCE at construction
+    (gram.hpp:48-53), solve() reuses the stored factor.  Woodbury (rows < cols, or on
+    request): the rows x rows (rho I + H H^H)^-1 through the inversion lemma; Direct: the
+    cols x cols (H^H H + rho I)^-1 applied to rhs."""
 
     class Strategy(enum.Enum):
         Direct = 0
@@ -443,16 +479,25 @@ class GramSolver:
         """gram.hpp:32-34: Woodbury iff rows < cols."""
         return GramSolver.Strategy.Woodbury if rows < cols else GramSolver.Strategy.Direct
 
-    def __init__(self, block: np.ndarray, rho: float, device: int = 0):
+    def __init__(self, block: np.ndarray, rho: float, strategy: Optional["GramSolver.Strategy"] = None,
+                 device: int = 0):
         block = _as_c128(block)
-        if block.size == 0:
-            raise ParameterError("GramSolver: empty block")
-        if not rho > 0.0:
-            raise ParameterError("GramSolver: rho must be positive")
-        if not np.all(np.isfinite(block.view(np.float64))):
-            raise NumericalError("GramSolver: non-finite entries in block")
-        self._block, self._rho, self._device = block, float(rho), device
-        self._strategy = self.strategy_for(*block.shape)
+        self._block, self._rho = block, float(rho)
+        handle = ctypes.c_void_p()
+        rows, cols = (block.shape if block.ndim == 2 and block.size else (0, 0))
+        s = -1 if strategy is None else strategy.value
+        check(_lib.lib.admm_gram_create(_ptr(block) if block.size else None, rows, cols, float(rho), s, device,
+                                        ctypes.byref(handle)))
+        self._g = handle
+        used, dim = ctypes.c_int(), ctypes.c_uint64()
+        check(_lib.lib.admm_gram_info(handle, ctypes.byref(used), ctypes.byref(dim)))
+        self._strategy = GramSolver.Strategy(used.value)
+        self._inner = int(dim.value)
+
+    def __del__(self):
+        if getattr(self, "_g", None):
+            _lib.lib.admm_gram_destroy(self._g)
+            self._g = None
 
     def strategy(self) -> "GramSolver.Strategy":
         return self._strategy
@@ -460,9 +505,11 @@ class GramSolver:
     def rho(self) -> float:
         return self._rho
 
+    def block(self) -> np.ndarray:
+        return self._block
+
     def inner_dim(self) -> int:
-        r, c = self._block.shape
-        return r if self._strategy == GramSolver.Strategy.Woodbury else c
+        return self._inner
 
     def solve(self, rhs: np.ndarray) -> np.ndarray:
         rhs = _as_c128(rhs)
@@ -470,6 +517,5 @@ class GramSolver:
             raise DimensionError(f"GramSolver::solve: rhs length {rhs.size} != block cols "
                                  f"{self._block.shape[1]}")
         x = np.zeros(self._block.shape[1], np.complex128)
-        check(_lib.lib.admm_gram_solve(_ptr(self._block), self._block.shape[0], self._block.shape[1],
-                                       self._rho, _ptr(rhs), _ptr(x), self._device))
+        check(_lib.lib.admm_gram_apply(self._g, _ptr(rhs), _ptr(x)))
         return x

@@ -10,6 +10,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <limits>
+#include <memory>
+#include <stdexcept>
 #include <string>
 #include <vector>
 
@@ -89,6 +91,102 @@ TEST_CASE(gram_solver) {  // test_linalg.cpp:74-98
   const CVector x = GramSolver(CMatrix(2, 2), 2.0).solve({Complex(4, 0), Complex(6, 0)});
   CHECK(std::abs(x[0] - Complex(2, 0)) < 1e-12 && std::abs(x[1] - Complex(3, 0)) < 1e-12);
   CHECK_THROWS_AS(GramSolver(CMatrix(2, 3), 0.0), ParameterError);
+}
+
+static CMatrix random_matrix(std::size_t rows, std::size_t cols, std::uint64_t seed) {
+  CMatrix a(rows, cols);
+  orc_random_gauss(rows * cols, seed, reinterpret_cast<double*>(a.data()));
+  return a;
+}
+static CVector random_vector(std::size_t n, std::uint64_t seed) {
+  CVector v(n);
+  orc_random_gauss(n, seed, reinterpret_cast<double*>(v.data()));
+  return v;
+}
+static double rel_error(const CVector& a, const CVector& b) {
+  double num = 0, den = 0;
+  for (std::size_t i = 0; i < a.size(); ++i) {
+    num += std::norm(a[i] - b[i]);
+    den += std::norm(b[i]);
+  }
+  return std::sqrt(num / den);
+}
+
+TEST_CASE(gram_solver_strategies) {  // test_linalg.cpp:100-161, gram.hpp:36-53
+  CHECK_THROWS_AS(GramSolver(random_matrix(2, 3, 5), -1.0), ParameterError);
+  CMatrix bad(2, 2);
+  bad(0, 0) = Complex(std::numeric_limits<double>::quiet_NaN(), 0.0);
+  CHECK_THROWS_AS(GramSolver(bad, 1.0), NumericalError);
+  const GramSolver ok(random_matrix(2, 3, 6), 1.0);
+  CHECK_THROWS_AS(ok.solve(CVector(2)), DimensionError);
+  for (std::uint64_t seed = 1; seed <= 10; ++seed) {  // "woodbury and direct strategies agree"
+    const CMatrix h = random_matrix(3 + seed % 4, 12, seed);
+    const double rho = 0.25 * static_cast<double>(1 + seed % 3);
+    const CVector rhs = random_vector(12, 50 + seed);
+    const GramSolver woodbury(h, rho, GramSolver::Strategy::Woodbury);
+    const GramSolver direct(h, rho, GramSolver::Strategy::Direct);
+    CHECK(woodbury.strategy() == GramSolver::Strategy::Woodbury && woodbury.inner_dim() == h.rows());
+    CHECK(direct.strategy() == GramSolver::Strategy::Direct && direct.inner_dim() == 12);
+    CHECK(rel_error(woodbury.solve(rhs), direct.solve(rhs)) <= 1e-8);
+  }
+  for (std::uint64_t seed = 1; seed <= 8; ++seed) {  // residual, both automatic strategies
+    const bool wide = seed % 2 == 0;
+    const CMatrix h = wide ? random_matrix(5, 14, seed) : random_matrix(14, 5, seed);
+    const GramSolver gram(h, 1.5);
+    CHECK(gram.strategy() == (wide ? GramSolver::Strategy::Woodbury : GramSolver::Strategy::Direct));
+    const CVector rhs = random_vector(h.cols(), 300 + seed);
+    const CVector x = gram.solve(rhs);
+    const CVector x2 = gram.solve(rhs);  // factored once, reused: bit-identical
+    CHECK(x == x2);
+    CVector hx(h.rows()), hthx(h.cols());
+    orc_matvec(reinterpret_cast<const double*>(h.data()), h.rows(), h.cols(), reinterpret_cast<const double*>(x.data()),
+               reinterpret_cast<double*>(hx.data()));
+    orc_adjoint_matvec(reinterpret_cast<const double*>(h.data()), h.rows(), h.cols(),
+                       reinterpret_cast<const double*>(hx.data()), reinterpret_cast<double*>(hthx.data()));
+    double num = 0, den = 0;
+    for (std::size_t i = 0; i < x.size(); ++i) {
+      num += std::norm(hthx[i] + 1.5 * x[i] - rhs[i]);
+      den += std::norm(rhs[i]);
+    }
+    CHECK(std::sqrt(num / den) <= 1e-8);
+  }
+  auto shared = std::make_shared<const CMatrix>(random_matrix(4, 9, 77));
+  const GramSolver from_shared(shared, 0.5);  // gram.hpp:36-37
+  CHECK(&from_shared.block() == shared.get());
+}
+
+TEST_CASE(problem_views_devices_and_observer) {
+  const SensingProblem p = desk_problem(48, 192, 4, 1011);
+  SolverConfig cfg;
+  cfg.lambda = lambda_rel(p, 0.05);
+  cfg.max_iters = 30;
+  const SolveReport base = hybrid_solve(p, cfg, 2, 4);
+  // the same problem through a non-owning view, and on the plan-owned NCCL path (one device)
+  CHECK(rel_error(hybrid_solve(view(p), cfg, 2, 4).solution, base.solution) == 0.0);
+  SolveOptions multi;
+  multi.devices = {0};
+  const SolveReport m1 = hybrid_solve(p, cfg, 2, 4, multi);
+  CHECK(rel_error(m1.solution, base.solution) <= 1e-12 && m1.iterations_run == base.iterations_run);
+  // complex64 H straight from the caller's memory into a c64 plan
+  std::vector<std::complex<float>> h64(p.h.size());
+  for (std::size_t i = 0; i < h64.size(); ++i) h64[i] = std::complex<float>((float)p.h.data()[i].real(), (float)p.h.data()[i].imag());
+  SolveOptions o64;
+  o64.dtype = ADMM_C64;
+  CHECK(rel_error(hybrid_solve(view_c64(h64.data(), 48, 192, p.g), cfg, 2, 4, o64).solution, base.solution) <= 1e-4);
+  // an exception thrown by the observer propagates out of the solve (solvers.hpp:150-160)
+  SolveOptions obs;
+  int calls = 0;
+  obs.observer = [&](const IterateSnapshot& s) {
+    ++calls;
+    if (s.iteration == 3) throw std::out_of_range("stop at 3");
+  };
+  CHECK_THROWS_AS(hybrid_solve(p, cfg, 2, 4, obs), std::out_of_range);
+  CHECK(calls == 3);
+  SensingProblem neg = p;  // problem.hpp:35-49 order: non-finite before negative noise_sigma
+  neg.noise_sigma = -1.0;
+  CHECK_THROWS_AS(hybrid_solve(neg, cfg, 2, 4), ParameterError);
+  neg.g[0] = Complex(std::numeric_limits<double>::infinity(), 0.0);
+  CHECK_THROWS_AS(hybrid_solve(neg, cfg, 2, 4), NumericalError);
 }
 
 TEST_CASE(degeneracy_lattice) {  // test_solvers.cpp:42-93
@@ -205,7 +303,9 @@ int main(int argc, char** argv) {
   struct { const char* name; void (*fn)(); } cases[] = {
       {"cmat_round_trip_and_malformed", cmat_round_trip_and_malformed},
       {"matvec_known_answers", matvec_known_answers}, {"prox_known_answers", prox_known_answers},
-      {"gram_solver", gram_solver}, {"degeneracy_lattice", degeneracy_lattice},
+      {"gram_solver", gram_solver}, {"gram_solver_strategies", gram_solver_strategies},
+      {"problem_views_devices_and_observer", problem_views_devices_and_observer},
+      {"degeneracy_lattice", degeneracy_lattice},
       {"oracle_parity_and_ledger", oracle_parity_and_ledger}, {"errors_follow_reference", errors_follow_reference}};
   for (auto& c : cases) {
     const int before = g_fail;

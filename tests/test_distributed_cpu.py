@@ -28,6 +28,7 @@ def _worker(rank, world, port, case, out):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
+        import dist_harness as DH
         import oracle_lib as orc
         import shard_engine_np as se
         from paper_1811_05571_b200 import distributed as D
@@ -37,7 +38,7 @@ def _worker(rank, world, port, case, out):
         Pr, Pc = D.choose_grid(world, method, M, N)
         pr, pc = divmod(rank, Pc)
         sh = se.NumpyShard(h, g, 1.0, lam, method, M, N, (Pr, Pc), (pr, pc))
-        D.run_iterations([sh], D.TorchComm(Pr, Pc), iters)
+        D.run_iterations([sh], DH.TorchComm(Pr, Pc), iters)
         segs = [None] * world
         dist.all_gather_object(segs, sh.segment_v())
         v = D.gather_solution(segs, shape[1], sh.col_bounds)
@@ -46,7 +47,11 @@ def _worker(rank, world, port, case, out):
             err = np.linalg.norm(v - ref["solution"]) / np.linalg.norm(ref["solution"])
             tr = np.array(sh.trace_rows)
             terr = np.max(np.abs(tr[:, 1] - ref["trace"][:, 1]) / np.maximum(np.abs(ref["trace"][:, 1]), 1e-300))
-            out.put((err, terr, sh.schedule, (Pr, Pc)))
+            # objective trace by the recurrence + gathered A regions; the two-pass schedule
+            # closes iteration k's in k + 1 (its last entry comes from the final exact pass)
+            n = iters if sh.schedule == "sweep" else iters - 1
+            oerr = np.max(np.abs(tr[:n, 2] - ref["trace"][:n, 2]) / np.abs(ref["trace"][:n, 2]))
+            out.put((err, terr, oerr, sh.schedule, (Pr, Pc)))
     finally:
         dist.destroy_process_group()
 
@@ -67,9 +72,17 @@ def test_two_rank_gloo_orchestration_matches_oracle(case):
     for p in procs:
         p.join(timeout=240)
         assert p.exitcode == 0
-    err, terr, sched, grid = out.get(timeout=5)
+    err, terr, oerr, sched, grid = out.get(timeout=5)
     assert err <= 1e-12, (err, sched, grid)
     assert terr <= 1e-10, (terr, sched, grid)
+    assert oerr <= 1e-10, (oerr, sched, grid)
+
+
+def test_phase_program():
+    from paper_1811_05571_b200.distributed import phase_program
+    assert phase_program("sweep", True) == [1, "ghat", 3, 4]
+    assert phase_program("sweep", False) == [1, "ghat", 3, "scal", 4]
+    assert phase_program("twopass", False) == [1, "ghat", 2, "outbox", 3, "scal", 4]
 
 
 def test_choose_grid_prefers_column_sharding():

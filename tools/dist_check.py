@@ -10,7 +10,10 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+sys.path.insert(0, os.path.join(REPO, "tests"))
+import dist_harness as DH  # noqa: E402  (test transport)
 import paper_1811_05571_b200 as admm  # noqa: E402
 from paper_1811_05571_b200 import distributed as D  # noqa: E402
 
@@ -29,13 +32,13 @@ def main():
         Pr, Pc = D.choose_grid(ws, method, M, N)
         sh = D.ShardPlan(p, cfg, method, M, N, (Pr, Pc), divmod(rank, Pc),
                          admm.SolveOptions(device=local, trace_objective=False))
-        comm = D.TorchComm(Pr, Pc)
+        comm = DH.TorchComm(Pr, Pc)
         D.run_iterations([sh], comm, 16)
         sh.sync()
         eager = sh.segment_v()
         sh.reset()
         D.prime([sh], comm)
-        g = D.GraphedIterations(sh, comm, iters_per_graph=8)  # captured from the current state
+        g = DH.GraphedIterations(sh, comm, iters_per_graph=8)  # captured from the current state
         sh.reset()
         D.prime([sh], comm)
         g.run(16)
