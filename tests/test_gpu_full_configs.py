@@ -49,6 +49,15 @@ def trace_of(r):
     return np.stack([r.trace.primal, r.trace.dual, r.trace.objective], 1)
 
 
+def trace_err(a, b):
+    """Max relative error over the entries the reference keeps finite; the diverging runs
+    overflow |v|^2 (and with it the residual norms and the objective) to inf at the same
+    iterations on both sides."""
+    fin = np.isfinite(b)
+    assert np.array_equal(np.isfinite(a), fin)
+    return float(np.max(np.abs(a[fin] - b[fin]) / np.abs(b[fin]))) if fin.any() else 0.0
+
+
 def plan_solve(admm, p, lam, method, M, N, iters, **opts):
     cfg = admm.SolverConfig(rho=1.0, lambda_=lam, max_iters=iters)
     with admm.AdmmPlan(p, cfg, method, M, N, admm.SolveOptions(**opts)) as plan:
@@ -71,13 +80,11 @@ def test_config2_all_300_iterations(cfg2_problem, schedule):
     assert r.iterations_run == 300
     assert rel(r.solution, ref["solution"]) <= 1e-9
     tr, rt = trace_of(r), ref["trace"]
-    assert rel(tr[:, 1], rt[:, 1]) <= 1e-8  # dual residual
+    assert trace_err(tr[:, 1], rt[:, 1]) <= 1e-8  # dual residual
     # the primal residual is ||u - v||, a difference of ~1e150-sized vectors on this diverging
     # run: the reference's own value moves by % under 1e-15 perturbations
-    assert rel(tr[:, 0], rt[:, 0]) <= 1e-2
-    fin = np.isfinite(rt[:, 2])  # the objective overflows to inf where the reference's does
-    assert np.array_equal(np.isfinite(tr[:, 2]), fin)
-    assert np.max(np.abs(tr[fin, 2] - rt[fin, 2]) / np.abs(rt[fin, 2])) <= 1e-8
+    assert trace_err(tr[:, 0], rt[:, 0]) <= 1e-2
+    assert trace_err(tr[:, 2], rt[:, 2]) <= 1e-8  # objective trace, every iteration
 
 
 @pytest.fixture(scope="module")
@@ -102,7 +109,7 @@ def test_config3_full_cra_vs_reference(cra3, dtype):
         assert err <= 1e-9, err
     else:  # + K stored in complex64
         assert err <= 1e-4 and np.array_equal(support(r.solution), support(ref["solution"])), err
-    assert rel(r.trace.dual, ref["trace"][:, 1]) <= (1e-8 if dtype == "c128" else 1e-4)
+    assert trace_err(r.trace.dual, ref["trace"][:, 1]) <= (1e-8 if dtype == "c128" else 1e-4)
 
 
 @pytest.fixture(scope="module")
@@ -131,7 +138,7 @@ def test_config4_full_width_1000_iterations(cfg4_rows, dtype):
         assert err <= 1e-4 and np.array_equal(support(r.solution), support(ref["solution"])), err
     tr, rt = trace_of(r), ref["trace"]
     tol = 1e-8 if dtype == "c128" else 1e-4
-    assert np.max(np.abs(tr[:, 2] - rt[:, 2]) / np.abs(rt[:, 2])) <= tol  # objective trace, every iteration
+    assert trace_err(tr[:, 2], rt[:, 2]) <= tol  # objective trace, every iteration
 
 
 def test_config4_full_size_c64_vs_c128_plan():
