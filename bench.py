@@ -320,6 +320,16 @@ def bench_ours(args):
         ms = float(t.item())
     ms_per_step = ms / args.steps
     value = args.steps / (ms / 1000.0)  # whole job: every rank runs its shard of the same iterations
+    support = None
+    if int(info["schedule"]) == 5:  # support schedule: the columns of v's support read per iteration
+        done, cols = plan.support_stats()
+        mean_cols = cols / max(done, 1)
+        sbytes = mean_cols * m * (8 if dtype == "c64" else 16)
+        support = {"mean_support_columns": mean_cols, "of_columns": n, "bytes_per_iter": sbytes,
+                   "frac_of_H": sbytes / info["h_bytes"],
+                   "note": "a' = H v' over the nonzero columns of the soft-thresholded v (exact: skipped terms "
+                           "are exact zeros); w' = 2a' - a - G q (DESIGN.md §4); averaged over warm-up + timed "
+                           "iterations"}
 
     if not sharded:
         roof, kern = kernel_roofline(plan, info, problem, args.config)
@@ -360,7 +370,8 @@ def bench_ours(args):
     h_stream_gbs = info["h_stream_bytes_per_iter"] / (ms_per_step / 1000.0) / 1e9
     peak, peak_kind = peaks()
     sched = {1: "two-pass", 2: "single-HBM-pass sweep", 3: "batched scenes (FP64 SIMT GEMMs)",
-             4: "resident (H in SMEM, one persistent cooperative kernel)"}[int(info["schedule"])]
+             4: "resident (H in SMEM, one persistent cooperative kernel)",
+             5: "support (one dense H pass + the columns of v's support)"}[int(info["schedule"])]
     line = {
         "metric": "ADMM iterations/s", "value": value, "unit": "iterations/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -376,14 +387,18 @@ def bench_ours(args):
         "h_stream_gbs": h_stream_gbs, "h_stream_frac_of_peak": h_stream_gbs / peak,
         "h_stream_note": "2 x |H| per iteration (SURVEY §8d's two-pass H-stream bytes) / time: a single-pass "
                          "schedule can exceed 1.0",
-        "hbm_compulsory_gbs": info["hbm_bytes_per_iter"] / (ms_per_step / 1000.0) / 1e9,
-        "hbm_compulsory_frac": info["hbm_bytes_per_iter"] / (ms_per_step / 1000.0) / 1e9 / peak,
+        "hbm_compulsory_gbs": (info["hbm_bytes_per_iter"] + (support["bytes_per_iter"] if support else 0))
+                              / (ms_per_step / 1000.0) / 1e9,
+        "hbm_compulsory_frac": (info["hbm_bytes_per_iter"] + (support["bytes_per_iter"] if support else 0))
+                               / (ms_per_step / 1000.0) / 1e9 / peak,
         "e2e": {"value": e2e_value, "unit": "iterations/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "step": f"one full solve ({iters} iterations) via AdmmPlan.set_g + solve from pinned host memory"},
         "gpu_launches": int(info["launches_per_iter"]) * args.steps if int(info["schedule"]) != 4 else 1,
         "clocks": clk.summary(),
     }
     line["roofline"] = roof
+    if support:
+        line["support"] = support
     if kern:
         line["kernels"] = kern
     if sharded:

@@ -87,8 +87,9 @@ typedef struct {
                           does at solvers.hpp:146); 0: objective of the final iterate only */
   int schedule;        /* 0 auto, 1 two-pass (H streamed twice per iteration), 2 single-HBM-pass
                           column-strip sweep, 4 resident (small problems: H in SMEM, one
-                          persistent kernel per launch); env ADMM_B200_SCHEDULE
-                          (twopass|sweep|resident) overrides */
+                          persistent kernel per launch), 5 support (one dense pass + the
+                          columns in the support of v); env ADMM_B200_SCHEDULE
+                          (twopass|sweep|resident|support) overrides */
   uint64_t batch;      /* 0/1: one scene; 2..64: independent scenes sharing H (BASELINE config 5):
                           g is n_meas x batch (scene fastest), solutions n_pix x batch, trace
                           iterations x batch x 3, lambda per scene via admm_plan_set_lambdas */
@@ -240,7 +241,8 @@ admm_status admm_plan_get_info(const admm_plan* plan, admm_plan_info* info);
 /* Current iterate getters (host copies): which = 0 v (n_pix), 1 v_prev (n_pix),
  * 2 u of every worker concatenated in worker order (sum of segment lengths),
  * 3 the trace (3 doubles per completed iteration), 4 {iterations completed,
- * first iteration with a non-finite u or -1}. */
+ * first iteration with a non-finite u or -1}, 5 (support schedule) {iterations completed,
+ * support columns of v summed over them}. */
 admm_status admm_plan_read(admm_plan* plan, int which, double* dst, uint64_t count);
 
 void admm_plan_destroy(admm_plan* plan);

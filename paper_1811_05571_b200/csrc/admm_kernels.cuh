@@ -356,13 +356,14 @@ template <int CH>
 __global__ void __launch_bounds__(kCtaThreads)
 zupdate_kernel(ColVecs cv, const double2* __restrict__ part, const MatDesc* __restrict__ mats,
                const BlockDesc* __restrict__ blocks, uint32_t M, uint32_t N, uint64_t U, uint64_t P,
-               const Params* __restrict__ prm, double* __restrict__ red, IterState* st) {
+               const Params* __restrict__ prm, double* __restrict__ red, IterState* st,
+               uint32_t* __restrict__ nzcnt = nullptr) {  // support counts per CTA (admm_sparse.cuh)
   __shared__ double sm[kCtaWarps];
   const uint32_t j = blockIdx.y;
   const BlockDesc b0 = blocks[j];  // replica 0 of segment j
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   double rp2 = 0.0, rd2 = 0.0, l1 = 0.0;
-  bool bad = false;
+  bool bad = false, nz = false;
   if (t < b0.cols) {
     const double kappa = prm->kappa;
     double2 mean = make_double2(0.0, 0.0);
@@ -377,6 +378,7 @@ zupdate_kernel(ColVecs cv, const double2* __restrict__ part, const MatDesc* __re
     }
     mean = make_double2(mean.x / prm->m_rep, mean.y / prm->m_rep);
     const double2 vn = soft_threshold(mean, kappa);
+    nz = vn.x != 0.0 || vn.y != 0.0;
     const uint32_t so = b0.seg_off + t;
     const double2 vo = cv.v[so];
     cv.vprev[so] = vo;
@@ -393,6 +395,10 @@ zupdate_kernel(ColVecs cv, const double2* __restrict__ part, const MatDesc* __re
     }
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) st->nonfinite = 1u;
+  if (nzcnt) {
+    const int c = __syncthreads_count(nz);
+    if (threadIdx.x == 0) nzcnt[blockIdx.y * gridDim.x + blockIdx.x] = (uint32_t)c;
+  }
   const uint32_t cta = blockIdx.y * gridDim.x + blockIdx.x;
   const uint32_t nct = gridDim.x * gridDim.y;
   double r = block_sum<kCtaThreads>(rp2, sm);

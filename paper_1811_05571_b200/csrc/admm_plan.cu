@@ -32,6 +32,7 @@
 #include "admm_slab.cuh"
 #include "admm_hemv.cuh"
 #include "admm_batched.cuh"
+#include "admm_sparse.cuh"
 #include "admm_resident.cuh"
 #include "admm_host.h"
 
@@ -220,6 +221,9 @@ struct admm_plan {
   // plan (dist != null), or a single-process container of one sub-plan per device (subs)
   struct Dist* dist = nullptr;
   std::vector<admm_plan*> subs;
+  // support schedule (5, admm_sparse.cuh): column-major H, packed G = H H^H, a = H v
+  DevBuf dHc, dhcoff, dhcld, dGp, dgq, danew, daold, dnzcnt, dnzlist, dnnz, dnnz_tot;
+  uint32_t nzstride = 0, supgx = 1, sup_np = 0, sup_rgx = 1;
   size_t res_smem = 0;
   uint64_t trace_cap = 0;
   cudaGraphExec_t exec = nullptr;
@@ -843,10 +847,30 @@ void launch_resident_any(admm_plan* p, cudaStream_t s, uint64_t iters, bool prol
   } while (iters > 0 && !prologue);
 }
 
+// Support schedule (admm_sparse.cuh): one dense H pass + a pass over the columns in the
+// support of v.  Automatic for a single-GPU, single-scene plan whose H exceeds L2 and whose
+// column update is a consensus one (M > 1, N = 1: every replica sees the whole v, whose
+// soft threshold makes it sparse); on request (schedule 5) for any shape.
+template <typename S>
+bool try_support(admm_plan* p, int requested) {
+  if (p->is_shard || p->batch > 1 || p->Pr * p->Pc > 1) return false;
+  if (requested != 5) {
+    if (requested != 0 || p->method != ADMM_CONSENSUS || p->M < 2) return false;
+    if (p->h_elems * sizeof(S) <= (256ull << 20)) return false;
+  }
+  if (p->Nc > kCtaThreads) return false;  // support_rows_kernel spreads <= 256 column blocks per row
+  return true;
+}
+
 template <typename S>
 void choose_schedule(admm_plan* p, int requested) {
   p->schedule = 1;
   if (requested == 1) return;
+  if (try_support<S>(p, requested)) {
+    p->schedule = 5;
+    return;
+  }
+  if (requested == 5) throw Fail{ADMM_E_PARAMETER, "support schedule not possible for this plan"};
   if (try_resident<S>(p, requested)) {
     p->schedule = 4;
     return;
@@ -1001,6 +1025,40 @@ void factor_blocks(admm_plan* p) {
   CK(cudaMemcpyAsync(&hf, flag.p, 4, cudaMemcpyDeviceToHost, p->stream));
   CK(cudaStreamSynchronize(p->stream));
   if (hf & 1u) throw Fail{ADMM_E_NUMERICAL, "CholeskyFactor: non-finite entries in input matrix"};
+  uint64_t kpacked_elems = 0;
+  if (p->kpacked) {  // packed Hermitian tile layout (shared by K and, for the support schedule, G)
+    uint64_t koff = 0, u0 = 0, po = 0, co = 0;
+    p->hv.assign(nb, HemvDesc{});
+    for (uint64_t b = 0; b < nb; ++b) {
+      HemvDesc& h = p->hv[b];
+      h.m = p->blocks[b].rows;
+      h.nT = (uint32_t)cdiv(h.m, kHT);
+      h.n_units = h.nT * (h.nT + 1) / 2;
+      h.k_off = koff;
+      h.unit0 = u0;
+      h.part_off = po;
+      h.x_off = p->blocks[b].mvec_off;
+      h.cnt_off = (uint32_t)co;
+      co += h.nT;
+      koff += (uint64_t)h.n_units * kHT * kHT;
+      u0 += h.n_units;
+      po += 2ull * h.n_units * kHT;
+    }
+    kpacked_elems = koff;
+    p->gP.U = u0;
+    p->dkppart.alloc(po * sizeof(double2));
+    p->dkcnt.alloc(std::max<uint64_t>(co, 1) * sizeof(unsigned));
+    CK(cudaMemset(p->dkcnt.p, 0, std::max<uint64_t>(co, 1) * sizeof(unsigned)));
+  }
+  if (p->schedule == 5) {  // G = rho I + H H^H - rho I = H H^H, packed before the in-place inverse
+    if (!p->kpacked) throw Fail{ADMM_E_PARAMETER, "support schedule needs the packed Hermitian apply"};
+    p->dGp.alloc(kpacked_elems * sizeof(S));
+    for (uint64_t b = 0; b < nb; ++b)
+      k_pack_kernel<S><<<p->num_sms * 4, 256, 0, p->stream>>>(A.as<double2>(), p->gram[b].a_off, p->hv[b].m,
+                                                             p->hv[b].nT, p->dGp.as<S>() + p->hv[b].k_off,
+                                                             p->cfg.rho);
+    CK(cudaGetLastError());
+  }
   const unsigned gx = (unsigned)std::min<uint64_t>(cdiv(p->max_m, 256), 8);
   for (uint32_t k = 0; k < p->max_m; ++k) {
     gj_save_kernel<<<dim3((unsigned)cdiv(p->max_m, 256), (unsigned)nb), 256, 0, p->stream>>>(
@@ -1020,33 +1078,13 @@ void factor_blocks(admm_plan* p) {
   k_store_kernel<S><<<dim3(gx, p->max_m, (unsigned)nb), 256, 0, p->stream>>>(
       A.as<double2>(), p->dgram.as<GramDesc>(), p->dK.as<S>(), flag.as<unsigned>());
   if (p->kpacked) {  // packed Hermitian tiles of the same inverse
-    uint64_t koff = 0, u0 = 0, po = 0, co = 0;
-    p->hv.assign(nb, HemvDesc{});
-    for (uint64_t b = 0; b < nb; ++b) {
-      HemvDesc& h = p->hv[b];
-      h.m = p->blocks[b].rows;
-      h.nT = (uint32_t)cdiv(h.m, kHT);
-      h.n_units = h.nT * (h.nT + 1) / 2;
-      h.k_off = koff;
-      h.unit0 = u0;
-      h.part_off = po;
-      h.x_off = p->blocks[b].mvec_off;
-      h.cnt_off = (uint32_t)co;
-      co += h.nT;
-      koff += (uint64_t)h.n_units * kHT * kHT;
-      u0 += h.n_units;
-      po += 2ull * h.n_units * kHT;
-    }
-    p->dKp.alloc(koff * sizeof(S));
+    p->dKp.alloc(kpacked_elems * sizeof(S));
     for (uint64_t b = 0; b < nb; ++b)
       k_pack_kernel<S><<<p->num_sms * 4, 256, 0, p->stream>>>(A.as<double2>(), p->gram[b].a_off, p->hv[b].m,
                                                              p->hv[b].nT, p->dKp.as<S>() + p->hv[b].k_off);
     upload_desc(p->dhv, p->hv.data(), nb * sizeof(HemvDesc));
-    p->dkppart.alloc(po * sizeof(double2));
-    p->dkcnt.alloc(std::max<uint64_t>(co, 1) * sizeof(unsigned));
-    CK(cudaMemset(p->dkcnt.p, 0, std::max<uint64_t>(co, 1) * sizeof(unsigned)));
-    if (const char* e = std::getenv("ADMM_B200_HEMV_FUSE")) p->hemv_fuse = e[0] == '1';
-    p->gP.U = u0;
+    const uint64_t u0 = p->gP.U;
+    if (const char* e = std::getenv("ADMM_B200_HEMV_FUSE")) p->hemv_fuse = e[0] == '1' && p->schedule != 5;
     if (const char* e = std::getenv("ADMM_B200_HEMV_OCC")) p->hemv_occ = std::atoi(e) == 2 ? 2 : 1;
     p->gP.P = p->hemv_occ == 2 ? grid_for<S>(hemv_kernel<S, 2, false>, u0, p->num_sms)
                                : grid_for<S>(hemv_kernel<S, 1, false>, u0, p->num_sms);
@@ -1137,6 +1175,108 @@ void enqueue_kapply(admm_plan* p, cudaStream_t s, Mid mid) {
 template <typename S>
 void enqueue_kapply(admm_plan* p, cudaStream_t s) {
   enqueue_kapply<S>(p, s, [] {});
+}
+
+// Support schedule: (G q) of every block from the packed G tiles (same kernels as K).
+template <typename S>
+void enqueue_gq(admm_plan* p, cudaStream_t s) {
+  const int nb = (int)p->blocks.size();
+  if (p->hemv_bulk) {
+    auto fb = p->hemv_bulk == 2 ? hemv_bulk_kernel<S, 2> : hemv_bulk_kernel<S, 1>;
+    const size_t sm = p->hemv_bulk == 2 ? hemv_bulk_smem<S, 2>(p->max_rows) : hemv_bulk_smem<S, 1>(p->max_rows);
+    launch_pdl(fb, dim3((unsigned)p->gP.P), dim3(kCtaThreads), sm, s, (const S*)p->dGp.as<S>(),
+               (const double2*)p->dq.as<double2>(), p->dkppart.as<double2>(), (const HemvDesc*)p->dhv.as<HemvDesc>(),
+               nb, p->gP.U, 0);
+  } else {
+    auto fn = p->hemv_occ == 2 ? hemv_kernel<S, 2, false> : hemv_kernel<S, 1, false>;
+    launch_pdl(fn, dim3((unsigned)p->gP.P), dim3(kCtaThreads), 0, s, (const S*)p->dGp.as<S>(),
+               (const double2*)p->dq.as<double2>(), p->dkppart.as<double2>(), (const HemvDesc*)p->dhv.as<HemvDesc>(),
+               nb, p->gP.U, 0, (unsigned*)nullptr, row_vecs(p), (const Params*)p->dparams.as<Params>());
+  }
+  launch_pdl(hemv_gq_kernel, dim3((unsigned)cdiv(p->max_rows, kHFinRows), nb), dim3(kHFinRows), 0, s,
+             (const double2*)p->dkppart.as<double2>(), (const HemvDesc*)p->dhv.as<HemvDesc>(), p->gP.U, p->gP.P,
+             p->dgq.as<double2>());
+}
+
+// Support schedule rows step: w' = 2a' - a - Gq, g_ij, r; objective rows (first: r = g_ij).
+void enqueue_support_rows(admm_plan* p, cudaStream_t s, bool first) {
+  support_rows_kernel<<<dim3(p->sup_rgx, (unsigned)p->Mr), kCtaThreads, 0, s>>>(
+      row_vecs(p), p->dblocks.as<BlockDesc>(), p->dgblocks.as<BlockDesc>(), (uint32_t)p->Nc, p->sup_np,
+      p->danew.as<double2>(), p->daold.as<double2>(), p->dgq.as<double2>(), first ? 1 : 0, p->dored.as<double>());
+}
+
+// One iteration of the support schedule (admm_sparse.cuh).
+template <typename S>
+void enqueue_iteration_support(admm_plan* p, cudaStream_t s, bool with_objective, std::vector<cudaEvent_t>* ev) {
+  constexpr int CH = chunk_h<S>();
+  const int nb = (int)p->blocks.size();
+  const uint32_t N = (uint32_t)p->Nc, M = (uint32_t)p->Mr;
+  auto mark = [&](size_t k) {
+    if (ev) CK(cudaEventRecord((*ev)[k], s));
+  };
+  mark(0);
+  gemv_h_kernel<S, kVH, kEvictFirst><<<(unsigned)p->gH.P, kCtaThreads, 0, s>>>(
+      p->dH.as<S>(), p->dq.as<double2>(), p->dzpart.as<double2>(), p->dhH.as<MatDesc>(), nb, p->gH.U);
+  mark(1);
+  enqueue_gq<S>(p, s);
+  mark(2);
+  zupdate_kernel<CH><<<dim3(p->zgx, N), kCtaThreads, 0, s>>>(
+      col_vecs(p), p->dzpart.as<double2>(), p->dhH.as<MatDesc>(), p->dblocks.as<BlockDesc>(), M, N, p->gH.U,
+      p->gH.P, p->dparams.as<Params>(), p->dred.as<double>(), p->dstate.as<IterState>(), p->dnzcnt.as<uint32_t>());
+  support_compact_kernel<<<dim3(p->zgx, N), kCtaThreads, 0, s>>>(
+      p->dv.as<double2>(), p->dblocks.as<BlockDesc>(), p->dnzcnt.as<uint32_t>(), p->zgx, p->dnzlist.as<uint32_t>(),
+      p->nzstride, p->dnnz.as<uint32_t>(), p->dnnz_tot.as<unsigned long long>());
+  mark(3);
+  support_a_kernel<S><<<dim3(p->supgx, (unsigned)nb), kSupRows, 0, s>>>(
+      p->dHc.as<S>(), p->dhcoff.as<uint64_t>(), p->dhcld.as<uint32_t>(), p->dblocks.as<BlockDesc>(),
+      p->dv.as<double2>(), p->dnzlist.as<uint32_t>(), p->nzstride, p->dnnz.as<uint32_t>(), p->danew.as<double2>());
+  mark(4);
+  enqueue_support_rows(p, s, false);
+  finalize_kernel<<<1, kCtaThreads, 0, s>>>(p->dred.as<double>(), p->nz, p->dored.as<double>(),
+                                            with_objective ? p->sup_rgx * M : 0, p->dparams.as<Params>(),
+                                            p->dtrace.as<double>(), p->trace_cap, p->dstate.as<IterState>());
+  mark(5);
+  enqueue_kapply<S>(p, s, [&] { mark(6); });
+  mark(7);
+  CK(cudaGetLastError());
+}
+
+// Setup of the support schedule: column-major copy of every block and the vectors.
+template <typename S>
+void build_support(admm_plan* p) {
+  const uint64_t nb = p->blocks.size();
+  std::vector<uint64_t> coff(nb);
+  std::vector<uint32_t> ld(nb);
+  uint64_t tot = 0;
+  for (uint64_t b = 0; b < nb; ++b) {
+    ld[b] = (uint32_t)round_up(p->blocks[b].rows, 8);
+    coff[b] = tot;
+    tot += (uint64_t)ld[b] * p->blocks[b].cols;
+  }
+  p->dHc.alloc(tot * sizeof(S));
+  upload_desc(p->dhcoff, coff.data(), nb * sizeof(uint64_t));
+  upload_desc(p->dhcld, ld.data(), nb * sizeof(uint32_t));
+  for (uint64_t b = 0; b < nb; ++b) {
+    const MatDesc& md = p->hN[b];
+    dim3 grid((unsigned)cdiv(md.cols, 32), (unsigned)cdiv(ld[b], 32));
+    colmajor_kernel<S><<<grid, dim3(32, 8), 0, p->stream>>>(p->dH.as<S>(), md.a_off, md.ld, md.rows, md.cols,
+                                                            p->dHc.as<S>(), coff[b], ld[b]);
+  }
+  CK(cudaGetLastError());
+  p->nzstride = (uint32_t)round_up(p->max_seg, 4);
+  p->dnzcnt.alloc((uint64_t)p->zgx * p->Nc * sizeof(uint32_t));
+  p->dnzlist.alloc((uint64_t)p->nzstride * p->Nc * sizeof(uint32_t));
+  p->dnnz.alloc(p->Nc * sizeof(uint32_t));
+  p->dnnz_tot.alloc(sizeof(unsigned long long));
+  p->dgq.alloc(p->mvec_total * 16);
+  p->danew.alloc(p->mvec_total * 16);
+  p->daold.alloc(p->mvec_total * 16);
+  p->supgx = (uint32_t)cdiv(p->max_rows, kSupRows);
+  while ((1u << p->sup_np) < p->Nc) ++p->sup_np;
+  p->sup_rgx = (uint32_t)std::max<uint64_t>(1, cdiv(p->max_rowblock, kCtaThreads >> p->sup_np));
+  p->dored.alloc((size_t)std::max<uint64_t>(p->dored.bytes / sizeof(double), (uint64_t)p->sup_rgx * p->Mr) *
+                 sizeof(double));
+  CK(cudaStreamSynchronize(p->stream));
 }
 
 // Launch list of one iteration (the order of solvers.hpp's phases).
@@ -1517,7 +1657,12 @@ void enqueue_iteration_any(admm_plan* p, cudaStream_t s, bool obj, std::vector<c
       enqueue_iteration_batched<float2>(p, s, obj, ev);
     return;
   }
-  if (p->schedule == 2) {
+  if (p->schedule == 5) {
+    if (p->dtype == ADMM_C128)
+      enqueue_iteration_support<double2>(p, s, obj, ev);
+    else
+      enqueue_iteration_support<float2>(p, s, obj, ev);
+  } else if (p->schedule == 2) {
     if (p->dtype == ADMM_C128)
       enqueue_iteration_sweep<double2>(p, s, obj, ev);
     else
@@ -1615,7 +1760,8 @@ void upload_g(admm_plan* p, const double* g) {
 
 void reset_state(admm_plan* p) {
   cudaStream_t s = p->stream;
-  for (DevBuf* d : {&p->du, &p->ds, &p->dc, &p->dv, &p->dvprev, &p->dgij, &p->dr, &p->dq, &p->dhs})
+  for (DevBuf* d : {&p->du, &p->ds, &p->dc, &p->dv, &p->dvprev, &p->dgij, &p->dr, &p->dq, &p->dhs, &p->danew,
+                    &p->daold, &p->dgq})
     if (d->p) CK(cudaMemsetAsync(d->p, 0, d->bytes, s));
   CK(cudaMemsetAsync(p->ghat_ptr, 0, p->mvec_total * 16 * p->batch, s));
   CK(cudaMemsetAsync(p->outbox_ptr, 0, p->outbox_total * 16, s));
@@ -1629,6 +1775,14 @@ void reset_state(admm_plan* p) {
       enqueue_sweep_prologue<float2>(p, s);
   }
   if (p->schedule == 4) launch_resident_any(p, s, 0, true, false);
+  if (p->schedule == 5) {  // prologue: r = g_ij (w = H c^0 = 0), q = K r, ghat
+    enqueue_support_rows(p, s, true);
+    if (p->dtype == ADMM_C128)
+      enqueue_kapply<double2>(p, s);
+    else
+      enqueue_kapply<float2>(p, s);
+    CK(cudaGetLastError());
+  }
 }
 
 void ensure_trace(admm_plan* p, uint64_t iters) {
@@ -1839,6 +1993,7 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
     if (!std::strcmp(env, "twopass")) requested = 1;
     if (!std::strcmp(env, "sweep")) requested = 2;
     if (!std::strcmp(env, "resident")) requested = 4;
+    if (!std::strcmp(env, "support")) requested = 5;
   }
   if (skip_cfg_validation || o.batch > 1) requested = 1;  // helper plans / batched scenes
   if (p->dtype == ADMM_C128) {
@@ -1912,11 +2067,13 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
     upload_h<double2>(p.get(), h, h_dtype);
     if (p->tile_rb) build_tile<double2>(p.get());
     if (p->slab_rpl) build_slab<double2>(p.get());
+    if (p->schedule == 5) build_support<double2>(p.get());
     factor_blocks<double2>(p.get());
   } else {
     upload_h<float2>(p.get(), h, h_dtype);
     if (p->tile_rb) build_tile<float2>(p.get());
     if (p->slab_rpl) build_slab<float2>(p.get());
+    if (p->schedule == 5) build_support<float2>(p.get());
     factor_blocks<float2>(p.get());
   }
   if (p->batch > 1) {
@@ -2113,7 +2270,7 @@ admm_status admm_plan_set_stream(admm_plan* p, void* stream) {
 }
 
 uint32_t admm_plan_kernel_count(const admm_plan* p) {
-  return !p ? 7 : p->schedule == 4 ? 1 : p->schedule == 2 ? 4 : 7;
+  return !p ? 7 : p->schedule == 4 ? 1 : p->schedule == 2 ? 4 : 7;  // (schedule 5: 7 launch groups)
 }
 
 admm_status admm_plan_set_lambdas(admm_plan* p, const double* lambdas) {
@@ -2176,7 +2333,10 @@ admm_status admm_plan_profile(admm_plan* p, uint64_t iters, const char** names, 
     const int nk = (int)admm_plan_kernel_count(p);
     const bool fused = p->kpacked && p->hemv_fuse;
     static const char* kNamesR[1] = {"resident(iteration)"};
-    const char* const* kn = p->schedule == 4   ? kNamesR
+    static const char* kNamesU[7] = {"gemv_h(H,q)", "hemv(G,q)+gq", "zupdate+support_list", "support_a(Hc,v)",
+                                     "support_rows+finalize", "hemv(Kpacked,r)", "hemv_finalize(q)"};
+    const char* const* kn = p->schedule == 5   ? kNamesU
+                            : p->schedule == 4 ? kNamesR
                             : p->schedule == 2 ? (fused ? kNamesSF : p->kpacked ? kNamesSP : kNamesS)
                             : p->schedule == 3 ? kNamesB
                                                : (fused ? kNames2F : p->kpacked ? kNames2P : kNames2);
@@ -2227,11 +2387,12 @@ admm_status admm_plan_get_info(const admm_plan* p, admm_plan_info* info) {
     r.h_stream_bytes_per_iter = 2 * hb;
     r.bytes_per_iter = 2 * hb + kb_dense + vb;  // two-pass algorithmic bytes
     // resident: ONE launch runs all the iterations of an enqueue (reported as 0 per iteration)
-    r.launches_per_iter = p->schedule == 4 ? 0 : p->schedule == 3 ? 7 : p->schedule == 2 ? (p->trace_obj ? (p->obj_pass ? 7 : 6) : 4) : (p->trace_obj ? 9 : 7);
+    r.launches_per_iter = p->schedule == 5 ? 10 : p->schedule == 4 ? 0 : p->schedule == 3 ? 7 : p->schedule == 2 ? (p->trace_obj ? (p->obj_pass ? 7 : 6) : 4) : (p->trace_obj ? 9 : 7);
     if (p->schedule != 3 && p->kpacked && p->hemv_fuse) r.launches_per_iter -= 1;  // finalize inside hemv
     r.schedule = (uint64_t)p->schedule;
     r.grid_sweep = p->gS.P;
-    r.hbm_bytes_per_iter = (p->schedule == 4 ? 0 : p->schedule == 2 ? hb : 2 * hb) + kb + vb;
+    // support schedule: one dense pass + K + G (+ the data-dependent support columns, admm_plan_read 5)
+    r.hbm_bytes_per_iter = p->schedule == 5 ? hb + 2 * kb + vb : (p->schedule == 4 ? 0 : p->schedule == 2 ? hb : 2 * hb) + kb + vb;
     r.sweep_variant = p->schedule != 2 ? 0 : p->slab_rpl ? 3 : p->tile_rb ? 2 : 1;
     r.slab_cluster = p->slab_rpl ? p->slab_C : 0;
     r.slab_row_bytes = p->slab_rpl ? p->slab_rb : 0;
@@ -2300,6 +2461,13 @@ admm_status admm_plan_read(admm_plan* p, int which, double* dst, uint64_t count)
                            cudaMemcpyDeviceToHost, p->stream));
         CK(cudaStreamSynchronize(p->stream));
       }
+    } else if (which == 5) {  // support schedule: {iterations completed, support columns summed over them}
+      if (count < 2) throw Fail{ADMM_E_DIMENSION, "destination too small"};
+      const IterState st = read_state(p);
+      unsigned long long tot = 0;
+      if (p->dnnz_tot.p) CK(cudaMemcpy(&tot, p->dnnz_tot.p, sizeof(tot), cudaMemcpyDeviceToHost));
+      dst[0] = (double)st.iter;
+      dst[1] = (double)tot;
     } else if (which == 4) {  // {iterations completed, first non-finite iteration or -1}
       if (count < 2) throw Fail{ADMM_E_DIMENSION, "destination too small"};
       const IterState st = read_state(p);

@@ -1,0 +1,191 @@
+// admm_sparse.cuh — the "support" schedule: ONE dense pass over H per iteration plus a pass
+// over only the columns in the support of the soft-thresholded variable v.
+//
+// Why it is the reference's iteration.  Per block b = (i, j) the column update of
+// solvers.hpp (u = c + z, v' = S_kappa(mean_i(u + s)), s' = s + u - v', c' = v' - s';
+// admm_core.hpp:80-89, prox.hpp:15) with c = v - s from the previous update gives
+//     s' = v + z - v'      and      c' = 2 v' - v - z,        z = H_b^H q_b,
+// so the next product the reference forms, w' = H_b c' (gram.hpp:71-77 inside the
+// Woodbury solve), is exactly
+//     w' = 2 a' - a - G_b q_b,      a = H_b v,  a' = H_b v',  G_b = H_b H_b^H.
+// G_b is the Gram matrix the setup already forms for the Woodbury factor (gram.hpp:92-122);
+// it is kept (packed Hermitian tiles, like K) and applied like K.  a' = H_b v' touches
+// only the columns where v' != 0: soft thresholding makes v sparse (config 4: ~1e3 of
+// 262144 columns), and a skipped term is an exact zero (H is validated finite), so a'
+// is bit-identical to the dense product in the same (ascending-column) order.  With v
+// dense the same kernels read every column: the iteration then streams H twice, like
+// the two-pass schedule.  Per iteration:
+//
+//   z = H^H q                 gemv_h_kernel (dense pass, row-major H)
+//   Gq = G q                  hemv (packed G) + gq finalize
+//   u, v', s', c', residuals  zupdate_kernel (+ per-CTA support counts)
+//   support list of v'        support_compact_kernel (ascending, deterministic)
+//   a' = H v' on the support  support_a_kernel (column-major copy of H)
+//   w', r, objective rows     support_rows_kernel
+//   trace[k]                  finalize_kernel
+//   q = K r, ghat             hemv (packed K) + hemv_finalize
+// Bit-reproducible: fixed-order sums, no atomics.
+#pragma once
+
+#include "admm_hemv.cuh"
+#include "admm_kernels.cuh"
+
+namespace admm {
+
+constexpr int kSupRows = 128;  // rows per support_a_kernel CTA (one thread per row)
+constexpr int kSupUnroll = 8;  // support columns in flight per thread
+
+// Column-major copy of a block: Hc[x * ldc + r] = H[r * ld + x] (setup only).
+template <typename S>
+__global__ void colmajor_kernel(const S* __restrict__ H, uint64_t a_off, uint32_t ld, uint32_t rows, uint32_t cols,
+                                S* __restrict__ Hc, uint64_t c_off, uint32_t ldc) {
+  __shared__ S tile[32][33];
+  const uint32_t c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  for (uint32_t k = threadIdx.y; k < 32; k += blockDim.y) {
+    const uint32_t r = r0 + k, c = c0 + threadIdx.x;
+    S v;
+    v.x = 0;
+    v.y = 0;
+    if (r < rows && c < cols) v = H[a_off + (uint64_t)r * ld + c];
+    tile[k][threadIdx.x] = v;
+  }
+  __syncthreads();
+  for (uint32_t k = threadIdx.y; k < 32; k += blockDim.y) {
+    const uint32_t c = c0 + k, r = r0 + threadIdx.x;
+    if (c < cols && r < ldc) Hc[c_off + (uint64_t)c * ldc + r] = r < rows ? tile[threadIdx.x][k] : S{};
+  }
+}
+
+// support list of segment j: CTA (x, j) covers columns [256x, 256x + 256); its offset is
+// the sum of the counts of the CTAs before it (zupdate wrote them), so the list is in
+// ascending column order.  The last CTA of a segment stores the segment's support size
+// and adds it to the running total (diagnostics: mean support per iteration).
+__global__ void __launch_bounds__(kCtaThreads)
+support_compact_kernel(const double2* __restrict__ v, const BlockDesc* __restrict__ blocks,
+                       const uint32_t* __restrict__ cnt, uint32_t gx, uint32_t* __restrict__ list,
+                       uint32_t list_stride, uint32_t* __restrict__ nnz, unsigned long long* __restrict__ nnz_total) {
+  __shared__ double sm[kCtaWarps];
+  __shared__ uint32_t wsum[kCtaWarps];
+  const uint32_t j = blockIdx.y, x = blockIdx.x;
+  const BlockDesc b0 = blocks[j];
+  double pre = 0.0;  // counts are < 2^32: exact in FP64 through block_sum
+  for (uint32_t k = threadIdx.x; k < x; k += kCtaThreads) pre += (double)cnt[j * gx + k];
+  pre = block_sum<kCtaThreads>(pre, sm);
+  __shared__ uint32_t off;
+  if (threadIdx.x == 0) off = (uint32_t)pre;
+  const uint32_t t = x * kCtaThreads + threadIdx.x;
+  bool nz = false;
+  if (t < b0.cols) {
+    const double2 a = v[b0.seg_off + t];
+    nz = a.x != 0.0 || a.y != 0.0;
+  }
+  const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+  const unsigned m = __ballot_sync(0xffffffffu, nz);
+  if (lane == 0) wsum[warp] = __popc(m);
+  __syncthreads();
+  uint32_t base = off;
+  for (int w = 0; w < warp; ++w) base += wsum[w];
+  if (nz) list[(uint64_t)j * list_stride + base + __popc(m & ((1u << lane) - 1u))] = t;
+  if (x == gridDim.x - 1 && threadIdx.x == 0) {
+    uint32_t tot = off;
+    for (int w = 0; w < kCtaWarps; ++w) tot += wsum[w];
+    nnz[j] = tot;
+    atomicAdd(nnz_total, (unsigned long long)tot);  // integer: order-independent
+  }
+}
+
+// a'_b = H_b v' over the support of segment j (ascending columns): one thread per row of
+// a kSupRows tile, kSupUnroll columns in flight.  Grid (row tiles, local blocks).
+template <typename S>
+__global__ void __launch_bounds__(kSupRows)
+support_a_kernel(const S* __restrict__ Hc, const uint64_t* __restrict__ coff, const uint32_t* __restrict__ ldc,
+                 const BlockDesc* __restrict__ blocks, const double2* __restrict__ v, const uint32_t* __restrict__ list,
+                 uint32_t list_stride, const uint32_t* __restrict__ nnz, double2* __restrict__ anew) {
+  const uint32_t b = blockIdx.y;
+  const BlockDesc bd = blocks[b];
+  const uint32_t row = blockIdx.x * kSupRows + threadIdx.x;
+  if (blockIdx.x * kSupRows >= bd.rows) return;
+  const uint32_t n = nnz[bd.jl];
+  const uint32_t* lj = list + (uint64_t)bd.jl * list_stride;
+  const S* hb = Hc + coff[b];
+  const uint32_t L = ldc[b];
+  const double2* vj = v + bd.seg_off;
+  const bool ok = row < bd.rows;
+  double2 acc = make_double2(0.0, 0.0);
+  uint32_t k = 0;
+  for (; k + kSupUnroll <= n; k += kSupUnroll) {
+    uint32_t xs[kSupUnroll];
+#pragma unroll
+    for (int u = 0; u < kSupUnroll; ++u) xs[u] = __ldg(lj + k + u);
+    S hv[kSupUnroll];
+#pragma unroll
+    for (int u = 0; u < kSupUnroll; ++u) {
+      if (ok) {
+        hv[u] = __ldcs(hb + (uint64_t)xs[u] * L + row);
+      } else {
+        hv[u].x = 0;
+        hv[u].y = 0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kSupUnroll; ++u) cmac(acc, Store<S>::widen(hv[u]), __ldg(vj + xs[u]));
+  }
+  for (; k < n; ++k) {
+    const uint32_t x = __ldg(lj + k);
+    if (ok) cmac(acc, Store<S>::widen(hb[(uint64_t)x * L + row]), __ldg(vj + x));
+  }
+  if (ok) anew[bd.mvec_off + row] = acc;
+}
+
+// Per row r of row block i (NP = 2^np_log2 lanes per row, lane j = column block): for every
+// local block b = (i, j): w' = 2 a' - a - (G q)_b (first: w' = 0), a <- a', g_ij, r = g_ij - w';
+// then |sum_j a'_ij - g_i|^2 (ascending j) into per-CTA objective partials.
+__global__ void __launch_bounds__(kCtaThreads)
+support_rows_kernel(RowVecs rv, const BlockDesc* __restrict__ blocks, const BlockDesc* __restrict__ gblocks,
+                    uint32_t N, uint32_t np_log2, const double2* __restrict__ anew, double2* __restrict__ aold,
+                    const double2* __restrict__ gq, int first, double* __restrict__ ored) {
+  __shared__ double2 sa[kCtaThreads];
+  __shared__ double sm[kCtaWarps];
+  const uint32_t i = blockIdx.y;
+  const BlockDesc b0 = blocks[i * N];
+  const uint32_t NP = 1u << np_log2, j = threadIdx.x & (NP - 1), rl = threadIdx.x >> np_log2;
+  const uint32_t row = blockIdx.x * (kCtaThreads >> np_log2) + rl;
+  const bool on = row < b0.rows && j < N;
+  double2 a = make_double2(0.0, 0.0);
+  if (on) {
+    const BlockDesc bd = blocks[i * N + j];
+    const uint64_t o = (uint64_t)bd.mvec_off + row;
+    double2 w = make_double2(0.0, 0.0);
+    if (!first) {
+      a = anew[o];
+      w = csub(csub(cscale(a, 2.0), aold[o]), gq[o]);
+      aold[o] = a;
+    }
+    const double2 gij = gij_row(rv, gblocks, bd, N, row);
+    rv.gij[o] = gij;
+    rv.r[o] = csub(gij, w);
+  }
+  sa[threadIdx.x] = a;
+  __syncthreads();
+  double q = 0.0;
+  if (!first && row < b0.rows && j == 0) {
+    double2 hv = make_double2(0.0, 0.0);
+    for (uint32_t jj = 0; jj < N; ++jj) hv = cadd(hv, sa[rl * NP + jj]);
+    q = cabs2(csub(hv, rv.g[b0.row0 + row]));
+  }
+  const double r = block_sum<kCtaThreads>(q, sm);
+  if (threadIdx.x == 0) ored[blockIdx.y * gridDim.x + blockIdx.x] = r;
+}
+
+// (G q)[row] of every block from the hemv partials (the fixed order of hemv_finalize).
+__global__ void __launch_bounds__(kHFinRows)
+hemv_gq_kernel(const double2* __restrict__ part, const HemvDesc* __restrict__ hd, uint64_t U, uint64_t P,
+               double2* __restrict__ out) {
+  const HemvDesc d = hd[blockIdx.y];
+  pdl_enter();
+  const uint32_t row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= d.m) return;
+  out[d.x_off + row] = hemv_sum_row(part, d, row / kHT, row % kHT, U, P);
+}
+
+}  // namespace admm

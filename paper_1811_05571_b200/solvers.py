@@ -117,7 +117,7 @@ class SolveOptions:
     dtype: str = "c128"
     device: int = 0
     trace_objective: bool = True
-    schedule: str = "auto"  # "auto" | "twopass" | "sweep" | "resident"
+    schedule: str = "auto"  # "auto" | "twopass" | "sweep" | "resident" | "support"
     devices: Optional[list] = None  # GPUs of this process, one shard each (plan-owned NCCL);
     #                                 None: the single-GPU plan on `device`
 
@@ -252,7 +252,7 @@ class AdmmPlan:
         self.opts = opts
         o = _lib.PlanOptionsC(_METHOD[method], self.M, self.N, int(opts.ragged),
                               _DTYPE[opts.dtype], int(opts.device), int(opts.trace_objective),
-                              {"auto": 0, "twopass": 1, "sweep": 2, "resident": 4}[opts.schedule], self.batch,
+                              {"auto": 0, "twopass": 1, "sweep": 2, "resident": 4, "support": 5}[opts.schedule], self.batch,
                               float(problem.noise_sigma))
         c = self.cfg._c()
         handle = ctypes.c_void_p()
@@ -391,6 +391,12 @@ class AdmmPlan:
         ms = (ctypes.c_double * n)()
         check(_lib.lib.admm_plan_profile(self._h, int(iters), names, ms))
         return {names[k].decode(): ms[k] for k in range(n)}
+
+    def support_stats(self) -> tuple:
+        """Support schedule: (iterations since reset, support columns summed over them)."""
+        out = np.zeros(2)
+        check(_lib.lib.admm_plan_read(self._h, 5, _ptr(out), 2))
+        return int(out[0]), int(out[1])
 
     def read(self, which: str) -> np.ndarray:
         w = {"v": 0, "v_prev": 1, "u": 2}[which]

@@ -73,7 +73,7 @@ def cfg2_problem():
     return admm, p, entry, ref
 
 
-@pytest.mark.parametrize("schedule", ["auto", "sweep", "twopass"])
+@pytest.mark.parametrize("schedule", ["auto", "sweep", "twopass", "support"])
 def test_config2_all_300_iterations(cfg2_problem, schedule):
     admm, p, entry, ref = cfg2_problem
     r, info = plan_solve(admm, p, entry["lambda"], "sectioning", 1, 8, 300, schedule=schedule)
@@ -123,12 +123,15 @@ def cfg4_rows():
     return admm, p, h64, entry, ref
 
 
+@pytest.mark.parametrize("schedule", ["auto", "twopass"])
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
-def test_config4_full_width_1000_iterations(cfg4_rows, dtype):
+def test_config4_full_width_1000_iterations(cfg4_rows, dtype, schedule):
+    """auto = the support schedule for this consensus shape (what the bench runs)."""
     admm, p, h64, entry, ref = cfg4_rows
     hp = h64 if dtype == "c64" else h64.astype(np.complex128)
     q = admm.SensingProblem(hp, p.g, p.truth)
-    r, _ = plan_solve(admm, q, entry["lambda"], "consensus", 8, 1, 1000, dtype=dtype)
+    r, info = plan_solve(admm, q, entry["lambda"], "consensus", 8, 1, 1000, dtype=dtype, schedule=schedule)
+    assert info["schedule"] == (5 if schedule == "auto" else 1)
     assert r.iterations_run == 1000
     err = rel(r.solution, ref["solution"])
     if dtype == "c128":
@@ -148,7 +151,10 @@ def test_config4_full_size_c64_vs_c128_plan():
     import paper_1811_05571_b200 as admm
     p = admm.gen_problem(16384, 262144, 1000, 30.0, 4, dtype="c64")
     cfg = admm.SolverConfig(rho=1.0, lambda_=1.0, max_iters=1000)
-    with admm.AdmmPlan(p, cfg, "consensus", 8, 1, admm.SolveOptions(dtype="c128", trace_objective=False)) as plan:
+    # two-pass for the 64 GiB c128 plan (the support schedule's column-major copy would not
+    # fit next to it); the c64 plan runs the bench's schedule (support)
+    with admm.AdmmPlan(p, cfg, "consensus", 8, 1, admm.SolveOptions(dtype="c128", trace_objective=False,
+                                                                    schedule="twopass")) as plan:
         lam = 0.05 * plan.max_abs_adjoint()
         plan.set_lambda(lam)
         r128 = plan.solve()

@@ -124,12 +124,13 @@ def test_gram_solver_known_answers_and_oracle():
 CASES = [c for c in gc.solve_cases()]
 
 
-@pytest.mark.parametrize("schedule", ["auto", "sweep", "twopass", "resident"])
+@pytest.mark.parametrize("schedule", ["auto", "sweep", "twopass", "resident", "support"])
 @pytest.mark.parametrize("name", CASES)
 def test_solver_parity_vs_reference_fixture(name, schedule):
     """Every fixture on every schedule: "sweep" the single-HBM-pass kernels, "twopass" the
     stream-K GEMV pair, "resident" the persistent SMEM-resident kernel (admm_resident.cuh),
-    "auto" whichever the plan picks."""
+    "support" one dense pass + the support of v (admm_sparse.cuh), "auto" whichever the
+    plan picks."""
     entry, ref = gc.load(name)
     args = gc.solver_args(entry)
     a = admm()
