@@ -1202,7 +1202,8 @@ void enqueue_gq(admm_plan* p, cudaStream_t s) {
 void enqueue_support_rows(admm_plan* p, cudaStream_t s, bool first) {
   support_rows_kernel<<<dim3(p->sup_rgx, (unsigned)p->Mr), kCtaThreads, 0, s>>>(
       row_vecs(p), p->dblocks.as<BlockDesc>(), p->dgblocks.as<BlockDesc>(), (uint32_t)p->Nc, p->sup_np,
-      p->danew.as<double2>(), p->daold.as<double2>(), p->dgq.as<double2>(), first ? 1 : 0, p->dored.as<double>());
+      p->danew.as<double2>(), p->mvec_total, p->daold.as<double2>(), p->dgq.as<double2>(), first ? 1 : 0,
+      p->dored.as<double>());
 }
 
 // One iteration of the support schedule (admm_sparse.cuh).
@@ -1227,9 +1228,10 @@ void enqueue_iteration_support(admm_plan* p, cudaStream_t s, bool with_objective
       p->dv.as<double2>(), p->dblocks.as<BlockDesc>(), p->dnzcnt.as<uint32_t>(), p->zgx, p->dnzlist.as<uint32_t>(),
       p->nzstride, p->dnnz.as<uint32_t>(), p->dnnz_tot.as<unsigned long long>());
   mark(3);
-  support_a_kernel<S><<<dim3(p->supgx, (unsigned)nb), kSupRows, 0, s>>>(
+  support_a_kernel<S><<<dim3(p->supgx, (unsigned)nb, kSupChunks), kSupThreads, 0, s>>>(
       p->dHc.as<S>(), p->dhcoff.as<uint64_t>(), p->dhcld.as<uint32_t>(), p->dblocks.as<BlockDesc>(),
-      p->dv.as<double2>(), p->dnzlist.as<uint32_t>(), p->nzstride, p->dnnz.as<uint32_t>(), p->danew.as<double2>());
+      p->dv.as<double2>(), p->dnzlist.as<uint32_t>(), p->nzstride, p->dnnz.as<uint32_t>(), p->danew.as<double2>(),
+      p->mvec_total);
   mark(4);
   enqueue_support_rows(p, s, false);
   finalize_kernel<<<1, kCtaThreads, 0, s>>>(p->dred.as<double>(), p->nz, p->dored.as<double>(),
@@ -1269,9 +1271,9 @@ void build_support(admm_plan* p) {
   p->dnnz.alloc(p->Nc * sizeof(uint32_t));
   p->dnnz_tot.alloc(sizeof(unsigned long long));
   p->dgq.alloc(p->mvec_total * 16);
-  p->danew.alloc(p->mvec_total * 16);
+  p->danew.alloc(p->mvec_total * 16 * kSupChunks);  // column-chunk partials of a'
   p->daold.alloc(p->mvec_total * 16);
-  p->supgx = (uint32_t)cdiv(p->max_rows, kSupRows);
+  p->supgx = (uint32_t)cdiv(p->max_rows, kSupTile);
   while ((1u << p->sup_np) < p->Nc) ++p->sup_np;
   p->sup_rgx = (uint32_t)std::max<uint64_t>(1, cdiv(p->max_rowblock, kCtaThreads >> p->sup_np));
   p->dored.alloc((size_t)std::max<uint64_t>(p->dored.bytes / sizeof(double), (uint64_t)p->sup_rgx * p->Mr) *

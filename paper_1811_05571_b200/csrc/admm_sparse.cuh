@@ -29,10 +29,10 @@
 
 #include "admm_hemv.cuh"
 #include "admm_kernels.cuh"
+#include <type_traits>
 
 namespace admm {
 
-constexpr int kSupRows = 128;  // rows per support_a_kernel CTA (one thread per row)
 constexpr int kSupUnroll = 8;  // support columns in flight per thread
 
 // Column-major copy of a block: Hc[x * ldc + r] = H[r * ld + x] (setup only).
@@ -94,47 +94,86 @@ support_compact_kernel(const double2* __restrict__ v, const BlockDesc* __restric
   }
 }
 
-// a'_b = H_b v' over the support of segment j (ascending columns): one thread per row of
-// a kSupRows tile, kSupUnroll columns in flight.  Grid (row tiles, local blocks).
+// a'_b = H_b v' over the support of segment j (ascending columns).  Grid (row tiles of
+// kSupTile rows, local blocks, kSupChunks column chunks): thread t owns kSupRPT consecutive
+// rows (one 32/64-byte load per support column), kSupUnroll columns in flight, so a CTA
+// keeps ~kSupUnroll x 8 KiB of the column-major H in flight.  Column chunk c of the
+// support list writes its partial; support_rows_kernel adds the kSupChunks partials of a
+// row in chunk order (fixed order: bit-reproducible).
+constexpr int kSupThreads = 256;
+constexpr int kSupRPT = 4;                          // rows per thread
+constexpr int kSupTile = kSupThreads * kSupRPT;     // rows per CTA
+constexpr int kSupChunks = 16;                      // column chunks of the support list
 template <typename S>
-__global__ void __launch_bounds__(kSupRows)
+__global__ void __launch_bounds__(kSupThreads)
 support_a_kernel(const S* __restrict__ Hc, const uint64_t* __restrict__ coff, const uint32_t* __restrict__ ldc,
                  const BlockDesc* __restrict__ blocks, const double2* __restrict__ v, const uint32_t* __restrict__ list,
-                 uint32_t list_stride, const uint32_t* __restrict__ nnz, double2* __restrict__ anew) {
-  const uint32_t b = blockIdx.y;
+                 uint32_t list_stride, const uint32_t* __restrict__ nnz, double2* __restrict__ apart,
+                 uint64_t chunk_stride) {
+  const uint32_t b = blockIdx.y, chunk = blockIdx.z;
   const BlockDesc bd = blocks[b];
-  const uint32_t row = blockIdx.x * kSupRows + threadIdx.x;
-  if (blockIdx.x * kSupRows >= bd.rows) return;
+  const uint32_t row0 = blockIdx.x * kSupTile + threadIdx.x * kSupRPT;
+  if (blockIdx.x * kSupTile >= bd.rows) return;
   const uint32_t n = nnz[bd.jl];
+  const uint32_t k0 = (uint32_t)((uint64_t)n * chunk / kSupChunks), k1 = (uint32_t)((uint64_t)n * (chunk + 1) / kSupChunks);
   const uint32_t* lj = list + (uint64_t)bd.jl * list_stride;
-  const S* hb = Hc + coff[b];
+  const S* hb = Hc + coff[b] + row0;
   const uint32_t L = ldc[b];
   const double2* vj = v + bd.seg_off;
-  const bool ok = row < bd.rows;
-  double2 acc = make_double2(0.0, 0.0);
-  uint32_t k = 0;
-  for (; k + kSupUnroll <= n; k += kSupUnroll) {
+  const bool ok = row0 < bd.rows;  // ldc is a multiple of 8 >= rows: a thread's rows are all in the padded column
+  double2 acc[kSupRPT];
+#pragma unroll
+  for (int e = 0; e < kSupRPT; ++e) acc[e] = make_double2(0.0, 0.0);
+  using Vec = typename std::conditional<sizeof(S) == 8, uint4, V256>::type;  // kSupRPT elements of S
+  uint32_t k = k0;
+  for (; k + kSupUnroll <= k1; k += kSupUnroll) {
     uint32_t xs[kSupUnroll];
 #pragma unroll
     for (int u = 0; u < kSupUnroll; ++u) xs[u] = __ldg(lj + k + u);
-    S hv[kSupUnroll];
+    S h[kSupUnroll][kSupRPT];
 #pragma unroll
     for (int u = 0; u < kSupUnroll; ++u) {
       if (ok) {
-        hv[u] = __ldcs(hb + (uint64_t)xs[u] * L + row);
+        const S* p = hb + (uint64_t)xs[u] * L;
+        if constexpr (sizeof(S) == 8) {
+          const uint4 w = __ldcs(reinterpret_cast<const uint4*>(p));
+          const uint4 w2 = __ldcs(reinterpret_cast<const uint4*>(p) + 1);
+          h[u][0] = make_float2(__uint_as_float(w.x), __uint_as_float(w.y));
+          h[u][1] = make_float2(__uint_as_float(w.z), __uint_as_float(w.w));
+          h[u][2] = make_float2(__uint_as_float(w2.x), __uint_as_float(w2.y));
+          h[u][3] = make_float2(__uint_as_float(w2.z), __uint_as_float(w2.w));
+        } else {
+          const V256 w = ld_stream256<kEvictFirst>(p);
+          const V256 w2 = ld_stream256<kEvictFirst>(p + 2);
+          h[u][0] = Store<double2>::get(w, 0);
+          h[u][1] = Store<double2>::get(w, 1);
+          h[u][2] = Store<double2>::get(w2, 0);
+          h[u][3] = Store<double2>::get(w2, 1);
+        }
       } else {
-        hv[u].x = 0;
-        hv[u].y = 0;
+#pragma unroll
+        for (int e = 0; e < kSupRPT; ++e) h[u][e] = S{};
       }
     }
 #pragma unroll
-    for (int u = 0; u < kSupUnroll; ++u) cmac(acc, Store<S>::widen(hv[u]), __ldg(vj + xs[u]));
+    for (int u = 0; u < kSupUnroll; ++u) {
+      const double2 vx = __ldg(vj + xs[u]);
+#pragma unroll
+      for (int e = 0; e < kSupRPT; ++e) cmac(acc[e], Store<S>::widen(h[u][e]), vx);
+    }
   }
-  for (; k < n; ++k) {
+  for (; k < k1; ++k) {
     const uint32_t x = __ldg(lj + k);
-    if (ok) cmac(acc, Store<S>::widen(hb[(uint64_t)x * L + row]), __ldg(vj + x));
+    const double2 vx = __ldg(vj + x);
+    if (ok)
+#pragma unroll
+      for (int e = 0; e < kSupRPT; ++e) cmac(acc[e], Store<S>::widen(hb[(uint64_t)x * L + e]), vx);
   }
-  if (ok) anew[bd.mvec_off + row] = acc;
+  (void)sizeof(Vec);
+  double2* dst = apart + chunk * chunk_stride + bd.mvec_off;
+#pragma unroll
+  for (int e = 0; e < kSupRPT; ++e)
+    if (row0 + e < bd.rows) dst[row0 + e] = acc[e];
 }
 
 // Per row r of row block i (NP = 2^np_log2 lanes per row, lane j = column block): for every
@@ -142,8 +181,8 @@ support_a_kernel(const S* __restrict__ Hc, const uint64_t* __restrict__ coff, co
 // then |sum_j a'_ij - g_i|^2 (ascending j) into per-CTA objective partials.
 __global__ void __launch_bounds__(kCtaThreads)
 support_rows_kernel(RowVecs rv, const BlockDesc* __restrict__ blocks, const BlockDesc* __restrict__ gblocks,
-                    uint32_t N, uint32_t np_log2, const double2* __restrict__ anew, double2* __restrict__ aold,
-                    const double2* __restrict__ gq, int first, double* __restrict__ ored) {
+                    uint32_t N, uint32_t np_log2, const double2* __restrict__ apart, uint64_t chunk_stride,
+                    double2* __restrict__ aold, const double2* __restrict__ gq, int first, double* __restrict__ ored) {
   __shared__ double2 sa[kCtaThreads];
   __shared__ double sm[kCtaWarps];
   const uint32_t i = blockIdx.y;
@@ -157,7 +196,9 @@ support_rows_kernel(RowVecs rv, const BlockDesc* __restrict__ blocks, const Bloc
     const uint64_t o = (uint64_t)bd.mvec_off + row;
     double2 w = make_double2(0.0, 0.0);
     if (!first) {
-      a = anew[o];
+      a = apart[o];  // a'_b = the column chunks' partials, in chunk order
+#pragma unroll 4
+      for (int c = 1; c < kSupChunks; ++c) a = cadd(a, apart[(uint64_t)c * chunk_stride + o]);
       w = csub(csub(cscale(a, 2.0), aold[o]), gq[o]);
       aold[o] = a;
     }

@@ -7,6 +7,8 @@ import pytest
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BIN = os.path.join(REPO, "tests", "cpp", "test_shim")
+DROPIN = os.path.join(REPO, "tests", "cpp", "test_dropin")
+REF_INC = "/root/reference/proj/include"
 
 
 def build():
@@ -15,6 +17,32 @@ def build():
            "-o", BIN, f"-L{REPO}/paper_1811_05571_b200", "-ladmm_b200", f"-L{REPO}/oracle", "-loracle",
            f"-Wl,-rpath,{REPO}/paper_1811_05571_b200", f"-Wl,-rpath,{REPO}/oracle"]
     subprocess.run(cmd, check=True, capture_output=True)
+
+
+def build_dropin():
+    """The drop-in header against the reference's own headers (build container only; the
+    binary travels to the GPU box)."""
+    cmd = ["g++", "-std=c++20", "-O2", "-ffp-contract=off", f"-I{REPO}/include", f"-I{REF_INC}",
+           os.path.join(REPO, "tests", "cpp", "test_dropin.cpp"), "-o", DROPIN, "-pthread",
+           f"-L{REPO}/paper_1811_05571_b200", "-ladmm_b200", f"-Wl,-rpath,{REPO}/paper_1811_05571_b200"]
+    subprocess.run(cmd, check=True, capture_output=True)
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_INC), reason="reference headers only in the build container")
+def test_dropin_header_compiles_against_the_reference():
+    build_dropin()
+    assert os.path.exists(DROPIN)
+
+
+@pytest.mark.gpu
+def test_dropin_matches_the_reference_in_process():
+    if os.path.isdir(REF_INC):
+        build_dropin()
+    if not os.path.exists(DROPIN):
+        pytest.skip("tests/cpp/test_dropin not built (needs the reference headers)")
+    r = subprocess.run([DROPIN], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0 and "0 failures" in r.stdout, r.stdout + r.stderr
 
 
 def test_cpp_shim_compiles():

@@ -49,13 +49,14 @@ def trace_of(r):
     return np.stack([r.trace.primal, r.trace.dual, r.trace.objective], 1)
 
 
-def trace_err(a, b):
+def trace_err(a, b, floor=None):
     """Max relative error over the entries the reference keeps finite; the diverging runs
     overflow |v|^2 (and with it the residual norms and the objective) to inf at the same
-    iterations on both sides."""
+    iterations on both sides.  `floor`: per-entry absolute rounding floor added to |b|."""
     fin = np.isfinite(b)
     assert np.array_equal(np.isfinite(a), fin)
-    return float(np.max(np.abs(a[fin] - b[fin]) / np.abs(b[fin]))) if fin.any() else 0.0
+    den = np.abs(b) if floor is None else np.abs(b) + floor
+    return float(np.max(np.abs(a[fin] - b[fin]) / den[fin])) if fin.any() else 0.0
 
 
 def plan_solve(admm, p, lam, method, M, N, iters, **opts):
@@ -82,8 +83,11 @@ def test_config2_all_300_iterations(cfg2_problem, schedule):
     tr, rt = trace_of(r), ref["trace"]
     assert trace_err(tr[:, 1], rt[:, 1]) <= 1e-8  # dual residual
     # the primal residual is ||u - v||, a difference of ~1e150-sized vectors on this diverging
-    # run: the reference's own value moves by % under 1e-15 perturbations
-    assert trace_err(tr[:, 0], rt[:, 0]) <= 1e-2
+    # run (the reference's own value moves by % under 1e-15 perturbations and is exactly 0
+    # where u == v to the last bit): relative to the rounding floor of the
+    # vectors it is a difference of, ~1e-12 ||v|| ~ 1e-12 r_d / rho
+    floor = 1e-12 * np.where(np.isfinite(rt[:, 1]), rt[:, 1], 0.0)
+    assert trace_err(tr[:, 0], rt[:, 0], floor) <= 1e-2
     assert trace_err(tr[:, 2], rt[:, 2]) <= 1e-8  # objective trace, every iteration
 
 
