@@ -28,7 +28,6 @@
 #include "admm_kernels.cuh"
 #include "admm_setup.cuh"
 #include "admm_sweep.cuh"
-#include "admm_tile.cuh"
 #include "admm_slab.cuh"
 #include "admm_hemv.cuh"
 #include "admm_batched.cuh"
@@ -178,11 +177,6 @@ struct admm_plan {
   // sweep schedule (admm_sweep.cuh)
   int schedule = 1;             // 1 two-pass, 2 single-HBM-pass sweep
   int sweep_lpr = 8;
-  bool sweep_bulk = false;  // TMA producer variant (sweep_bulk_kernel)
-  int tile_rb = 0;          // > 0: strip-major SMEM-resident sweep (sweep_tile_kernel), row bytes
-  uint32_t tile_ns = 0;     // its SMEM ring slots (32-row tasks)
-  int tile_cps = 1;         // its CTAs per SM
-  DevBuf dHt;               // strip-major copy of H for sweep_tile_kernel
   int slab_rpl = 0;         // > 0: per-warp slab sweep (sweep_slab_kernel), rows per lane
   uint32_t slab_C = 1, slab_nw = 0, slab_ns = 0, slab_Ns = 0, slab_lag = 1, slab_nd = 1, slab_rb = 64;  // cluster size, compute warps, stages, slabs, (A) lag
   std::vector<SlabDesc> slabs;
@@ -190,15 +184,12 @@ struct admm_plan {
   bool kpacked = false;     // K applied from the packed Hermitian tiles (hemv_kernel)
   bool h_evict_first = false;  // two-pass GEMVs stream H with L2 evict_first
   bool kkeep = false;       // ... with an L2 evict_last policy (ADMM_B200_KKEEP)
-  int hemv_occ = 1;         // hemv_kernel CTAs per SM (1: register prefetch of the next tile)
-  bool hemv_fuse = false;   // q / ghat finalized inside hemv_kernel (tile-row completion counters)
   int hemv_bulk = 0;        // hemv_bulk_kernel CTAs per SM (0: register variant hemv_kernel)
   DevBuf dkcnt;
   std::vector<HemvDesc> hv;
   DevBuf dKp, dhv, dkppart;
   Geom gP;
-  DevBuf dtrace_tile;       // ADMM_B200_TILE_TRACE: per-strip phase timestamps
-  DevBuf dtmaps;            // one CUtensorMap per local block
+  DevBuf dtrace_tile;       // ADMM_B200_SLAB_TRACE: per-strip phase timestamps
   std::vector<SweepDesc> segs;
   DevBuf dsegs, dwpart_s;
   Geom gS;
@@ -252,13 +243,7 @@ uint64_t grid_for(K kernel, uint64_t U, int sms, size_t smem = 0) {
 // while its predecessor runs; it must call pdl_enter() before touching the
 // predecessor's output (sweep_kernel, rows_finalize_sweep_kernel, hemv_kernel,
 // hemv_finalize_kernel do).  ADMM_B200_PDL=0 launches plainly.
-bool pdl_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("ADMM_B200_PDL");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
+bool pdl_enabled() { return true; }
 template <typename... KArgs, typename... Args>
 void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
   cudaLaunchConfig_t cfg = {};
@@ -375,72 +360,13 @@ size_t sweep_smem_bytes(const admm_plan* p) {
   return ((size_t)p->n_meas + (2 * (size_t)kProdWarps + 4) * p->Mr * W) * sizeof(double2);
 }
 
-// Try to configure the single-HBM-pass sweep with LPR lanes per row.  Returns false
-// when the segment rows do not fit the SMEM accumulator or the resident strips would
-// not fit in L2 (then the two-pass schedule is used).
-// CUtensorMap per local block for the TMA sweep producer: H_b as a rows x (2*ld) real
-// matrix, box = {row_bytes / sizeof(real), rows_per_stage}.
-template <typename S>
-bool build_tensor_maps(admm_plan* p, int row_bytes, int rows_per_stage) {
-  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-  if (!encode) {
-    cudaDriverEntryPointQueryResult q;
-    void* fn = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess || !fn)
-      return false;
-    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-  }
-  constexpr size_t real = sizeof(S) / 2;
-  std::vector<CUtensorMap> maps(p->blocks.size());
-  for (size_t b = 0; b < p->blocks.size(); ++b) {
-    const MatDesc& md = p->hN[b];
-    const cuuint64_t dims[2] = {(cuuint64_t)md.ld * 2, (cuuint64_t)md.rows};
-    const cuuint64_t strides[1] = {(cuuint64_t)md.ld * sizeof(S)};
-    const cuuint32_t box[2] = {(cuuint32_t)(row_bytes / real), (cuuint32_t)rows_per_stage};
-    const cuuint32_t estr[2] = {1, 1};
-    void* base = p->dH.as<S>() + md.a_off;
-    const CUresult r = encode(&maps[b], real == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
-                              base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return false;
-  }
-  upload_desc(p->dtmaps, maps.data(), maps.size() * sizeof(CUtensorMap));
-  return true;
-}
-
-template <typename S, int LPR>
-size_t sweep_bulk_smem_bytes(const admm_plan* p) {
-  constexpr int W = LPR * Store<S>::kPerVec;
-  constexpr int R = (kWarp / LPR) * kBulkCompute * kBulkRI;
-  return (size_t)kBulkStages * R * W * sizeof(S) + 2 * kBulkStages * sizeof(uint64_t) +
-         ((size_t)p->n_meas + (2 * (size_t)kBulkCompute + 4) * p->Mr * W) * sizeof(double2);
-}
-
+// The L2-re-read sweep with LPR lanes per row (the fallback single-pass kernel when the slab
+// geometry does not fit).  False when the segment rows do not fit the SMEM accumulator or
+// the open strips would not fit in L2 (then the two-pass schedule is used).
 template <typename S, int LPR>
 bool try_sweep(admm_plan* p, size_t l2_budget) {
   constexpr int W = LPR * Store<S>::kPerVec;
-  size_t smem = sweep_smem_bytes<S, LPR>(p);
-  if constexpr (LPR >= 4) {
-    // TMA producer only on request: measured 206 us vs 126 us for the LDG producer on
-    // config 2 (it runs ahead of the L2 re-read and loses the reuse; profiles/r01_summary.md)
-    const char* env = std::getenv("ADMM_B200_SWEEP");
-    p->sweep_bulk = env && !std::strcmp(env, "tma");
-    if (p->sweep_bulk) {
-      smem = sweep_bulk_smem_bytes<S, LPR>(p);
-      if (smem > 225 * 1024) p->sweep_bulk = false, smem = sweep_smem_bytes<S, LPR>(p);
-    }
-    if (p->sweep_bulk && !build_tensor_maps<S>(p, LPR * Store<S>::kPerVec * (int)sizeof(S),
-                                                  (kWarp / LPR) * kBulkCompute * kBulkRI)) {
-      p->sweep_bulk = false;
-      smem = sweep_smem_bytes<S, LPR>(p);
-    }
-    if (p->sweep_bulk)
-      CK(cudaFuncSetAttribute(sweep_bulk_kernel<S, LPR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  } else {
-    p->sweep_bulk = false;
-  }
+  const size_t smem = sweep_smem_bytes<S, LPR>(p);
   if (smem > 225 * 1024) return false;
   for (auto fn : {sweep_kernel<S, LPR, false>, sweep_kernel<S, LPR, true>})
     CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::min<size_t>(smem, 225 * 1024)));
@@ -470,75 +396,8 @@ bool try_sweep(admm_plan* p, size_t l2_budget) {
   p->sweep_lpr = LPR;
   p->sweep_smem = smem;
   p->keep_l2 = (p->h_elems + p->k_elems) * sizeof(S) <= (96ull << 20);
-  if (const char* env = std::getenv("ADMM_B200_KEEP_L2")) p->keep_l2 = env[0] == '1';
   p->dwpart_s.alloc(po * sizeof(double2));
   upload_desc(p->dsegs, segs.data(), segs.size() * sizeof(SweepDesc));
-  return true;
-}
-
-// Strip-major SMEM-resident sweep with RB bytes per strip row: possible when a whole
-// strip (n_meas x RB) plus two chunks of slack fits the SMEM ring next to q, w and the
-// per-strip scratch.  No L2 budget: each strip crosses L2 once.
-template <typename S, int RB>
-bool try_tile(admm_plan* p) {
-  using G = TileGeom<S, RB>;
-  constexpr int W = G::W;
-  if (p->Pr != 1) return false;  // the replica mean needs every row block of a strip
-  // opt-in while it trails the LDG sweep (profiles/r01_summary.md)
-  const char* env = std::getenv("ADMM_B200_SWEEP");
-  if (!env || std::strcmp(env, "tile") != 0) return false;
-  if (const char* rb = std::getenv("ADMM_B200_TILE_RB"))      // diagnostics: force the row width
-    if (std::atoi(rb) != RB) return false;
-  int cps = 1;  // CTAs per SM
-  if (const char* e = std::getenv("ADMM_B200_TILE_CTAS")) cps = std::max(1, std::atoi(e));
-  // dynamic SMEM per CTA: 228 KB per SM less 1 KB per CTA and the static part
-  const size_t cap = (228 * 1024) / cps - 2 * 1024;
-  const size_t fixed = tile_smem_bytes(0, G::TB, (uint32_t)p->n_meas, (uint32_t)p->Mr, (uint32_t)p->Nc, W);
-  if (fixed >= cap) return false;
-  const uint32_t ns = (uint32_t)std::min<size_t>((cap - fixed) / (G::TB + 2 * sizeof(uint64_t)), 256);
-  const uint32_t ntask = (uint32_t)cdiv(p->n_meas, kTileRows);
-  if (ns < 2 * ntask + 2) return false;  // (C) runs a strip ahead of (A)
-  const size_t smem = tile_smem_bytes(ns, G::TB, (uint32_t)p->n_meas, (uint32_t)p->Mr, (uint32_t)p->Nc, W);
-  auto k0 = cps == 2 ? sweep_tile_kernel<S, RB, false, 2> : sweep_tile_kernel<S, RB, false, 1>;
-  auto k1 = cps == 2 ? sweep_tile_kernel<S, RB, true, 2> : sweep_tile_kernel<S, RB, true, 1>;
-  for (auto fn : {k0, k1}) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int occ = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k0, kTileThreads, smem));
-  if (occ < cps) return false;
-  std::vector<SweepDesc> segs(p->Nc);
-  uint64_t u = 0;
-  for (uint64_t j = 0; j < p->Nc; ++j) {
-    const uint32_t cols = p->blocks[j].cols;
-    segs[j] = SweepDesc{u, 0, (uint32_t)cdiv(cols, W), cols};
-    u += segs[j].n_strips;
-  }
-  const uint64_t P = std::min<uint64_t>(u, (uint64_t)p->num_sms * cps);
-  uint64_t po = 0;
-  for (auto& sd : segs) {  // one partial slot per CTA overlapping the segment
-    sd.part_off = po;
-    po += (uint64_t)seg_count(sd.unit0, sd.n_strips, u, P) * p->n_meas;
-  }
-  p->segs = segs;
-  p->gS.U = u;
-  p->gS.P = P;
-  p->tile_rb = RB;
-  p->tile_ns = ns;
-  p->tile_cps = cps;
-  p->sweep_smem = smem;
-  p->sweep_bulk = false;
-  p->keep_l2 = (u * p->n_meas * W + p->k_elems) * sizeof(S) <= (96ull << 20);
-  if (const char* e2 = std::getenv("ADMM_B200_KEEP_L2")) p->keep_l2 = e2[0] == '1';
-  p->dwpart_s.alloc(po * sizeof(double2));
-  upload_desc(p->dsegs, segs.data(), segs.size() * sizeof(SweepDesc));
-  p->dHt.alloc(u * p->n_meas * W * sizeof(S));
-  if (std::getenv("ADMM_B200_TILE_TRACE")) {
-    p->dtrace_tile.alloc(P * 64 * 8 * sizeof(unsigned long long));
-    CK(cudaMemset(p->dtrace_tile.p, 0, P * 64 * 8 * sizeof(unsigned long long)));
-    if (std::getenv("ADMM_B200_TILE_NOLOAD")) {  // trace[7] = 1: consumer-only timing
-      const unsigned long long one = 1;
-      CK(cudaMemcpy(p->dtrace_tile.as<unsigned long long>() + 7, &one, sizeof(one), cudaMemcpyHostToDevice));
-    }
-  }
   return true;
 }
 
@@ -564,8 +423,6 @@ SlabFn<S> slab_fn(int rpl, uint32_t rb, bool tr) {
 template <typename S>
 bool try_slab(admm_plan* p) {
   if (p->Pr != 1) return false;  // the replica mean needs every row block of a strip
-  if (const char* env = std::getenv("ADMM_B200_SWEEP"))
-    if (std::strcmp(env, "slab") != 0) return false;  // another sweep variant requested
   const uint32_t M = (uint32_t)p->Mr, N = (uint32_t)p->Nc;
   int fC = 0, fR = 0, fB = 0;
   if (const char* e = std::getenv("ADMM_B200_SLAB_C")) fC = std::atoi(e);
@@ -689,7 +546,6 @@ bool try_slab(admm_plan* p) {
   p->slab_lag = lag;
   p->slab_nd = nd;
   p->sweep_smem = smem;
-  p->sweep_bulk = false;
   p->dwpart_s.alloc(po * sizeof(double2));
   upload_desc(p->dsegs, segs.data(), segs.size() * sizeof(SweepDesc));
   upload_desc(p->dslabs, slabs.data(), slabs.size() * sizeof(SlabDesc));
@@ -722,7 +578,6 @@ bool try_resident(admm_plan* p, int requested) {
   // shorten phase B (the owners sum one w partial per CTA) and the grid barriers:
   // at least kResMinCols columns per CTA.
   uint64_t min_cols = 32;
-  if (const char* e = std::getenv("ADMM_B200_RES_COLS")) min_cols = std::max(1, std::atoi(e));
   const uint64_t Pmax = std::max<uint64_t>(std::min<uint64_t>(p->num_sms, cdiv(p->n_pix, min_cols)),
                                            p->blocks.size()),
                  ncol = p->n_pix;
@@ -876,7 +731,7 @@ void choose_schedule(admm_plan* p, int requested) {
     return;
   }
   if (requested == 4) throw Fail{ADMM_E_PARAMETER, "resident schedule not possible for this shape"};
-  if (try_slab<S>(p) || try_tile<S, 128>(p) || try_tile<S, 64>(p)) {
+  if (try_slab<S>(p)) {
     p->schedule = 2;
     return;
   }
@@ -887,35 +742,6 @@ void choose_schedule(admm_plan* p, int requested) {
     return;
   }
   if (requested == 2) throw Fail{ADMM_E_PARAMETER, "sweep schedule not possible for this shape"};
-}
-
-// Persisting-L2 window over the packed K (read once per iteration, 71 MB on config 2):
-// with the H stream marked evict_first, an access-policy window keeps K resident across
-// iterations.  Applied to the plan's stream (captured graphs inherit it).
-void pin_k_l2(admm_plan* p, cudaStream_t s) {
-  if (!p->kkeep || !p->dKp.p) return;
-  // opt-in (ADMM_B200_KPERSIST=1): measured no faster than the evict_last hint alone on
-  // config 2 (K apply 15.6 vs 16.1 us), and the set-aside is device-wide
-  const char* e = std::getenv("ADMM_B200_KPERSIST");
-  if (!e || e[0] != '1') return;
-  int max_persist = 0, max_win = 0;
-  CK(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, p->device));
-  CK(cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, p->device));
-  if (max_persist <= 0 || max_win <= 0) return;
-  const size_t kbytes = p->dKp.bytes;
-  const size_t win = std::min<size_t>(kbytes, (size_t)max_win);
-  const size_t setaside = std::min<size_t>(win, (size_t)max_persist);
-  CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, setaside));
-  cudaStreamAttrValue a = {};
-  a.accessPolicyWindow.base_ptr = p->dKp.p;
-  a.accessPolicyWindow.num_bytes = win;
-  a.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)setaside / (double)win);
-  a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-  a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-  CK(cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &a));
-  if (std::getenv("ADMM_B200_DEBUG"))
-    std::fprintf(stderr, "K persisting window: %zu of %zu bytes, set-aside %zu (max %d)\n", win, kbytes, setaside,
-                 max_persist);
 }
 
 void upload_desc(DevBuf& d, const void* src, size_t bytes) {
@@ -978,19 +804,6 @@ void upload_h(admm_plan* p, const void* h, admm_dtype h_dtype) {
   CK(cudaMemcpyAsync(&hf, flag.p, 4, cudaMemcpyDeviceToHost, p->stream));
   CK(cudaStreamSynchronize(p->stream));
   if (hf) throw Fail{ADMM_E_NUMERICAL, "SensingProblem: non-finite entries"};
-}
-
-// Strip-major copy of the (scaled) H for sweep_tile_kernel.
-template <typename S>
-void build_tile(admm_plan* p) {
-  const uint32_t W = (uint32_t)(p->tile_rb / sizeof(S));
-  const uint64_t total = p->gS.U * p->n_meas * W;
-  tile_h_kernel<S><<<p->num_sms * 8, 256, 0, p->stream>>>(p->dH.as<S>(), p->dhN.as<MatDesc>(),
-                                                          p->dblocks.as<BlockDesc>(), p->dsegs.as<SweepDesc>(),
-                                                          (uint32_t)p->Mr, (uint32_t)p->Nc, (uint32_t)p->n_meas, W,
-                                                          total, p->dHt.as<S>());
-  CK(cudaGetLastError());
-  CK(cudaStreamSynchronize(p->stream));
 }
 
 // Slab-major copy of the (scaled) H for sweep_slab_kernel.
@@ -1084,22 +897,15 @@ void factor_blocks(admm_plan* p) {
                                                              p->hv[b].nT, p->dKp.as<S>() + p->hv[b].k_off);
     upload_desc(p->dhv, p->hv.data(), nb * sizeof(HemvDesc));
     const uint64_t u0 = p->gP.U;
-    if (const char* e = std::getenv("ADMM_B200_HEMV_FUSE")) p->hemv_fuse = e[0] == '1' && p->schedule != 5;
-    if (const char* e = std::getenv("ADMM_B200_HEMV_OCC")) p->hemv_occ = std::atoi(e) == 2 ? 2 : 1;
-    p->gP.P = p->hemv_occ == 2 ? grid_for<S>(hemv_kernel<S, 2, false>, u0, p->num_sms)
-                               : grid_for<S>(hemv_kernel<S, 1, false>, u0, p->num_sms);
-    // bulk-copy ring variant unless the register variants are requested (same P: one CTA per SM)
-    const char* hv = std::getenv("ADMM_B200_HEMV");
-    // default for complex64 K (streamed from HBM: configs 3/4, 35 -> 2x us); complex128 K
-    // on config 2 is L2-resident and the register variant is faster there (15.0 vs 18.4 us)
-    const bool want = hv ? !std::strcmp(hv, "bulk") : sizeof(S) == 8;
-    const int bocc = std::getenv("ADMM_B200_HEMV_BOCC") ? std::atoi(std::getenv("ADMM_B200_HEMV_BOCC")) : 1;
-    const size_t bsm = bocc == 2 ? hemv_bulk_smem<S, 2>(p->max_rows) : hemv_bulk_smem<S, 1>(p->max_rows);
-    p->hemv_bulk = want && !p->hemv_fuse && p->hemv_occ == 1 && bsm * bocc <= 227 * 1024 ? bocc : 0;
+    p->gP.P = grid_for<S>(hemv_kernel<S, 1, false>, u0, p->num_sms);
+    // complex64 K (streamed from HBM: configs 3/4): the bulk-copy ring variant, one CTA per
+    // SM (35 -> 25 us on config 3); complex128 K (config 2, L2-resident between iterations):
+    // the register variant (15.0 vs 18.4 us)
+    const size_t bsm = hemv_bulk_smem<S, 1>(p->max_rows);
+    p->hemv_bulk = sizeof(S) == 8 && bsm <= 227 * 1024 ? 1 : 0;
     if (p->hemv_bulk) {
-      CK(cudaFuncSetAttribute(p->hemv_bulk == 2 ? hemv_bulk_kernel<S, 2> : hemv_bulk_kernel<S, 1>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
-      p->gP.P = std::max<uint64_t>(1, std::min<uint64_t>(u0, (uint64_t)p->num_sms * p->hemv_bulk));
+      CK(cudaFuncSetAttribute(hemv_bulk_kernel<S, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
+      p->gP.P = std::max<uint64_t>(1, std::min<uint64_t>(u0, (uint64_t)p->num_sms));
     }
   }
   CK(cudaGetLastError());
@@ -1143,8 +949,8 @@ void enqueue_kapply(admm_plan* p, cudaStream_t s, Mid mid) {
   const int nb = (int)p->blocks.size();
   if (p->kpacked) {
     if (p->hemv_bulk) {
-      auto fb = p->hemv_bulk == 2 ? hemv_bulk_kernel<S, 2> : hemv_bulk_kernel<S, 1>;
-      const size_t sm = p->hemv_bulk == 2 ? hemv_bulk_smem<S, 2>(p->max_rows) : hemv_bulk_smem<S, 1>(p->max_rows);
+      auto fb = hemv_bulk_kernel<S, 1>;
+      const size_t sm = hemv_bulk_smem<S, 1>(p->max_rows);
       launch_pdl(fb, dim3((unsigned)p->gP.P), dim3(kCtaThreads), sm, s,
                  p->dKp.as<S>(), p->dr.as<double2>(), p->dkppart.as<double2>(), p->dhv.as<HemvDesc>(), nb, p->gP.U,
                  p->kkeep ? 1 : 0);
@@ -1154,13 +960,12 @@ void enqueue_kapply(admm_plan* p, cudaStream_t s, Mid mid) {
                  p->dparams.as<Params>());
       return;
     }
-    auto fn = p->hemv_fuse ? hemv_kernel<S, 1, true> : p->hemv_occ == 2 ? hemv_kernel<S, 2, false> : hemv_kernel<S, 1, false>;
+    auto fn = hemv_kernel<S, 1, false>;
     launch_pdl(fn, dim3((unsigned)p->gP.P), dim3(kCtaThreads), 0, s, p->dKp.as<S>(), p->dr.as<double2>(),
                p->dkppart.as<double2>(), p->dhv.as<HemvDesc>(), nb, p->gP.U, p->kkeep ? 1 : 0,
-               p->hemv_fuse ? p->dkcnt.as<unsigned>() : nullptr, row_vecs(p), p->dparams.as<Params>());
+               (unsigned*)nullptr, row_vecs(p), p->dparams.as<Params>());
     mid();
-    if (!p->hemv_fuse)
-      launch_pdl(hemv_finalize_kernel, dim3((unsigned)cdiv(p->max_rows, kHFinRows), nb), dim3(kHFinRows), 0, s,
+    launch_pdl(hemv_finalize_kernel, dim3((unsigned)cdiv(p->max_rows, kHFinRows), nb), dim3(kHFinRows), 0, s,
                  row_vecs(p), p->dkppart.as<double2>(), p->dhv.as<HemvDesc>(), p->gP.U, p->gP.P,
                  p->dparams.as<Params>());
     return;
@@ -1182,13 +987,13 @@ template <typename S>
 void enqueue_gq(admm_plan* p, cudaStream_t s) {
   const int nb = (int)p->blocks.size();
   if (p->hemv_bulk) {
-    auto fb = p->hemv_bulk == 2 ? hemv_bulk_kernel<S, 2> : hemv_bulk_kernel<S, 1>;
-    const size_t sm = p->hemv_bulk == 2 ? hemv_bulk_smem<S, 2>(p->max_rows) : hemv_bulk_smem<S, 1>(p->max_rows);
+    auto fb = hemv_bulk_kernel<S, 1>;
+    const size_t sm = hemv_bulk_smem<S, 1>(p->max_rows);
     launch_pdl(fb, dim3((unsigned)p->gP.P), dim3(kCtaThreads), sm, s, (const S*)p->dGp.as<S>(),
                (const double2*)p->dq.as<double2>(), p->dkppart.as<double2>(), (const HemvDesc*)p->dhv.as<HemvDesc>(),
                nb, p->gP.U, 0);
   } else {
-    auto fn = p->hemv_occ == 2 ? hemv_kernel<S, 2, false> : hemv_kernel<S, 1, false>;
+    auto fn = hemv_kernel<S, 1, false>;
     launch_pdl(fn, dim3((unsigned)p->gP.P), dim3(kCtaThreads), 0, s, (const S*)p->dGp.as<S>(),
                (const double2*)p->dq.as<double2>(), p->dkppart.as<double2>(), (const HemvDesc*)p->dhv.as<HemvDesc>(),
                nb, p->gP.U, 0, (unsigned*)nullptr, row_vecs(p), (const Params*)p->dparams.as<Params>());
@@ -1348,31 +1153,11 @@ void enqueue_sweep_prologue(admm_plan* p, cudaStream_t s) {
 
 template <typename S, int LPR>
 void launch_sweep_lpr(admm_plan* p, cudaStream_t s) {
-  if constexpr (LPR >= 4) {
-    if (p->sweep_bulk) {
-      sweep_bulk_kernel<S, LPR><<<(unsigned)p->gS.P, kBulkThreads, p->sweep_smem, s>>>(
-          p->dH.as<S>(), p->dhN.as<MatDesc>(), p->dblocks.as<BlockDesc>(), p->dsegs.as<SweepDesc>(), (uint32_t)p->Mr,
-          (uint32_t)p->Nc, (uint32_t)p->n_meas, p->gS.U, p->dq.as<double2>(), col_vecs(p), p->dwpart_s.as<double2>(),
-          p->dparams.as<Params>(), p->dred.as<double>(), p->dstate.as<IterState>(), p->dtmaps.as<unsigned char>());
-      return;
-    }
-  }
   auto fn = p->keep_l2 ? sweep_kernel<S, LPR, true> : sweep_kernel<S, LPR, false>;
   launch_pdl(fn, dim3((unsigned)p->gS.P), dim3(kSweepThreads), p->sweep_smem, s, p->dH.as<S>(),
              p->dhN.as<MatDesc>(), p->dblocks.as<BlockDesc>(), p->dsegs.as<SweepDesc>(), (uint32_t)p->Mr,
              (uint32_t)p->Nc, (uint32_t)p->n_meas, p->gS.U, p->dq.as<double2>(), col_vecs(p),
              p->dwpart_s.as<double2>(), p->dparams.as<Params>(), p->dred.as<double>(), p->dstate.as<IterState>());
-}
-
-template <typename S, int RB>
-void launch_tile_rb(admm_plan* p, cudaStream_t s) {
-  auto fn = p->tile_cps == 2 ? (p->keep_l2 ? sweep_tile_kernel<S, RB, true, 2> : sweep_tile_kernel<S, RB, false, 2>)
-                             : (p->keep_l2 ? sweep_tile_kernel<S, RB, true, 1> : sweep_tile_kernel<S, RB, false, 1>);
-  fn<<<(unsigned)p->gS.P, kTileThreads, p->sweep_smem, s>>>(
-      p->dHt.as<S>(), p->dblocks.as<BlockDesc>(), p->dsegs.as<SweepDesc>(), (uint32_t)p->Mr, (uint32_t)p->Nc,
-      (uint32_t)p->n_meas, p->gS.U, p->tile_ns, p->dq.as<double2>(), col_vecs(p), p->dwpart_s.as<double2>(),
-      p->dparams.as<Params>(), p->dred.as<double>(), p->dstate.as<IterState>(),
-      p->dtrace_tile.p ? p->dtrace_tile.as<unsigned long long>() : nullptr);
 }
 
 template <typename S>
@@ -1404,11 +1189,7 @@ void launch_slab(admm_plan* p, cudaStream_t s) {
 template <typename S>
 void launch_sweep(admm_plan* p, cudaStream_t s) {
   if (p->slab_rpl) return launch_slab<S>(p, s);
-  if (p->tile_rb == 128)
-    launch_tile_rb<S, 128>(p, s);
-  else if (p->tile_rb == 64)
-    launch_tile_rb<S, 64>(p, s);
-  else if (p->sweep_lpr == 8)
+  if (p->sweep_lpr == 8)
     launch_sweep_lpr<S, 8>(p, s);
   else if (p->sweep_lpr == 4)
     launch_sweep_lpr<S, 4>(p, s);
@@ -1508,7 +1289,6 @@ void build_batched(admm_plan* p) {
   // (x2 -> 6.9 waves) instead of 2.6 / 3.5 waves
   int occ = 0;
   p->bsb = 64;
-  if (const char* e = std::getenv("ADMM_B200_BSB")) p->bsb = std::atoi(e) == 32 ? 32 : 64;
   if (p->dtype == ADMM_C128)
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, p->bsb == 32 ? bgemm_kernel<double2, false, 32> : bgemm_kernel<double2, false, 64>, 256,
                                                      p->bsb == 32 ? bgemm_smem<double2, false, 32>() : bgemm_smem<double2, false, 64>()));
@@ -1568,7 +1348,6 @@ void build_batched(admm_plan* p) {
   p->dz.alloc((size_t)p->splitH * p->vec_total * B * 16);
   p->dkappa.alloc(B * sizeof(double));
   uint64_t pzm = 5;  // bzupdate CTAs per SM (48 registers: 5 x 256 threads fit; 127 -> 113 us on config 5)
-  if (const char* e = std::getenv("ADMM_B200_BPZ")) pzm = std::max(1, std::atoi(e));
   p->pz = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(pzm * p->num_sms, cdiv(p->max_seg, 4)));
   p->dbred.alloc((size_t)3 * p->pz * kBB * sizeof(double));
   p->dblam.alloc(B * sizeof(double));
@@ -2020,17 +1799,13 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
   p->outbox_ptr = p->doutbox.as<double2>();
   p->fused_scal = p->Pr == 1 && p->Pc > 1 && p->schedule == 2;
   {  // packed Hermitian K for the per-iteration K apply (the batched schedule uses bgemm)
-    const char* e = std::getenv("ADMM_B200_KPACK");
-    p->kpacked = p->batch == 1 && !(e && e[0] == '0');
+    p->kpacked = p->batch == 1;
     // keep the packed K in L2 (evict_last) when the H stream cannot evict it: the slab
-    // sweep streams H with evict_first, so a K of <= ~96 MiB stays resident across
-    // iterations (config 2: K apply 19 -> 15 us)
-    const char* e2 = std::getenv("ADMM_B200_KKEEP");
-    p->kkeep = e2 ? e2[0] == '1' : (p->slab_rpl > 0 && p->k_elems * p->elem / 2 <= (96ull << 20));
-    // two-pass: H evict_first and the packed K evict_last when K fits next to the stream
-    const char* e3 = std::getenv("ADMM_B200_HFIRST");
-    p->h_evict_first = e3 ? e3[0] == '1' : (p->schedule == 1 && p->k_elems * p->elem / 2 <= (96ull << 20));
-    if (p->schedule == 1 && p->h_evict_first && !e2) p->kkeep = true;
+    // sweep and (two-pass) the GEMVs stream H with evict_first, so a K of <= ~96 MiB stays
+    // resident across iterations (config 2: K apply 19 -> 15 us)
+    const bool kfits = p->k_elems * p->elem / 2 <= (96ull << 20);
+    p->h_evict_first = p->schedule == 1 && kfits;
+    p->kkeep = (p->slab_rpl > 0 || p->schedule == 1) && kfits;
   }
   p->scal_ptr = p->fused_scal ? reinterpret_cast<double*>(p->ghat_ptr + p->Mr * p->Nc * p->mpad + p->aoff)
                               : p->dscal.as<double>();
@@ -2067,13 +1842,11 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
 
   if (p->dtype == ADMM_C128) {
     upload_h<double2>(p.get(), h, h_dtype);
-    if (p->tile_rb) build_tile<double2>(p.get());
     if (p->slab_rpl) build_slab<double2>(p.get());
     if (p->schedule == 5) build_support<double2>(p.get());
     factor_blocks<double2>(p.get());
   } else {
     upload_h<float2>(p.get(), h, h_dtype);
-    if (p->tile_rb) build_tile<float2>(p.get());
     if (p->slab_rpl) build_slab<float2>(p.get());
     if (p->schedule == 5) build_support<float2>(p.get());
     factor_blocks<float2>(p.get());
@@ -2085,7 +1858,6 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
   upload_g(p.get(), g);
   set_params(p.get());
   reset_state(p.get());
-  pin_k_l2(p.get(), p->stream);
   CK(cudaStreamSynchronize(p->stream));
   p->setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return p.release();
@@ -2140,27 +1912,6 @@ void admm_plan_destroy(admm_plan* plan) {
         std::fwrite(t.data(), sizeof(unsigned long long), n, f);
         std::fclose(f);
       }
-    } else if (plan->dtrace_tile.p) {  // diagnostics: mean phase durations of the last sweep launch
-      const size_t n = plan->gS.P * 64 * 8;
-      std::vector<unsigned long long> t(n);
-      cudaMemcpy(t.data(), plan->dtrace_tile.p, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
-      double acc[5] = {0, 0, 0, 0, 0};
-      uint64_t cnt = 0;
-      for (uint64_t c = 0; c < plan->gS.P; ++c)
-        for (int x = 1; x + 1 < 64; ++x) {
-          const unsigned long long* d = &t[(c * 64 + x - 1) * 8];
-          const unsigned long long* e = &t[(c * 64 + x) * 8];
-          if (!e[0] || !e[4] || !d[4]) continue;
-          acc[0] += (double)(e[1] - e[0]);  // (C)
-          acc[1] += (double)(e[0] - d[1]);  // (C) side: waiting for zred / loop
-          acc[2] += (double)(e[2] - d[4]);  // (A) side: waiting for (C)
-          acc[3] += (double)(e[3] - e[2]);  // (D)
-          acc[4] += (double)(e[4] - e[3]);  // stores + (A)
-          ++cnt;
-        }
-      if (cnt)
-        std::fprintf(stderr, "tile trace (SM cycles/strip over %llu strips): C %.0f  C-wait %.0f | A-wait %.0f  D %.0f  A %.0f\n",
-                     (unsigned long long)cnt, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt);
     }
     delete plan;
   }
@@ -2267,7 +2018,6 @@ admm_status admm_plan_set_stream(admm_plan* p, void* stream) {
     check_plan(p);
     if (is_dist(p)) throw Fail{ADMM_E_STATE, "set_stream: a distributed plan launches on its own streams"};
     p->stream = stream ? static_cast<cudaStream_t>(stream) : p->own_stream;
-    pin_k_l2(p, p->stream);
   });
 }
 
@@ -2323,25 +2073,20 @@ admm_status admm_plan_profile(admm_plan* p, uint64_t iters, const char** names, 
                                     "gemv_h(H,q)", "zupdate", "finalize"};
   static const char* kNamesSP[4] = {"sweep(H)", "rows_finalize(rhs)+finalize", "hemv(Kpacked,r)",
                                     "hemv_finalize(q)"};
-  static const char* kNamesSF[4] = {"sweep(H)", "rows_finalize(rhs)+finalize", "hemv(Kpacked,r)+finalize",
-                                    "(none)"};
-  static const char* kNames2F[7] = {"gemv_n(H,c)", "rows_finalize(rhs)", "hemv(Kpacked,r)+finalize", "(none)",
-                                    "gemv_h(H,q)", "zupdate", "finalize"};
   static const char* kNamesB[7] = {"bgemm(H,C)", "brows(rhs)", "bgemm(K,R)", "brows(q)", "bgemm_adj(H,Q)",
                                    "bzupdate", "bfinalize"};
   return run_guarded([&] {
     check_plan(p);
     if (is_dist(p)) throw Fail{ADMM_E_STATE, "profile: single-GPU plans only"};
     const int nk = (int)admm_plan_kernel_count(p);
-    const bool fused = p->kpacked && p->hemv_fuse;
     static const char* kNamesR[1] = {"resident(iteration)"};
     static const char* kNamesU[7] = {"gemv_h(H,q)", "hemv(G,q)+gq", "zupdate+support_list", "support_a(Hc,v)",
                                      "support_rows+finalize", "hemv(Kpacked,r)", "hemv_finalize(q)"};
     const char* const* kn = p->schedule == 5   ? kNamesU
                             : p->schedule == 4 ? kNamesR
-                            : p->schedule == 2 ? (fused ? kNamesSF : p->kpacked ? kNamesSP : kNamesS)
+                            : p->schedule == 2 ? (p->kpacked ? kNamesSP : kNamesS)
                             : p->schedule == 3 ? kNamesB
-                                               : (fused ? kNames2F : p->kpacked ? kNames2P : kNames2);
+                                               : (p->kpacked ? kNames2P : kNames2);
     std::vector<cudaEvent_t> ev(nk + 1);
     for (auto& e : ev) CK(cudaEventCreate(&e));
     std::vector<double> acc(nk, 0.0);
@@ -2390,12 +2135,11 @@ admm_status admm_plan_get_info(const admm_plan* p, admm_plan_info* info) {
     r.bytes_per_iter = 2 * hb + kb_dense + vb;  // two-pass algorithmic bytes
     // resident: ONE launch runs all the iterations of an enqueue (reported as 0 per iteration)
     r.launches_per_iter = p->schedule == 5 ? 10 : p->schedule == 4 ? 0 : p->schedule == 3 ? 7 : p->schedule == 2 ? (p->trace_obj ? (p->obj_pass ? 7 : 6) : 4) : (p->trace_obj ? 9 : 7);
-    if (p->schedule != 3 && p->kpacked && p->hemv_fuse) r.launches_per_iter -= 1;  // finalize inside hemv
     r.schedule = (uint64_t)p->schedule;
     r.grid_sweep = p->gS.P;
     // support schedule: one dense pass + K + G (+ the data-dependent support columns, admm_plan_read 5)
     r.hbm_bytes_per_iter = p->schedule == 5 ? hb + 2 * kb + vb : (p->schedule == 4 ? 0 : p->schedule == 2 ? hb : 2 * hb) + kb + vb;
-    r.sweep_variant = p->schedule != 2 ? 0 : p->slab_rpl ? 3 : p->tile_rb ? 2 : 1;
+    r.sweep_variant = p->schedule != 2 ? 0 : p->slab_rpl ? 3 : 1;
     r.slab_cluster = p->slab_rpl ? p->slab_C : 0;
     r.slab_row_bytes = p->slab_rpl ? p->slab_rb : 0;
     r.slab_rows = p->slab_rpl ? (uint64_t)p->slab_rpl * kWarp : 0;

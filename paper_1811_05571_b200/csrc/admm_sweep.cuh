@@ -265,20 +265,7 @@ sweep_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const Bloc
   if (threadIdx.x == 0) red[2 * P + p] = r;
 }
 
-// ---- bulk-copy producer variant -------------------------------------------------------
-// Loader warp: per stage (kBulkRI row-instructions x 8 compute warps of rows of one
-// (strip, block)), every lane issues cp.async.bulk of one 256/128-byte row segment into
-// a kBulkStages-deep SMEM ring; completion is counted by the stage's mbarrier
-// (complete_tx), so nothing occupies registers or scoreboards while in flight.  8 compute
-// warps reduce z from SMEM and release the stage; 7 consumer warps do (D) and (A) as in
-// sweep_kernel.
-constexpr int kBulkStages = 8;
-constexpr int kBulkRI = 2;            // row-instructions per compute warp per stage
-constexpr int kBulkCompute = 8;       // compute warps (warps 1..8)
-constexpr int kBulkCons = 7;          // consumer warps (warps 9..15)
-constexpr int kBulkHandoff = (kBulkCompute + kBulkCons) * kWarp;  // FULL/EMPTY participants
-constexpr int kBulkThreads = 512;                                  // loader + compute + consumer warps
-
+// ---- mbarrier / bulk-copy helpers (slab sweep, K apply) ---------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
@@ -301,259 +288,6 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
-}
-
-// 2-D TMA: one box (inner: the strip's row segment, outer: R rows) per stage.
-__device__ __forceinline__ void tma_2d(uint32_t dst, const void* tmap, int c0, int c1, uint64_t* bar, uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(
-          dst),
-      "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
-      : "memory");
-}
-
-// tmaps: one 128-byte CUtensorMap per local block (H_b viewed as rows x 2*ld reals),
-// box = {ROWB / sizeof(real), R}; rows past the block and columns past ld are zero-filled.
-template <typename S, int LPR>
-__global__ void __launch_bounds__(kBulkThreads, 1)
-sweep_bulk_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const BlockDesc* __restrict__ blocks,
-                  const SweepDesc* __restrict__ segs, uint32_t M, uint32_t N, uint32_t n_meas, uint64_t Utot,
-                  const double2* __restrict__ q, ColVecs cv, double2* __restrict__ wpart,
-                  const Params* __restrict__ prm, double* __restrict__ red, IterState* st,
-                  const unsigned char* __restrict__ tmaps) {
-  constexpr int PV = Store<S>::kPerVec;
-  constexpr int W = LPR * PV;
-  constexpr int RPI = kWarp / LPR;
-  constexpr int ROWB = W * (int)sizeof(S);            // bytes per row segment (256 or 128)
-  constexpr int R = RPI * kBulkCompute * kBulkRI;     // rows per stage
-  constexpr int STAGEB = R * ROWB;
-  constexpr int CSTEP = kBulkCons * RPI;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  unsigned char* ring = smem_raw;                                            // kBulkStages x STAGEB
-  uint64_t* fullb = reinterpret_cast<uint64_t*>(ring + (size_t)kBulkStages * STAGEB);
-  uint64_t* emptyb = fullb + kBulkStages;
-  double2* wacc = reinterpret_cast<double2*>(emptyb + kBulkStages);         // n_meas
-  double2* zbuf = wacc + n_meas;                                             // 2 x 8 x M x W
-  double2* us = zbuf + 2 * (size_t)kBulkCompute * M * W;
-  double2* cs = us + (size_t)M * W;
-  double2* pre = cs + (size_t)M * W;
-  __shared__ double sm_red[kBulkThreads / kWarp];
-
-  const uint64_t P = gridDim.x, p = blockIdx.x;
-  const uint64_t x0 = sk_lo(p, Utot, P);
-  const uint64_t xe = sk_lo(p + 1, Utot, P);
-  const int gwarp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
-  const int lr = lane / LPR, lc = lane % LPR;
-  double rp2 = 0.0, rd2 = 0.0, l1 = 0.0;
-  bool bad = false;
-  if (threadIdx.x == 0) {
-    for (int s2 = 0; s2 < kBulkStages; ++s2) {
-      mbar_init(&fullb[s2], 1);
-      mbar_init(&emptyb[s2], kBulkCompute);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-
-  if (x0 < xe) {
-    uint32_t j = 0;
-    while (j + 1 < N && segs[j + 1].unit0 <= x0) ++j;
-    SweepDesc sd = segs[j];
-    if (gwarp == 0) {
-      // ------------------------------------------------------------ loader warp
-      uint64_t pol;
-      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-      uint32_t seq = 0;
-      constexpr int kRealsPerComplex = 2;
-      for (uint64_t x = x0; x < xe; ++x) {
-        if (x == sd.unit0 + sd.n_strips) sd = segs[++j];
-        const int c0 = (int)((x - sd.unit0) * W * kRealsPerComplex);
-        for (uint32_t i = 0; i < M; ++i) {
-          const MatDesc md = hm[i * N + j];
-          const unsigned char* tm = tmaps + (size_t)(i * N + j) * 128;
-          for (uint32_t r0 = 0; r0 < md.rows; r0 += R, ++seq) {
-            const uint32_t slot = seq % kBulkStages, ph = (seq / kBulkStages) & 1;
-            if (lane == 0) {
-              mbar_wait(&emptyb[slot], ph ^ 1);
-              mbar_expect_tx(&fullb[slot], STAGEB);
-              tma_2d(smem_u32(ring) + slot * STAGEB, tm, c0, (int)r0, &fullb[slot], pol);
-            }
-            __syncwarp();
-          }
-        }
-      }
-    } else if (gwarp <= kBulkCompute) {
-      // ------------------------------------------------------------ (C) compute warps
-      const int warp = gwarp - 1;
-      uint32_t seq = 0, k = 0;
-      for (uint64_t x = x0; x < xe; ++x, ++k) {
-        if (x == sd.unit0 + sd.n_strips) sd = segs[++j];
-        const int zslot = k & 1;
-        const uint32_t col = (uint32_t)(x - sd.unit0) * W + lc * PV;
-        const bool cok = col < sd.cols;
-        for (uint32_t i = 0; i < M; ++i) {
-          const MatDesc md = hm[i * N + j];
-          const double2* qb = q + blocks[i * N + j].mvec_off;
-          double2 acc[PV];
-#pragma unroll
-          for (int e = 0; e < PV; ++e) acc[e] = make_double2(0.0, 0.0);
-          for (uint32_t r0 = 0; r0 < md.rows; r0 += R, ++seq) {
-            const uint32_t slot = seq % kBulkStages, ph = (seq / kBulkStages) & 1;
-            mbar_wait(&fullb[slot], ph);
-            const uint32_t base = smem_u32(ring) + slot * STAGEB;
-#pragma unroll
-            for (int ri = 0; ri < kBulkRI; ++ri) {
-              const uint32_t rs = (ri * kBulkCompute + warp) * RPI + lr;  // row within the stage
-              const uint32_t row = r0 + rs;
-              if (row < md.rows && cok) {
-                V256 hv;
-                const uint32_t a = base + rs * ROWB + lc * 32;
-                asm volatile("ld.shared.v2.b64 {%0,%1}, [%2];" : "=l"(hv.w[0]), "=l"(hv.w[1]) : "r"(a));
-                asm volatile("ld.shared.v2.b64 {%0,%1}, [%2];" : "=l"(hv.w[2]), "=l"(hv.w[3]) : "r"(a + 16));
-                const double2 qv = __ldg(qb + row);
-#pragma unroll
-                for (int e = 0; e < PV; ++e) cmac_conj(acc[e], Store<S>::get(hv, e), qv);
-              }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&emptyb[slot]);
-          }
-          if (i == 0 && k >= 2) nb_sync(kBarEmpty0 + zslot, kBulkHandoff);  // consumer released zbuf[zslot]
-#pragma unroll
-          for (int e = 0; e < PV; ++e) {
-#pragma unroll
-            for (int o = LPR; o < kWarp; o <<= 1) {
-              acc[e].x += __shfl_xor_sync(0xffffffffu, acc[e].x, o);
-              acc[e].y += __shfl_xor_sync(0xffffffffu, acc[e].y, o);
-            }
-            if (lr == 0) zbuf[(((size_t)zslot * kBulkCompute + warp) * M + i) * W + lc * PV + e] = acc[e];
-          }
-        }
-        nb_arrive(kBarFull0 + zslot, kBulkHandoff);  // z of this strip is ready
-      }
-      const uint32_t nk = k;
-      for (uint32_t kk = (nk >= 2 ? nk - 2 : 0); kk < nk; ++kk) nb_sync(kBarEmpty0 + (kk & 1), kBulkHandoff);
-    } else {
-      // ------------------------------------------------------------ consumer warps
-      const int warp = gwarp - 1 - kBulkCompute;
-      const int gt = threadIdx.x - (1 + kBulkCompute) * kWarp;
-      constexpr int kCT = kBulkCons * kWarp;
-      for (uint32_t r = gt; r < n_meas; r += kCT) wacc[r] = make_double2(0.0, 0.0);
-      uint32_t k = 0;
-      for (uint64_t x = x0; x < xe; ++x, ++k) {
-        const int slot = k & 1;
-        const uint32_t col_lo = (uint32_t)(x - sd.unit0) * W;
-        const uint32_t t = gt, cc = col_lo + t;
-        const bool dcol = gt < W && cc < sd.cols;
-        double2 vo = make_double2(0.0, 0.0);
-        if (dcol) {
-          for (uint32_t i = 0; i < M; ++i) {
-            const uint32_t o = blocks[i * N + j].vec_off + cc;
-            pre[i * W + t] = cv.c[o];
-            pre[(M + i) * W + t] = cv.s[o];
-          }
-          vo = cv.v[blocks[j].seg_off + cc];
-        }
-        nb_sync(kBarFull0 + slot, kBulkHandoff);  // wait for z of strip x
-        if (gt < W) {
-          if (dcol) {
-            double2 mean = make_double2(0.0, 0.0);
-            for (uint32_t i = 0; i < M; ++i) {
-              const uint32_t o = blocks[i * N + j].vec_off + cc;
-              double2 z = zbuf[((size_t)slot * kBulkCompute * M + i) * W + t];
-#pragma unroll
-              for (int w = 1; w < kBulkCompute; ++w) z = cadd(z, zbuf[(((size_t)slot * kBulkCompute + w) * M + i) * W + t]);
-              const double2 u = cadd(pre[i * W + t], z);
-              bad |= !cfinite(u);
-              cv.u[o] = u;
-              us[i * W + t] = u;
-              mean = cadd(mean, cadd(u, pre[(M + i) * W + t]));
-            }
-            mean = make_double2(mean.x / prm->m_rep, mean.y / prm->m_rep);
-            const double2 vn = soft_threshold(mean, prm->kappa);
-            const uint32_t so = blocks[j].seg_off + cc;
-            cv.vprev[so] = vo;
-            cv.v[so] = vn;
-            rd2 += cabs2(csub(vn, vo));
-            l1 += hypot(vn.x, vn.y);
-            for (uint32_t i = 0; i < M; ++i) {
-              const uint32_t o = blocks[i * N + j].vec_off + cc;
-              const double2 u = us[i * W + t];
-              rp2 += cabs2(csub(u, vn));
-              const double2 s2 = csub(cadd(pre[(M + i) * W + t], u), vn);
-              cv.s[o] = s2;
-              const double2 c = csub(vn, s2);
-              cv.c[o] = c;
-              cs[i * W + t] = c;
-            }
-          } else {
-            for (uint32_t i = 0; i < M; ++i) cs[i * W + t] = make_double2(0.0, 0.0);
-          }
-        }
-        nb_sync(kBarA, kCT);
-        nb_arrive(kBarEmpty0 + slot, kBulkHandoff);
-        const uint32_t col = col_lo + lc * PV;
-        const bool cok = col < sd.cols;
-        for (uint32_t i = 0; i < M; ++i) {
-          const MatDesc md = hm[i * N + j];
-          const uint32_t row0 = blocks[i * N + j].row0;
-          const S* hb = H + md.a_off + col;
-          double2 cx[PV];
-#pragma unroll
-          for (int e = 0; e < PV; ++e) cx[e] = cs[i * W + lc * PV + e];
-          for (uint32_t rb = warp * RPI; rb < md.rows; rb += CSTEP * kSweepUA) {  // warp-uniform
-            const uint32_t r0 = rb + lr;
-            V256 hv[kSweepUA];
-#pragma unroll
-            for (int u = 0; u < kSweepUA; ++u) {
-              const uint32_t row = r0 + u * CSTEP;
-              if (row < md.rows && cok) {
-                hv[u] = ld_stream256<kEvictFirst>(hb + (uint64_t)row * md.ld);
-              } else {
-                hv[u].w[0] = hv[u].w[1] = hv[u].w[2] = hv[u].w[3] = 0;
-              }
-            }
-#pragma unroll
-            for (int u = 0; u < kSweepUA; ++u) {
-              double2 a = make_double2(0.0, 0.0);
-#pragma unroll
-              for (int e = 0; e < PV; ++e) cmac(a, Store<S>::get(hv[u], e), cx[e]);
-#pragma unroll
-              for (int o = 1; o < LPR; o <<= 1) {
-                a.x += __shfl_xor_sync(0xffffffffu, a.x, o);
-                a.y += __shfl_xor_sync(0xffffffffu, a.y, o);
-              }
-              const uint32_t row = r0 + u * CSTEP;
-              if (lc == 0 && row < md.rows) {
-                double2& dst = wacc[row0 + row];
-                dst = cadd(dst, a);
-              }
-            }
-          }
-        }
-        const bool seg_end = (x + 1 == sd.unit0 + sd.n_strips);
-        if (seg_end || x + 1 == xe) {
-          nb_sync(kBarA, kCT);
-          const uint64_t slotp = p - sk_owner(sd.unit0, Utot, P);
-          double2* dst = wpart + sd.part_off + slotp * n_meas;
-          for (uint32_t r = gt; r < n_meas; r += kCT) {
-            dst[r] = wacc[r];
-            wacc[r] = make_double2(0.0, 0.0);
-          }
-          nb_sync(kBarA, kCT);
-          if (seg_end && x + 1 < xe) sd = segs[++j];
-        }
-        nb_sync(kBarA, kCT);
-      }
-    }
-  }
-  if (__syncthreads_or(bad) && threadIdx.x == 0) st->nonfinite = 1u;
-  double r = block_sum<kBulkThreads>(rp2, sm_red);
-  if (threadIdx.x == 0) red[p] = r;
-  r = block_sum<kBulkThreads>(rd2, sm_red);
-  if (threadIdx.x == 0) red[P + p] = r;
-  r = block_sum<kBulkThreads>(l1, sm_red);
-  if (threadIdx.x == 0) red[2 * P + p] = r;
 }
 
 // r_b = g_ij - w_b with w_b summed from the sweep partials of segment j in fixed

@@ -56,7 +56,11 @@ def trace_err(a, b, floor=None):
     fin = np.isfinite(b)
     assert np.array_equal(np.isfinite(a), fin)
     den = np.abs(b) if floor is None else np.abs(b) + floor
-    return float(np.max(np.abs(a[fin] - b[fin]) / den[fin])) if fin.any() else 0.0
+    diff = np.abs(a[fin] - b[fin])
+    exact = diff == 0.0  # includes b == 0 reproduced exactly (e.g. u == v to the last bit)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        rel_ = np.where(exact, 0.0, diff / den[fin])
+    return float(np.max(rel_)) if fin.any() else 0.0
 
 
 def plan_solve(admm, p, lam, method, M, N, iters, **opts):
