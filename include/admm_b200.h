@@ -235,6 +235,8 @@ typedef struct {
   uint64_t grid_pr, grid_pc;    /* process grid of a multi-GPU plan (1 x 1 on one GPU) */
   uint64_t n_ranks;             /* GPUs of the plan */
   uint64_t exchange_bytes_per_iter; /* NCCL bytes this rank receives per iteration */
+  double setup_phase_s[4];      /* setup_seconds split: host validation, upload (+ layout copies),
+                                   Gram (rho I + H H^H), inverse + packing */
 } admm_plan_info;
 admm_status admm_plan_get_info(const admm_plan* plan, admm_plan_info* info);
 

@@ -45,7 +45,8 @@ class PlanInfoC(ctypes.Structure):
                 ("setup_seconds", _dbl), ("inner_dim_max", _u64), ("schedule", _u64),
                 ("grid_sweep", _u64), ("hbm_bytes_per_iter", _u64), ("sweep_variant", _u64),
                 ("slab_cluster", _u64), ("slab_row_bytes", _u64), ("slab_rows", _u64),
-                ("grid_pr", _u64), ("grid_pc", _u64), ("n_ranks", _u64), ("exchange_bytes_per_iter", _u64)]
+                ("grid_pr", _u64), ("grid_pc", _u64), ("n_ranks", _u64), ("exchange_bytes_per_iter", _u64),
+                ("setup_phase_s", _dbl * 4)]
 
 
 class ShardC(ctypes.Structure):

@@ -220,6 +220,7 @@ struct admm_plan {
   cudaGraphExec_t exec = nullptr;
   uint64_t graph_iters = 0;
   double setup_s = 0.0;
+  double setup_phase[4] = {0, 0, 0, 0};  // validate (host scans), upload (+ layouts), Gram, inverse + packing
   size_t elem = 16;
   int num_sms = 148;
   Params params{};
@@ -751,46 +752,116 @@ void upload_desc(DevBuf& d, const void* src, size_t bytes) {
 
 // Upload the blocks of the host matrix into the storage arena (partition.hpp:79-125
 // materialises the same blocks as host copies).
+// Host rows -> pinned staging (pitch n_pix -> the block's ld, zero pad), on every host
+// core (OpenMP), checking finiteness of what it copies when asked (problem.hpp:44-46 for
+// the large matrices whose separate scan would cost a pass).  Returns false on a
+// non-finite entry.
+bool pack_rows(void* dst, const char* src, uint64_t nr, uint64_t cols, uint64_t src_pitch, uint64_t ld,
+               size_t esz, bool check) {
+  int bad = 0;
+#pragma omp parallel for schedule(static) reduction(| : bad)
+  for (int64_t r = 0; r < (int64_t)nr; ++r) {
+    char* d = static_cast<char*>(dst) + (uint64_t)r * ld * esz;
+    const char* s = src + (uint64_t)r * src_pitch * esz;
+    std::memcpy(d, s, cols * esz);
+    if (ld > cols) std::memset(d + cols * esz, 0, (ld - cols) * esz);
+    if (check) {
+      if (esz == 16) {
+        const double* v = reinterpret_cast<const double*>(d);
+        for (uint64_t e = 0; e < 2 * cols; ++e) bad |= !std::isfinite(v[e]);
+      } else {
+        const float* v = reinterpret_cast<const float*>(d);
+        for (uint64_t e = 0; e < 2 * cols; ++e) bad |= !std::isfinite(v[e]);
+      }
+    }
+  }
+  return !bad;
+}
+
+// Upload the blocks of the host matrix into the storage arena (partition.hpp:79-125
+// materialises the same blocks as host copies).  Large matrices go through two pinned
+// staging buffers: host cores pack chunk k + 1 while the copy engine moves chunk k, so H
+// crosses PCIe at DMA speed with one host pass that also checks finiteness
+// (check_finite).  c128 <-> c64 conversions run on the device (scl applied in FP64).
 template <typename S>
-void upload_h(admm_plan* p, const void* h, admm_dtype h_dtype) {
-  // p->dH was allocated by build_geometry (tensor maps need its address before upload)
+void upload_h(admm_plan* p, const void* h, admm_dtype h_dtype, bool check_finite) {
   const size_t hsz = h_dtype == ADMM_C128 ? 16 : 8;
   const bool direct = (h_dtype == ADMM_C128) == std::is_same<S, double2>::value;
-  DevBuf tmp;
-  if (!direct) {
-    uint64_t maxe = 0;
-    for (auto& b : p->blocks) maxe = std::max<uint64_t>(maxe, (uint64_t)b.rows * b.cols);
-    tmp.alloc(std::min<uint64_t>(maxe, 1ull << 26) * 16);
+  uint64_t total = 0, maxld = 0;
+  for (size_t b = 0; b < p->blocks.size(); ++b) {
+    total += (uint64_t)p->blocks[b].rows * p->hN[b].ld * hsz;
+    maxld = std::max<uint64_t>(maxld, p->hN[b].ld);
   }
+  const bool staged = check_finite || total >= (256ull << 20);
+  DevBuf tmp;
+  const size_t chunk = staged ? std::min<uint64_t>(total, 128ull << 20) : (size_t)std::min<uint64_t>(total, 1ull << 30);
+  if (!direct) tmp.alloc(std::max<size_t>(chunk, maxld * hsz));
+  void* pin[2] = {nullptr, nullptr};
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  struct Cleanup {
+    void** pin;
+    cudaEvent_t* ev;
+    ~Cleanup() {
+      for (int k = 0; k < 2; ++k) {
+        if (ev[k]) cudaEventDestroy(ev[k]);
+        if (pin[k]) cudaFreeHost(pin[k]);
+      }
+    }
+  } cleanup{pin, done};
+  if (staged)
+    for (int k = 0; k < 2; ++k) {
+      CK(cudaHostAlloc(&pin[k], std::max<size_t>(chunk, maxld * hsz), cudaHostAllocDefault));
+      CK(cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming));
+    }
+  int slot = 0;
+  bool finite = true;
   for (size_t b = 0; b < p->blocks.size(); ++b) {
     const BlockDesc& bd = p->blocks[b];
     const MatDesc& md = p->hN[b];
     const char* src = static_cast<const char*>(h) + ((uint64_t)bd.row0 * p->n_pix + bd.col0) * hsz;
-    if (direct) {
+    if (!staged && direct) {
       CK(cudaMemcpy2DAsync(p->dH.as<S>() + md.a_off, (size_t)md.ld * sizeof(S), src, p->n_pix * hsz,
                            (size_t)bd.cols * sizeof(S), bd.rows, cudaMemcpyHostToDevice, p->stream));
       continue;
     }
-    // convert through a device staging buffer in the host's element type, a slab of rows
-    // at a time (c128 -> c64 rounds, c64 -> c128 widens; scl applied in FP64)
-    const uint64_t slab = std::max<uint64_t>(1, (tmp.bytes / hsz) / std::max<uint32_t>(bd.cols, 1));
-    for (uint64_t r0 = 0; r0 < bd.rows; r0 += slab) {
-      const uint32_t nr = (uint32_t)std::min<uint64_t>(slab, bd.rows - r0);
-      CK(cudaMemcpy2DAsync(tmp.p, (size_t)bd.cols * hsz, src + r0 * p->n_pix * hsz, p->n_pix * hsz,
-                           (size_t)bd.cols * hsz, nr, cudaMemcpyHostToDevice, p->stream));
-      dim3 grid((unsigned)std::min<uint64_t>(cdiv(bd.cols, 256), 64), nr);
-      if (h_dtype == ADMM_C64)
-        widen_rows_kernel<S><<<grid, 256, 0, p->stream>>>(tmp.as<float2>(), bd.cols,
-                                                           p->dH.as<S>() + md.a_off + r0 * md.ld, md.ld, nr,
-                                                           bd.cols, p->cfg.scl);
-      else
-        narrow_rows_kernel<S><<<grid, 256, 0, p->stream>>>(tmp.as<double2>(), bd.cols,
-                                                            p->dH.as<S>() + md.a_off + r0 * md.ld, md.ld,
-                                                            nr, bd.cols, p->cfg.scl);
-      CK(cudaGetLastError());
-      CK(cudaStreamSynchronize(p->stream));
+    const uint64_t rows_per = std::max<uint64_t>(1, chunk / ((uint64_t)md.ld * hsz));
+    for (uint64_t r0 = 0; r0 < bd.rows; r0 += rows_per) {
+      const uint32_t nr = (uint32_t)std::min<uint64_t>(rows_per, bd.rows - r0);
+      const void* dev_src = nullptr;  // where the chunk's rows are on the device (pitch ld)
+      if (staged) {
+        CK(cudaEventSynchronize(done[slot]));  // the copy out of this buffer has finished
+        finite &= pack_rows(pin[slot], src + r0 * p->n_pix * hsz, nr, bd.cols, p->n_pix, md.ld, hsz, check_finite);
+        void* dst = direct ? (void*)(p->dH.as<S>() + md.a_off + r0 * md.ld) : tmp.p;
+        CK(cudaMemcpyAsync(dst, pin[slot], (size_t)nr * md.ld * hsz, cudaMemcpyHostToDevice, p->stream));
+        dev_src = tmp.p;
+      } else {
+        CK(cudaMemcpy2DAsync(tmp.p, (size_t)md.ld * hsz, src + r0 * p->n_pix * hsz, p->n_pix * hsz,
+                             (size_t)bd.cols * hsz, nr, cudaMemcpyHostToDevice, p->stream));
+        dev_src = tmp.p;
+      }
+      if (!direct) {
+        dim3 grid((unsigned)std::min<uint64_t>(cdiv(bd.cols, 256), 64), nr);
+        if (h_dtype == ADMM_C64)
+          widen_rows_kernel<S><<<grid, 256, 0, p->stream>>>(static_cast<const float2*>(dev_src), md.ld,
+                                                             p->dH.as<S>() + md.a_off + r0 * md.ld, md.ld, nr,
+                                                             bd.cols, p->cfg.scl);
+        else
+          narrow_rows_kernel<S><<<grid, 256, 0, p->stream>>>(static_cast<const double2*>(dev_src), md.ld,
+                                                              p->dH.as<S>() + md.a_off + r0 * md.ld, md.ld, nr,
+                                                              bd.cols, p->cfg.scl);
+        CK(cudaGetLastError());
+      }
+      if (staged) {
+        CK(cudaEventRecord(done[slot], p->stream));
+        if (!direct) CK(cudaStreamSynchronize(p->stream));  // tmp is reused by the next chunk
+        slot ^= 1;
+      } else {
+        CK(cudaStreamSynchronize(p->stream));
+      }
     }
   }
+  CK(cudaStreamSynchronize(p->stream));
+  if (!finite) throw Fail{ADMM_E_NUMERICAL, "SensingProblem: non-finite entries"};
   if (direct && p->cfg.scl != 1.0) {  // apply_scaling, problem.hpp:59-66 (converted
                                       // uploads scale in FP64 before rounding)
     scale_kernel<S><<<p->num_sms * 8, 256, 0, p->stream>>>(p->dH.as<S>(), p->h_elems, p->cfg.scl);
@@ -823,6 +894,7 @@ void build_slab(admm_plan* p) {
 // cholesky.hpp:48-74).
 template <typename S>
 void factor_blocks(admm_plan* p) {
+  const auto tf0 = std::chrono::steady_clock::now();
   const uint64_t nb = p->blocks.size();
   upload_desc(p->dgram, p->gram.data(), nb * sizeof(GramDesc));
   DevBuf A, rowk, colk, flag;
@@ -838,6 +910,8 @@ void factor_blocks(admm_plan* p) {
   CK(cudaMemcpyAsync(&hf, flag.p, 4, cudaMemcpyDeviceToHost, p->stream));
   CK(cudaStreamSynchronize(p->stream));
   if (hf & 1u) throw Fail{ADMM_E_NUMERICAL, "CholeskyFactor: non-finite entries in input matrix"};
+  const auto tf1 = std::chrono::steady_clock::now();
+  p->setup_phase[2] = std::chrono::duration<double>(tf1 - tf0).count();
   uint64_t kpacked_elems = 0;
   if (p->kpacked) {  // packed Hermitian tile layout (shared by K and, for the support schedule, G)
     uint64_t koff = 0, u0 = 0, po = 0, co = 0;
@@ -912,6 +986,7 @@ void factor_blocks(admm_plan* p) {
   CK(cudaMemcpyAsync(&hf, flag.p, 4, cudaMemcpyDeviceToHost, p->stream));
   CK(cudaStreamSynchronize(p->stream));
   if (hf & 1u) throw Fail{ADMM_E_NUMERICAL, "GramSolver: non-finite inverse"};
+  p->setup_phase[3] = std::chrono::duration<double>(std::chrono::steady_clock::now() - tf1).count();
 }
 
 // Sweep schedule with a per-iteration objective: trace[k-1].objective after the
@@ -1654,20 +1729,31 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
                        uint64_t n_pix, const void* h, admm_dtype h_dtype, const double* g,
                        bool skip_cfg_validation, const admm_shard* shard = nullptr) {
   const auto t0 = std::chrono::steady_clock::now();
+  auto since = [](std::chrono::steady_clock::time_point a) {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - a).count();
+  };
   if (!skip_cfg_validation) validate_cfg(cfg);
   // SensingProblem::validate (problem.hpp:35-49)
   if (n_meas == 0 || n_pix == 0 || !h || !g)
     throw Fail{ADMM_E_DIMENSION, "SensingProblem: empty sensing matrix"};
-  const bool hfin = h_dtype == ADMM_C128
-                        ? host_all_finite(static_cast<const double*>(h), 2 * n_meas * n_pix)
-                        : host_all_finite(static_cast<const float*>(h), 2 * n_meas * n_pix);
-  if (!hfin || !host_all_finite(g, 2 * n_meas * std::max<uint64_t>(1, o.batch)))
+  // Finiteness of H: a separate host pass for small matrices; large ones are checked by the
+  // staged upload's packing pass (upload_h).  Any error raised before that point is then
+  // preceded by the scan, so NumericalError keeps its place in the reference's order
+  // (problem.hpp:35-49 before the partition, partition.hpp:56-65).
+  auto h_finite = [&] {
+    return h_dtype == ADMM_C128 ? host_all_finite(static_cast<const double*>(h), 2 * n_meas * n_pix)
+                                : host_all_finite(static_cast<const float*>(h), 2 * n_meas * n_pix);
+  };
+  const bool defer_h = n_meas * n_pix * (h_dtype == ADMM_C128 ? 16 : 8) >= (256ull << 20);
+  if ((!defer_h && !h_finite()) || !host_all_finite(g, 2 * n_meas * std::max<uint64_t>(1, o.batch)))
     throw Fail{ADMM_E_NUMERICAL, "SensingProblem: non-finite entries"};
+  std::unique_ptr<admm_plan> p;
+  try {
   if (o.noise_sigma < 0.0) throw Fail{ADMM_E_PARAMETER, "SensingProblem: negative noise_sigma"};
   if (o.method < ADMM_REFERENCE || o.method > ADMM_HYBRID) throw Fail{ADMM_E_PARAMETER, "unknown method"};
   if (o.dtype != ADMM_C128 && o.dtype != ADMM_C64) throw Fail{ADMM_E_PARAMETER, "unknown dtype"};
 
-  auto p = std::make_unique<admm_plan>();
+  p = std::make_unique<admm_plan>();
   p->device = o.device;
   p->dtype = o.dtype;
   p->method = o.method;
@@ -1840,15 +1926,24 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
   }
   ensure_trace(p.get(), std::max<uint64_t>(cfg.max_iters, 1));
 
+  p->setup_phase[0] = since(t0);
+  if (p->dtype == ADMM_C128)
+    upload_h<double2>(p.get(), h, h_dtype, defer_h);
+  else
+    upload_h<float2>(p.get(), h, h_dtype, defer_h);
+  } catch (const Fail& f) {
+    if (defer_h && f.st != ADMM_E_NUMERICAL && !h_finite()) throw Fail{ADMM_E_NUMERICAL, "SensingProblem: non-finite entries"};
+    throw;
+  }
   if (p->dtype == ADMM_C128) {
-    upload_h<double2>(p.get(), h, h_dtype);
     if (p->slab_rpl) build_slab<double2>(p.get());
     if (p->schedule == 5) build_support<double2>(p.get());
+    p->setup_phase[1] = since(t0) - p->setup_phase[0];
     factor_blocks<double2>(p.get());
   } else {
-    upload_h<float2>(p.get(), h, h_dtype);
     if (p->slab_rpl) build_slab<float2>(p.get());
     if (p->schedule == 5) build_support<float2>(p.get());
+    p->setup_phase[1] = since(t0) - p->setup_phase[0];
     factor_blocks<float2>(p.get());
   }
   if (p->batch > 1) {
@@ -2147,6 +2242,7 @@ admm_status admm_plan_get_info(const admm_plan* p, admm_plan_info* info) {
     r.grid_gemv_h = p->gH.P;
     r.setup_seconds = p->setup_s;
     r.inner_dim_max = p->max_m;
+    for (int k = 0; k < 4; ++k) r.setup_phase_s[k] = p->setup_phase[k];
     r.grid_pr = p->Pr;
     r.grid_pc = p->Pc;
     r.n_ranks = p->Pr * p->Pc;

@@ -319,7 +319,9 @@ class AdmmPlan:
     def info(self) -> dict:
         i = _lib.PlanInfoC()
         check(_lib.lib.admm_plan_get_info(self._h, ctypes.byref(i)))
-        return {f: getattr(i, f) for f, _ in _lib.PlanInfoC._fields_}
+        out = {f: getattr(i, f) for f, _ in _lib.PlanInfoC._fields_}
+        out["setup_phase_s"] = dict(zip(("validate", "upload", "gram", "inverse"), list(i.setup_phase_s)))
+        return out
 
     # -- running -------------------------------------------------------------------
     def solve(self, observer: Optional[IterateObserver] = None) -> SolveReport:

@@ -1,6 +1,6 @@
 #!/usr/bin/env python3
 """Opcode histogram and hottest instructions of one kernel from an ncu report's SASS page:
-  python tools/sass_hot.py REPORT.ncu-rep [top]"""
+  python tools/sass_hot.py REPORT.ncu-rep [top] [kernel-index]"""
 import collections
 import csv
 import io
@@ -14,6 +14,10 @@ def main():
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
+    kidx = int(sys.argv[3]) if len(sys.argv) > 3 else 0  # which kernel of the report
+    starts = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"] + [len(rows)]
+    rows = rows[starts[kidx]:starts[kidx + 1]]
+    print(rows[0][1][:120])
     hdr = rows[1]
     ix = {h: i for i, h in enumerate(hdr)}
     ops, stalls, tot_i, tot_s = collections.Counter(), collections.Counter(), 0, 0
