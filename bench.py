@@ -382,7 +382,14 @@ def bench_ours(args):
                                                     f"by the plan" if sharded else "single GPU, all blocks"),
                 "l2": f"inputs larger than L2 (H {hb * ws / 2**20:.0f} MiB over {ws} GPU(s)), no flush needed",
                 "lambda": plan.cfg.lambda_, "trace_objective": bool(args.trace_objective),
-                "setup_s": setup_s, "setup_phase_s": info["setup_phase_s"], "timing": "CUDA events on the plan's stream around K graph-replayed "
+                "setup_s": setup_s, "setup_phase_s": info["setup_phase_s"],
+                "setup_gram": {"device_s": info["gram_device_s"],
+                               "tflops_fp64": info["gram_flops"] / max(info["gram_device_s"], 1e-12) / 1e12,
+                               "kernel": "gram_dmma_kernel (mma.sync m8n8k4 f64), launched per block under the upload"},
+                "setup_inverse": {"device_s": info["inverse_device_s"],
+                                  "tflops_fp64": info["inverse_flops"] / max(info["inverse_device_s"], 1e-12) / 1e12,
+                                  "kernel": "blocked Gauss-Jordan, 64-wide panels, DMMA rank-64 updates"},
+                "timing": "CUDA events on the plan's stream around K graph-replayed "
                                               "iterations, max over ranks"},
         "h_stream_gbs": h_stream_gbs, "h_stream_frac_of_peak": h_stream_gbs / peak,
         "h_stream_note": "2 x |H| per iteration (SURVEY §8d's two-pass H-stream bytes) / time: a single-pass "

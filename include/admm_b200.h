@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define ADMM_B200_ABI_VERSION 2
+#define ADMM_B200_ABI_VERSION 3
 
 /* Exception classes of errors.hpp:10-81, in validation order. */
 typedef enum {
@@ -235,8 +235,13 @@ typedef struct {
   uint64_t grid_pr, grid_pc;    /* process grid of a multi-GPU plan (1 x 1 on one GPU) */
   uint64_t n_ranks;             /* GPUs of the plan */
   uint64_t exchange_bytes_per_iter; /* NCCL bytes this rank receives per iteration */
-  double setup_phase_s[4];      /* setup_seconds split: host validation, upload (+ layout copies),
-                                   Gram (rho I + H H^H), inverse + packing */
+  double setup_phase_s[4];      /* setup_seconds split: host validation, upload (+ layout copies; the
+                                   Gram launches of the blocks already uploaded run under it), the Gram
+                                   time left after the upload, inverse + packing */
+  double gram_device_s;         /* device time of the Gram launches (rho I + H_b H_b^H, FP64 tensor cores) */
+  double gram_flops;            /* their real FP64 flops: 8 per complex MAC of the lower tiles */
+  double inverse_device_s;      /* device time of the blocked Gauss-Jordan inverse */
+  double inverse_flops;         /* 8 m^3 per block (rank-64 updates of the whole work matrix) */
 } admm_plan_info;
 admm_status admm_plan_get_info(const admm_plan* plan, admm_plan_info* info);
 

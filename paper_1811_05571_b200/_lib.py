@@ -46,7 +46,8 @@ class PlanInfoC(ctypes.Structure):
                 ("grid_sweep", _u64), ("hbm_bytes_per_iter", _u64), ("sweep_variant", _u64),
                 ("slab_cluster", _u64), ("slab_row_bytes", _u64), ("slab_rows", _u64),
                 ("grid_pr", _u64), ("grid_pc", _u64), ("n_ranks", _u64), ("exchange_bytes_per_iter", _u64),
-                ("setup_phase_s", _dbl * 4)]
+                ("setup_phase_s", _dbl * 4), ("gram_device_s", _dbl), ("gram_flops", _dbl),
+                ("inverse_device_s", _dbl), ("inverse_flops", _dbl)]
 
 
 class ShardC(ctypes.Structure):
@@ -56,7 +57,7 @@ class ShardC(ctypes.Structure):
 OBSERVER = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.POINTER(SnapshotC), ctypes.c_void_p)
 
 lib = ctypes.CDLL(LIB_PATH)
-ABI_VERSION = 2
+ABI_VERSION = 3
 if lib.admm_abi_version() != ABI_VERSION:
     raise ImportError(f"{LIB_PATH}: ABI {lib.admm_abi_version()} != {ABI_VERSION}; rebuild (__graft_entry__.build())")
 

@@ -466,7 +466,8 @@ hemv_finalize_kernel(RowVecs rv, const double2* __restrict__ part, const HemvDes
   rv.ghat[o] = csub(rv.gij[o], cscale(s, prm->rho));
 }
 
-// Packed tiles from the dense FP64 inverse (GramDesc a_off, m x m): tile (I, J), I >= J.
+// Packed tiles from the dense FP64 inverse (GramDesc a_off, leading dimension nT * 64 — the
+// padded work matrix of admm_factor.cuh): tile (I, J), I >= J.
 template <typename S>
 __global__ void k_pack_kernel(const double2* __restrict__ Aar, uint64_t a_off, uint32_t m, uint32_t nT,
                               S* __restrict__ Kp, double diag = 0.0) {  // diag subtracted on the diagonal
@@ -478,7 +479,7 @@ __global__ void k_pack_kernel(const double2* __restrict__ Aar, uint64_t a_off, u
     while ((I + 1) * (I + 2) / 2 <= u) ++I;
     const uint32_t J = u - I * (I + 1) / 2;
     const uint32_t row = I * kHT + e / kHT, col = J * kHT + e % kHT;
-    double2 v = (row < m && col < m) ? Aar[a_off + (uint64_t)row * m + col] : make_double2(0.0, 0.0);
+    double2 v = (row < m && col < m) ? Aar[a_off + (uint64_t)row * (nT * kHT) + col] : make_double2(0.0, 0.0);
     if (row == col && row < m) v.x -= diag;
     Kp[idx] = Store<S>::narrow(v);
   }

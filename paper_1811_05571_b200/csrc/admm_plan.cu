@@ -221,6 +221,7 @@ struct admm_plan {
   uint64_t graph_iters = 0;
   double setup_s = 0.0;
   double setup_phase[4] = {0, 0, 0, 0};  // validate (host scans), upload (+ layouts), Gram, inverse + packing
+  double gram_device_s = 0.0, gram_flops = 0.0, inverse_device_s = 0.0, inverse_flops = 0.0;
   size_t elem = 16;
   int num_sms = 148;
   Params params{};
@@ -327,10 +328,11 @@ void build_geometry(admm_plan* p) {
     gd.n = bd.cols;
     gd.ld = ld;
     gd.ldk = ldk;
+    gd.mp = (uint32_t)round_up(bd.rows, kFT);
     p->gram[b] = gd;
     hoff += (uint64_t)bd.rows * ld;
     koff += (uint64_t)bd.rows * ldk;
-    aoff += (uint64_t)bd.rows * bd.rows;
+    aoff += (uint64_t)gd.mp * gd.mp;
   }
   p->h_elems = hoff;
   p->k_elems = koff;
@@ -783,8 +785,9 @@ bool pack_rows(void* dst, const char* src, uint64_t nr, uint64_t cols, uint64_t 
 // staging buffers: host cores pack chunk k + 1 while the copy engine moves chunk k, so H
 // crosses PCIe at DMA speed with one host pass that also checks finiteness
 // (check_finite).  c128 <-> c64 conversions run on the device (scl applied in FP64).
-template <typename S>
-void upload_h(admm_plan* p, const void* h, admm_dtype h_dtype, bool check_finite) {
+// on_block(b) runs once block b's rows (final values) are enqueued on p->stream.
+template <typename S, typename OnBlock>
+void upload_h(admm_plan* p, const void* h, admm_dtype h_dtype, bool check_finite, OnBlock on_block) {
   const size_t hsz = h_dtype == ADMM_C128 ? 16 : 8;
   const bool direct = (h_dtype == ADMM_C128) == std::is_same<S, double2>::value;
   uint64_t total = 0, maxld = 0;
@@ -822,6 +825,7 @@ void upload_h(admm_plan* p, const void* h, admm_dtype h_dtype, bool check_finite
     if (!staged && direct) {
       CK(cudaMemcpy2DAsync(p->dH.as<S>() + md.a_off, (size_t)md.ld * sizeof(S), src, p->n_pix * hsz,
                            (size_t)bd.cols * sizeof(S), bd.rows, cudaMemcpyHostToDevice, p->stream));
+      on_block(b);
       continue;
     }
     const uint64_t rows_per = std::max<uint64_t>(1, chunk / ((uint64_t)md.ld * hsz));
@@ -859,6 +863,7 @@ void upload_h(admm_plan* p, const void* h, admm_dtype h_dtype, bool check_finite
         CK(cudaStreamSynchronize(p->stream));
       }
     }
+    on_block(b);
   }
   CK(cudaStreamSynchronize(p->stream));
   if (!finite) throw Fail{ADMM_E_NUMERICAL, "SensingProblem: non-finite entries"};
@@ -890,28 +895,76 @@ void build_slab(admm_plan* p) {
   CK(cudaStreamSynchronize(p->stream));
 }
 
-// rho I + H H^H per block, Gauss-Jordan inverse, store K (gram.hpp:48-53,92-122;
-// cholesky.hpp:48-74).
+// Gram phase (gram.hpp:92-122): A_b = rho I + H_b H_b^H on the FP64 tensor cores, one launch
+// per block on a second stream as soon as the block's rows are on the device, so the Gram of
+// block b runs under the PCIe upload of block b + 1.
+struct GramWork {
+  DevBuf A, flag;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev = nullptr;
+  std::vector<cudaEvent_t> marks;  // start / stop of every Gram launch (device time of the phase)
+  ~GramWork() {
+    for (cudaEvent_t e : marks) cudaEventDestroy(e);
+    if (ev) cudaEventDestroy(ev);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
 template <typename S>
-void factor_blocks(admm_plan* p) {
-  const auto tf0 = std::chrono::steady_clock::now();
-  const uint64_t nb = p->blocks.size();
-  upload_desc(p->dgram, p->gram.data(), nb * sizeof(GramDesc));
-  DevBuf A, rowk, colk, flag;
-  A.alloc(p->a_elems * sizeof(double2));
-  rowk.alloc((uint64_t)nb * p->max_m * sizeof(double2));
-  colk.alloc((uint64_t)nb * p->max_m * sizeof(double2));
-  flag.alloc(4);
-  const uint32_t tiles = (uint32_t)cdiv(p->max_m, kGT);
-  gram_kernel<S><<<dim3(tiles, tiles, (unsigned)nb), 256, 0, p->stream>>>(
-      p->dH.as<S>(), p->dgram.as<GramDesc>(), A.as<double2>(), p->cfg.rho, flag.as<unsigned>());
+void gram_begin(admm_plan* p, GramWork& w) {
+  upload_desc(p->dgram, p->gram.data(), p->blocks.size() * sizeof(GramDesc));
+  w.A.alloc(p->a_elems * sizeof(double2));
+  w.flag.alloc(4);
+  CK(cudaMemsetAsync(w.flag.p, 0, 4, p->stream));
+  CK(cudaStreamCreateWithFlags(&w.stream, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&w.ev, cudaEventDisableTiming));
+  CK(cudaFuncSetAttribute(gram_dmma_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * kFStage)));
+  CK(cudaStreamSynchronize(p->stream));
+}
+
+// Blocks [b0, b1): their rows are complete on p->stream.
+template <typename S>
+void gram_blocks(admm_plan* p, GramWork& w, size_t b0, size_t b1) {
+  uint32_t mp = 0;
+  for (size_t b = b0; b < b1; ++b) mp = std::max(mp, p->gram[b].mp);
+  const uint32_t nT = mp / kFT;
+  CK(cudaEventRecord(w.ev, p->stream));
+  CK(cudaStreamWaitEvent(w.stream, w.ev, 0));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  w.marks.push_back(e0);
+  CK(cudaEventCreate(&e1));
+  w.marks.push_back(e1);
+  CK(cudaEventRecord(e0, w.stream));
+  gram_dmma_kernel<S><<<dim3(nT * (nT + 1) / 2, (unsigned)(b1 - b0)), kFThreads, 2 * kFStage, w.stream>>>(
+      p->dH.as<S>(), p->dgram.as<GramDesc>(), (uint32_t)b0, w.A.as<double2>(), p->cfg.rho, w.flag.as<unsigned>());
   CK(cudaGetLastError());
+  CK(cudaEventRecord(e1, w.stream));
+  for (size_t b = b0; b < b1; ++b) {  // lower tiles (diagonal ones whole) x n complex MACs x 8 flops
+    const double nt = p->gram[b].mp / kFT;
+    p->gram_flops += nt * (nt + 1) / 2 * kFT * kFT * (double)p->gram[b].n * 8.0;
+  }
+}
+
+// Gram done -> blocked Gauss-Jordan inverse, store K (cholesky.hpp:48-74; admm_factor.cuh).
+template <typename S>
+void factor_blocks(admm_plan* p, GramWork& w) {
+  const uint64_t nb = p->blocks.size();
+  DevBuf& A = w.A;
+  DevBuf& flag = w.flag;
   unsigned hf = 0;
+  const auto tf0 = std::chrono::steady_clock::now();
+  CK(cudaStreamSynchronize(w.stream));
   CK(cudaMemcpyAsync(&hf, flag.p, 4, cudaMemcpyDeviceToHost, p->stream));
   CK(cudaStreamSynchronize(p->stream));
   if (hf & 1u) throw Fail{ADMM_E_NUMERICAL, "CholeskyFactor: non-finite entries in input matrix"};
+  for (size_t k = 0; k + 1 < w.marks.size(); k += 2) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, w.marks[k], w.marks[k + 1]));
+    p->gram_device_s += ms * 1e-3;
+  }
   const auto tf1 = std::chrono::steady_clock::now();
-  p->setup_phase[2] = std::chrono::duration<double>(tf1 - tf0).count();
+  p->setup_phase[2] = std::chrono::duration<double>(tf1 - tf0).count();  // Gram time not hidden under the upload
   uint64_t kpacked_elems = 0;
   if (p->kpacked) {  // packed Hermitian tile layout (shared by K and, for the support schedule, G)
     uint64_t koff = 0, u0 = 0, po = 0, co = 0;
@@ -947,12 +1000,40 @@ void factor_blocks(admm_plan* p) {
     CK(cudaGetLastError());
   }
   const unsigned gx = (unsigned)std::min<uint64_t>(cdiv(p->max_m, 256), 8);
-  for (uint32_t k = 0; k < p->max_m; ++k) {
-    gj_save_kernel<<<dim3((unsigned)cdiv(p->max_m, 256), (unsigned)nb), 256, 0, p->stream>>>(
-        A.as<double2>(), p->dgram.as<GramDesc>(), rowk.as<double2>(), colk.as<double2>(), p->max_m, k,
-        flag.as<unsigned>());
-    gj_update_kernel<<<dim3(gx, p->max_m, (unsigned)nb), 256, 0, p->stream>>>(
-        A.as<double2>(), p->dgram.as<GramDesc>(), rowk.as<double2>(), colk.as<double2>(), p->max_m, k);
+  {  // blocked Gauss-Jordan: per 64-wide panel the diagonal inverse, the row panel, the rank-64 update
+    const uint32_t mpmax = (uint32_t)round_up(p->max_m, kFT), np = mpmax / kFT;
+    DevBuf P, PH, WH, C;
+    P.alloc(nb * kFT * kFT * sizeof(double2));
+    PH.alloc(nb * kFT * kFT * sizeof(double2));
+    WH.alloc(nb * (uint64_t)mpmax * kFT * sizeof(double2));
+    C.alloc(nb * (uint64_t)mpmax * kFT * sizeof(double2));
+    const GjScratch sc{P.as<double2>(), PH.as<double2>(), WH.as<double2>(), C.as<double2>(), mpmax};
+    CK(cudaFuncSetAttribute(gj_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGjDiagSmem));
+    CK(cudaFuncSetAttribute(gj_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGjPanelSmem));
+    CK(cudaFuncSetAttribute(gj_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * kFStage)));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, p->stream));
+    for (uint32_t kp = 0; kp < np; ++kp) {
+      gj_diag_kernel<<<(unsigned)nb, kFThreads, kGjDiagSmem, p->stream>>>(A.as<double2>(), p->dgram.as<GramDesc>(), kp,
+                                                                         sc, flag.as<unsigned>());
+      if (np > 1) {
+        gj_panel_kernel<<<dim3(np, (unsigned)nb), kFThreads, kGjPanelSmem, p->stream>>>(
+            A.as<double2>(), p->dgram.as<GramDesc>(), kp, sc);
+        gj_update_kernel<<<dim3(np, np, (unsigned)nb), kFThreads, 2 * kFStage, p->stream>>>(
+            A.as<double2>(), p->dgram.as<GramDesc>(), kp, sc);
+      }
+    }
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(e1, p->stream));
+    CK(cudaStreamSynchronize(p->stream));  // the scratch buffers are released here
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    p->inverse_device_s = ms * 1e-3;
+    for (uint64_t b = 0; b < nb; ++b) p->inverse_flops += 8.0 * std::pow((double)p->gram[b].mp, 3.0);
   }
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(&hf, flag.p, 4, cudaMemcpyDeviceToHost, p->stream));
@@ -1748,6 +1829,7 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
   if ((!defer_h && !h_finite()) || !host_all_finite(g, 2 * n_meas * std::max<uint64_t>(1, o.batch)))
     throw Fail{ADMM_E_NUMERICAL, "SensingProblem: non-finite entries"};
   std::unique_ptr<admm_plan> p;
+  bool h_checked = false;  // the staged upload has scanned H
   try {
   if (o.noise_sigma < 0.0) throw Fail{ADMM_E_PARAMETER, "SensingProblem: negative noise_sigma"};
   if (o.method < ADMM_REFERENCE || o.method > ADMM_HYBRID) throw Fail{ADMM_E_PARAMETER, "unknown method"};
@@ -1927,24 +2009,32 @@ admm_plan* create_plan(const admm_plan_options& o, const admm_solver_config& cfg
   ensure_trace(p.get(), std::max<uint64_t>(cfg.max_iters, 1));
 
   p->setup_phase[0] = since(t0);
+  // In-place scaling of a directly copied H (problem.hpp:59-66) runs after the whole upload:
+  // only then are the blocks final, so their Gram launches follow the upload instead of
+  // overlapping it.
+  const bool direct_scaled = ((h_dtype == ADMM_C128) == (p->dtype == ADMM_C128)) && cfg.scl != 1.0;
+  auto setup_dtype = [&](auto tag) {
+    using S = decltype(tag);
+    GramWork gw;
+    gram_begin<S>(p.get(), gw);
+    upload_h<S>(p.get(), h, h_dtype, defer_h, [&](size_t b) {
+      if (!direct_scaled) gram_blocks<S>(p.get(), gw, b, b + 1);
+    });
+    h_checked = true;
+    if (direct_scaled) gram_blocks<S>(p.get(), gw, 0, p->blocks.size());
+    if (p->slab_rpl) build_slab<S>(p.get());
+    if (p->schedule == 5) build_support<S>(p.get());
+    p->setup_phase[1] = since(t0) - p->setup_phase[0];
+    factor_blocks<S>(p.get(), gw);
+  };
   if (p->dtype == ADMM_C128)
-    upload_h<double2>(p.get(), h, h_dtype, defer_h);
+    setup_dtype(double2{});
   else
-    upload_h<float2>(p.get(), h, h_dtype, defer_h);
+    setup_dtype(float2{});
   } catch (const Fail& f) {
-    if (defer_h && f.st != ADMM_E_NUMERICAL && !h_finite()) throw Fail{ADMM_E_NUMERICAL, "SensingProblem: non-finite entries"};
+    if (defer_h && !h_checked && f.st != ADMM_E_NUMERICAL && !h_finite())
+      throw Fail{ADMM_E_NUMERICAL, "SensingProblem: non-finite entries"};
     throw;
-  }
-  if (p->dtype == ADMM_C128) {
-    if (p->slab_rpl) build_slab<double2>(p.get());
-    if (p->schedule == 5) build_support<double2>(p.get());
-    p->setup_phase[1] = since(t0) - p->setup_phase[0];
-    factor_blocks<double2>(p.get());
-  } else {
-    if (p->slab_rpl) build_slab<float2>(p.get());
-    if (p->schedule == 5) build_support<float2>(p.get());
-    p->setup_phase[1] = since(t0) - p->setup_phase[0];
-    factor_blocks<float2>(p.get());
   }
   if (p->batch > 1) {
     build_batched(p.get());
@@ -2243,6 +2333,10 @@ admm_status admm_plan_get_info(const admm_plan* p, admm_plan_info* info) {
     r.setup_seconds = p->setup_s;
     r.inner_dim_max = p->max_m;
     for (int k = 0; k < 4; ++k) r.setup_phase_s[k] = p->setup_phase[k];
+    r.gram_device_s = p->gram_device_s;
+    r.gram_flops = p->gram_flops;
+    r.inverse_device_s = p->inverse_device_s;
+    r.inverse_flops = p->inverse_flops;
     r.grid_pr = p->Pr;
     r.grid_pc = p->Pc;
     r.n_ranks = p->Pr * p->Pc;

@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     assert len(syms) >= 20
     for s in syms:
         assert hasattr(lib, s), s
-    assert lib.admm_abi_version() == 2
+    assert lib.admm_abi_version() == 3
 
 
 def test_python_binding_covers_the_header():
