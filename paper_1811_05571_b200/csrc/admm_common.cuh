@@ -125,12 +125,20 @@ __host__ __device__ __forceinline__ uint64_t sk_owner(uint64_t x, uint64_t U, ui
   return ((x + 1) * P - 1) / U;
 }
 
+// Warp index through a lane-0 broadcast.  ptxas cannot prove that threadIdx.x / 32 is the
+// same in every lane, so a shuffle under a branch on it compiles to an out-of-line
+// WARPSYNC.COLLECTIVE / ENDCOLLECTIVE sequence with fixed-register moves (about 7
+// instructions per SHFL); the broadcast value is warp-uniform by construction, the role /
+// tile branches move to the uniform datapath and the shuffles become bare SHFLs (slab sweep
+// on config 3: 245 -> 169 us).  Call with all 32 lanes converged (kernel entry).
+__device__ __forceinline__ int warp_index() { return __shfl_sync(0xffffffffu, (int)(threadIdx.x / kWarp), 0); }
+
 // ---- deterministic block reduction (fixed tree, no atomics) -----------------
 template <int kThreads>
 __device__ __forceinline__ double block_sum(double v, double* smem) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+  const int warp = warp_index(), lane = threadIdx.x % kWarp;
   __syncthreads();
   if (lane == 0) smem[warp] = v;
   __syncthreads();

@@ -130,7 +130,7 @@ hemv_kernel(const S* __restrict__ Kp, const double2* __restrict__ X, double2* __
     pdl_enter();
     return;
   }
-  const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+  const int warp = warp_index(), lane = threadIdx.x % kWarp;
   // descriptors and K do not depend on the predecessor: located / requested before the
   // PDL wait, r (rows_finalize) only after it
   int b = find_desc(hd, nb, x);
@@ -322,7 +322,7 @@ hemv_bulk_kernel(const S* __restrict__ Kp, const double2* __restrict__ X, double
       bulk_g2s_s(ring_s + (uint32_t)t * TB, Kp + (x0 + t) * (uint64_t)(kHT * kHT), TB, full_s + 8 * (uint32_t)t, pol);
     }
   }
-  const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+  const int warp = warp_index(), lane = threadIdx.x % kWarp;
   int b = find_desc(hd, nb, x);  // descriptors are constant: located before the PDL wait
   HemvDesc d = hd[b];
   __syncthreads();

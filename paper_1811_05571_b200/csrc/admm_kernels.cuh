@@ -107,7 +107,7 @@ gemv_n_kernel(const S* __restrict__ A, const double2* __restrict__ X, double2* _
   uint64_t x = sk_lo(p, U, P);
   const uint64_t xe = sk_lo(p + 1, U, P);
   if (x >= xe) return;
-  const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+  const int warp = warp_index(), lane = threadIdx.x % kWarp;
   int b = find_desc(mats, nmats, x);
   MatDesc md = mats[b];
   uint64_t local = x - md.unit0;
@@ -189,7 +189,7 @@ gemv_h_kernel(const S* __restrict__ A, const double2* __restrict__ Q, double2* _
   uint64_t x = sk_lo(p, U, P);
   const uint64_t xe = sk_lo(p + 1, U, P);
   if (x >= xe) return;
-  const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+  const int warp = warp_index(), lane = threadIdx.x % kWarp;
   int b = find_desc(mats, nmats, x);
   MatDesc md = mats[b];
   uint64_t local = x - md.unit0;

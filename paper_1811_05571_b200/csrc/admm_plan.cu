@@ -414,8 +414,15 @@ SlabFn<S> slab_fn_rb(int rpl, bool tr) {
   if (rpl == 2) return tr ? sweep_slab_kernel<S, 2, RB, true> : sweep_slab_kernel<S, 2, RB, false>;
   return tr ? sweep_slab_kernel<S, 4, RB, true> : sweep_slab_kernel<S, 4, RB, false>;
 }
+// 16-byte strip rows: tall strips (many rows per segment) in one CTA, slabs of 128 / 192 rows
+template <typename S>
+SlabFn<S> slab_fn_rb16(int rpl, bool tr) {
+  if (rpl == 6) return tr ? sweep_slab_kernel<S, 6, 16, true> : sweep_slab_kernel<S, 6, 16, false>;
+  return tr ? sweep_slab_kernel<S, 4, 16, true> : sweep_slab_kernel<S, 4, 16, false>;
+}
 template <typename S>
 SlabFn<S> slab_fn(int rpl, uint32_t rb, bool tr) {
+  if (rb == 16) return slab_fn_rb16<S>(rpl, tr);
   return rb == 32 ? slab_fn_rb<S, 32>(rpl, tr) : slab_fn_rb<S, 64>(rpl, tr);
 }
 
@@ -435,11 +442,13 @@ bool try_slab(admm_plan* p) {
   struct Cand { uint32_t rb, rpl, C, nw, ns, Ns; uint64_t pad; };
   bool have = false;
   Cand best{};
-  for (uint32_t rb : {64u, 32u}) {
+  for (uint32_t rb : {64u, 32u, 16u}) {
     if (fB && (uint32_t)fB != rb) continue;
     const uint32_t W = rb / 16 * (16 / sizeof(S));
     if (M * W > kWarp) continue;  // the D warp maps (replica, column) onto lanes
-    for (uint32_t rpl : {2u, 1u, 4u}) {
+    for (uint32_t rpl : {2u, 1u, 4u, 6u}) {
+      if ((rpl == 6 || rb == 16) && !(rb == 16 && rpl >= 4)) continue;  // instantiated pairs
+      if (rb == 16 && rpl == 4 && !fR) continue;  // 24 x 128-row slabs measured slower than 16 x 192 (config 3)
       const uint32_t rpw = rpl * kWarp;
       if (fR && (uint32_t)fR != rpw) continue;
       uint32_t Ns = 0;
@@ -456,7 +465,7 @@ bool try_slab(admm_plan* p) {
         // 265 us) -- the per-strip DSMEM exchange sits on the D warps' critical path
         if (!fC && C > 1) continue;
         const uint32_t nw = (uint32_t)cdiv(Ns, C);
-        if (nw > (uint32_t)kSlabMaxW || (C > 1 && nw * (C - 1) >= Ns)) continue;  // no empty rank
+        if (nw > (uint32_t)slab_max_warps((int)rpl, (int)rb) || (C > 1 && nw * (C - 1) >= Ns)) continue;  // no empty rank
         const size_t fixed = slab_smem_bytes(0, nw, kSlabMaxD, rpw, rb, C, M, W, N);
         const size_t per = (size_t)nw * rpw * rb + nw * sizeof(uint64_t);
         const uint32_t ns = (uint32_t)std::min<size_t>((cap - fixed) / per, 8);
@@ -886,7 +895,7 @@ void upload_h(admm_plan* p, const void* h, admm_dtype h_dtype, bool check_finite
 template <typename S>
 void build_slab(admm_plan* p) {
   const uint64_t chunks = p->gS.U * p->slab_Ns * (uint64_t)p->slab_rpl * kWarp * (p->slab_rb / 16);
-  auto kern = p->slab_rb == 32 ? slab_h_kernel<S, 32> : slab_h_kernel<S, 64>;
+  auto kern = p->slab_rb == 16 ? slab_h_kernel<S, 16> : p->slab_rb == 32 ? slab_h_kernel<S, 32> : slab_h_kernel<S, 64>;
   kern<<<p->num_sms * 8, 256, 0, p->stream>>>(p->dH.as<S>(), p->dhN.as<MatDesc>(),
                                                           p->dsegs.as<SweepDesc>(), p->dslabs.as<SlabDesc>(),
                                                           (uint32_t)p->Nc, p->slab_Ns, (uint32_t)p->slab_rpl * kWarp,

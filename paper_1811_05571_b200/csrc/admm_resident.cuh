@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1) resident_kernel(ResArgs a) {
   }
   __syncthreads();
 
-  const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+  const int warp = warp_index(), lane = threadIdx.x % kWarp;
   const uint32_t niter = a.prologue ? 1 : a.iters;
   for (uint32_t it = 0; it < niter; ++it) {
     const uint64_t k = ld_acquire_gpu64(&a.st->iter);  // iterations completed before this one

@@ -35,8 +35,8 @@
 
 namespace admm {
 
-// Slab row width RB (bytes of one strip row): 64 (4 c128 / 8 c64 columns per strip) or
-// 32 (half the strip, for blocks with many rows).  16-byte chunk c of row r is stored at
+// Slab row width RB (bytes of one strip row): 64 (4 c128 / 8 c64 columns per strip), 32 or
+// 16 (narrower strips for segments with many rows: the whole strip still fits one CTA's ring).  16-byte chunk c of row r is stored at
 // position c ^ slab_swz<RB>(r): both SMEM access patterns below are then conflict-free.
 template <int RB>
 __host__ __device__ constexpr uint32_t slab_swz(uint32_t row) {
@@ -44,6 +44,11 @@ __host__ __device__ constexpr uint32_t slab_swz(uint32_t row) {
 }
 constexpr int kSlabMaxW = 16;        // compute warps per CTA (+ D warps)
 constexpr int kSlabThreads = (kSlabMaxW + 4) * kWarp;  // + up to 4 D warps; 20 warps keep the 96-register cap
+// 16-byte strip rows with 128-row slabs: 24 compute warps (3072 rows of a complex64 strip in
+// one CTA) + 4 D warps at a 72-register cap -- the narrow-strip passes are latency-bound, so
+// warps, not registers, are what they need.
+__host__ __device__ constexpr int slab_max_warps(int rpl, int rb) { return rb == 16 && rpl == 4 ? 24 : kSlabMaxW; }
+__host__ __device__ constexpr int slab_max_threads(int rpl, int rb) { return (slab_max_warps(rpl, rb) + 4) * kWarp; }
 
 struct SlabDesc {
   uint32_t rep;    // replica (row block) i
@@ -213,7 +218,7 @@ __host__ __device__ inline bool slab_lag_ok(uint32_t L, uint32_t ND) {
 // 20 warps x 32 lanes: the register allocation granularity (4 warps) caps this at 96
 // registers per thread (65536 / (20 x 32)).
 template <typename S, int RPL, int RB, bool kTrace>
-__global__ void __launch_bounds__(kSlabThreads, 1)
+__global__ void __launch_bounds__(slab_max_threads(RPL, RB), 1)
 sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, const BlockDesc* __restrict__ blocks,
                   const SweepDesc* __restrict__ segs, uint32_t M, uint32_t N, uint32_t n_meas, uint64_t U, uint32_t NS,
                   uint32_t L, uint32_t Ns, uint32_t NW, const double2* __restrict__ q, ColVecs cv,
@@ -260,7 +265,8 @@ sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, 
   const uint64_t NCl = cluster_count(), cl = cluster_id();
   const uint64_t x0 = sk_lo(cl, U, NCl), xe = sk_lo(cl + 1, U, NCl);
   const uint32_t nstrip = (uint32_t)(xe - x0);
-  const uint32_t warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+  // warp-uniform by construction (admm_common.cuh warp_index): bare SHFLs below
+  const uint32_t warp = (uint32_t)warp_index(), lane = threadIdx.x % kWarp;
   // diagnostics: per-strip timestamps of compute warp 0 and the D warps (first 64 strips)
   auto mark = [&](uint32_t k, int ev) {
     if (kTrace && lane == 0 && k < 64 && (warp == 0 || warp >= NW))
@@ -338,7 +344,111 @@ sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, 
     const double2* cb_rep = cb + (size_t)sd.rep * W;
     double2* zp_w = zp + (size_t)warp * W + ccol * PV;
 
+    // flush of a finished segment's w partial, then the next segment ((A) side)
+    auto flush_w = [&](uint32_t kk) {
+      if (kk + 1 == kendA || kk + 1 == nstrip) {
+        if (act) {
+          const SweepDesc sg = tseg[jA];
+          const uint64_t slotp = cl - sk_owner(sg.unit0, U, NCl);
+          double2* dst = wpart + sg.part_off + slotp * n_meas + sd.mrow0;
+#pragma unroll
+          for (int m = 0; m < RPL; ++m) {
+            const uint32_t r = lane + kWarp * m;
+            if (r < sd.nrows) dst[r] = wacc[m];
+            wacc[m] = make_double2(0.0, 0.0);
+          }
+        }
+        if (kk + 1 < nstrip) {
+          ++jA;
+          kendA = (uint32_t)(tseg[jA].unit0 + tseg[jA].n_strips - x0);
+        }
+      }
+    };
+
     for (uint32_t k = 0; k < nstrip + L; ++k) {
+      if (NSL == 1 && k < nstrip && k >= L) {
+        // ------------------------------------------- (C) strip k and (A) strip k - L, fused
+        // 16-byte strip rows: both passes map lane -> rows lane + 32 m, so one loop feeds the
+        // z partial of strip k and the w accumulators from strip k - L; their loads, widenings
+        // and FMAs interleave (the two passes alone are dependent chains: latency-bound with
+        // five warps per scheduler).  The z partial is reduce-scattered over the lanes
+        // (6 shuffle rounds of one double instead of 5 rounds of four).
+        const uint32_t kk = k - L;
+        if (k == kend) {
+          ++j;
+          kend = (uint32_t)(tseg[j].unit0 + tseg[j].n_strips - x0);
+          load_q(j);
+        }
+        if (act) mbar_wait_s(full_s + stgC * 8, phC);
+        mbar_wait_s(cfull_s + (kk % kSlabZB) * 8, (kk / kSlabZB) & 1);
+        mark(k, 0);
+        mark(kk, 2);
+        if (act) {
+          const double2* cbi = cb_rep + (size_t)(kk % kSlabZB) * M * W;
+          double2 cr[PV];
+#pragma unroll
+          for (int e = 0; e < PV; ++e) cr[e] = cbi[e];
+          const unsigned char* baseC = ring + ring_off + stgC * stage_stride + lane * RB;
+          const unsigned char* baseA = ring + ring_off + stgA * stage_stride + lane * RB;
+          double2 acc[2][PV];
+#pragma unroll
+          for (int a2 = 0; a2 < 2; ++a2)
+#pragma unroll
+            for (int e = 0; e < PV; ++e) acc[a2][e] = make_double2(0.0, 0.0);
+          constexpr int FB = RPL % 3 == 0 ? 3 : RPL % 2 == 0 ? 2 : 1;  // rows per batch (register cap)
+#pragma unroll
+          for (int m0 = 0; m0 < RPL; m0 += FB) {
+            CK hc[FB], ha[FB];
+#pragma unroll
+            for (int m = 0; m < FB; ++m) {
+              hc[m].ld(baseC + (m0 + m) * kWarp * RB);
+              ha[m].ld(baseA + (m0 + m) * kWarp * RB);
+            }
+#pragma unroll
+            for (int m = 0; m < FB; ++m) {
+#pragma unroll
+              for (int e = 0; e < PV; ++e) cmac_conj(acc[(m0 + m) & 1][e], hc[m].get(e), qr[m0 + m]);
+              double2 ae = make_double2(0.0, 0.0);
+#pragma unroll
+              for (int e = 0; e < PV; ++e) cmac(ae, ha[m].get(e), cr[e]);
+              wacc[m0 + m] = cadd(wacc[m0 + m], ae);
+            }
+          }
+          __syncwarp();  // every lane has consumed stage stgA
+          if (lane == 0 && kk + NS < nstrip) issue(kk + NS, stgA);
+          // reduce-scatter of the 2 PV doubles of z over the 32 lanes
+          double v0, v1 = 0.0;
+          if constexpr (PV == 2) {
+            const double2 z0 = cadd(acc[0][0], acc[1][0]), z1 = cadd(acc[0][1], acc[1][1]);
+            const bool hi = (lane & 16) != 0;
+            const double sx = hi ? z0.x : z1.x, sy = hi ? z0.y : z1.y;
+            v0 = (hi ? z1.x : z0.x) + __shfl_xor_sync(0xffffffffu, sx, 16);
+            v1 = (hi ? z1.y : z0.y) + __shfl_xor_sync(0xffffffffu, sy, 16);
+          } else {
+            const double2 z0 = cadd(acc[0][0], acc[1][0]);
+            v0 = z0.x;
+            v1 = z0.y;
+          }
+          constexpr int O1 = PV == 2 ? 8 : 16;  // x / y split
+          {
+            const bool hi = (lane & O1) != 0;
+            const double snd = hi ? v0 : v1;
+            v0 = (hi ? v1 : v0) + __shfl_xor_sync(0xffffffffu, snd, O1);
+          }
+#pragma unroll
+          for (int o = O1 / 2; o > 0; o >>= 1) v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+          if ((lane & (O1 - 1)) == 0)  // lane = (column e, component) * O1
+            reinterpret_cast<double*>(zp + (size_t)(k % kSlabZB) * NW * W + (size_t)warp * W)[lane / O1] = v0;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_s(zfull_s + (k % kSlabZB) * 8);
+        mark(k, 1);
+        mark(kk, 3);
+        if (++stgC == NS) stgC = 0, phC ^= 1u;
+        if (++stgA == NS) stgA = 0;
+        flush_w(kk);
+        continue;
+      }
       if (k < nstrip) {
         // ---------------------------------------------------------- (C) strip k
         if (k == kend) {
@@ -355,7 +465,8 @@ sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, 
           for (int a4 = 0; a4 < 4; ++a4)
 #pragma unroll
             for (int e = 0; e < PV; ++e) acc[a4][e] = make_double2(0.0, 0.0);
-          constexpr int CB = CNU > 4 ? 4 : CNU;  // loads in flight per batch (register cap)
+          // loads in flight per batch (register cap); CB divides CNU
+          constexpr int CB = CNU % 4 == 0 ? 4 : CNU % 3 == 0 ? 3 : CNU <= 4 ? CNU : 1;
 #pragma unroll
           for (int u0 = 0; u0 < CNU; u0 += CB) {
             CK h[CB];
@@ -419,23 +530,7 @@ sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, 
           mark(kk, 3);
         }
         if (++stgA == NS) stgA = 0;
-        if (kk + 1 == kendA || kk + 1 == nstrip) {  // flush this segment's w partial
-          if (act) {
-            const SweepDesc sg = tseg[jA];
-            const uint64_t slotp = cl - sk_owner(sg.unit0, U, NCl);
-            double2* dst = wpart + sg.part_off + slotp * n_meas + sd.mrow0;
-#pragma unroll
-            for (int m = 0; m < RPL; ++m) {
-              const uint32_t r = lane + kWarp * m;
-              if (r < sd.nrows) dst[r] = wacc[m];
-              wacc[m] = make_double2(0.0, 0.0);
-            }
-          }
-          if (kk + 1 < nstrip) {
-            ++jA;
-            kendA = (uint32_t)(tseg[jA].unit0 + tseg[jA].n_strips - x0);
-          }
-        }
+        flush_w(kk);
       }
     }
   } else {

@@ -79,7 +79,7 @@ support_compact_kernel(const double2* __restrict__ v, const BlockDesc* __restric
     const double2 a = v[b0.seg_off + t];
     nz = a.x != 0.0 || a.y != 0.0;
   }
-  const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+  const int warp = warp_index(), lane = threadIdx.x % kWarp;
   const unsigned m = __ballot_sync(0xffffffffu, nz);
   if (lane == 0) wsum[warp] = __popc(m);
   __syncthreads();

@@ -75,7 +75,7 @@ sweep_kernel(const S* __restrict__ H, const MatDesc* __restrict__ hm, const Bloc
   const uint64_t P = gridDim.x, p = blockIdx.x;
   const uint64_t x0 = sk_lo(p, Utot, P);
   const uint64_t xe = sk_lo(p + 1, Utot, P);
-  const int gwarp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+  const int gwarp = warp_index(), lane = threadIdx.x % kWarp;
   const bool producer = gwarp < kProdWarps;
   const int warp = producer ? gwarp : gwarp - kProdWarps;
   const int gt = threadIdx.x - (producer ? 0 : kProdWarps * kWarp);  // index within the group
