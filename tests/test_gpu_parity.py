@@ -120,6 +120,41 @@ def test_gram_solver_known_answers_and_oracle():
         a.GramSolver(bad, 1.0)
 
 
+@pytest.mark.parametrize("shape", [(70, 150), (129, 257), (200, 333), (64, 64), (65, 1000), (300, 90)])
+def test_factor_multi_panel_sizes_vs_oracle(shape):
+    """The DMMA Gram and the blocked Gauss-Jordan inverse (admm_factor.cuh) on inner dimensions
+    that are not multiples of the 64-wide panel, with k-lengths that are not multiples of the
+    16-column chunk, for both strategies (gram.hpp:32-34, 63-78, 92-122; cholesky.hpp:24-74)."""
+    a = admm()
+    m, n = shape
+    h = orc.random_gauss(m * n, 900 + m).reshape(m, n) / np.sqrt(m)
+    rhs = orc.random_gauss(n, 901 + n)
+    want = orc.gram_solve(h, 0.7, rhs)
+    for strategy in (a.GramSolver.Strategy.Woodbury, a.GramSolver.Strategy.Direct):
+        gs = a.GramSolver(h, 0.7, strategy)
+        assert gs.inner_dim() == (m if strategy == a.GramSolver.Strategy.Woodbury else n)
+        got = gs.solve(rhs)
+        assert rel(got, want) <= 1e-11, (strategy, rel(got, want))
+        got2 = gs.solve(2.0 * rhs)  # factored once, applied again
+        assert rel(got2, 2.0 * want) <= 1e-11
+
+
+def test_factor_ragged_blocks_c64_plan():
+    """Blocks of different, non-panel-aligned sizes in one plan (padded work matrices of
+    different dimensions side by side), complex64 storage."""
+    a = admm()
+    h, g, t, _ = orc.gen_problem(331, 1030, 12, 30.0, 21)
+    lam = 0.05 * float(np.max(np.abs(orc.adjoint_matvec(h, g))))
+    ref = orc.solve("hybrid", h, g, M=3, N=2, ragged=True, lam=lam, iters=40)
+    p = a.SensingProblem(h.astype(np.complex64), g, t)
+    ref64 = orc.solve("hybrid", p.h.astype(np.complex128), g, M=3, N=2, ragged=True, lam=lam, iters=40)
+    cfg = a.SolverConfig(rho=1.0, lambda_=lam, max_iters=40)
+    r = a.hybrid_solve(p, cfg, 3, 2, a.SolveOptions(ragged=True, dtype="c64"))
+    assert rel(r.solution, ref64["solution"]) <= 1e-4
+    r128 = a.hybrid_solve(a.SensingProblem(h, g, t), cfg, 3, 2, a.SolveOptions(ragged=True))
+    assert rel(r128.solution, ref["solution"]) <= 1e-9
+
+
 # -------------------------------------------------------- solver parity vs reference
 CASES = [c for c in gc.solve_cases()]
 
