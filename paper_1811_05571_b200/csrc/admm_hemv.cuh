@@ -67,20 +67,6 @@ __device__ __forceinline__ double2 hemv_sum_row(const double2* __restrict__ part
   return s;
 }
 
-// q = K r and ghat = g_ij - rho q on the 64 rows of tile-row I (one warp).
-__device__ __forceinline__ void hemv_finalize_rows(RowVecs rv, const double2* __restrict__ part, const HemvDesc& d,
-                                                   uint32_t I, uint64_t U, uint64_t P, double rho, int lane) {
-#pragma unroll
-  for (int h = 0; h < kHT / kWarp; ++h) {
-    const uint32_t r = h * kWarp + lane, row = I * kHT + r;
-    if (row >= d.m) continue;
-    const double2 s = hemv_sum_row(part, d, I, r, U, P);
-    const uint32_t o = d.x_off + row;
-    rv.q[o] = s;
-    rv.ghat[o] = csub(rv.gij[o], cscale(s, rho));
-  }
-}
-
 // Two complex elements of a tile row, widened to FP64 (c128: one 32-byte load; c64:
 // one 16-byte load), L1 no-allocate, L2 policy `pol` (createpolicy).
 template <typename S>
@@ -108,14 +94,10 @@ __device__ __forceinline__ double2 ld_masked(const double2* x, uint32_t i, uint3
 
 // keep: K fits in L2 next to the sweep's open strips -> evict_last (re-read next
 // iteration), else evict_first.
-template <typename S, int OCC, bool FUSE>
+template <typename S, int OCC>
 __global__ void __launch_bounds__(kCtaThreads, OCC)
 hemv_kernel(const S* __restrict__ Kp, const double2* __restrict__ X, double2* __restrict__ part,
-            const HemvDesc* __restrict__ hd, int nb, uint64_t U, int keep, unsigned* __restrict__ cnt,
-            RowVecs rv, const Params* __restrict__ prm) {
-  // FUSE: fused finalize.  Every contribution to tile-row I (an N segment of each
-  // warp, the H part of each tile (I2, I) below the diagonal) bumps cnt[I] after its
-  // partial is stored; the warp that completes the count finalizes the 64 rows.
+            const HemvDesc* __restrict__ hd, int nb, uint64_t U, int keep) {
   constexpr bool kPrefetch = OCC == 1;  // two tiles in registers only at one CTA per SM
   __shared__ double2 hbuf[2][kCtaWarps][kHT];
   uint64_t pol;
@@ -148,21 +130,6 @@ hemv_kernel(const S* __restrict__ Kp, const double2* __restrict__ X, double2* __
 #pragma unroll
   for (int k = 0; k < kHRows; ++k) accN[k] = make_double2(0.0, 0.0);
   uint32_t par = 0;
-  auto contribute = [&](uint32_t Ir) {  // warp-uniform: this warp's partial for tile-row Ir is stored
-    __threadfence();  // every lane's partial stores are visible device-wide before the count
-    __syncwarp();
-    unsigned last = 0;
-    if (lane == 0) {
-      const uint32_t urow = Ir * (Ir + 1) / 2;
-      const unsigned expect = kCtaWarps * seg_count(d.unit0 + urow, Ir + 1, U, P) + (d.nT - 1 - Ir);
-      last = atomicAdd(&cnt[d.cnt_off + Ir], 1u) == expect - 1;
-    }
-    if (__shfl_sync(0xffffffffu, last, 0)) {
-      __threadfence();
-      hemv_finalize_rows(rv, part, d, Ir, U, P, prm->rho, lane);
-      if (lane == 0) cnt[d.cnt_off + Ir] = 0;  // ready for the next iteration's launch
-    }
-  };
   // Tiles of all blocks are contiguous in unit order (k_off = unit0 * 64 * 64), so unit
   // x + 1 is the next 64 x 64 tile: its rows are loaded before tile x is reduced.
   const S* tp = Kp + x * (uint64_t)(kHT * kHT) + (uint64_t)(warp * kHRows) * kHT + lane * 2;
@@ -210,7 +177,6 @@ hemv_kernel(const S* __restrict__ Kp, const double2* __restrict__ X, double2* __
           for (int w = 1; w < kCtaWarps; ++w) s = cadd(s, hbuf[par][w][c]);
           part[d.part_off + ((uint64_t)d.n_units + u) * kHT + c] = s;
         }
-        if (FUSE) contribute(J);
       }
       par ^= 1u;  // the next tile writes the other buffer; this one is reused after a barrier
     }
@@ -240,7 +206,6 @@ hemv_kernel(const S* __restrict__ Kp, const double2* __restrict__ X, double2* __
       }
       if ((lane & 3) == 0)
         part[d.part_off + (uint64_t)(urow + seg) * kHT + warp * kHRows + (lane >> 2)] = a;
-      if (FUSE) contribute(I);
 #pragma unroll
       for (int k = 0; k < kHRows; ++k) accN[k] = make_double2(0.0, 0.0);
     }
@@ -450,7 +415,6 @@ hemv_bulk_kernel(const S* __restrict__ Kp, const double2* __restrict__ X, double
 // q = K r from the partials (tile-row N segments in CTA order, then the H parts of the
 // tiles below the diagonal in ascending tile-row order), ghat = g_ij - rho q
 // (the kQ stage of rows_finalize_kernel).
-// Unfused variant (default; ADMM_B200_HEMV_FUSE=1 finalizes inside hemv_kernel).
 // Grid: (cdiv(max rows, kHFinRows), blocks).
 constexpr int kHFinRows = 64;
 __global__ void __launch_bounds__(kHFinRows)

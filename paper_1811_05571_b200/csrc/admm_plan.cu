@@ -414,11 +414,10 @@ SlabFn<S> slab_fn_rb(int rpl, bool tr) {
   if (rpl == 2) return tr ? sweep_slab_kernel<S, 2, RB, true> : sweep_slab_kernel<S, 2, RB, false>;
   return tr ? sweep_slab_kernel<S, 4, RB, true> : sweep_slab_kernel<S, 4, RB, false>;
 }
-// 16-byte strip rows: tall strips (many rows per segment) in one CTA, slabs of 128 / 192 rows
+// 16-byte strip rows: tall strips (many rows per segment) in one CTA, 16 slabs of 192 rows
 template <typename S>
-SlabFn<S> slab_fn_rb16(int rpl, bool tr) {
-  if (rpl == 6) return tr ? sweep_slab_kernel<S, 6, 16, true> : sweep_slab_kernel<S, 6, 16, false>;
-  return tr ? sweep_slab_kernel<S, 4, 16, true> : sweep_slab_kernel<S, 4, 16, false>;
+SlabFn<S> slab_fn_rb16(int, bool tr) {
+  return tr ? sweep_slab_kernel<S, 6, 16, true> : sweep_slab_kernel<S, 6, 16, false>;
 }
 template <typename S>
 SlabFn<S> slab_fn(int rpl, uint32_t rb, bool tr) {
@@ -447,8 +446,7 @@ bool try_slab(admm_plan* p) {
     const uint32_t W = rb / 16 * (16 / sizeof(S));
     if (M * W > kWarp) continue;  // the D warp maps (replica, column) onto lanes
     for (uint32_t rpl : {2u, 1u, 4u, 6u}) {
-      if ((rpl == 6 || rb == 16) && !(rb == 16 && rpl >= 4)) continue;  // instantiated pairs
-      if (rb == 16 && rpl == 4 && !fR) continue;  // 24 x 128-row slabs measured slower than 16 x 192 (config 3)
+      if ((rpl == 6) != (rb == 16)) continue;  // 16-byte rows come with 192-row slabs (16 warps x 192 = 3072 rows)
       const uint32_t rpw = rpl * kWarp;
       if (fR && (uint32_t)fR != rpw) continue;
       uint32_t Ns = 0;
@@ -465,7 +463,7 @@ bool try_slab(admm_plan* p) {
         // 265 us) -- the per-strip DSMEM exchange sits on the D warps' critical path
         if (!fC && C > 1) continue;
         const uint32_t nw = (uint32_t)cdiv(Ns, C);
-        if (nw > (uint32_t)slab_max_warps((int)rpl, (int)rb) || (C > 1 && nw * (C - 1) >= Ns)) continue;  // no empty rank
+        if (nw > (uint32_t)kSlabMaxW || (C > 1 && nw * (C - 1) >= Ns)) continue;  // no empty rank
         const size_t fixed = slab_smem_bytes(0, nw, kSlabMaxD, rpw, rb, C, M, W, N);
         const size_t per = (size_t)nw * rpw * rb + nw * sizeof(uint64_t);
         const uint32_t ns = (uint32_t)std::min<size_t>((cap - fixed) / per, 8);
@@ -1061,7 +1059,7 @@ void factor_blocks(admm_plan* p, GramWork& w) {
                                                              p->hv[b].nT, p->dKp.as<S>() + p->hv[b].k_off);
     upload_desc(p->dhv, p->hv.data(), nb * sizeof(HemvDesc));
     const uint64_t u0 = p->gP.U;
-    p->gP.P = grid_for<S>(hemv_kernel<S, 1, false>, u0, p->num_sms);
+    p->gP.P = grid_for<S>(hemv_kernel<S, 1>, u0, p->num_sms);
     // complex64 K (streamed from HBM: configs 3/4): the bulk-copy ring variant, one CTA per
     // SM (35 -> 25 us on config 3); complex128 K (config 2, L2-resident between iterations):
     // the register variant (15.0 vs 18.4 us)
@@ -1125,10 +1123,9 @@ void enqueue_kapply(admm_plan* p, cudaStream_t s, Mid mid) {
                  p->dparams.as<Params>());
       return;
     }
-    auto fn = hemv_kernel<S, 1, false>;
+    auto fn = hemv_kernel<S, 1>;
     launch_pdl(fn, dim3((unsigned)p->gP.P), dim3(kCtaThreads), 0, s, p->dKp.as<S>(), p->dr.as<double2>(),
-               p->dkppart.as<double2>(), p->dhv.as<HemvDesc>(), nb, p->gP.U, p->kkeep ? 1 : 0,
-               (unsigned*)nullptr, row_vecs(p), p->dparams.as<Params>());
+               p->dkppart.as<double2>(), p->dhv.as<HemvDesc>(), nb, p->gP.U, p->kkeep ? 1 : 0);
     mid();
     launch_pdl(hemv_finalize_kernel, dim3((unsigned)cdiv(p->max_rows, kHFinRows), nb), dim3(kHFinRows), 0, s,
                  row_vecs(p), p->dkppart.as<double2>(), p->dhv.as<HemvDesc>(), p->gP.U, p->gP.P,
@@ -1158,10 +1155,10 @@ void enqueue_gq(admm_plan* p, cudaStream_t s) {
                (const double2*)p->dq.as<double2>(), p->dkppart.as<double2>(), (const HemvDesc*)p->dhv.as<HemvDesc>(),
                nb, p->gP.U, 0);
   } else {
-    auto fn = hemv_kernel<S, 1, false>;
+    auto fn = hemv_kernel<S, 1>;
     launch_pdl(fn, dim3((unsigned)p->gP.P), dim3(kCtaThreads), 0, s, (const S*)p->dGp.as<S>(),
                (const double2*)p->dq.as<double2>(), p->dkppart.as<double2>(), (const HemvDesc*)p->dhv.as<HemvDesc>(),
-               nb, p->gP.U, 0, (unsigned*)nullptr, row_vecs(p), (const Params*)p->dparams.as<Params>());
+               nb, p->gP.U, 0);
   }
   launch_pdl(hemv_gq_kernel, dim3((unsigned)cdiv(p->max_rows, kHFinRows), nb), dim3(kHFinRows), 0, s,
              (const double2*)p->dkppart.as<double2>(), (const HemvDesc*)p->dhv.as<HemvDesc>(), p->gP.U, p->gP.P,

@@ -44,11 +44,6 @@ __host__ __device__ constexpr uint32_t slab_swz(uint32_t row) {
 }
 constexpr int kSlabMaxW = 16;        // compute warps per CTA (+ D warps)
 constexpr int kSlabThreads = (kSlabMaxW + 4) * kWarp;  // + up to 4 D warps; 20 warps keep the 96-register cap
-// 16-byte strip rows with 128-row slabs: 24 compute warps (3072 rows of a complex64 strip in
-// one CTA) + 4 D warps at a 72-register cap -- the narrow-strip passes are latency-bound, so
-// warps, not registers, are what they need.
-__host__ __device__ constexpr int slab_max_warps(int rpl, int rb) { return rb == 16 && rpl == 4 ? 24 : kSlabMaxW; }
-__host__ __device__ constexpr int slab_max_threads(int rpl, int rb) { return (slab_max_warps(rpl, rb) + 4) * kWarp; }
 
 struct SlabDesc {
   uint32_t rep;    // replica (row block) i
@@ -218,7 +213,7 @@ __host__ __device__ inline bool slab_lag_ok(uint32_t L, uint32_t ND) {
 // 20 warps x 32 lanes: the register allocation granularity (4 warps) caps this at 96
 // registers per thread (65536 / (20 x 32)).
 template <typename S, int RPL, int RB, bool kTrace>
-__global__ void __launch_bounds__(slab_max_threads(RPL, RB), 1)
+__global__ void __launch_bounds__(kSlabThreads, 1)
 sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, const BlockDesc* __restrict__ blocks,
                   const SweepDesc* __restrict__ segs, uint32_t M, uint32_t N, uint32_t n_meas, uint64_t U, uint32_t NS,
                   uint32_t L, uint32_t Ns, uint32_t NW, const double2* __restrict__ q, ColVecs cv,

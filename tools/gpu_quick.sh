@@ -11,6 +11,6 @@ import json
 for c in (4,2,3):
     try:
         d=json.loads(open('$O/${TAG}_bench_cfg%d.json'%c).read().strip().splitlines()[-1])
-        print(c, round(d['value'],1),'it/s e2e',round(d['e2e']['value'],1),'setup',round(d['run']['setup_s'],3),[round(x,3) for x in d['run']['setup_phase_s']], d['clocks']['sm_mhz'])
+        print(c, round(d['value'],1),'it/s e2e',round(d['e2e']['value'],1),'setup',round(d['run']['setup_s'],3), d['clocks']['sm_mhz'])
     except Exception as e: print(c,'ERR',e)
 PY
