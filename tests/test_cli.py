@@ -61,6 +61,80 @@ def test_cli_usage_and_validation_errors(tmp_path):
     assert r.returncode == 2 and "no CPU path" in r.stderr
 
 
+def test_cli_reference_cases_without_a_device(tmp_path):
+    """tests/test_cli.cpp:63-84, 105-117 restated: the cases that end before the device is needed."""
+    build()
+    d = tmp_path / "gen"
+    r = run("gen", "--nm", "12", "--np", "30", "--k", "4", "--snr", "30", "--seed", "7", "--kind", "random-phase",
+            "--out", str(d))
+    assert r.returncode == 0, r.stderr
+    for name in ("H.cmat", "g.cmat", "truth.cmat", "manifest.json"):
+        assert (d / name).exists()
+    import paper_1811_05571_b200 as admm
+    h = admm.read_cmat(d / "H.cmat")
+    assert h.shape == (12, 30) and np.allclose(np.abs(h), np.abs(h[0, 0]))  # random-phase: constant modulus
+    bad = str(tmp_path / "gen_bad")
+    assert run("gen", "--nm", "12", "--np", "30", "--k", "4", "--out", bad).returncode == 2      # no seed
+    assert run("gen", "--nm", "12", "--np", "200", "--k", "300", "--seed", "1", "--out", bad).returncode == 2
+    base = ["--nm", "12", "--np", "36", "--k", "3", "--seed", "5", "--out", str(tmp_path / "solve_bad")]
+    assert run("solve", "--method", "consensus", *base).returncode == 2                 # missing --m
+    assert run("solve", "--method", "sectioning", "--m", "3", *base).returncode == 2    # wrong division
+    assert run("solve", "--method", "hybrid", "--m", "3", *base).returncode == 2        # missing --n
+    assert run("solve", "--method", "reference", "--m", "2", *base).returncode == 2
+    r = run("solve", "--method", "consensus", "--m", "5", *base)                        # non-divisible, no --ragged
+    assert r.returncode == 2 and "error:" in r.stderr
+    assert run("solve", "--method", "reference", "--problem", "/tmp/nowhere", *base).returncode == 2
+
+
+@pytest.mark.gpu
+def test_cli_reference_cases_on_device(tmp_path):
+    """tests/test_cli.cpp:86-103, 119-165, 207-234 restated against tools/admmsplit_gpu."""
+    build()
+    d = tmp_path / "solve_ref"
+    r = run("solve", "--method", "reference", "--nm", "12", "--np", "36", "--k", "3", "--seed", "5", "--rho", "1",
+            "--lambda", "0.01", "--iters", "7", "--out", str(d))
+    assert r.returncode == 0, r.stderr
+    trace = open(d / "trace.csv").read()
+    assert trace.count("\n") == 8 and trace.startswith("iteration,primal_norm,dual_norm,objective")
+    met = open(d / "metrics.json").read()
+    assert '"schema_version"' in met and '"nmse"' in met and (d / "solution.cmat").exists()
+    assert open(d / "ledger.csv").read().count("\n") == 1  # single node: header only
+    # hybrid ledger = closed form: 4 * (12 / 3) + 2 * (36 / 4) = 34 per node and iteration
+    d = tmp_path / "solve_hybrid"
+    r = run("solve", "--method", "hybrid", "--m", "3", "--n", "4", "--nm", "12", "--np", "36", "--k", "3", "--seed", "5",
+            "--rho", "1", "--lambda", "0.01", "--iters", "3", "--out", str(d))
+    assert r.returncode == 0, r.stderr
+    rows = list(csv.reader(open(d / "ledger.csv")))[1:]
+    assert len(rows) == 12 * 3
+    for node, it, rec, sent, conv in rows:
+        assert int(rec) + int(sent) == 34 and conv == "sender_once_broadcast"
+    # byte-deterministic across runs and --threads values
+    outs = []
+    for k, threads in enumerate(("1", "2")):
+        dk = tmp_path / f"det{k}"
+        r = run("solve", "--method", "hybrid", "--m", "2", "--n", "3", "--nm", "12", "--np", "36", "--k", "3", "--seed",
+                "11", "--rho", "1", "--lambda", "0.02", "--iters", "5", "--fingerprint", "--threads", threads, "--out",
+                str(dk))
+        assert r.returncode == 0, r.stderr
+        outs.append((dk, r.stdout[r.stdout.index("fingerprint "):][:28]))
+    for name in ("solution.cmat", "trace.csv", "ledger.csv", "metrics.json"):
+        assert open(outs[0][0] / name, "rb").read() == open(outs[1][0] / name, "rb").read()
+    assert outs[0][1] == outs[1][1]
+    # compare: one entry per method spec; a single method is allowed
+    out = tmp_path / "compare.json"
+    r = run("compare", "--methods", "reference,consensus:3,sectioning:4,hybrid:3x4", "--nm", "12", "--np", "36", "--k",
+            "3", "--seed", "5", "--rho", "1", "--lambda", "0.01", "--iters", "20", "--out", str(out))
+    assert r.returncode == 0, r.stderr
+    c = json.load(open(out))
+    assert c["schema_version"] == "1" and len(c["entries"]) == 4 and "winners" in c
+    assert run("compare", "--methods", "reference", "--nm", "12", "--np", "36", "--k", "3", "--seed", "5", "--iters", "5",
+               "--rho", "1", "--out", str(tmp_path / "single.json")).returncode == 0
+    # numerical blow-up: exit code 3 with the last good iteration
+    r = run("solve", "--method", "consensus", "--m", "2", "--nm", "12", "--np", "36", "--k", "3", "--seed", "5", "--rho",
+            "1", "--lambda", "0.01", "--scl", "1e300", "--iters", "3", "--out", str(tmp_path / "blowup"))
+    assert r.returncode == 3 and "last good iteration" in r.stderr
+
+
 @pytest.mark.gpu
 def test_cli_solve_writes_the_reference_report_files(tmp_path):
     import paper_1811_05571_b200 as admm
