@@ -214,7 +214,7 @@ struct admm_plan {
   std::vector<admm_plan*> subs;
   // support schedule (5, admm_sparse.cuh): column-major H, packed G = H H^H, a = H v
   DevBuf dHc, dhcoff, dhcld, dGp, dgq, danew, daold, dnzcnt, dnzlist, dnnz, dnnz_tot;
-  uint32_t nzstride = 0, supgx = 1, sup_np = 0, sup_rgx = 1;
+  uint32_t nzstride = 0, supgx = 1, sup_np = 0, sup_rgx = 1, sup_chunks = 16;
   size_t res_smem = 0;
   uint64_t trace_cap = 0;
   cudaGraphExec_t exec = nullptr;
@@ -1169,7 +1169,7 @@ void enqueue_gq(admm_plan* p, cudaStream_t s) {
 void enqueue_support_rows(admm_plan* p, cudaStream_t s, bool first) {
   support_rows_kernel<<<dim3(p->sup_rgx, (unsigned)p->Mr), kCtaThreads, 0, s>>>(
       row_vecs(p), p->dblocks.as<BlockDesc>(), p->dgblocks.as<BlockDesc>(), (uint32_t)p->Nc, p->sup_np,
-      p->danew.as<double2>(), p->mvec_total, p->daold.as<double2>(), p->dgq.as<double2>(), first ? 1 : 0,
+      p->danew.as<double2>(), p->mvec_total, p->sup_chunks, p->daold.as<double2>(), p->dgq.as<double2>(), first ? 1 : 0,
       p->dored.as<double>());
 }
 
@@ -1195,7 +1195,7 @@ void enqueue_iteration_support(admm_plan* p, cudaStream_t s, bool with_objective
       p->dv.as<double2>(), p->dblocks.as<BlockDesc>(), p->dnzcnt.as<uint32_t>(), p->zgx, p->dnzlist.as<uint32_t>(),
       p->nzstride, p->dnnz.as<uint32_t>(), p->dnnz_tot.as<unsigned long long>());
   mark(3);
-  support_a_kernel<S><<<dim3(p->supgx, (unsigned)nb, kSupChunks), kSupThreads, 0, s>>>(
+  support_a_kernel<S><<<dim3(p->supgx, (unsigned)nb, p->sup_chunks), kSupThreads, 0, s>>>(
       p->dHc.as<S>(), p->dhcoff.as<uint64_t>(), p->dhcld.as<uint32_t>(), p->dblocks.as<BlockDesc>(),
       p->dv.as<double2>(), p->dnzlist.as<uint32_t>(), p->nzstride, p->dnnz.as<uint32_t>(), p->danew.as<double2>(),
       p->mvec_total);
@@ -1238,9 +1238,11 @@ void build_support(admm_plan* p) {
   p->dnnz.alloc(p->Nc * sizeof(uint32_t));
   p->dnnz_tot.alloc(sizeof(unsigned long long));
   p->dgq.alloc(p->mvec_total * 16);
-  p->danew.alloc(p->mvec_total * 16 * kSupChunks);  // column-chunk partials of a'
-  p->daold.alloc(p->mvec_total * 16);
   p->supgx = (uint32_t)cdiv(p->max_rows, kSupTile);
+  // column chunks: ~4 CTAs of support_a per SM (a whole number of waves when it divides)
+  p->sup_chunks = (uint32_t)std::min<uint64_t>(kSupMaxChunks, std::max<uint64_t>(1, cdiv((uint64_t)4 * p->num_sms, p->supgx * nb)));
+  p->danew.alloc(p->mvec_total * 16 * p->sup_chunks);  // column-chunk partials of a'
+  p->daold.alloc(p->mvec_total * 16);
   while ((1u << p->sup_np) < p->Nc) ++p->sup_np;
   p->sup_rgx = (uint32_t)std::max<uint64_t>(1, cdiv(p->max_rowblock, kCtaThreads >> p->sup_np));
   p->dored.alloc((size_t)std::max<uint64_t>(p->dored.bytes / sizeof(double), (uint64_t)p->sup_rgx * p->Mr) *

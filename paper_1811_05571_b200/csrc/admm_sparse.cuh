@@ -95,27 +95,29 @@ support_compact_kernel(const double2* __restrict__ v, const BlockDesc* __restric
 }
 
 // a'_b = H_b v' over the support of segment j (ascending columns).  Grid (row tiles of
-// kSupTile rows, local blocks, kSupChunks column chunks): thread t owns kSupRPT consecutive
+// kSupTile rows, local blocks, column chunks): thread t owns kSupRPT consecutive
 // rows (one 32/64-byte load per support column), kSupUnroll columns in flight, so a CTA
 // keeps ~kSupUnroll x 8 KiB of the column-major H in flight.  Column chunk c of the
-// support list writes its partial; support_rows_kernel adds the kSupChunks partials of a
+// support list writes its partial; support_rows_kernel adds the chunks' partials of a
 // row in chunk order (fixed order: bit-reproducible).
 constexpr int kSupThreads = 256;
 constexpr int kSupRPT = 4;                          // rows per thread
 constexpr int kSupTile = kSupThreads * kSupRPT;     // rows per CTA
-constexpr int kSupChunks = 16;                      // column chunks of the support list
+constexpr int kSupMaxChunks = 64;                   // column chunks of the support list: chosen per plan so that the
+                                                    // grid is ~4 CTAs (32 warps) per SM -- with 16 chunks (1-2 CTAs per
+                                                    // SM) the dense early iterations of config 4 ran at 3.5 TB/s
 template <typename S>
 __global__ void __launch_bounds__(kSupThreads)
 support_a_kernel(const S* __restrict__ Hc, const uint64_t* __restrict__ coff, const uint32_t* __restrict__ ldc,
                  const BlockDesc* __restrict__ blocks, const double2* __restrict__ v, const uint32_t* __restrict__ list,
                  uint32_t list_stride, const uint32_t* __restrict__ nnz, double2* __restrict__ apart,
                  uint64_t chunk_stride) {
-  const uint32_t b = blockIdx.y, chunk = blockIdx.z;
+  const uint32_t b = blockIdx.y, chunk = blockIdx.z, chunks = gridDim.z;
   const BlockDesc bd = blocks[b];
   const uint32_t row0 = blockIdx.x * kSupTile + threadIdx.x * kSupRPT;
   if (blockIdx.x * kSupTile >= bd.rows) return;
   const uint32_t n = nnz[bd.jl];
-  const uint32_t k0 = (uint32_t)((uint64_t)n * chunk / kSupChunks), k1 = (uint32_t)((uint64_t)n * (chunk + 1) / kSupChunks);
+  const uint32_t k0 = (uint32_t)((uint64_t)n * chunk / chunks), k1 = (uint32_t)((uint64_t)n * (chunk + 1) / chunks);
   const uint32_t* lj = list + (uint64_t)bd.jl * list_stride;
   const S* hb = Hc + coff[b] + row0;
   const uint32_t L = ldc[b];
@@ -124,7 +126,6 @@ support_a_kernel(const S* __restrict__ Hc, const uint64_t* __restrict__ coff, co
   double2 acc[kSupRPT];
 #pragma unroll
   for (int e = 0; e < kSupRPT; ++e) acc[e] = make_double2(0.0, 0.0);
-  using Vec = typename std::conditional<sizeof(S) == 8, uint4, V256>::type;  // kSupRPT elements of S
   uint32_t k = k0;
   for (; k + kSupUnroll <= k1; k += kSupUnroll) {
     uint32_t xs[kSupUnroll];
@@ -136,12 +137,10 @@ support_a_kernel(const S* __restrict__ Hc, const uint64_t* __restrict__ coff, co
       if (ok) {
         const S* p = hb + (uint64_t)xs[u] * L;
         if constexpr (sizeof(S) == 8) {
-          const uint4 w = __ldcs(reinterpret_cast<const uint4*>(p));
-          const uint4 w2 = __ldcs(reinterpret_cast<const uint4*>(p) + 1);
-          h[u][0] = make_float2(__uint_as_float(w.x), __uint_as_float(w.y));
-          h[u][1] = make_float2(__uint_as_float(w.z), __uint_as_float(w.w));
-          h[u][2] = make_float2(__uint_as_float(w2.x), __uint_as_float(w2.y));
-          h[u][3] = make_float2(__uint_as_float(w2.z), __uint_as_float(w2.w));
+          const V256 w = ld_stream256<kEvictFirst>(p);  // the thread's 4 rows in one 32-byte load
+#pragma unroll
+          for (int e = 0; e < kSupRPT; ++e)
+            h[u][e] = make_float2(__uint_as_float((unsigned)(w.w[e] & 0xffffffffu)), __uint_as_float((unsigned)(w.w[e] >> 32)));
         } else {
           const V256 w = ld_stream256<kEvictFirst>(p);
           const V256 w2 = ld_stream256<kEvictFirst>(p + 2);
@@ -169,7 +168,6 @@ support_a_kernel(const S* __restrict__ Hc, const uint64_t* __restrict__ coff, co
 #pragma unroll
       for (int e = 0; e < kSupRPT; ++e) cmac(acc[e], Store<S>::widen(hb[(uint64_t)x * L + e]), vx);
   }
-  (void)sizeof(Vec);
   double2* dst = apart + chunk * chunk_stride + bd.mvec_off;
 #pragma unroll
   for (int e = 0; e < kSupRPT; ++e)
@@ -182,7 +180,7 @@ support_a_kernel(const S* __restrict__ Hc, const uint64_t* __restrict__ coff, co
 __global__ void __launch_bounds__(kCtaThreads)
 support_rows_kernel(RowVecs rv, const BlockDesc* __restrict__ blocks, const BlockDesc* __restrict__ gblocks,
                     uint32_t N, uint32_t np_log2, const double2* __restrict__ apart, uint64_t chunk_stride,
-                    double2* __restrict__ aold, const double2* __restrict__ gq, int first, double* __restrict__ ored) {
+                    uint32_t chunks, double2* __restrict__ aold, const double2* __restrict__ gq, int first, double* __restrict__ ored) {
   __shared__ double2 sa[kCtaThreads];
   __shared__ double sm[kCtaWarps];
   const uint32_t i = blockIdx.y;
@@ -198,7 +196,7 @@ support_rows_kernel(RowVecs rv, const BlockDesc* __restrict__ blocks, const Bloc
     if (!first) {
       a = apart[o];  // a'_b = the column chunks' partials, in chunk order
 #pragma unroll 4
-      for (int c = 1; c < kSupChunks; ++c) a = cadd(a, apart[(uint64_t)c * chunk_stride + o]);
+      for (uint32_t c = 1; c < chunks; ++c) a = cadd(a, apart[(uint64_t)c * chunk_stride + o]);
       w = csub(csub(cscale(a, 2.0), aold[o]), gq[o]);
       aold[o] = a;
     }
