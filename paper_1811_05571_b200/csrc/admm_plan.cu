@@ -213,7 +213,7 @@ struct admm_plan {
   struct Dist* dist = nullptr;
   std::vector<admm_plan*> subs;
   // support schedule (5, admm_sparse.cuh): column-major H, packed G = H H^H, a = H v
-  DevBuf dHc, dhcoff, dhcld, dGp, dgq, danew, daold, dnzcnt, dnzlist, dnnz, dnnz_tot;
+  DevBuf dHc, dhcoff, dhcld, danew, daold, dnzcnt, dnzlist, dnnz, dnnz_tot;
   uint32_t nzstride = 0, supgx = 1, sup_np = 0, sup_rgx = 1, sup_chunks = 16;
   size_t res_smem = 0;
   uint64_t trace_cap = 0;
@@ -997,15 +997,7 @@ void factor_blocks(admm_plan* p, GramWork& w) {
     p->dkcnt.alloc(std::max<uint64_t>(co, 1) * sizeof(unsigned));
     CK(cudaMemset(p->dkcnt.p, 0, std::max<uint64_t>(co, 1) * sizeof(unsigned)));
   }
-  if (p->schedule == 5) {  // G = rho I + H H^H - rho I = H H^H, packed before the in-place inverse
-    if (!p->kpacked) throw Fail{ADMM_E_PARAMETER, "support schedule needs the packed Hermitian apply"};
-    p->dGp.alloc(kpacked_elems * sizeof(S));
-    for (uint64_t b = 0; b < nb; ++b)
-      k_pack_kernel<S><<<p->num_sms * 4, 256, 0, p->stream>>>(A.as<double2>(), p->gram[b].a_off, p->hv[b].m,
-                                                             p->hv[b].nT, p->dGp.as<S>() + p->hv[b].k_off,
-                                                             p->cfg.rho);
-    CK(cudaGetLastError());
-  }
+  if (p->schedule == 5 && !p->kpacked) throw Fail{ADMM_E_PARAMETER, "support schedule needs the packed Hermitian apply"};
   const unsigned gx = (unsigned)std::min<uint64_t>(cdiv(p->max_m, 256), 8);
   {  // blocked Gauss-Jordan: per 64-wide panel the diagonal inverse, the row panel, the rank-64 update
     const uint32_t mpmax = (uint32_t)round_up(p->max_m, kFT), np = mpmax / kFT;
@@ -1144,32 +1136,11 @@ void enqueue_kapply(admm_plan* p, cudaStream_t s) {
   enqueue_kapply<S>(p, s, [] {});
 }
 
-// Support schedule: (G q) of every block from the packed G tiles (same kernels as K).
-template <typename S>
-void enqueue_gq(admm_plan* p, cudaStream_t s) {
-  const int nb = (int)p->blocks.size();
-  if (p->hemv_bulk) {
-    auto fb = hemv_bulk_kernel<S, 1>;
-    const size_t sm = hemv_bulk_smem<S, 1>(p->max_rows);
-    launch_pdl(fb, dim3((unsigned)p->gP.P), dim3(kCtaThreads), sm, s, (const S*)p->dGp.as<S>(),
-               (const double2*)p->dq.as<double2>(), p->dkppart.as<double2>(), (const HemvDesc*)p->dhv.as<HemvDesc>(),
-               nb, p->gP.U, 0);
-  } else {
-    auto fn = hemv_kernel<S, 1>;
-    launch_pdl(fn, dim3((unsigned)p->gP.P), dim3(kCtaThreads), 0, s, (const S*)p->dGp.as<S>(),
-               (const double2*)p->dq.as<double2>(), p->dkppart.as<double2>(), (const HemvDesc*)p->dhv.as<HemvDesc>(),
-               nb, p->gP.U, 0);
-  }
-  launch_pdl(hemv_gq_kernel, dim3((unsigned)cdiv(p->max_rows, kHFinRows), nb), dim3(kHFinRows), 0, s,
-             (const double2*)p->dkppart.as<double2>(), (const HemvDesc*)p->dhv.as<HemvDesc>(), p->gP.U, p->gP.P,
-             p->dgq.as<double2>());
-}
-
-// Support schedule rows step: w' = 2a' - a - Gq, g_ij, r; objective rows (first: r = g_ij).
+// Support schedule rows step: w' = 2a' - a - (r - rho q), g_ij, r; objective rows (first: r = g_ij).
 void enqueue_support_rows(admm_plan* p, cudaStream_t s, bool first) {
   support_rows_kernel<<<dim3(p->sup_rgx, (unsigned)p->Mr), kCtaThreads, 0, s>>>(
       row_vecs(p), p->dblocks.as<BlockDesc>(), p->dgblocks.as<BlockDesc>(), (uint32_t)p->Nc, p->sup_np,
-      p->danew.as<double2>(), p->mvec_total, p->sup_chunks, p->daold.as<double2>(), p->dgq.as<double2>(), first ? 1 : 0,
+      p->danew.as<double2>(), p->mvec_total, p->sup_chunks, p->daold.as<double2>(), p->dparams.as<Params>(), first ? 1 : 0,
       p->dored.as<double>());
 }
 
@@ -1186,27 +1157,25 @@ void enqueue_iteration_support(admm_plan* p, cudaStream_t s, bool with_objective
   gemv_h_kernel<S, kVH, kEvictFirst><<<(unsigned)p->gH.P, kCtaThreads, 0, s>>>(
       p->dH.as<S>(), p->dq.as<double2>(), p->dzpart.as<double2>(), p->dhH.as<MatDesc>(), nb, p->gH.U);
   mark(1);
-  enqueue_gq<S>(p, s);
-  mark(2);
   zupdate_kernel<CH><<<dim3(p->zgx, N), kCtaThreads, 0, s>>>(
       col_vecs(p), p->dzpart.as<double2>(), p->dhH.as<MatDesc>(), p->dblocks.as<BlockDesc>(), M, N, p->gH.U,
       p->gH.P, p->dparams.as<Params>(), p->dred.as<double>(), p->dstate.as<IterState>(), p->dnzcnt.as<uint32_t>());
   support_compact_kernel<<<dim3(p->zgx, N), kCtaThreads, 0, s>>>(
       p->dv.as<double2>(), p->dblocks.as<BlockDesc>(), p->dnzcnt.as<uint32_t>(), p->zgx, p->dnzlist.as<uint32_t>(),
       p->nzstride, p->dnnz.as<uint32_t>(), p->dnnz_tot.as<unsigned long long>());
-  mark(3);
+  mark(2);
   support_a_kernel<S><<<dim3(p->supgx, (unsigned)nb, p->sup_chunks), kSupThreads, 0, s>>>(
       p->dHc.as<S>(), p->dhcoff.as<uint64_t>(), p->dhcld.as<uint32_t>(), p->dblocks.as<BlockDesc>(),
       p->dv.as<double2>(), p->dnzlist.as<uint32_t>(), p->nzstride, p->dnnz.as<uint32_t>(), p->danew.as<double2>(),
       p->mvec_total);
-  mark(4);
+  mark(3);
   enqueue_support_rows(p, s, false);
   finalize_kernel<<<1, kCtaThreads, 0, s>>>(p->dred.as<double>(), p->nz, p->dored.as<double>(),
                                             with_objective ? p->sup_rgx * M : 0, p->dparams.as<Params>(),
                                             p->dtrace.as<double>(), p->trace_cap, p->dstate.as<IterState>());
-  mark(5);
-  enqueue_kapply<S>(p, s, [&] { mark(6); });
-  mark(7);
+  mark(4);
+  enqueue_kapply<S>(p, s, [&] { mark(5); });
+  mark(6);
   CK(cudaGetLastError());
 }
 
@@ -1237,7 +1206,6 @@ void build_support(admm_plan* p) {
   p->dnzlist.alloc((uint64_t)p->nzstride * p->Nc * sizeof(uint32_t));
   p->dnnz.alloc(p->Nc * sizeof(uint32_t));
   p->dnnz_tot.alloc(sizeof(unsigned long long));
-  p->dgq.alloc(p->mvec_total * 16);
   p->supgx = (uint32_t)cdiv(p->max_rows, kSupTile);
   // column chunks: ~4 CTAs of support_a per SM (a whole number of waves when it divides)
   p->sup_chunks = (uint32_t)std::min<uint64_t>(kSupMaxChunks, std::max<uint64_t>(1, cdiv((uint64_t)4 * p->num_sms, p->supgx * nb)));
@@ -1706,7 +1674,7 @@ void upload_g(admm_plan* p, const double* g) {
 void reset_state(admm_plan* p) {
   cudaStream_t s = p->stream;
   for (DevBuf* d : {&p->du, &p->ds, &p->dc, &p->dv, &p->dvprev, &p->dgij, &p->dr, &p->dq, &p->dhs, &p->danew,
-                    &p->daold, &p->dgq})
+                    &p->daold})
     if (d->p) CK(cudaMemsetAsync(d->p, 0, d->bytes, s));
   CK(cudaMemsetAsync(p->ghat_ptr, 0, p->mvec_total * 16 * p->batch, s));
   CK(cudaMemsetAsync(p->outbox_ptr, 0, p->outbox_total * 16, s));
@@ -2215,7 +2183,7 @@ admm_status admm_plan_set_stream(admm_plan* p, void* stream) {
 }
 
 uint32_t admm_plan_kernel_count(const admm_plan* p) {
-  return !p ? 7 : p->schedule == 4 ? 1 : p->schedule == 2 ? 4 : 7;  // (schedule 5: 7 launch groups)
+  return !p ? 7 : p->schedule == 4 ? 1 : p->schedule == 2 ? 4 : p->schedule == 5 ? 6 : 7;
 }
 
 admm_status admm_plan_set_lambdas(admm_plan* p, const double* lambdas) {
@@ -2273,7 +2241,7 @@ admm_status admm_plan_profile(admm_plan* p, uint64_t iters, const char** names, 
     if (is_dist(p)) throw Fail{ADMM_E_STATE, "profile: single-GPU plans only"};
     const int nk = (int)admm_plan_kernel_count(p);
     static const char* kNamesR[1] = {"resident(iteration)"};
-    static const char* kNamesU[7] = {"gemv_h(H,q)", "hemv(G,q)+gq", "zupdate+support_list", "support_a(Hc,v)",
+    static const char* kNamesU[6] = {"gemv_h(H,q)", "zupdate+support_list", "support_a(Hc,v)",
                                      "support_rows+finalize", "hemv(Kpacked,r)", "hemv_finalize(q)"};
     const char* const* kn = p->schedule == 5   ? kNamesU
                             : p->schedule == 4 ? kNamesR
@@ -2327,7 +2295,7 @@ admm_status admm_plan_get_info(const admm_plan* p, admm_plan_info* info) {
     r.h_stream_bytes_per_iter = 2 * hb;
     r.bytes_per_iter = 2 * hb + kb_dense + vb;  // two-pass algorithmic bytes
     // resident: ONE launch runs all the iterations of an enqueue (reported as 0 per iteration)
-    r.launches_per_iter = p->schedule == 5 ? 10 : p->schedule == 4 ? 0 : p->schedule == 3 ? 7 : p->schedule == 2 ? (p->trace_obj ? (p->obj_pass ? 7 : 6) : 4) : (p->trace_obj ? 9 : 7);
+    r.launches_per_iter = p->schedule == 5 ? 8 : p->schedule == 4 ? 0 : p->schedule == 3 ? 7 : p->schedule == 2 ? (p->trace_obj ? (p->obj_pass ? 7 : 6) : 4) : (p->trace_obj ? 9 : 7);
     r.schedule = (uint64_t)p->schedule;
     r.grid_sweep = p->gS.P;
     // support schedule: one dense pass + K + G (+ the data-dependent support columns, admm_plan_read 5)

@@ -8,8 +8,10 @@
 // so the next product the reference forms, w' = H_b c' (gram.hpp:71-77 inside the
 // Woodbury solve), is exactly
 //     w' = 2 a' - a - G_b q_b,      a = H_b v,  a' = H_b v',  G_b = H_b H_b^H.
-// G_b is the Gram matrix the setup already forms for the Woodbury factor (gram.hpp:92-122);
-// it is kept (packed Hermitian tiles, like K) and applied like K.  a' = H_b v' touches
+// G_b q_b needs no product: q_b = K_b r_b with K_b = (rho I + G_b)^-1 (gram.hpp:63-78), so
+//     G_b q_b = r_b - rho q_b
+// from the r and q the iteration already holds (exact up to the rounding of the stored K,
+// the same rounding the q-form's u = c + H^H q already carries).  a' = H_b v' touches
 // only the columns where v' != 0: soft thresholding makes v sparse (config 4: ~1e3 of
 // 262144 columns), and a skipped term is an exact zero (H is validated finite), so a'
 // is bit-identical to the dense product in the same (ascending-column) order.  With v
@@ -17,11 +19,10 @@
 // the two-pass schedule.  Per iteration:
 //
 //   z = H^H q                 gemv_h_kernel (dense pass, row-major H)
-//   Gq = G q                  hemv (packed G) + gq finalize
 //   u, v', s', c', residuals  zupdate_kernel (+ per-CTA support counts)
 //   support list of v'        support_compact_kernel (ascending, deterministic)
 //   a' = H v' on the support  support_a_kernel (column-major copy of H)
-//   w', r, objective rows     support_rows_kernel
+//   w' (Gq = r - rho q), r, objective rows     support_rows_kernel
 //   trace[k]                  finalize_kernel
 //   q = K r, ghat             hemv (packed K) + hemv_finalize
 // Bit-reproducible: fixed-order sums, no atomics.
@@ -175,12 +176,13 @@ support_a_kernel(const S* __restrict__ Hc, const uint64_t* __restrict__ coff, co
 }
 
 // Per row r of row block i (NP = 2^np_log2 lanes per row, lane j = column block): for every
-// local block b = (i, j): w' = 2 a' - a - (G q)_b (first: w' = 0), a <- a', g_ij, r = g_ij - w';
+// local block b = (i, j): w' = 2 a' - a - (r - rho q)_b (first: w' = 0), a <- a', g_ij, r = g_ij - w';
 // then |sum_j a'_ij - g_i|^2 (ascending j) into per-CTA objective partials.
 __global__ void __launch_bounds__(kCtaThreads)
 support_rows_kernel(RowVecs rv, const BlockDesc* __restrict__ blocks, const BlockDesc* __restrict__ gblocks,
                     uint32_t N, uint32_t np_log2, const double2* __restrict__ apart, uint64_t chunk_stride,
-                    uint32_t chunks, double2* __restrict__ aold, const double2* __restrict__ gq, int first, double* __restrict__ ored) {
+                    uint32_t chunks, double2* __restrict__ aold, const Params* __restrict__ prm, int first,
+                    double* __restrict__ ored) {
   __shared__ double2 sa[kCtaThreads];
   __shared__ double sm[kCtaWarps];
   const uint32_t i = blockIdx.y;
@@ -197,7 +199,8 @@ support_rows_kernel(RowVecs rv, const BlockDesc* __restrict__ blocks, const Bloc
       a = apart[o];  // a'_b = the column chunks' partials, in chunk order
 #pragma unroll 4
       for (uint32_t c = 1; c < chunks; ++c) a = cadd(a, apart[(uint64_t)c * chunk_stride + o]);
-      w = csub(csub(cscale(a, 2.0), aold[o]), gq[o]);
+      const double2 gq = csub(rv.r[o], cscale(rv.q[o], prm->rho));  // G q = (K^-1 - rho I) q = r - rho q
+      w = csub(csub(cscale(a, 2.0), aold[o]), gq);
       aold[o] = a;
     }
     const double2 gij = gij_row(rv, gblocks, bd, N, row);
@@ -214,17 +217,6 @@ support_rows_kernel(RowVecs rv, const BlockDesc* __restrict__ blocks, const Bloc
   }
   const double r = block_sum<kCtaThreads>(q, sm);
   if (threadIdx.x == 0) ored[blockIdx.y * gridDim.x + blockIdx.x] = r;
-}
-
-// (G q)[row] of every block from the hemv partials (the fixed order of hemv_finalize).
-__global__ void __launch_bounds__(kHFinRows)
-hemv_gq_kernel(const double2* __restrict__ part, const HemvDesc* __restrict__ hd, uint64_t U, uint64_t P,
-               double2* __restrict__ out) {
-  const HemvDesc d = hd[blockIdx.y];
-  pdl_enter();
-  const uint32_t row = blockIdx.x * blockDim.x + threadIdx.x;
-  if (row >= d.m) return;
-  out[d.x_off + row] = hemv_sum_row(part, d, row / kHT, row % kHT, U, P);
 }
 
 }  // namespace admm
