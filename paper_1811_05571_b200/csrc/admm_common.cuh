@@ -51,6 +51,27 @@ __device__ __forceinline__ double2 soft_threshold_fast(double2 a, double kappa, 
   return make_double2(0.0, 0.0);
 }
 
+// Latency-optimised variant for the slab sweep's D warps (4 active lanes, the result gates the
+// next (A) pass): |a|^2 clearly above kappa^2 and inside the range where x^2 + y^2 neither
+// overflows nor loses bits takes  a (1 - kappa rsqrt(|a|^2))  -- one rsqrt (MUFU.RSQ64H + Newton)
+// instead of hypot and a division, equal to the reference expression to ~2 ulp (the soft
+// threshold is continuous, so an ulp near |a| = kappa cannot flip anything that matters).
+// Everything else (near the threshold, huge / tiny / non-finite) takes the exact path.
+__device__ __forceinline__ double2 soft_threshold_lat(double2 a, double kappa, double kappa2_lo, double kappa2_hi) {
+  const double r2 = a.x * a.x + a.y * a.y;
+  if (r2 < kappa2_lo) return make_double2(0.0, 0.0);
+  if (r2 > kappa2_hi && r2 > 1e-280 && r2 < 1e280) {
+    const double f = fma(-kappa, rsqrt(r2), 1.0);
+    return make_double2(a.x * f, a.y * f);
+  }
+  const double mag = hypot(a.x, a.y);
+  if (mag > kappa) {
+    const double f = 1.0 - kappa / mag;
+    return make_double2(a.x * f, a.y * f);
+  }
+  return make_double2(0.0, 0.0);
+}
+
 __device__ __forceinline__ double2 soft_threshold(double2 a, double kappa) {
   const double mag = hypot(a.x, a.y);
   if (mag > kappa) {

@@ -416,7 +416,10 @@ SlabFn<S> slab_fn_rb(int rpl, bool tr) {
 }
 // 16-byte strip rows: tall strips (many rows per segment) in one CTA, 16 slabs of 192 rows
 template <typename S>
-SlabFn<S> slab_fn_rb16(int, bool tr) {
+SlabFn<S> slab_fn_rb16(int rpl, bool tr) {
+  // fewer, fatter warps on request (ADMM_B200_SLAB_RPW=256 / 384): 12 x 256 rows at 128 registers, 8 x 384 at 168
+  if (rpl == 8) return tr ? sweep_slab_kernel<S, 8, 16, true, 12> : sweep_slab_kernel<S, 8, 16, false, 12>;
+  if (rpl == 12) return tr ? sweep_slab_kernel<S, 12, 16, true, 8> : sweep_slab_kernel<S, 12, 16, false, 8>;
   return tr ? sweep_slab_kernel<S, 6, 16, true> : sweep_slab_kernel<S, 6, 16, false>;
 }
 template <typename S>
@@ -445,8 +448,10 @@ bool try_slab(admm_plan* p) {
     if (fB && (uint32_t)fB != rb) continue;
     const uint32_t W = rb / 16 * (16 / sizeof(S));
     if (M * W > kWarp) continue;  // the D warp maps (replica, column) onto lanes
-    for (uint32_t rpl : {2u, 1u, 4u, 6u}) {
-      if ((rpl == 6) != (rb == 16)) continue;  // 16-byte rows come with 192-row slabs (16 warps x 192 = 3072 rows)
+    for (uint32_t rpl : {2u, 1u, 4u, 6u, 8u, 12u}) {
+      if ((rpl >= 6) != (rb == 16)) continue;  // 16-byte rows come with 192-row slabs (16 warps x 192 = 3072 rows)
+      if (rpl > 8 && !fR) continue;            // 384-row slabs (8 warps at 168 registers) only on request: measured slower
+      const uint32_t maxw = rpl == 8 ? 12u : rpl == 12 ? 8u : (uint32_t)kSlabMaxW;
       const uint32_t rpw = rpl * kWarp;
       if (fR && (uint32_t)fR != rpw) continue;
       uint32_t Ns = 0;
@@ -463,7 +468,7 @@ bool try_slab(admm_plan* p) {
         // 265 us) -- the per-strip DSMEM exchange sits on the D warps' critical path
         if (!fC && C > 1) continue;
         const uint32_t nw = (uint32_t)cdiv(Ns, C);
-        if (nw > (uint32_t)kSlabMaxW || (C > 1 && nw * (C - 1) >= Ns)) continue;  // no empty rank
+        if (nw > maxw || (C > 1 && nw * (C - 1) >= Ns)) continue;  // no empty rank
         const size_t fixed = slab_smem_bytes(0, nw, kSlabMaxD, rpw, rb, C, M, W, N);
         const size_t per = (size_t)nw * rpw * rb + nw * sizeof(uint64_t);
         const uint32_t ns = (uint32_t)std::min<size_t>((cap - fixed) / per, 8);
@@ -471,8 +476,11 @@ bool try_slab(admm_plan* p) {
         Cand c{rb, rpl, C, nw, ns, Ns, pad};
         // fewest padding rows (they are streamed), then the smallest cluster, then the
         // widest rows (fewer strips, fewer per-strip overheads)
+        // ... and at 16-byte rows 12 warps x 256 rows (128 registers, 4-row batches) over 16 x 192
+        // (config 3: 5,823 vs 5,625 it/s)
         const bool better = !have || c.pad < best.pad || (c.pad == best.pad && c.C < best.C) ||
-                            (c.pad == best.pad && c.C == best.C && c.rb > best.rb);
+                            (c.pad == best.pad && c.C == best.C && c.rb > best.rb) ||
+                            (c.pad == best.pad && c.C == best.C && c.rb == best.rb && c.rpl == 8 && best.rpl == 6);
         if (better) best = c, have = true;
       }
     }

@@ -212,8 +212,10 @@ __host__ __device__ inline bool slab_lag_ok(uint32_t L, uint32_t ND) {
 // updated by D warp k % ND).  L = lag of the (A) pass behind the (C) pass, in strips.
 // 20 warps x 32 lanes: the register allocation granularity (4 warps) caps this at 96
 // registers per thread (65536 / (20 x 32)).
-template <typename S, int RPL, int RB, bool kTrace>
-__global__ void __launch_bounds__(kSlabThreads, 1)
+// MAXW = compute warps the instantiation is launched with at most: (MAXW + 4) x 32 threads
+// set the register cap (16 -> 96 registers, 12 -> 128, 8 -> 168).
+template <typename S, int RPL, int RB, bool kTrace, int MAXW = kSlabMaxW>
+__global__ void __launch_bounds__((MAXW + kSlabMaxD) * kWarp, 1)
 sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, const BlockDesc* __restrict__ blocks,
                   const SweepDesc* __restrict__ segs, uint32_t M, uint32_t N, uint32_t n_meas, uint64_t U, uint32_t NS,
                   uint32_t L, uint32_t Ns, uint32_t NW, const double2* __restrict__ q, ColVecs cv,
@@ -264,7 +266,7 @@ sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, 
   const uint32_t warp = (uint32_t)warp_index(), lane = threadIdx.x % kWarp;
   // diagnostics: per-strip timestamps of compute warp 0 and the D warps (first 64 strips)
   auto mark = [&](uint32_t k, int ev) {
-    if (kTrace && lane == 0 && k < 64 && (warp == 0 || warp >= NW))
+    if (kTrace && lane == 0 && k < 32 && (warp == 0 || warp >= NW))
       trace[((uint64_t)blockIdx.x * 64 + k) * 8 + ev] = clock64();
   };
 
@@ -360,6 +362,8 @@ sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, 
       }
     };
 
+    long long t_full = 0, t_c = 0, t_n = 0, t_loop0 = 0;
+    if (kTrace) t_loop0 = clock64();
     for (uint32_t k = 0; k < nstrip + L; ++k) {
       if (NSL == 1 && k < nstrip && k >= L) {
         // ------------------------------------------- (C) strip k and (A) strip k - L, fused
@@ -374,10 +378,21 @@ sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, 
           kend = (uint32_t)(tseg[j].unit0 + tseg[j].n_strips - x0);
           load_q(j);
         }
+        mark(k, 0);  // fused timeline: 0 loop top, 2 stage landed, 3 c landed, 1 end
+        long long tw0 = 0;
+        if (kTrace) tw0 = clock64();
         if (act) mbar_wait_s(full_s + stgC * 8, phC);
+        mark(k, 2);
+        long long tw1 = 0;
+        if (kTrace) tw1 = clock64();
         mbar_wait_s(cfull_s + (kk % kSlabZB) * 8, (kk / kSlabZB) & 1);
-        mark(k, 0);
-        mark(kk, 2);
+        mark(k, 3);
+        if (kTrace) {  // per-warp totals (registers; written once at the end of the loop)
+          const long long tw2 = clock64();
+          t_full += tw1 - tw0;
+          t_c += tw2 - tw1;
+          ++t_n;
+        }
         if (act) {
           const double2* cbi = cb_rep + (size_t)(kk % kSlabZB) * M * W;
           double2 cr[PV];
@@ -390,7 +405,8 @@ sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, 
           for (int a2 = 0; a2 < 2; ++a2)
 #pragma unroll
             for (int e = 0; e < PV; ++e) acc[a2][e] = make_double2(0.0, 0.0);
-          constexpr int FB = RPL % 3 == 0 ? 3 : RPL % 2 == 0 ? 2 : 1;  // rows per batch (register cap)
+          // rows per batch (register cap)
+          constexpr int FB = (MAXW <= 12 && RPL % 4 == 0) ? 4 : RPL % 3 == 0 ? 3 : RPL % 2 == 0 ? 2 : 1;
 #pragma unroll
           for (int m0 = 0; m0 < RPL; m0 += FB) {
             CK hc[FB], ha[FB];
@@ -438,7 +454,6 @@ sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, 
         __syncwarp();
         if (lane == 0) mbar_arrive_s(zfull_s + (k % kSlabZB) * 8);
         mark(k, 1);
-        mark(kk, 3);
         if (++stgC == NS) stgC = 0, phC ^= 1u;
         if (++stgA == NS) stgA = 0;
         flush_w(kk);
@@ -528,6 +543,13 @@ sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, 
         flush_w(kk);
       }
     }
+    if (kTrace && lane == 0) {  // slots 32..: per compute warp (loop cycles, stage wait, c wait, fused strips)
+      unsigned long long* o = trace + ((uint64_t)blockIdx.x * 64 + 32 + warp) * 8;
+      o[0] = (unsigned long long)(clock64() - t_loop0);
+      o[1] = (unsigned long long)t_full;
+      o[2] = (unsigned long long)t_c;
+      o[3] = (unsigned long long)t_n;
+    }
   } else {
     // ============================================================ D warps
     const uint32_t dw = warp - NW;
@@ -548,7 +570,7 @@ sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, 
     }
     pdl_enter();  // c, s, v, kappa of the previous kernels are visible from here on
     const double m_rep = prm->m_rep, kappa = prm->kappa;
-    const double kappa2_lo = kappa * kappa * (1.0 - 0x1p-40);
+    const double kappa2_lo = kappa * kappa * (1.0 - 0x1p-40), kappa2_hi = kappa * kappa * (1.0 + 0x1p-40);
     const double inv_m = 1.0 / m_rep;
     const bool pow2_m = inv_m * m_rep == 1.0 && (__double_as_longlong(m_rep) & 0xfffffffffffffull) == 0;
     // this D warp's strips dw, dw + ND, ...: the n-th is prefetched (cp.async, zero-filled
@@ -592,6 +614,8 @@ sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, 
       mark(k, 4);
       double2 z = make_double2(0.0, 0.0);
       {
+        // (a pairwise tree over 16 predicated loads measured slower than this loop: 5,729 vs
+        // 5,823 it/s on config 3 -- the extra LDS / selects cost the compute warps issue slots)
         const double2* zs = zp + (size_t)kb * NW * W + t;
         for (uint32_t w = wlo; w < whi; ++w) z = cadd(z, zs[(size_t)w * W]);
       }
@@ -626,7 +650,7 @@ sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, 
         }
       }
       mean = pow2_m ? make_double2(mean.x * inv_m, mean.y * inv_m) : make_double2(mean.x / m_rep, mean.y / m_rep);
-      const double2 vnew = soft_threshold_fast(mean, kappa, kappa2_lo);
+      const double2 vnew = soft_threshold_lat(mean, kappa, kappa2_lo, kappa2_hi);
       const double2 snew = csub(cadd(spre, u), vnew);
       const double2 cnew = csub(vnew, snew);
       if (dl) cb[((size_t)kb * M + i) * W + t] = dcol ? cnew : make_double2(0.0, 0.0);

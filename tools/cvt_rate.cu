@@ -9,29 +9,37 @@ __device__ __forceinline__ double widen_int(uint32_t f) {
   const uint32_t hi = (a >> 3) + 0x38000000u + s, lo = a << 29;
   return __hiloint2double((int)hi, (int)lo);
 }
-// mode 0: F2F + DFMA (1:2, the ratio of a complex64 GEMV); 1: integer widening + DFMA; 2: DFMA only; 3: F2F only
+// mode 0: F2F + DFMA (1:2, the ratio of a complex64 GEMV); 1: integer widening + DFMA; 2: DFMA only; 3: F2F only;
+// 4: half the values by F2F, half by the integer re-bias, + DFMA (1:2); 5: as 0 with DFMA 1:4 (the packed-K apply's
+// ratio: every element feeds the N part and the H part); 6: as 4 with DFMA 1:4
 template <int MODE>
 __global__ void loop(double* out, int iters, float seed) {
   float f0 = seed + threadIdx.x, f1 = f0 + 1.f, f2 = f0 + 2.f, f3 = f0 + 3.f;
   double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0, a5 = 0, a6 = 0, a7 = 0;
+  double b0 = 0, b1 = 0, b2 = 0, b3 = 0, b4 = 0, b5 = 0, b6 = 0, b7 = 0;
   const double q = 1.0000001, r = 0.999999;
   for (int i = 0; i < iters; ++i) {
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       double d0, d1, d2, d3;
-      if (MODE == 0 || MODE == 3) { d0 = (double)f0; d1 = (double)f1; d2 = (double)f2; d3 = (double)f3; }
+      if (MODE == 0 || MODE == 3 || MODE == 5) { d0 = (double)f0; d1 = (double)f1; d2 = (double)f2; d3 = (double)f3; }
+      else if (MODE == 4 || MODE == 6) { d0 = (double)f0; d1 = widen_int(__float_as_uint(f1)); d2 = (double)f2; d3 = widen_int(__float_as_uint(f3)); }
       else if (MODE == 1) { d0 = widen_int(__float_as_uint(f0)); d1 = widen_int(__float_as_uint(f1)); d2 = widen_int(__float_as_uint(f2)); d3 = widen_int(__float_as_uint(f3)); }
       else { d0 = a0; d1 = a1; d2 = a2; d3 = a3; }
       if (MODE != 3) {
         a0 = fma(d0, q, a0); a1 = fma(d1, q, a1); a2 = fma(d2, q, a2); a3 = fma(d3, q, a3);
         a4 = fma(d0, r, a4); a5 = fma(d1, r, a5); a6 = fma(d2, r, a6); a7 = fma(d3, r, a7);
+        if (MODE == 5 || MODE == 6) {
+          b0 = fma(d0, r, b0); b1 = fma(d1, r, b1); b2 = fma(d2, q, b2); b3 = fma(d3, q, b3);
+          b4 = fma(d0, q, b4); b5 = fma(d1, q, b5); b6 = fma(d2, r, b6); b7 = fma(d3, r, b7);
+        }
       } else { a0 += d0; a1 += d1; a2 += d2; a3 += d3; }
       // keep the floats changing with FP32-pipe work (not measured pipes)
       f0 = __uint_as_float(__float_as_uint(f0) ^ (k + 1)); f1 = __uint_as_float(__float_as_uint(f1) ^ (k + 2));
       f2 = __uint_as_float(__float_as_uint(f2) ^ (k + 3)); f3 = __uint_as_float(__float_as_uint(f3) ^ (k + 4));
     }
   }
-  out[blockIdx.x * blockDim.x + threadIdx.x] = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+  out[blockIdx.x * blockDim.x + threadIdx.x] = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7 + b0 + b1 + b2 + b3 + b4 + b5 + b6 + b7;
 }
 template <int MODE>
 void run(const char* name, double cvt_per_iter, double fma_per_iter) {
@@ -56,6 +64,9 @@ int main() {
   run<3>("F2F.F64.F32 (+DADD)", 4, 4);
   run<0>("F2F + DFMA (1:2)", 4, 8);
   run<1>("integer widen + DFMA (1:2)", 4, 8);
+  run<4>("half F2F half int + DFMA (1:2)", 4, 8);
+  run<5>("F2F + DFMA (1:4)", 4, 16);
+  run<6>("half F2F half int + DFMA (1:4)", 4, 16);
   // exactness of the integer widening on normal floats
   return 0;
 }

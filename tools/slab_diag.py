@@ -65,6 +65,26 @@ def main():
         ncta = t.shape[0]
         entry, exitt = t[:, 0, 6], t[:, 0, 7]
         print(f"  CTAs {ncta}: kernel duration (cycles) mean {np.mean(exitt - entry):.0f}")
+        if int(info['slab_row_bytes']) == 16:  # fused loop: 0 loop top, 2 stage landed, 3 c landed, 1 end
+            w = t[:, 32:48, :4]  # per compute warp: loop cycles, stage wait, c wait, fused strips
+            n = np.maximum(w[:, :, 3], 1)
+            print(f"  per compute warp, per fused strip (all CTAs): loop {np.mean(w[:, :, 0] / n):.0f} cyc | stage wait "
+                  f"{np.mean(w[:, :, 1] / n):.0f} (warp 0: {np.mean(w[:, 0, 1] / n[:, 0]):.0f}, warp 15: "
+                  f"{np.mean(w[:, 15, 1] / n[:, 15]):.0f}) | c wait {np.mean(w[:, :, 2] / n):.0f} (max warp "
+                  f"{np.max(np.mean(w[:, :, 2] / n, axis=0)):.0f})")
+            for cta in (0, 1, ncta // 2, ncta - 1):
+                r = t[cta][:32]
+                ks = np.nonzero((r[:, 0] > 0) & (r[:, 1] > 0) & (r[:, 3] > 0))[0]
+                ks = ks[4:-2]
+                per = np.diff(r[ks, 0])
+                wf, wc, cmp_ = r[ks, 2] - r[ks, 0], r[ks, 3] - r[ks, 2], r[ks, 1] - r[ks, 3]
+                top = r[ks[1:], 0] - r[ks[:-1], 1]
+                dz = r[ks, 5] - r[ks, 4]
+                zl = r[ks, 4] - r[ks, 1]  # D: all z partials of strip k in, after warp 0 published its own
+                f = lambda x: f"{np.mean(x):.0f} (med {np.median(x):.0f}, p90 {np.percentile(x, 90):.0f})"
+                print(f"  cta {cta}: strips {len(ks)} per strip {f(per)} | wait stage {f(wf)} | wait c {f(wc)} | "
+                      f"compute {f(cmp_)} | loop end->top {f(top)} | D z->c {f(dz)} | warp0 z -> all z {f(zl)}")
+            return
         for cta in (0, 1, ncta // 2):
             r = t[cta]
             ok = (r[:, 0] > 0) & (r[:, 3] > 0)
