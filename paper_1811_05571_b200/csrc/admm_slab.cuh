@@ -106,6 +106,14 @@ __device__ __forceinline__ void mbar_wait_s(uint32_t a, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// ... with a suspend-time hint: the warp sleeps in the barrier unit instead of re-polling (the
+// compute warps' wait for c re-polled ~12 times per strip, issue slots the other warps want)
+__device__ __forceinline__ void mbar_wait_hint_s(uint32_t a, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAITH_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n @!p bra WAITH_%=;\n}\n" ::"r"(a),
+      "r"(parity), "r"(0x989680u)
+      : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_s(uint32_t a) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
 }
@@ -385,7 +393,7 @@ sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, 
         mark(k, 2);
         long long tw1 = 0;
         if (kTrace) tw1 = clock64();
-        mbar_wait_s(cfull_s + (kk % kSlabZB) * 8, (kk / kSlabZB) & 1);
+        mbar_wait_hint_s(cfull_s + (kk % kSlabZB) * 8, (kk / kSlabZB) & 1);
         mark(k, 3);
         if (kTrace) {  // per-warp totals (registers; written once at the end of the loop)
           const long long tw2 = clock64();
@@ -506,7 +514,7 @@ sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, 
       if (k >= L) {
         // ---------------------------------------------------------- (A) strip k - L
         const uint32_t kk = k - L;
-        mbar_wait_s(cfull_s + (kk % kSlabZB) * 8, (kk / kSlabZB) & 1);
+        mbar_wait_hint_s(cfull_s + (kk % kSlabZB) * 8, (kk / kSlabZB) & 1);
         mark(kk, 2);
         if (act) {
           const double2* cbi = cb_rep + (size_t)(kk % kSlabZB) * M * W;
