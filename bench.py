@@ -367,7 +367,7 @@ def bench_ours(args):
         roof, kern = kernel_roofline(plan, info, problem, args.config)
     else:  # the plan's kernels are not launched one by one: whole-iteration HBM roofline
         peak, peak_kind = peaks()
-        passes = 1 if int(info["schedule"]) == 2 else 2
+        passes = 1 if int(info["schedule"]) in (2, 5) else 2  # sweep / support: one dense pass over this rank's H
         achieved = info["h_bytes"] * passes / (ms_per_step / 1000.0) / 1e9
         roof = {"bound": "hbm", "kernel": f"whole iteration ({passes} pass(es) over this rank's H)",
                 "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,

@@ -534,17 +534,20 @@ uupdate_kernel(ColVecs cv, double2* __restrict__ outbox, const double2* __restri
 __global__ void __launch_bounds__(kCtaThreads)
 zfinal_kernel(ColVecs cv, const double2* __restrict__ outbox, const BlockDesc* __restrict__ blocks,
               uint32_t M, uint32_t Mr, uint32_t Nc, uint32_t npad, int count_v, const Params* __restrict__ prm,
-              double* __restrict__ red) {
+              double* __restrict__ red,
+              uint32_t* __restrict__ nzcnt = nullptr) {  // support counts per CTA (sharded support schedule)
   __shared__ double sm[kCtaWarps];
   const uint32_t jl = blockIdx.y;
   const BlockDesc b0 = blocks[jl];
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   double rp2 = 0.0, rd2 = 0.0, l1 = 0.0;
+  bool nz = false;
   if (t < b0.cols) {
     double2 mean = make_double2(0.0, 0.0);
     for (uint32_t i = 0; i < M; ++i) mean = cadd(mean, outbox[((uint64_t)i * Nc + jl) * npad + t]);
     mean = make_double2(mean.x / prm->m_rep, mean.y / prm->m_rep);
     const double2 vn = soft_threshold(mean, prm->kappa);
+    nz = vn.x != 0.0 || vn.y != 0.0;
     const uint32_t so = b0.seg_off + t;
     const double2 vo = cv.v[so];
     cv.vprev[so] = vo;
@@ -563,6 +566,10 @@ zfinal_kernel(ColVecs cv, const double2* __restrict__ outbox, const BlockDesc* _
     }
   }
   const uint32_t cta = blockIdx.y * gridDim.x + blockIdx.x, nct = gridDim.x * gridDim.y;
+  if (nzcnt) {
+    const int c = __syncthreads_count(nz);
+    if (threadIdx.x == 0) nzcnt[cta] = (uint32_t)c;
+  }
   double r = block_sum<kCtaThreads>(rp2, sm);
   if (threadIdx.x == 0) red[cta] = r;
   r = block_sum<kCtaThreads>(rd2, sm);

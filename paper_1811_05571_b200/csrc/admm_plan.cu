@@ -726,7 +726,11 @@ void launch_resident_any(admm_plan* p, cudaStream_t s, uint64_t iters, bool prol
 // soft threshold makes it sparse); on request (schedule 5) for any shape.
 template <typename S>
 bool try_support(admm_plan* p, int requested) {
-  if (p->is_shard || p->batch > 1 || p->Pr * p->Pc > 1) return false;
+  if (p->batch > 1) return false;
+  // a shard of a multi-GPU plan: consensus over row-block ranks (Pc = 1, every rank holds the whole
+  // v after the replica-mean exchange); driven by the two-pass phase program with phase 1 replaced
+  if (p->is_shard && (p->method != ADMM_CONSENSUS || p->Pc != 1 || p->Nc != 1)) return false;
+  if (!p->is_shard && p->Pr * p->Pc > 1) return false;
   if (requested != 5) {
     if (requested != 0 || p->method != ADMM_CONSENSUS || p->M < 2) return false;
     if (p->h_elems * sizeof(S) <= (256ull << 20)) return false;
@@ -1696,7 +1700,9 @@ void reset_state(admm_plan* p) {
       enqueue_sweep_prologue<float2>(p, s);
   }
   if (p->schedule == 4) launch_resident_any(p, s, 0, true, false);
-  if (p->schedule == 5) {  // prologue: r = g_ij (w = H c^0 = 0), q = K r, ghat
+  if (p->schedule == 5 && p->is_shard) {  // phase 1 of the first iteration is the prologue (v = 0: empty support)
+    CK(cudaMemsetAsync(p->dnzcnt.p, 0, p->dnzcnt.bytes, s));
+  } else if (p->schedule == 5) {  // prologue: r = g_ij (w = H c^0 = 0), q = K r, ghat
     enqueue_support_rows(p, s, true);
     if (p->dtype == ADMM_C128)
       enqueue_kapply<double2>(p, s);
@@ -2306,8 +2312,8 @@ admm_status admm_plan_get_info(const admm_plan* p, admm_plan_info* info) {
     r.launches_per_iter = p->schedule == 5 ? 8 : p->schedule == 4 ? 0 : p->schedule == 3 ? 7 : p->schedule == 2 ? (p->trace_obj ? (p->obj_pass ? 7 : 6) : 4) : (p->trace_obj ? 9 : 7);
     r.schedule = (uint64_t)p->schedule;
     r.grid_sweep = p->gS.P;
-    // support schedule: one dense pass + K + G (+ the data-dependent support columns, admm_plan_read 5)
-    r.hbm_bytes_per_iter = p->schedule == 5 ? hb + 2 * kb + vb : (p->schedule == 4 ? 0 : p->schedule == 2 ? hb : 2 * hb) + kb + vb;
+    // support schedule: one dense pass + K (+ the data-dependent support columns, admm_plan_read 5)
+    r.hbm_bytes_per_iter = p->schedule == 5 ? hb + kb + vb : (p->schedule == 4 ? 0 : p->schedule == 2 ? hb : 2 * hb) + kb + vb;
     r.sweep_variant = p->schedule != 2 ? 0 : p->slab_rpl ? 3 : 1;
     r.slab_cluster = p->slab_rpl ? p->slab_C : 0;
     r.slab_row_bytes = p->slab_rpl ? p->slab_rb : 0;
@@ -2555,6 +2561,17 @@ void enqueue_phase(admm_plan* p, int phase) {
           p->dgblocks.as<BlockDesc>(), (uint32_t)p->N, (uint32_t)p->n_meas, p->gS.U, p->gS.P, 0, 2,
           p->dred.as<double>(), p->dparams.as<Params>(), p->dtrace.as<double>(), p->trace_cap,
           p->dstate.as<IterState>(), p->scal_ptr + scal_stride(p) * (p->pr * p->Pc + p->pc));
+    } else if (p->schedule == 5) {
+      // support schedule (admm_sparse.cuh) on a consensus shard: w = H c from the support of the v
+      // every rank formed in phase 3 (v = 0 after a reset: empty support, w = 0, r = g)
+      support_compact_kernel<<<dim3(p->zgx, (unsigned)p->Nc), kCtaThreads, 0, s>>>(
+          p->dv.as<double2>(), p->dblocks.as<BlockDesc>(), p->dnzcnt.as<uint32_t>(), p->zgx, p->dnzlist.as<uint32_t>(),
+          p->nzstride, p->dnnz.as<uint32_t>(), p->dnnz_tot.as<unsigned long long>());
+      support_a_kernel<S><<<dim3(p->supgx, (unsigned)nb, p->sup_chunks), kSupThreads, 0, s>>>(
+          p->dHc.as<S>(), p->dhcoff.as<uint64_t>(), p->dhcld.as<uint32_t>(), p->dblocks.as<BlockDesc>(),
+          p->dv.as<double2>(), p->dnzlist.as<uint32_t>(), p->nzstride, p->dnnz.as<uint32_t>(), p->danew.as<double2>(),
+          p->mvec_total);
+      enqueue_support_rows(p, s, false);
     } else {
       gemv_n_kernel<S, kVN, kEvictNormal><<<(unsigned)p->gN.P, kCtaThreads, 0, s>>>(
           p->dH.as<S>(), p->dc.as<double2>(), p->dwpart.as<double2>(), p->dhN.as<MatDesc>(), nb, p->gN.U);
@@ -2577,7 +2594,8 @@ void enqueue_phase(admm_plan* p, int phase) {
     } else {
       zfinal_kernel<<<dim3(p->zgx, (unsigned)p->Nc), kCtaThreads, 0, s>>>(
           col_vecs(p), p->outbox_ptr, p->dblocks.as<BlockDesc>(), (uint32_t)p->M, (uint32_t)p->Mr,
-          (uint32_t)p->Nc, (uint32_t)p->npad, p->pr == 0 ? 1 : 0, p->dparams.as<Params>(), p->dred.as<double>());
+          (uint32_t)p->Nc, (uint32_t)p->npad, p->pr == 0 ? 1 : 0, p->dparams.as<Params>(), p->dred.as<double>(),
+          p->schedule == 5 ? p->dnzcnt.as<uint32_t>() : nullptr);
       if (p->shard_obj) enqueue_grows(p, s, p->pc == 0, 1);  // iteration k-1's rows, one rank per row block
       local_scalars_kernel<<<1, kCtaThreads, 0, s>>>(
           p->dred.as<double>(), p->nz, p->shard_obj ? p->dobjp.as<double>() : nullptr, p->objgx * (uint32_t)p->Mr,

@@ -108,7 +108,7 @@ class ShardPlan:
         h = np.ascontiguousarray(h) if h_dtype else _as_c128(h)
         g = _as_c128(problem.g)
         o = _lib.PlanOptionsC(_METHOD[method], M, N, int(opts.ragged), _DTYPE[opts.dtype], int(opts.device),
-                              int(opts.trace_objective), {"auto": 0, "twopass": 1, "sweep": 2}[opts.schedule], 1,
+                              int(opts.trace_objective), {"auto": 0, "twopass": 1, "sweep": 2, "support": 5}[opts.schedule], 1,
                               float(problem.noise_sigma))
         c = cfg._c()
         sh = _lib.ShardC(self.Pr, self.Pc, self.pr, self.pc)
@@ -148,6 +148,11 @@ class ShardPlan:
 
     def reset(self) -> None:
         self._check(self._lib.lib.admm_plan_reset(self._h))
+
+    def info(self) -> dict:
+        i = self._lib.PlanInfoC()
+        self._check(self._lib.lib.admm_plan_get_info(self._h, ctypes.byref(i)))
+        return {f: getattr(i, f) for f, _ in self._lib.PlanInfoC._fields_ if f != "setup_phase_s"}
 
     def set_stream(self, stream) -> None:
         """Launch on `stream` (a torch.cuda.Stream; None: the plan's own stream)."""

@@ -60,6 +60,56 @@ def test_sharded_plans_match_oracle(method, M, N, shape, P, iters):
     assert np.max(np.abs(ob - ref["trace"][:n, 2]) / np.abs(ref["trace"][:n, 2])) <= 1e-9
 
 
+@pytest.mark.parametrize("P,dtype", [(2, "c128"), (4, "c128"), (4, "c64")])
+def test_sharded_support_schedule_matches_oracle(P, dtype):
+    """Consensus shards on the support schedule (one dense H pass per rank and iteration: w = H c
+    from the support of the v every rank holds after the replica-mean exchange, G q = r - rho q;
+    admm_sparse.cuh) driven by the two-pass phase program, through the test transport."""
+    import paper_1811_05571_b200 as admm
+    from paper_1811_05571_b200 import distributed as D
+    M, shape, iters = 4, (256, 2048), 60
+    p = admm.gen_problem(shape[0], shape[1], 8, 30.0, 31, dtype=dtype)
+    h128 = p.h.astype(np.complex128)
+    lam = 0.05 * float(np.max(np.abs(orc.adjoint_matvec(h128, p.g))))
+    cfg = admm.SolverConfig(rho=1.0, lambda_=lam, max_iters=iters)
+    opts = admm.SolveOptions(dtype=dtype, schedule="support")
+    shards = [D.ShardPlan(p, cfg, "consensus", M, 1, (P, 1), (r, 0), opts) for r in range(P)]
+    assert all(sh.info()["schedule"] == 5 for sh in shards)
+    D.run_iterations(shards, DH.LoopbackComm(P, 1), iters)
+    for sh in shards:
+        sh.sync()
+    v = D.gather_solution([sh.segment_v() for sh in shards], shape[1], shards[0].col_bounds)
+    ref = orc.solve("consensus", h128, p.g, M=M, N=1, lam=lam, iters=iters)
+    assert rel(v, ref["solution"]) <= (1e-9 if dtype == "c128" else 1e-4)
+    trs = [sh.trace() for sh in shards]
+    for tr in trs:
+        np.testing.assert_array_equal(tr, trs[0])
+    tol = 1e-8 if dtype == "c128" else 1e-3
+    assert np.max(np.abs(trs[0][:, 1] - ref["trace"][:, 1]) / np.abs(ref["trace"][:, 1])) <= tol
+    ob = trs[0][:iters - 1, 2]  # the two-pass program closes iteration k-1's objective in iteration k
+    assert np.max(np.abs(ob - ref["trace"][:iters - 1, 2]) / np.abs(ref["trace"][:iters - 1, 2])) <= (1e-9 if dtype == "c128" else 1e-4)
+
+
+def test_plan_owned_nccl_support_schedule():
+    """The plan-owned NCCL driver (graph-captured phases + collectives) on the support schedule."""
+    import paper_1811_05571_b200 as admm
+    from paper_1811_05571_b200 import distributed as D
+    p = admm.gen_problem(256, 2048, 8, 30.0, 29)
+    lam = 0.05 * float(np.max(np.abs(orc.adjoint_matvec(p.h, p.g))))
+    cfg = admm.SolverConfig(rho=1.0, lambda_=lam, max_iters=40)
+    with D.dist_plan(p, cfg, "consensus", 4, 1, admm.SolveOptions(schedule="support")) as plan:
+        assert plan.info()["schedule"] == 5
+        r = plan.solve()
+        r2 = plan.solve()
+    np.testing.assert_array_equal(r.solution, r2.solution)
+    ref = orc.solve("consensus", p.h, p.g, M=4, N=1, lam=lam, iters=40)
+    assert rel(r.solution, ref["solution"]) <= 1e-9
+    tr = np.stack([r.trace.primal, r.trace.dual, r.trace.objective], 1)
+    assert np.max(np.abs(tr[:, 1] - ref["trace"][:, 1]) / np.abs(ref["trace"][:, 1])) <= 1e-8
+    assert np.max(np.abs(tr[:, 2] - ref["trace"][:, 2]) / np.abs(ref["trace"][:, 2])) <= 1e-9
+    assert abs(r.objective - ref["objective"]) <= 1e-9 * abs(ref["objective"])
+
+
 CASES = [("sectioning", 1, 8, (64, 2048), 25, "c128"), ("consensus", 4, 1, (256, 2048), 40, "c128"),
          ("hybrid", 2, 4, (96, 1024), 20, "c128"), ("consensus", 8, 1, (512, 4096), 30, "c64"),
          ("reference", 1, 1, (40, 120), 30, "c128")]
