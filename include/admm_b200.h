@@ -131,6 +131,8 @@ admm_status admm_plan_create(const admm_plan_options* opts, const admm_solver_co
  * buffers it attaches; the engine never waits on a peer inside a kernel.
  *   iteration (sweep schedule, Pr == 1):  phase 1, X_ghat, X_scal, phase 4
  *   iteration (two-pass schedule):        phase 1, X_ghat, phase 2, X_outbox, phase 3, X_scal, phase 4
+ *   (a consensus shard on the support schedule runs the two-pass program: its phase 1 forms
+ *   w = H c from the support of the v every rank holds after phase 3 -- one dense pass per rank)
  * X_ghat: all-gather over the row communicator (ranks with the same pr, ordered by pc);
  * X_outbox: all-gather over the column communicator (same pc, ordered by pr);
  * X_scal: all-gather over all Pr*Pc ranks (rank = pr*Pc + pc).  Each rank's slot is
@@ -225,7 +227,7 @@ typedef struct {
   uint64_t grid_gemv_n, grid_gemv_h;
   double setup_seconds;         /* upload + Gram + inverse (host wall clock) */
   uint64_t inner_dim_max;       /* largest factored dimension */
-  uint64_t schedule;            /* 1 two-pass, 2 sweep, 3 batched scenes, 4 resident */
+  uint64_t schedule;            /* 1 two-pass, 2 sweep, 3 batched scenes, 4 resident, 5 support */
   uint64_t grid_sweep;
   uint64_t hbm_bytes_per_iter;  /* compulsory HBM bytes of the chosen schedule */
   uint64_t sweep_variant;       /* schedule 2 kernel: 1 L2 re-read sweep, 2 strip-major tile, 3 slab */
