@@ -206,15 +206,15 @@ gemv_h_kernel(const S* __restrict__ A, const double2* __restrict__ Q, double2* _
       const uint32_t row = rt * kRowTileH + r * kCtaWarps + warp;
       const bool rok = row < md.rows;
       qv[r] = rok ? Q[md.x_off + row] : make_double2(0.0, 0.0);
-      const S* arow = A + md.a_off + (uint64_t)row * md.ld;
+      // Unconditional loads from clamped addresses (no zero-fill, no predicated LDG): a row past
+      // the block reads the last row against q = 0 (H is validated finite), a column past the
+      // padded row reads the row's last vector into accumulators of columns >= cols, which no
+      // consumer reads (columns in [cols, ld) are the arena's zero padding).
+      const S* arow = A + md.a_off + (uint64_t)(rok ? row : md.rows - 1) * md.ld;
 #pragma unroll
       for (int v = 0; v < VH; ++v) {
         const uint32_t col = c0 + v * kWarp * PV;
-        if (rok && col < md.cols) {
-          hv[r][v] = ld_stream256<EF>(arow + col);
-        } else {
-          hv[r][v].w[0] = hv[r][v].w[1] = hv[r][v].w[2] = hv[r][v].w[3] = 0;
-        }
+        hv[r][v] = ld_stream256<EF>(arow + min(col, md.ld - PV));
       }
     }
 #pragma unroll
