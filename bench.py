@@ -178,7 +178,8 @@ def run_reference(name, iters, threads=None):
                 f"{s['cols']} columns, M={s['M']} N={s['N']}), it/s x {s['scale']:g} (cost linear in H size)")
         if s["scenes"] > 1:
             what += f"; one scene per reference solve, it/s / {s['scenes']} scenes"
-        return {"value": value, "measured": measured, "setup_s": float(md["setup_s"]), "threads": threads,
+        return {"value": value, "measured": measured, "scale": s["scale"] / s["scenes"],
+                "setup_s": float(md["setup_s"]), "threads": threads,
                 "iters": max(2, iters),
                 "sample": (f"unmodified reference ({s['method']}_solve, oracle/_ref) on {what}; {max(2, iters)} "
                            f"iterations after its serial setup ({float(md['setup_s']):.1f} s, excluded); it/s "
@@ -199,7 +200,10 @@ def bench_reference(args):
         return
     v = r["value"]
     line = {"metric": "ADMM iterations/s", "value": v, "unit": "iterations/s", "impl": "reference",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / v,
+            # a step = one reference iteration on the bounded sample (what was executed and timed);
+            # `value` scales it to the whole workload (cpu_baseline.sample says how)
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / r["measured"],
+            "sample_scale": r["scale"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
             "data": "synthetic", "config": config_dict(args.config),
             "cpu_baseline": {"value": v, "unit": "iterations/s", "cores": r["threads"], "kind": "reference",
