@@ -35,8 +35,7 @@ __global__ void loop(double* out, int iters, float seed) {
         }
       } else { a0 += d0; a1 += d1; a2 += d2; a3 += d3; }
       // keep the floats changing with FP32-pipe work (not measured pipes)
-      f0 = __uint_as_float(__float_as_uint(f0) ^ (k + 1)); f1 = __uint_as_float(__float_as_uint(f1) ^ (k + 2));
-      f2 = __uint_as_float(__float_as_uint(f2) ^ (k + 3)); f3 = __uint_as_float(__float_as_uint(f3) ^ (k + 4));
+      f0 += 1.0f; f1 += 2.0f; f2 += 3.0f; f3 += 5.0f;  // loop-carried: no two conversions share a value
     }
   }
   out[blockIdx.x * blockDim.x + threadIdx.x] = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7 + b0 + b1 + b2 + b3 + b4 + b5 + b6 + b7;

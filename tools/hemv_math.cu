@@ -15,12 +15,30 @@ __device__ __forceinline__ void cmac_conj(double2& acc, double2 a, double2 b) {
   acc.x = fma(a.x, b.x, acc.x); acc.x = fma(a.y, b.y, acc.x);
   acc.y = fma(a.x, b.y, acc.y); acc.y = fma(-a.y, b.x, acc.y);
 }
-template <int MODE, int WARPS>
+// binary32 -> binary64 on the integer pipes (normal, non-zero values; zero maps to 2^-127-ish garbage)
+__device__ __forceinline__ double widen_int(float f) {
+  const unsigned u = __float_as_uint(f);
+  const unsigned a = u & 0x7fffffffu;
+  const unsigned hi = ((a >> 3) + 0x38000000u) | (u & 0x80000000u), lo = u << 29;
+  return __hiloint2double((int)hi, (int)lo);
+}
+// WM: 0 F2F for both components, 1 integer widening for both, 2 F2F for re / integer for im
+template <int WM>
+__device__ __forceinline__ double2 widen2(float x, float y) {
+  if (WM == 0) return make_double2((double)x, (double)y);
+  if (WM == 1) return make_double2(widen_int(x), widen_int(y));
+  return make_double2((double)x, widen_int(y));
+}
+template <int MODE, int WARPS, int WM = 0>
 __global__ void __launch_bounds__(WARPS * 32, 1) loop(double* out, long long* cyc, int tiles, float seed) {
   extern __shared__ __align__(16) unsigned char sm[];
   float2* tile = reinterpret_cast<float2*>(sm);           // 2 tiles of 64 x 64
-  double2* xs = reinterpret_cast<double2*>(sm + 2 * 32768);  // 128 entries
-  for (int e = threadIdx.x; e < 2 * 4096; e += blockDim.x) tile[e] = make_float2(seed + e * 1e-4f, seed - e * 2e-4f);
+  double2* tiled = reinterpret_cast<double2*>(sm);       // WM == 3: the tiles as complex128
+  double2* xs = reinterpret_cast<double2*>(sm + 2 * 65536);  // 128 entries
+  if (WM == 3)
+    for (int e = threadIdx.x; e < 2 * 4096; e += blockDim.x) tiled[e] = make_double2(seed + e * 1e-4, seed - e * 2e-4);
+  else
+    for (int e = threadIdx.x; e < 2 * 4096; e += blockDim.x) tile[e] = make_float2(seed + e * 1e-4f, seed - e * 2e-4f);
   for (int e = threadIdx.x; e < 128; e += blockDim.x) xs[e] = make_double2(1.0 + e * 1e-3, 0.5 - e * 1e-3);
   __syncthreads();
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -35,9 +53,15 @@ __global__ void __launch_bounds__(WARPS * 32, 1) loop(double* out, long long* cy
     double2 h[RW][2];
 #pragma unroll
     for (int k = 0; k < RW; ++k) {
-      const float4 f = *reinterpret_cast<const float4*>(ts + k * 64);
-      h[k][0] = make_double2(f.x, f.y);
-      h[k][1] = make_double2(f.z, f.w);
+      if (WM == 3) {
+        const double2* td = tiled + (t & 1) * 4096 + (warp * RW + k) * 64 + lane * 2;
+        h[k][0] = td[0];
+        h[k][1] = td[1];
+      } else {
+        const float4 f = *reinterpret_cast<const float4*>(ts + k * 64);
+        h[k][0] = widen2<WM>(f.x, f.y);
+        h[k][1] = widen2<WM>(f.z, f.w);
+      }
     }
     if (MODE != 3) {
 #pragma unroll
@@ -59,15 +83,15 @@ __global__ void __launch_bounds__(WARPS * 32, 1) loop(double* out, long long* cy
   out[blockIdx.x * blockDim.x + threadIdx.x] = r;
   if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
-template <int MODE, int WARPS>
+template <int MODE, int WARPS, int WM = 0>
 void run(const char* name) {
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   double* out; long long* cyc; cudaMalloc(&out, sizeof(double) * sms * WARPS * 32); cudaMalloc(&cyc, sizeof(long long) * sms);
-  const size_t smem = 2 * 32768 + 128 * 16;
-  cudaFuncSetAttribute(loop<MODE, WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const size_t smem = 2 * 65536 + 128 * 16;
+  cudaFuncSetAttribute(loop<MODE, WARPS, WM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int tiles = 4000;
-  loop<MODE, WARPS><<<sms, WARPS * 32, smem>>>(out, cyc, 16, 1.5f);
-  loop<MODE, WARPS><<<sms, WARPS * 32, smem>>>(out, cyc, tiles, 1.5f);
+  loop<MODE, WARPS, WM><<<sms, WARPS * 32, smem>>>(out, cyc, 16, 1.5f);
+  loop<MODE, WARPS, WM><<<sms, WARPS * 32, smem>>>(out, cyc, tiles, 1.5f);
   long long c0 = 0; cudaMemcpy(&c0, cyc, sizeof(c0), cudaMemcpyDeviceToHost);
   printf("%-52s %2d warps: %7.0f cycles per tile\n", name, WARPS, (double)c0 / tiles);
   cudaFree(out); cudaFree(cyc);
@@ -79,6 +103,13 @@ int main() {
   run<3, 8>("H part only");
   run<0, 16>("N + H parts as in the kernel, 4 rows per warp");
   run<1, 16>("N + H parts, H in 8 chains, 4 rows per warp");
+  run<0, 8, 1>("N + H parts, integer widening");
+  run<0, 8, 2>("N + H parts, re by F2F / im by integer widening");
+  run<2, 8, 1>("N part only, integer widening");
+  run<2, 8, 2>("N part only, half F2F / half integer");
+  run<1, 8, 2>("N + H (8 chains), half F2F / half integer");
+  run<2, 8, 3>("N part only, tile stored as complex128 (no widening)");
+  run<0, 8, 3>("N + H parts, tile stored as complex128 (no widening)");
   run<0, 4>("N + H parts, 16 rows per warp");
   run<1, 4>("N + H parts, H in 8 chains, 16 rows per warp");
   return 0;
