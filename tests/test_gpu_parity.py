@@ -380,6 +380,9 @@ def test_sweep_schedule_equals_twopass(shape, method, M, N, ragged, dtype):
     {"ADMM_B200_SLAB_C": "2", "ADMM_B200_SLAB_RB": "32"},           # half-width strips
     {"ADMM_B200_SLAB_C": "4", "ADMM_B200_SLAB_RB": "32", "ADMM_B200_SLAB_RPW": "64"},
     {"ADMM_B200_SLAB_ND": "1", "ADMM_B200_SLAB_LAG": "1"},          # one D warp
+    {"ADMM_B200_SLAB_RB": "16", "ADMM_B200_SLAB_RPW": "192"},       # 16-byte rows: 16 warps x 192 rows, fused loop
+    {"ADMM_B200_SLAB_RB": "16", "ADMM_B200_SLAB_RPW": "256"},       # ... 12 warps x 256 rows at 128 registers
+    {"ADMM_B200_SLAB_RB": "16", "ADMM_B200_SLAB_RPW": "384"},       # ... 8 warps x 384 rows at 168 registers
 ])
 @pytest.mark.parametrize("shape,method,M,N,dtype", [
     ((512, 4096), "sectioning", 1, 4, "c128"),
@@ -408,6 +411,8 @@ def test_slab_geometries_equal_twopass(monkeypatch, geom, shape, method, M, N, d
                         assert info["slab_cluster"] == int(geom["ADMM_B200_SLAB_C"])
                     if "ADMM_B200_SLAB_RB" in geom:
                         assert info["slab_row_bytes"] == int(geom["ADMM_B200_SLAB_RB"])
+                    if "ADMM_B200_SLAB_RPW" in geom:
+                        assert info["slab_rows"] == int(geom["ADMM_B200_SLAB_RPW"])
                 outs[sched] = plan.solve()
     t, s = outs["twopass"], outs["sweep"]
     assert rel(s.solution, t.solution) <= 1e-12
