@@ -618,7 +618,13 @@ sweep_slab_kernel(const S* __restrict__ Hs, const SlabDesc* __restrict__ slabs, 
       cpa_wait<kSlabPF - 1>();  // this strip's iterates
       const double2* pk = pfw + (size_t)(n % (kSlabPF + 1)) * 3 * kWarp;
       const double2 cpre = pk[0], spre = pk[kWarp], vpre = pk[2 * kWarp];
-      mbar_wait(&zfull[kb], (k / kSlabZB) & 1);
+      // tall strips (16-byte rows): a D warp is idle ~90% of a strip period and its spin loop (~220
+      // polls per strip) takes issue slots from the compute warps, so it sleeps in the barrier unit;
+      // short strips keep the spin (the hint costs config 1, where the wake-up latency shows, 5%)
+      if constexpr (RB == 16)
+        mbar_wait_sleep(&zfull[kb], (k / kSlabZB) & 1);
+      else
+        mbar_wait(&zfull[kb], (k / kSlabZB) & 1);
       mark(k, 4);
       double2 z = make_double2(0.0, 0.0);
       {
