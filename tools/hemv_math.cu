@@ -96,7 +96,69 @@ void run(const char* name) {
   printf("%-52s %2d warps: %7.0f cycles per tile\n", name, WARPS, (double)c0 / tiles);
   cudaFree(out); cudaFree(cyc);
 }
+
+// Software-pipelined variant: the raw rows of tile t + 1 are loaded (LDS.128) before the arithmetic of
+// tile t, so the SMEM read latency / bandwidth phase of a warp overlaps its own FP64 phase.
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 1) loop_pipe(double* out, long long* cyc, int tiles, float seed) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  float2* tile = reinterpret_cast<float2*>(sm);
+  double2* xs = reinterpret_cast<double2*>(sm + 2 * 65536);
+  for (int e = threadIdx.x; e < 2 * 4096; e += blockDim.x) tile[e] = make_float2(seed + e * 1e-4f, seed - e * 2e-4f);
+  for (int e = threadIdx.x; e < 128; e += blockDim.x) xs[e] = make_double2(1.0 + e * 1e-3, 0.5 - e * 1e-3);
+  __syncthreads();
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  constexpr int RW = 64 / WARPS;
+  double2 accN[RW], xI[RW];
+  for (int k = 0; k < RW; ++k) accN[k] = make_double2(0, 0), xI[k] = xs[64 + warp * RW + k];
+  double2 hsum = make_double2(0, 0);
+  float4 raw[RW], nxt[RW];
+  {
+    const float2* ts = tile + (warp * RW) * 64 + lane * 2;
+#pragma unroll
+    for (int k = 0; k < RW; ++k) raw[k] = *reinterpret_cast<const float4*>(ts + k * 64);
+  }
+  const long long t0 = clock64();
+  for (int t = 0; t < tiles; ++t) {
+    const double2 xj0 = xs[(lane * 2 + t) & 63], xj1 = xs[(lane * 2 + 1 + t) & 63];
+    const float2* tn = tile + ((t + 1) & 1) * 4096 + (warp * RW) * 64 + lane * 2;
+#pragma unroll
+    for (int k = 0; k < RW; ++k) nxt[k] = *reinterpret_cast<const float4*>(tn + k * 64);
+    double2 a0 = make_double2(0, 0), a1 = a0;
+#pragma unroll
+    for (int k = 0; k < RW; ++k) {
+      const double2 h0 = make_double2(raw[k].x, raw[k].y), h1 = make_double2(raw[k].z, raw[k].w);
+      cmac(accN[k], h0, xj0);
+      cmac(accN[k], h1, xj1);
+      cmac_conj(a0, h0, xI[k]);
+      cmac_conj(a1, h1, xI[k]);
+    }
+    hsum.x += a0.x + a1.x; hsum.y += a0.y + a1.y;
+#pragma unroll
+    for (int k = 0; k < RW; ++k) raw[k] = nxt[k];
+  }
+  const long long t1 = clock64();
+  double r = hsum.x + hsum.y;
+  for (int k = 0; k < RW; ++k) r += accN[k].x + accN[k].y;
+  out[blockIdx.x * blockDim.x + threadIdx.x] = r;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+template <int WARPS>
+void run_pipe(const char* name) {
+  int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  double* out; long long* cyc; cudaMalloc(&out, sizeof(double) * sms * WARPS * 32); cudaMalloc(&cyc, sizeof(long long) * sms);
+  const size_t smem = 2 * 65536 + 128 * 16;
+  cudaFuncSetAttribute(loop_pipe<WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int tiles = 4000;
+  loop_pipe<WARPS><<<sms, WARPS * 32, smem>>>(out, cyc, 16, 1.5f);
+  loop_pipe<WARPS><<<sms, WARPS * 32, smem>>>(out, cyc, tiles, 1.5f);
+  long long c0 = 0; cudaMemcpy(&c0, cyc, sizeof(c0), cudaMemcpyDeviceToHost);
+  printf("%-52s %2d warps: %7.0f cycles per tile\n", name, WARPS, (double)c0 / tiles);
+  cudaFree(out); cudaFree(cyc);
+}
 int main() {
+  run_pipe<8>("N + H parts, next tile's rows loaded ahead");
+  run_pipe<16>("N + H parts, next tile's rows loaded ahead");
   run<0, 8>("N + H parts as in hemv_bulk_kernel");
   run<1, 8>("N + H parts, H in 8 chains");
   run<2, 8>("N part only");
